@@ -1,0 +1,124 @@
+/*
+ * skycell_gpu.h -- C ABI of the B200-native SkyCell skyline path.
+ *
+ * Drop-in for the reference entry point
+ *
+ *   SkylineResult skycell::compute_skyline(const Dataset& ds, int rho, Mode mode,
+ *                                          ThreadPool& pool, bool merge_cross_cell = true);
+ *       (/root/reference/proj/include/skycell/refine.hpp:61-62,
+ *        /root/reference/proj/src/refine.cpp:108-158)
+ *
+ * and its only library caller
+ *
+ *   SkylineResult skycell::quadrant_skyline(const Dataset&, std::span<const double> origin,
+ *                                           int rho, Mode, ThreadPool&);
+ *       (refine.hpp:66-68, refine.cpp:160-184)
+ *
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary.
+ * The C++ wrapper with the reference's exact signature and exception types is
+ * include/skycell_gpu.hpp; the ctypes binding is paper_2107_09993_b200/skycell.py.
+ *
+ * Every entry point returns a status code and, on failure, writes the
+ * reference's exception message into err (truncated to err_len).  The codes map
+ * 1:1 onto the reference's exception taxonomy (proj/include/skycell/error.hpp:9-26).
+ */
+#ifndef SKYCELL_GPU_H_
+#define SKYCELL_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum skycell_status {
+  SKYCELL_OK = 0,
+  SKYCELL_INPUT = 1,    /* skycell::InputError  (dataset.cpp:23-43)               */
+  SKYCELL_CONFIG = 2,   /* skycell::ConfigError (grid.cpp:38-43)                  */
+  SKYCELL_USAGE = 3,    /* skycell::UsageError  (refine.cpp:162-163)              */
+  SKYCELL_IO = 4,       /* skycell::IoError                                       */
+  SKYCELL_CUDA = 5,     /* CUDA runtime failure (no reference equivalent)         */
+  SKYCELL_NCCL = 6,     /* collective failure  (no reference equivalent)          */
+  SKYCELL_UNSUPPORTED = 7 /* valid for the reference, not (yet) for this build    */
+};
+
+/* Mode, refine.hpp:40.  Ids never depend on it; it only selects whether
+ * per-layer candidate counts are reported (kSequential reports -1 except at
+ * layer rho, refine.cpp:132-135). */
+enum skycell_mode { SKYCELL_SEQUENTIAL = 0, SKYCELL_PARALLEL = 1 };
+
+/* Mirrors SkylineResult minus the ids (refine.hpp:19-38).  keys[i] and
+ * candidates[i] are |KS_{i+1}| and |CS_{i+1}| for i = 0..n_layers-1. */
+typedef struct skycell_gpu_stats {
+  double normalize_ms, grid_ms, shrink_ms, refine_ms, total_ms;
+  uint64_t points_examined;
+  int32_t n_layers;
+  int32_t pad_;
+  uint64_t keys[64];
+  int64_t candidates[64];
+  /* diagnostics beyond the reference's SkylineResult */
+  uint64_t survivors_stream;   /* points leaving the streaming pass (K1)          */
+  uint64_t survivors_filter;   /* points entering the exact dominance pass (K5)   */
+  uint64_t kernel_launches;    /* kernels this call launched                      */
+} skycell_gpu_stats;
+
+typedef struct skycell_gpu_ctx skycell_gpu_ctx;
+
+/* Opaque per-device handle: device, stream, scratch buffers.  Not shared across
+ * concurrent calls (callers serialise per handle; use one handle per thread). */
+int skycell_gpu_create(int device, skycell_gpu_ctx** out, char* err, size_t err_len);
+void skycell_gpu_destroy(skycell_gpu_ctx* ctx);
+
+/* compute_skyline over n x d row-major coordinates.
+ *   coords      host or device pointer (detected); n*d values
+ *   dim_min/max host arrays of d doubles -- the declared normalisation range
+ *               (Dataset::dim_min/dim_max, dataset.hpp:24-25)
+ *   ids_out     host or device pointer with room for n uint32 ids; receives the
+ *               skyline record ids in ascending order
+ *   n_out       host pointer; receives the skyline size
+ *   stats       optional (NULL)
+ * The f32 entry point is the benchmark path: coords are widened to double
+ * exactly as the reference would see them, so results are identical to the
+ * reference fed Dataset{coords = (double)x, dim_min, dim_max}. */
+int skycell_gpu_skyline_f64(skycell_gpu_ctx* ctx, const double* coords, uint64_t n, int d,
+                            const double* dim_min, const double* dim_max, int rho, int mode,
+                            int merge_cross_cell, uint32_t* ids_out, uint64_t* n_out,
+                            skycell_gpu_stats* stats, char* err, size_t err_len);
+int skycell_gpu_skyline_f32(skycell_gpu_ctx* ctx, const float* coords, uint64_t n, int d,
+                            const double* dim_min, const double* dim_max, int rho, int mode,
+                            int merge_cross_cell, uint32_t* ids_out, uint64_t* n_out,
+                            skycell_gpu_stats* stats, char* err, size_t err_len);
+
+/* quadrant_skyline (refine.cpp:160-184): skyline of the points >= origin in every
+ * dimension, renormalised by the subset's own min/max; ids refer to the
+ * original records.  origin has origin_len doubles (must equal d). */
+int skycell_gpu_quadrant_f64(skycell_gpu_ctx* ctx, const double* coords, uint64_t n, int d,
+                             const double* origin, int origin_len, int rho, int mode,
+                             uint32_t* ids_out, uint64_t* n_out, skycell_gpu_stats* stats,
+                             char* err, size_t err_len);
+
+/* On-device synthetic data with the reference generator's streams
+ * (skycell::generate, datagen.cpp:62-87): dist 0 independent, 1 correlated,
+ * 2 anti-correlated.  kind 0 writes n*d raw doubles, kind 1 writes n*d floats
+ * quantised to the 2^-24 grid (x = (float)(floor(v * 2^24) * 2^-24), the
+ * benchmark input rule of BASELINE.md §2).  dev_out is a device pointer. */
+int skycell_gpu_generate(skycell_gpu_ctx* ctx, int dist, uint64_t n, int d, uint64_t seed, int kind,
+                         void* dev_out, char* err, size_t err_len);
+
+/* MultiLayerGrid::default_rho (grid.cpp:30-33). */
+int skycell_default_rho(uint64_t n, int d);
+
+/* Host-side argument validation in the reference's order (dataset.cpp:23-24,
+ * grid.cpp:38-43) without touching a device; used by CPU tests.  Non-finite
+ * coordinates are a device-side check and are not covered here. */
+int skycell_validate(uint64_t n, int d, int rho, char* err, size_t err_len);
+
+/* Build identification string (arch, version). */
+const char* skycell_gpu_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SKYCELL_GPU_H_ */

@@ -1,0 +1,336 @@
+"""Python mirror of the reference's public skyline API over the B200 C ABI.
+
+Same names, argument meaning and error behaviour as the reference C++ API
+(/root/reference/proj/include/skycell/{dataset,refine,grid,error}.hpp):
+
+    Dataset                 dataset.hpp:20-32   (coords n x d row-major, dim_min/dim_max)
+    compute_skyline(...)    refine.hpp:61-62    -> SkylineResult (refine.hpp:33-38)
+    quadrant_skyline(...)   refine.hpp:66-68
+    default_rho(n, d)       grid.cpp:30-33
+    InputError / ConfigError / UsageError / IoError   error.hpp:9-26
+
+Every call goes through ``libskycell_gpu.so`` (include/skycell_gpu.h).  There
+is no CPU fallback: if the library or a CUDA device is missing, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libskycell_gpu.so")
+
+
+# ------------------------------------------------------------------ errors
+class SkycellError(Exception):
+    """Base of the status-code exceptions."""
+
+
+class InputError(SkycellError, RuntimeError):
+    """Bad input data (dataset.cpp:23-43)."""
+
+
+class ConfigError(SkycellError, RuntimeError):
+    """Partition ratio out of budget (grid.cpp:38-43)."""
+
+
+class UsageError(SkycellError):
+    """API misuse (refine.cpp:162-163)."""
+
+
+class IoError(SkycellError, RuntimeError):
+    pass
+
+
+class CudaError(SkycellError, RuntimeError):
+    """CUDA runtime failure (no reference equivalent)."""
+
+
+class UnsupportedError(SkycellError):
+    """Valid for the reference but not implemented by this build."""
+
+
+_ERRORS = {1: InputError, 2: ConfigError, 3: UsageError, 4: IoError, 5: CudaError, 6: CudaError, 7: UnsupportedError}
+
+
+class Mode(enum.IntEnum):
+    """refine.hpp:40."""
+    kSequential = 0
+    kParallel = 1
+
+
+# ----------------------------------------------------------------- records
+@dataclass
+class Dataset:
+    """dataset.hpp:20-32: n records of d coordinates, row-major, plus the
+    declared normalisation range per dimension."""
+    coords: np.ndarray
+    dim_min: np.ndarray
+    dim_max: np.ndarray
+
+    @property
+    def n(self) -> int:
+        return int(self.coords.shape[0])
+
+    @property
+    def d(self) -> int:
+        return int(self.coords.shape[1]) if self.coords.ndim == 2 else 0
+
+    @staticmethod
+    def from_coords(coords, dim_min=None, dim_max=None) -> "Dataset":
+        x = np.asarray(coords)
+        if x.dtype not in (np.float32, np.float64):
+            x = x.astype(np.float64)
+        x = np.ascontiguousarray(x)
+        d = x.shape[1] if x.ndim == 2 else 0
+        ds = Dataset(x, np.zeros(d), np.ones(d))
+        if dim_min is None or dim_max is None:
+            ds.compute_minmax()
+        else:
+            ds.dim_min = np.asarray(dim_min, dtype=np.float64)
+            ds.dim_max = np.asarray(dim_max, dtype=np.float64)
+        return ds
+
+    def compute_minmax(self) -> None:
+        """Dataset::compute_minmax (dataset.cpp:10-20)."""
+        x = np.asarray(self.coords, dtype=np.float64)
+        if x.shape[0] == 0:
+            self.dim_min = np.full(self.d, np.inf)
+            self.dim_max = np.full(self.d, -np.inf)
+        else:
+            self.dim_min = x.min(axis=0)
+            self.dim_max = x.max(axis=0)
+
+
+@dataclass
+class StageTimes:
+    normalize_ms: float = 0.0
+    grid_ms: float = 0.0
+    shrink_ms: float = 0.0
+    refine_ms: float = 0.0
+    total_ms: float = 0.0
+
+
+@dataclass
+class LayerCounts:
+    keys: list = field(default_factory=list)        # |KS_i|, i = 1..rho (auxiliary included)
+    candidates: list = field(default_factory=list)  # |CS_i|; -1 when not materialised
+
+
+@dataclass
+class SkylineResult:
+    ids: np.ndarray
+    times: StageTimes = field(default_factory=StageTimes)
+    layers: LayerCounts = field(default_factory=LayerCounts)
+    points_examined: int = 0
+    survivors_stream: int = 0
+    survivors_filter: int = 0
+    kernel_launches: int = 0
+
+
+class _Stats(C.Structure):
+    _fields_ = [
+        ("normalize_ms", C.c_double), ("grid_ms", C.c_double), ("shrink_ms", C.c_double),
+        ("refine_ms", C.c_double), ("total_ms", C.c_double),
+        ("points_examined", C.c_uint64), ("n_layers", C.c_int32), ("pad_", C.c_int32),
+        ("keys", C.c_uint64 * 64), ("candidates", C.c_int64 * 64),
+        ("survivors_stream", C.c_uint64), ("survivors_filter", C.c_uint64), ("kernel_launches", C.c_uint64),
+    ]
+
+
+# ----------------------------------------------------------------- library
+_lib = None
+_lib_lock = threading.Lock()
+
+EXPORTS = (
+    "skycell_gpu_create", "skycell_gpu_destroy", "skycell_gpu_skyline_f64", "skycell_gpu_skyline_f32",
+    "skycell_gpu_quadrant_f64", "skycell_gpu_generate", "skycell_default_rho", "skycell_validate",
+    "skycell_gpu_version",
+)
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libskycell_gpu.so (fails loudly: there is no fallback path)."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise ImportError(f"libskycell_gpu.so not built at {path}; run __graft_entry__.build()")
+        lib = C.CDLL(path)
+        vp, u64, i32, dp, fp, u32p = C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_double), C.c_void_p, C.c_void_p
+        lib.skycell_gpu_create.argtypes = [i32, C.POINTER(vp), C.c_char_p, C.c_size_t]
+        lib.skycell_gpu_destroy.argtypes = [vp]
+        lib.skycell_gpu_destroy.restype = None
+        for fn in (lib.skycell_gpu_skyline_f64, lib.skycell_gpu_skyline_f32):
+            fn.argtypes = [vp, fp, u64, i32, dp, dp, i32, i32, i32, u32p, C.POINTER(C.c_uint64),
+                           C.POINTER(_Stats), C.c_char_p, C.c_size_t]
+        lib.skycell_gpu_quadrant_f64.argtypes = [vp, fp, u64, i32, dp, i32, i32, i32, u32p, C.POINTER(C.c_uint64),
+                                                 C.POINTER(_Stats), C.c_char_p, C.c_size_t]
+        lib.skycell_gpu_generate.argtypes = [vp, i32, u64, i32, u64, i32, vp, C.c_char_p, C.c_size_t]
+        lib.skycell_default_rho.argtypes = [u64, i32]
+        lib.skycell_validate.argtypes = [u64, i32, i32, C.c_char_p, C.c_size_t]
+        lib.skycell_gpu_version.restype = C.c_char_p
+        _lib = lib
+        return lib
+
+
+def _raise(code: int, err) -> None:
+    if code != 0:
+        raise _ERRORS.get(code, SkycellError)(err.value.decode(errors="replace"))
+
+
+def default_rho(n: int, d: int) -> int:
+    """MultiLayerGrid::default_rho (grid.cpp:30-33)."""
+    return int(load_library().skycell_default_rho(n, d))
+
+
+def validate(n: int, d: int, rho: int) -> None:
+    """Host-side argument checks in the reference's order (no device needed)."""
+    err = C.create_string_buffer(512)
+    _raise(load_library().skycell_validate(n, d, rho, err, 512), err)
+
+
+# ------------------------------------------------------------------ engine
+class Engine:
+    """One device context (include/skycell_gpu.h: skycell_gpu_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load_library()
+        self.device = device
+        self._ctx = C.c_void_p()
+        err = C.create_string_buffer(512)
+        _raise(self.lib.skycell_gpu_create(device, C.byref(self._ctx), err, 512), err)
+        self._lock = threading.Lock()
+
+    def close(self) -> None:
+        if self._ctx:
+            self.lib.skycell_gpu_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # raw entry point: coords may be a numpy array (host) or a CUDA tensor
+    # (device pointer, used in place); ids_out likewise.
+    def skyline_raw(self, coords, n: int, d: int, dim_min, dim_max, rho: int, mode: int = 1,
+                    merge_cross_cell: bool = True, ids_out=None, with_stats: bool = True):
+        ptr, is_f32 = _data_ptr(coords)
+        mn = np.ascontiguousarray(dim_min, dtype=np.float64)
+        mx = np.ascontiguousarray(dim_max, dtype=np.float64)
+        if mn.shape[0] < d or mx.shape[0] < d:
+            raise UsageError("dim_min/dim_max must hold d values")
+        own = ids_out is None
+        if own:
+            ids_out = np.empty(max(n, 1), dtype=np.uint32)
+        out_ptr, _ = _data_ptr(ids_out)
+        n_out = C.c_uint64(0)
+        st = _Stats()
+        err = C.create_string_buffer(512)
+        fn = self.lib.skycell_gpu_skyline_f32 if is_f32 else self.lib.skycell_gpu_skyline_f64
+        with self._lock:
+            rc = fn(self._ctx, ptr, n, d, mn.ctypes.data_as(C.POINTER(C.c_double)),
+                    mx.ctypes.data_as(C.POINTER(C.c_double)), rho, int(mode), int(bool(merge_cross_cell)),
+                    out_ptr, C.byref(n_out), C.byref(st) if with_stats else None, err, 512)
+        _raise(rc, err)
+        k = int(n_out.value)
+        ids = ids_out[:k].copy() if own else ids_out[:k]
+        return _to_result(ids, st if with_stats else None)
+
+    def generate(self, dist: int, n: int, d: int, seed: int, quantized: bool = True, out=None):
+        """Synthetic data on the device (skycell_gpu_generate).  Returns a CUDA
+        tensor of shape (n, d): float32 on the 2^-24 grid, or raw float64."""
+        import torch
+        if out is None:
+            out = torch.empty((n, d), dtype=torch.float32 if quantized else torch.float64,
+                              device=f"cuda:{self.device}")
+        err = C.create_string_buffer(512)
+        _raise(self.lib.skycell_gpu_generate(self._ctx, int(dist), n, d, seed, 1 if quantized else 0,
+                                             C.c_void_p(out.data_ptr()), err, 512), err)
+        return out
+
+    def compute_skyline(self, ds: Dataset, rho: int, mode: Mode = Mode.kParallel, pool=None,
+                        merge_cross_cell: bool = True) -> SkylineResult:
+        """compute_skyline (refine.hpp:61-62).  `pool` is accepted for
+        signature parity and ignored: the GPU does not use host threads."""
+        x = np.asarray(ds.coords)
+        if x.ndim != 2:
+            x = x.reshape(0, 0) if x.size == 0 else x.reshape(x.shape[0], -1)
+        if x.dtype not in (np.float32, np.float64):
+            x = x.astype(np.float64)
+        x = np.ascontiguousarray(x)
+        n, d = x.shape
+        return self.skyline_raw(x, n, d, ds.dim_min, ds.dim_max, rho, int(mode), merge_cross_cell)
+
+    def quadrant_skyline(self, ds: Dataset, origin, rho: int, mode: Mode = Mode.kParallel, pool=None) -> SkylineResult:
+        """quadrant_skyline (refine.hpp:66-68, refine.cpp:160-184)."""
+        x = np.ascontiguousarray(ds.coords, dtype=np.float64)
+        n, d = x.shape
+        o = np.ascontiguousarray(origin, dtype=np.float64)
+        ids = np.empty(max(n, 1), dtype=np.uint32)
+        n_out = C.c_uint64(0)
+        st = _Stats()
+        err = C.create_string_buffer(512)
+        with self._lock:
+            rc = self.lib.skycell_gpu_quadrant_f64(self._ctx, x.ctypes.data, n, d,
+                                                   o.ctypes.data_as(C.POINTER(C.c_double)), int(o.shape[0]),
+                                                   rho, int(mode), ids.ctypes.data, C.byref(n_out), C.byref(st),
+                                                   err, 512)
+        _raise(rc, err)
+        return _to_result(ids[: n_out.value].copy(), st)
+
+
+def _data_ptr(a):
+    """(pointer, is_f32) of a numpy array or a torch tensor (host or CUDA)."""
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise UsageError("arrays must be C-contiguous")
+        return C.c_void_p(a.ctypes.data), a.dtype == np.float32
+    if hasattr(a, "data_ptr"):
+        import torch
+        if not a.is_contiguous():
+            raise UsageError("tensors must be contiguous")
+        return C.c_void_p(a.data_ptr()), a.dtype == torch.float32
+    raise UsageError(f"unsupported array type {type(a)!r}")
+
+
+def _to_result(ids, st) -> SkylineResult:
+    r = SkylineResult(ids=ids)
+    if st is not None:
+        L = st.n_layers
+        r.times = StageTimes(st.normalize_ms, st.grid_ms, st.shrink_ms, st.refine_ms, st.total_ms)
+        r.layers = LayerCounts([int(st.keys[i]) for i in range(L)], [int(st.candidates[i]) for i in range(L)])
+        r.points_examined = int(st.points_examined)
+        r.survivors_stream = int(st.survivors_stream)
+        r.survivors_filter = int(st.survivors_filter)
+        r.kernel_launches = int(st.kernel_launches)
+    return r
+
+
+_default_engines: dict[int, Engine] = {}
+
+
+def engine(device: int = 0) -> Engine:
+    e = _default_engines.get(device)
+    if e is None:
+        e = _default_engines[device] = Engine(device)
+    return e
+
+
+def compute_skyline(ds: Dataset, rho: int, mode: Mode = Mode.kParallel, pool=None,
+                    merge_cross_cell: bool = True) -> SkylineResult:
+    """Drop-in for skycell::compute_skyline (refine.hpp:61-62) on cuda:0."""
+    return engine(0).compute_skyline(ds, rho, mode, pool, merge_cross_cell)
+
+
+def quadrant_skyline(ds: Dataset, origin, rho: int, mode: Mode = Mode.kParallel, pool=None) -> SkylineResult:
+    """Drop-in for skycell::quadrant_skyline (refine.hpp:66-68) on cuda:0."""
+    return engine(0).quadrant_skyline(ds, origin, rho, mode, pool)

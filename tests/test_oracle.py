@@ -1,0 +1,92 @@
+"""Pin the CPU oracle (oracle/skycell_oracle.c) before trusting it.
+
+1. Against the reference's own known-answer tests (tests/golden/kat.json).
+2. Against golden outputs of the unmodified reference (random_small, c1).
+3. Against the reference library itself where it is built (oracle/_ref).
+"""
+import numpy as np
+import pytest
+
+from golden_io import inputs_for, load_ids, load_json
+
+MODES = {0: "seq", 1: "par"}
+
+
+@pytest.mark.parametrize("case", load_json("kat.json")["cases"], ids=lambda c: c["name"])
+def test_oracle_kats(oracle, case):
+    x = np.asarray(case["rows"], dtype=np.float64)
+    for mode, key in MODES.items():
+        r = oracle.compute_skyline(x, case["dim_min"], case["dim_max"], case["rho"], mode, case["merge"])
+        want = case[key]
+        assert r.ids.tolist() == want["ids"]
+        assert r.points_examined == want["points_examined"]
+        assert r.keys == want["keys"]
+        assert r.candidates == want["candidates"]
+
+
+@pytest.mark.parametrize("case", load_json("kat.json")["errors"], ids=lambda c: c["name"])
+def test_oracle_errors(oracle, case):
+    from oracle.oracle import CpuError
+    x = np.asarray(case["rows"], dtype=np.float64)
+    if case["code"] == 0:
+        oracle.compute_skyline(x, case["dim_min"], case["dim_max"], case["rho"])
+        return
+    with pytest.raises(CpuError) as ei:
+        oracle.compute_skyline(x, case["dim_min"], case["dim_max"], case["rho"])
+    assert ei.value.code == case["code"]
+    assert str(ei.value) == case["message"]
+
+
+def test_oracle_random_small(oracle):
+    ids = load_ids("random_small_ids.npz")
+    for rec in load_json("random_small.json")["records"]:
+        x, mn, mx = inputs_for(oracle, rec)
+        r = oracle.compute_skyline(x.astype(np.float64), mn, mx, rec["rho"], rec["mode"])
+        assert np.array_equal(r.ids, ids[rec["key"]]), rec
+        assert r.points_examined == rec["points_examined"], rec
+        assert r.keys == rec["keys"] and r.candidates == rec["candidates"], rec
+
+
+@pytest.mark.parametrize("rec", load_json("c1.json")["records"], ids=lambda r: r["key"])
+def test_oracle_c1_golden(oracle, rec):
+    from oracle.oracle import fnv1a64_ids
+    x, mn, mx = inputs_for(oracle, rec)
+    r = oracle.compute_skyline(x.astype(np.float64), mn, mx, rec["rho"], rec["mode"])
+    assert r.ids.size == rec["size"]
+    assert fnv1a64_ids(r.ids) == rec["fnv1a64"]
+    assert r.points_examined == rec["points_examined"]
+    assert r.keys == rec["keys"] and r.candidates == rec["candidates"]
+    assert np.array_equal(r.ids, load_ids("c1_ids.npz")[rec["key"]])
+
+
+def test_generator_matches_reference(oracle, reference):
+    for dist in range(3):
+        a = oracle.generate(dist, 70001, 5, 9)
+        b = reference.generate(dist, 70001, 5, 9)
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_oracle_equals_reference(oracle, reference, seed):
+    from oracle.oracle import quantize_f32
+    dist, d, n, rho = seed % 3, 2 + seed % 5, 400 + 211 * seed, 1 + seed % 4
+    v = reference.generate(dist, n, d, 500 + seed)
+    for x, mn, mx in ((quantize_f32(v).astype(np.float64), np.zeros(d), np.ones(d)),
+                      (v * 5 - 2, (v * 5 - 2).min(0), (v * 5 - 2).max(0))):
+        for mode in (0, 1):
+            for merge in (True, False):
+                a = oracle.compute_skyline(x, mn, mx, rho, mode, merge)
+                b = reference.compute_skyline(x, mn, mx, rho, mode, merge, workers=2)
+                assert np.array_equal(a.ids, b.ids)
+                assert (a.points_examined, a.keys, a.candidates) == (b.points_examined, b.keys, b.candidates)
+
+
+def test_oracle_quadrant_equals_reference(oracle, reference):
+    v = reference.generate(0, 2000, 3, 19)
+    mn, mx = v.min(0), v.max(0)
+    rng = np.random.default_rng(5)
+    for _ in range(10):
+        origin = rng.uniform(0, 0.8, 3)
+        a = oracle.quadrant_skyline(v, origin, 4)
+        b = reference.quadrant_skyline(v, mn, mx, origin, 4)
+        assert np.array_equal(a.ids, b.ids)
