@@ -61,6 +61,7 @@ typedef struct skycell_gpu_stats {
   uint64_t survivors_stream;   /* points leaving the streaming pass (K1)          */
   uint64_t survivors_filter;   /* points entering the exact dominance pass (K5)   */
   uint64_t kernel_launches;    /* kernels this call launched                      */
+  double stream_kernel_ms;     /* CUDA-event time of the streaming kernel K1 alone */
 } skycell_gpu_stats;
 
 typedef struct skycell_gpu_ctx skycell_gpu_ctx;

@@ -32,8 +32,11 @@ struct DevCounters {
   u64 nonfinite;
   u64 s1, s2, examined;
   u64 zero;
+  u64 m, xs, nf;
   u64 zmid[kMaxLevels];
   u64 znext[kMaxLevels];
+  u64 szmid[kMaxLevels];
+  u64 sznext[kMaxLevels];
   u64 cand[kMaxLayers];
   u64 key[kMaxLayers];
 };
@@ -73,11 +76,14 @@ struct skycell_gpu_ctx {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
-  DevBuf reset, slabs, H, table, staging, out_ids;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  DevBuf reset, slabs, H, table, table2, table_s, staging;
+  DevBuf smp_rows, smp_ids, smp_fsum, f_rows, f_fsum;
   DevBuf s1_rows, s1_ids, s2_rows, s2_ids, s2_fsum, flags;
   DevBuf z_rows[2], z_ids[2], z_fsum[2];
   DevCounters* host_ctr = nullptr;  // pinned
-  cudaEvent_t ev[6] = {};
+  cudaEvent_t ev[8] = {};
   u64 launches = 0;
   int result_buf = 0;     // z buffer holding the last query's ids
   int result_level = 0;   // level whose znext counter is the skyline size
@@ -166,55 +172,159 @@ struct Query {
 };
 
 template <typename TT>
-void launch_layer_tables(Query& q, uint32_t* bits, int L, TT* table, u64* cand, u64* key) {
-  cudaStream_t s = q.ctx->stream;
-  const int d = q.d;
+void launch_tables(skycell_gpu_ctx* ctx, cudaStream_t s, const uint32_t* bits, int L, int d, TT* table) {
   const u64 rows = 1ull << (u64)(L * (d - 1));
-  const u64 words = std::max<u64>(1, (1ull << (u64)(L * d)) / 32);
-  const int nsm = q.ctx->num_sms;
-  auto grid_for = [&](u64 items) { return (unsigned)std::max<u64>(1, std::min<u64>((items + 255) / 256, (u64)nsm * 16)); };
-  sk::k_rowmin<TT><<<grid_for(rows), 256, 0, s>>>(bits, L, rows, table);
-  ++q.ctx->launches;
-  for (int k = 1; k < d; ++k) {
-    const u64 lines = rows >> L;
-    sk::k_prefix_min<TT><<<grid_for(lines), 256, 0, s>>>(table, L, k, lines);
-    ++q.ctx->launches;
+  const u64 lines1 = rows >> L;
+  const int nsm = ctx->num_sms;
+  auto grid_for = [&](u64 items) {
+    return (unsigned)std::max<u64>(1, std::min<u64>((items + 127) / 128, (u64)nsm * 16));
+  };
+  sk::k_rowmin_prefix1<TT><<<grid_for(lines1), 128, 0, s>>>(bits, L, d, lines1, table);
+  ++ctx->launches;
+  for (int k = 2; k < d; ++k) {
+    sk::k_prefix_min<TT><<<grid_for(lines1), 128, 0, s>>>(table, L, k, lines1);
+    ++ctx->launches;
   }
-  sk::k_count_cells<TT><<<grid_for(words), 256, 0, s>>>(bits, L, d, words, table, cand, key);
-  ++q.ctx->launches;
+}
+
+template <typename TT>
+void launch_count(skycell_gpu_ctx* ctx, cudaStream_t s, const uint32_t* bits, int L, int d, const TT* table, u64* cand,
+                  u64* key) {
+  const u64 words = std::max<u64>(1, (1ull << (u64)(L * d)) / 32);
+  const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((words + 255) / 256, (u64)ctx->num_sms * 16));
+  sk::k_count_cells<TT><<<g, 256, 0, s>>>(bits, L, d, words, table, cand, key);
+  ++ctx->launches;
+}
+
+// Per-query device bookkeeping carved out of one zeroed region.
+struct Layout {
+  Carver cv;
+  size_t o_ctr = 0;
+};
+
+// Block-recursive exact sort-first pass over src (ascending ids) -- refine.cpp:
+// 31-59 applied as in phase 2 (refine.cpp:98-99):
+//   Z_0 = src[0, b0);  F_0 = {p in Z_0 : no q in Z_0 precedes and dominates p}
+//   Z_k = F_{k-1} ++ {p in src[b_{k-1}, b_k) : no f in F_{k-1}[:f_max] precedes
+//         and dominates p};  F_k = skyline of Z_k
+// A point removed by a filter point is removed by the reference too, and every
+// dominator of a surviving point that the reference would use is itself in
+// Z_k (minimal-key argument), so F_last is exactly the
+// reference's output.  Returns the z buffer index holding F_last; *count_out
+// points at its device-side size.
+struct LevelSlots {
+  std::vector<Slot> filter, compact;
+};
+
+template <typename TOut, int D>
+int run_levels(skycell_gpu_ctx* ctx, cudaStream_t s, char* R, DevCounters* ctr, const void* src_rows,
+               const uint32_t* src_ids, const u64* src_fsum, const u64* src_count, const std::vector<u64>& bounds,
+               const LevelSlots& slots, u64* zmid, u64* znext, int f_max, size_t smem_f, const u64** count_out) {
+  constexpr int PPTc = ppt_for<TOut, D>();
+  constexpr u64 TILEc = (u64)kThreads * PPTc;
+  constexpr int QCHUNK = 512;
+  const int nsm = ctx->num_sms;
+  auto at = [&](size_t off) { return reinterpret_cast<void*>(R + off); };
+  auto kfilter = sk::k_filter_append<TOut, D, kThreads, PPTc>;
+  ck(cudaFuncSetAttribute(kfilter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f), "smem attr");
+  int cur = 0;
+  const u64* cnt_prev = &ctr->zero;
+  for (size_t k = 0; k < bounds.size(); ++k) {
+    const u64 b0 = k == 0 ? 0 : bounds[k - 1];
+    const u64 b1 = bounds[k];
+    sk::FilterParams pf{};
+    pf.src_rows = src_rows;
+    pf.src_ids = src_ids;
+    pf.src_fsum = src_fsum;
+    pf.src_count = src_count;
+    pf.begin = b0;
+    pf.end = b1;
+    pf.f_rows = ctx->z_rows[cur].p;
+    pf.f_ids = static_cast<const uint32_t*>(ctx->z_ids[cur].p);
+    pf.f_fsum = static_cast<const u64*>(ctx->z_fsum[cur].p);
+    pf.f_count = cnt_prev;
+    pf.f_max = (uint32_t)f_max;
+    pf.dst_rows = ctx->z_rows[cur].p;
+    pf.dst_ids = static_cast<uint32_t*>(ctx->z_ids[cur].p);
+    pf.dst_fsum = static_cast<u64*>(ctx->z_fsum[cur].p);
+    pf.dst_count_in = cnt_prev;
+    pf.dst_count_out = &zmid[k];
+    pf.status = static_cast<u64*>(at(slots.filter[k].status_off));
+    pf.claim = static_cast<u64*>(at(slots.filter[k].claim_off));
+    const u64 span = b1 - b0;
+    const unsigned gf = (unsigned)std::max<u64>(1, std::min<u64>((span + TILEc - 1) / TILEc, (u64)nsm * 2));
+    kfilter<<<gf, kThreads, smem_f, s>>>(pf);
+
+    const u64 zmax = b1;
+    ck(cudaMemsetAsync(ctx->flags.p, 1, zmax, s), "flags");
+    dim3 ga((unsigned)std::max<u64>(1, std::min<u64>((zmax + kThreads - 1) / kThreads, 128)),
+            (unsigned)std::max<u64>(1, std::min<u64>((zmax + QCHUNK - 1) / QCHUNK, 32)));
+    sk::k_allpairs<TOut, D, kThreads, QCHUNK><<<ga, kThreads, 0, s>>>(
+        static_cast<const TOut*>(ctx->z_rows[cur].p), static_cast<const uint32_t*>(ctx->z_ids[cur].p),
+        static_cast<const u64*>(ctx->z_fsum[cur].p), &zmid[k], static_cast<uint8_t*>(ctx->flags.p));
+
+    sk::CompactParams pk{};
+    pk.src_rows = ctx->z_rows[cur].p;
+    pk.src_ids = static_cast<const uint32_t*>(ctx->z_ids[cur].p);
+    pk.src_fsum = static_cast<const u64*>(ctx->z_fsum[cur].p);
+    pk.count = &zmid[k];
+    pk.flag = static_cast<const uint8_t*>(ctx->flags.p);
+    pk.dst_rows = ctx->z_rows[cur ^ 1].p;
+    pk.dst_ids = static_cast<uint32_t*>(ctx->z_ids[cur ^ 1].p);
+    pk.dst_fsum = static_cast<u64*>(ctx->z_fsum[cur ^ 1].p);
+    pk.dst_count = &znext[k];
+    pk.status = static_cast<u64*>(at(slots.compact[k].status_off));
+    pk.claim = static_cast<u64*>(at(slots.compact[k].claim_off));
+    const unsigned gk = (unsigned)std::max<u64>(1, std::min<u64>((zmax + TILEc - 1) / TILEc, (u64)nsm * 4));
+    sk::k_compact<TOut, D, kThreads, PPTc><<<gk, kThreads, 0, s>>>(pk);
+    ctx->launches += 3;
+    cur ^= 1;
+    cnt_prev = &znext[k];
+  }
+  *count_out = cnt_prev;
+  return cur;
+}
+
+std::vector<u64> level_bounds(u64 n) {
+  std::vector<u64> b;
+  for (u64 x = kLevel0;; x <<= kLevelGrowthLog2) {
+    b.push_back(std::min(x, n));
+    if (x >= n) break;
+  }
+  return b;
 }
 
 template <typename TIn, typename TOut, bool IDENT, int D>
 void run_pipeline(Query& q) {
   skycell_gpu_ctx* ctx = q.ctx;
   cudaStream_t s = ctx->stream;
+  cudaStream_t s2 = ctx->side;
   const u64 n = q.n;
   const int rho = q.rho;
   const int nsm = ctx->num_sms;
 
-  // ---- sizes
-  const u64 words_rho = std::max<u64>(1, (1ull << (u64)(rho * D)) / 32);
-  const int lrm1 = rho - 1;
-  const u64 words_rm1 = lrm1 >= 1 ? std::max<u64>(1, (1ull << (u64)(lrm1 * D)) / 32) : 0;
-  int rm1_mode = 0;
-  if (lrm1 >= 1) rm1_mode = (words_rm1 * 4 <= 128 * 1024) ? 1 : 2;
-  int lf = 0;
+  // ---- levels and sizes
+  int la = 1;
   for (int L = std::min(rho, 7); L >= 1; --L) {
     if ((1ull << (u64)(L * (D - 1))) <= 32768 && L * D <= 30) {
-      lf = L;
+      la = L;
       break;
     }
   }
-  const u64 m_sample = std::min<u64>(n, 1ull << 20);
-  const uint32_t h_entries = lf ? (uint32_t)(1ull << (u64)(lf * (D - 1))) : 0;
-  const u64 words_lf = lf ? std::max<u64>(1, (1ull << (u64)(lf * D)) / 32) : 0;
+  const bool test_b = rho > la;
+  const u64 m = std::min<u64>(n, 1ull << 20);
+  const uint32_t h_entries = (uint32_t)(1ull << (u64)(la * (D - 1)));
+  auto words_at = [&](int L) { return std::max<u64>(1, (1ull << (u64)(L * D)) / 32); };
+  const uint32_t lo_words = la >= 2 ? (uint32_t)words_at(la - 1) : 0;
+  const bool wide = rho > 7;
+  const size_t tt = wide ? 4 : 1;
+  const u64 table_entries = 1ull << (u64)(rho * (D - 1));
 
-  // ---- K1 launch geometry
+  // ---- K1 geometry
   constexpr int PPT1 = ppt_for<TIn, D>();
   constexpr u64 TILE1 = (u64)kStreamThreads * PPT1;
   const u64 tiles1 = (n + TILE1 - 1) / TILE1;
-  const size_t occ_smem = rm1_mode == 1 ? words_rm1 * 4 : 0;
-  const size_t smem1 = occ_smem + ((h_entries + 15) & ~15u) + (PPT1 * (kStreamThreads / 32) + 1) * 4 + 16;
+  const size_t smem1 = (size_t)lo_words * 4 + ((h_entries + 15) & ~15u) + (PPT1 * (kStreamThreads / 32) + 1) * 4 + 16;
   auto kstream = sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1>;
   ck(cudaFuncSetAttribute(kstream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1), "smem attr");
   int occ_blocks = 0;
@@ -226,47 +336,57 @@ void run_pipeline(Query& q) {
   constexpr int PPTc = ppt_for<TOut, D>();
   constexpr u64 TILEc = (u64)kThreads * PPTc;
   const u64 tilesc = (n + TILEc - 1) / TILEc + 1;
-  std::vector<u64> bounds;
-  for (u64 b = kLevel0;; b <<= kLevelGrowthLog2) {
-    bounds.push_back(std::min(b, n));
-    if (b >= n) break;
-  }
-  const int levels = (int)bounds.size();
-  if (levels > kMaxLevels) throw CudaFail{cudaErrorInvalidValue, "too many levels"};
+  const std::vector<u64> bounds = level_bounds(n);
+  const std::vector<u64> sbounds = level_bounds(m);
+  if (bounds.size() > (size_t)kMaxLevels) throw CudaFail{cudaErrorInvalidValue, "too many levels"};
   const size_t rec = D * sizeof(TOut) + 12;
-  const uint32_t f_max = (uint32_t)std::min<u64>(4096, (96 * 1024) / rec);
+  const int f_max = (int)std::min<u64>(4096, (64 * 1024) / rec);
   const size_t smem_f = (((u64)f_max * D * sizeof(TOut) + 15) & ~15ull) + (u64)f_max * 12;
+  const int pf_max = (int)std::min<u64>(1024, (32 * 1024) / (D * sizeof(TOut) + 8));  // K4 point filter
+  const size_t smem_pf = (((u64)pf_max * D * sizeof(TOut) + 15) & ~15ull) + (u64)pf_max * 8;
 
   // ---- zeroed region
   Carver cv;
   const size_t o_ctr = cv.take(sizeof(DevCounters));
-  const size_t o_occ_rho = cv.take(words_rho * 4);
-  const size_t o_occ_rm1 = cv.take(std::max<u64>(words_rm1, 1) * 4);
-  std::vector<size_t> o_occ_layer(rho + 1, 0);
-  for (int L = 1; L <= rho - 2; ++L) o_occ_layer[L] = cv.take(std::max<u64>(1, (1ull << (u64)(L * D)) / 32) * 4);
-  const size_t o_occ_lf = cv.take(std::max<u64>(words_lf, 1) * 4);
-  auto slot = [&](u64 tiles) { Slot sl; sl.claim_off = cv.take(8); sl.status_off = cv.take(tiles * 8); return sl; };
+  std::vector<size_t> o_occ(rho + 1, 0);
+  for (int L = 1; L <= rho; ++L) o_occ[L] = cv.take(words_at(L) * 4);
+  const size_t o_sla = cv.take(words_at(la) * 4);
+  const size_t o_srho = test_b ? cv.take(words_at(rho) * 4) : 0;
+  auto slot = [&](u64 tiles) {
+    Slot sl;
+    sl.claim_off = cv.take(8);
+    sl.status_off = cv.take(tiles * 8);
+    return sl;
+  };
   const Slot sl_stream = slot(tiles1 + 1);
+  const Slot sl_scand = slot((m + TILEc - 1) / TILEc + 1);
   const Slot sl_cand = slot(tilesc);
-  std::vector<Slot> sl_filter, sl_compact;
-  for (int k = 0; k < levels; ++k) {
-    sl_filter.push_back(slot(tilesc));
-    sl_compact.push_back(slot(tilesc));
+  LevelSlots sls, mls;
+  for (size_t k = 0; k < sbounds.size(); ++k) {
+    sls.filter.push_back(slot((m + TILEc - 1) / TILEc + 1));
+    sls.compact.push_back(slot((m + TILEc - 1) / TILEc + 1));
+  }
+  for (size_t k = 0; k < bounds.size(); ++k) {
+    mls.filter.push_back(slot(tilesc));
+    mls.compact.push_back(slot(tilesc));
   }
   ensure(ctx->reset, cv.off);
   char* R = static_cast<char*>(ctx->reset.p);
   auto at = [&](size_t off) { return reinterpret_cast<void*>(R + off); };
+  auto occ = [&](int L) { return static_cast<uint32_t*>(at(o_occ[L])); };
   DevCounters* ctr = static_cast<DevCounters*>(at(o_ctr));
-  uint32_t* occ_rho = static_cast<uint32_t*>(at(o_occ_rho));
-  uint32_t* occ_rm1 = static_cast<uint32_t*>(at(o_occ_rm1));
-  uint32_t* occ_lf = static_cast<uint32_t*>(at(o_occ_lf));
 
   // ---- working buffers
   ensure(ctx->H, std::max<u64>(h_entries, 16));
-  if (rm1_mode == 1) ensure(ctx->slabs, (size_t)grid1 * words_rm1 * 4);
-  const bool small_table = rho <= 7;
-  const size_t tt = small_table ? 1 : 4;
-  ensure(ctx->table, (1ull << (u64)(rho * (D - 1))) * tt);
+  if (lo_words) ensure(ctx->slabs, (size_t)grid1 * lo_words * 4);
+  ensure(ctx->table, table_entries * tt);
+  ensure(ctx->table2, table_entries * tt);
+  if (test_b) ensure(ctx->table_s, table_entries * tt);
+  ensure(ctx->smp_rows, m * D * sizeof(TOut));
+  ensure(ctx->smp_ids, m * 4);
+  ensure(ctx->smp_fsum, m * 8);
+  ensure(ctx->f_rows, (size_t)pf_max * D * sizeof(TOut));
+  ensure(ctx->f_fsum, (size_t)pf_max * 8);
   ensure(ctx->s1_rows, n * D * sizeof(TOut));
   ensure(ctx->s1_ids, n * 4);
   ensure(ctx->s2_rows, n * D * sizeof(TOut));
@@ -282,19 +402,58 @@ void run_pipeline(Query& q) {
   if (q.timed) ck(cudaEventRecord(ctx->ev[0], s), "event");
   ck(cudaMemsetAsync(ctx->reset.p, 0, cv.off, s), "memset");
 
-  // ---- K0: sample filter
-  if (lf > 0) {
+  // ---- K0: sample occupancy, filter tables, sample skyline
+  {
     sk::SampleParams sp{};
     sp.coords = q.dev_coords;
-    sp.m = m_sample;
+    sp.m = m;
     sp.rho = rho;
-    sp.lf = lf;
+    sp.la = la;
     sp.nm = q.nm;
-    sp.occ = occ_lf;
-    const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((m_sample + 255) / 256, (u64)nsm * 8));
-    sk::k_sample_occ<TIn, TOut, D, IDENT><<<g, 256, 0, s>>>(sp);
-    sk::k_build_filter<<<1, 1024, h_entries, s>>>(occ_lf, lf, D, static_cast<uint8_t*>(ctx->H.p));
+    sp.occ_la = static_cast<uint32_t*>(at(o_sla));
+    sp.occ_rho = test_b ? static_cast<uint32_t*>(at(o_srho)) : nullptr;
+    sp.rows = ctx->smp_rows.p;
+    sp.ids = static_cast<uint32_t*>(ctx->smp_ids.p);
+    sp.fsum = static_cast<u64*>(ctx->smp_fsum.p);
+    const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((m + 255) / 256, (u64)nsm * 8));
+    sk::k_sample<TIn, TOut, D, IDENT><<<g, 256, 0, s>>>(sp);
+    sk::k_build_filter<<<1, 1024, h_entries, s>>>(static_cast<uint32_t*>(at(o_sla)), la, D,
+                                                  static_cast<uint8_t*>(ctx->H.p));
     ctx->launches += 2;
+    if (test_b) {
+      if (wide) launch_tables<uint32_t>(ctx, s, static_cast<uint32_t*>(at(o_srho)), rho, D, static_cast<uint32_t*>(ctx->table_s.p));
+      else launch_tables<uint8_t>(ctx, s, static_cast<uint32_t*>(at(o_srho)), rho, D, static_cast<uint8_t*>(ctx->table_s.p));
+    }
+    // sample points not strictly dominated at layer rho -> X (in the s2 buffers)
+    sk::CandParams pc{};
+    pc.rows = ctx->smp_rows.p;
+    pc.ids = static_cast<const uint32_t*>(ctx->smp_ids.p);
+    pc.count = &ctr->m;
+    pc.rho = rho;
+    pc.PM = test_b ? ctx->table_s.p : nullptr;
+    pc.f_max = 0;
+    pc.out_rows = ctx->s2_rows.p;
+    pc.out_ids = static_cast<uint32_t*>(ctx->s2_ids.p);
+    pc.out_fsum = static_cast<u64*>(ctx->s2_fsum.p);
+    pc.status = static_cast<u64*>(at(sl_scand.status_off));
+    pc.claim = static_cast<u64*>(at(sl_scand.claim_off));
+    pc.out_count = &ctr->xs;
+    pc.examined = nullptr;
+    ctx->host_ctr->m = m;  // staged through pinned memory
+    ck(cudaMemcpyAsync(&ctr->m, &ctx->host_ctr->m, 8, cudaMemcpyHostToDevice, s), "m");
+    const unsigned gs = (unsigned)std::max<u64>(1, std::min<u64>((m + TILEc - 1) / TILEc, (u64)nsm * 4));
+    if (wide) sk::k_candidates<TOut, D, uint32_t, kThreads, PPTc><<<gs, kThreads, 0, s>>>(pc);
+    else sk::k_candidates<TOut, D, uint8_t, kThreads, PPTc><<<gs, kThreads, 0, s>>>(pc);
+    ++ctx->launches;
+    const u64* fcount = nullptr;
+    const int fb = run_levels<TOut, D>(ctx, s, R, ctr, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
+                                       static_cast<const u64*>(ctx->s2_fsum.p), &ctr->xs, sbounds, sls, ctr->szmid,
+                                       ctr->sznext, f_max, smem_f, &fcount);
+    sk::k_strength_order<TOut, D><<<1, 1024, 0, s>>>(static_cast<const TOut*>(ctx->z_rows[fb].p),
+                                                     static_cast<const u64*>(ctx->z_fsum[fb].p), fcount,
+                                                     (uint32_t)pf_max, static_cast<TOut*>(ctx->f_rows.p),
+                                                     static_cast<u64*>(ctx->f_fsum.p), &ctr->nf);
+    ++ctx->launches;
   }
 
   // ---- K1: the streaming pass
@@ -302,14 +461,15 @@ void run_pipeline(Query& q) {
   p1.coords = q.dev_coords;
   p1.n = n;
   p1.rho = rho;
-  p1.lf = lf;
-  p1.rm1_mode = rm1_mode;
-  p1.rm1_words = (uint32_t)words_rm1;
+  p1.la = la;
+  p1.lo_words = lo_words;
   p1.h_entries = h_entries;
   p1.nm = q.nm;
   p1.H = static_cast<const uint8_t*>(ctx->H.p);
-  p1.occ_rho = occ_rho;
-  p1.occ_rm1 = occ_rm1;
+  p1.PMs = test_b ? ctx->table_s.p : nullptr;
+  p1.pms_wide = wide;
+  p1.occ_rho = occ(rho);
+  p1.occ_rm1 = rho >= 2 ? occ(rho - 1) : nullptr;
   p1.slabs = static_cast<uint32_t*>(ctx->slabs.p);
   p1.out_rows = ctx->s1_rows.p;
   p1.out_ids = static_cast<uint32_t*>(ctx->s1_ids.p);
@@ -317,122 +477,92 @@ void run_pipeline(Query& q) {
   p1.claim = static_cast<u64*>(at(sl_stream.claim_off));
   p1.out_count = &ctr->s1;
   p1.nonfinite = &ctr->nonfinite;
+  if (q.timed) ck(cudaEventRecord(ctx->ev[4], s), "event");
   kstream<<<grid1, kStreamThreads, smem1, s>>>(p1);
   ++ctx->launches;
-  if (rm1_mode == 1) {
-    const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((words_rm1 + 255) / 256, (u64)nsm * 8));
-    sk::k_reduce_slabs<<<g, 256, 0, s>>>(static_cast<uint32_t*>(ctx->slabs.p), grid1, (uint32_t)words_rm1, occ_rm1);
+  if (q.timed) ck(cudaEventRecord(ctx->ev[5], s), "event");
+  if (lo_words) {
+    const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((lo_words + 255) / 256, (u64)nsm * 8));
+    sk::k_reduce_slabs<<<g, 256, 0, s>>>(static_cast<uint32_t*>(ctx->slabs.p), grid1, lo_words, occ(la - 1));
     ++ctx->launches;
   }
   if (q.timed) ck(cudaEventRecord(ctx->ev[1], s), "event");
 
-  // ---- K3: layer tables and per-layer counts (layers rho, rho-1, ..., 1)
-  auto tables_at = [&](uint32_t* bits, int L) {
-    if (L <= 7)
-      launch_layer_tables<uint8_t>(q, bits, L, static_cast<uint8_t*>(ctx->table.p), &ctr->cand[L - 1], &ctr->key[L - 1]);
-    else
-      launch_layer_tables<uint32_t>(q, bits, L, static_cast<uint32_t*>(ctx->table.p), &ctr->cand[L - 1], &ctr->key[L - 1]);
-  };
-  {
-    uint32_t* prev = occ_rm1;
-    for (int L = rho - 2; L >= 1; --L) {
-      uint32_t* dst = static_cast<uint32_t*>(at(o_occ_layer[L]));
-      const u64 src_words = std::max<u64>(1, (1ull << (u64)((L + 1) * D)) / 32);
-      const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((src_words + 255) / 256, (u64)nsm * 8));
-      sk::k_downsample<<<g, 256, 0, s>>>(prev, L, D, src_words, dst);
-      ++ctx->launches;
-      prev = dst;
-    }
-  }
-  for (int L = 1; L <= rho - 1; ++L) tables_at(L == rho - 1 ? occ_rm1 : static_cast<uint32_t*>(at(o_occ_layer[L])), L);
-  tables_at(occ_rho, rho);  // last: K4 reads this table
+  // ---- K3: layer-rho prefix-min table of the survivors' occupancy
+  if (wide) launch_tables<uint32_t>(ctx, s, occ(rho), rho, D, static_cast<uint32_t*>(ctx->table.p));
+  else launch_tables<uint8_t>(ctx, s, occ(rho), rho, D, static_cast<uint8_t*>(ctx->table.p));
   if (q.timed) ck(cudaEventRecord(ctx->ev[2], s), "event");
 
-  // ---- K4: candidate-cell filter
-  sk::CandParams pc{};
-  pc.rows = ctx->s1_rows.p;
-  pc.ids = static_cast<const uint32_t*>(ctx->s1_ids.p);
-  pc.count = &ctr->s1;
-  pc.rho = rho;
-  pc.PM = ctx->table.p;
-  pc.out_rows = ctx->s2_rows.p;
-  pc.out_ids = static_cast<uint32_t*>(ctx->s2_ids.p);
-  pc.out_fsum = static_cast<u64*>(ctx->s2_fsum.p);
-  pc.status = static_cast<u64*>(at(sl_cand.status_off));
-  pc.claim = static_cast<u64*>(at(sl_cand.claim_off));
-  pc.out_count = &ctr->s2;
-  pc.examined = &ctr->examined;
-  const unsigned gc = (unsigned)std::max<u64>(1, std::min<u64>(tilesc, (u64)nsm * 4));
-  if (small_table)
-    sk::k_candidates<TOut, D, uint8_t, kThreads, PPTc><<<gc, kThreads, 0, s>>>(pc);
-  else
-    sk::k_candidates<TOut, D, uint32_t, kThreads, PPTc><<<gc, kThreads, 0, s>>>(pc);
-  ++ctx->launches;
-
-  // ---- K5: block-recursive exact dominance
-  auto kfilter = sk::k_filter_append<TOut, D, kThreads, PPTc>;
-  ck(cudaFuncSetAttribute(kfilter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f), "smem attr");
-  int cur = 0;
-  const u64* cnt_prev = &ctr->zero;
-  for (int k = 0; k < levels; ++k) {
-    const u64 b0 = k == 0 ? 0 : bounds[k - 1];
-    const u64 b1 = bounds[k];
-    sk::FilterParams pf{};
-    pf.src_rows = ctx->s2_rows.p;
-    pf.src_ids = static_cast<const uint32_t*>(ctx->s2_ids.p);
-    pf.src_fsum = static_cast<const u64*>(ctx->s2_fsum.p);
-    pf.src_count = &ctr->s2;
-    pf.begin = b0;
-    pf.end = b1;
-    pf.f_rows = ctx->z_rows[cur].p;
-    pf.f_ids = static_cast<const uint32_t*>(ctx->z_ids[cur].p);
-    pf.f_fsum = static_cast<const u64*>(ctx->z_fsum[cur].p);
-    pf.f_count = cnt_prev;
-    pf.f_max = f_max;
-    pf.dst_rows = ctx->z_rows[cur].p;
-    pf.dst_ids = static_cast<uint32_t*>(ctx->z_ids[cur].p);
-    pf.dst_fsum = static_cast<u64*>(ctx->z_fsum[cur].p);
-    pf.dst_count_in = cnt_prev;
-    pf.dst_count_out = &ctr->zmid[k];
-    pf.status = static_cast<u64*>(at(sl_filter[k].status_off));
-    pf.claim = static_cast<u64*>(at(sl_filter[k].claim_off));
-    const u64 span = b1 - b0;
-    const unsigned gf = (unsigned)std::max<u64>(1, std::min<u64>((span + TILEc - 1) / TILEc, (u64)nsm * 2));
-    kfilter<<<gf, kThreads, smem_f, s>>>(pf);
-
-    const u64 zmax = b1;  // |F_{k-1}| + |Y_k| <= b1
-    const unsigned ga = (unsigned)std::max<u64>(1, std::min<u64>((zmax + kThreads - 1) / kThreads, (u64)nsm * 8));
-    sk::k_allpairs<TOut, D, kThreads><<<ga, kThreads, 0, s>>>(
-        static_cast<const TOut*>(ctx->z_rows[cur].p), static_cast<const uint32_t*>(ctx->z_ids[cur].p),
-        static_cast<const u64*>(ctx->z_fsum[cur].p), &ctr->zmid[k], static_cast<uint8_t*>(ctx->flags.p));
-
-    sk::CompactParams pk{};
-    pk.src_rows = ctx->z_rows[cur].p;
-    pk.src_ids = static_cast<const uint32_t*>(ctx->z_ids[cur].p);
-    pk.src_fsum = static_cast<const u64*>(ctx->z_fsum[cur].p);
-    pk.count = &ctr->zmid[k];
-    pk.flag = static_cast<const uint8_t*>(ctx->flags.p);
-    pk.dst_rows = ctx->z_rows[cur ^ 1].p;
-    pk.dst_ids = static_cast<uint32_t*>(ctx->z_ids[cur ^ 1].p);
-    pk.dst_fsum = static_cast<u64*>(ctx->z_fsum[cur ^ 1].p);
-    pk.dst_count = &ctr->znext[k];
-    pk.status = static_cast<u64*>(at(sl_compact[k].status_off));
-    pk.claim = static_cast<u64*>(at(sl_compact[k].claim_off));
-    const unsigned gk = (unsigned)std::max<u64>(1, std::min<u64>((zmax + TILEc - 1) / TILEc, (u64)nsm * 4));
-    sk::k_compact<TOut, D, kThreads, PPTc><<<gk, kThreads, 0, s>>>(pk);
-    ctx->launches += 3;
-    cur ^= 1;
-    cnt_prev = &ctr->znext[k];
+  // ---- side stream: per-layer |KS_i|, |CS_i| (refine.cpp:125-147), overlapped with K4/K5.
+  // Layer rho from O'_rho; below, O'_rho is OR-ed down into the partial
+  // occupancies recorded by the filter.
+  ck(cudaEventRecord(ctx->ev_fork, s), "event");
+  ck(cudaStreamWaitEvent(s2, ctx->ev_fork, 0), "wait");
+  {
+    if (wide) launch_count<uint32_t>(ctx, s2, occ(rho), rho, D, static_cast<const uint32_t*>(ctx->table.p), &ctr->cand[rho - 1], &ctr->key[rho - 1]);
+    else launch_count<uint8_t>(ctx, s2, occ(rho), rho, D, static_cast<const uint8_t*>(ctx->table.p), &ctr->cand[rho - 1], &ctr->key[rho - 1]);
+    for (int L = rho - 1; L >= 1; --L) {
+      const u64 src_words = words_at(L + 1);
+      const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((src_words + 255) / 256, (u64)nsm * 8));
+      sk::k_downsample<<<g, 256, 0, s2>>>(occ(L + 1), L, D, src_words, occ(L));
+      ++ctx->launches;
+      if (L > 7) {
+        launch_tables<uint32_t>(ctx, s2, occ(L), L, D, static_cast<uint32_t*>(ctx->table2.p));
+        launch_count<uint32_t>(ctx, s2, occ(L), L, D, static_cast<const uint32_t*>(ctx->table2.p), &ctr->cand[L - 1], &ctr->key[L - 1]);
+      } else {
+        launch_tables<uint8_t>(ctx, s2, occ(L), L, D, static_cast<uint8_t*>(ctx->table2.p));
+        launch_count<uint8_t>(ctx, s2, occ(L), L, D, static_cast<const uint8_t*>(ctx->table2.p), &ctr->cand[L - 1], &ctr->key[L - 1]);
+      }
+    }
   }
+  ck(cudaEventRecord(ctx->ev_join, s2), "event");
+
+  // ---- K4: candidate cells + sample-skyline point filter
+  {
+    sk::CandParams pc{};
+    pc.rows = ctx->s1_rows.p;
+    pc.ids = static_cast<const uint32_t*>(ctx->s1_ids.p);
+    pc.count = &ctr->s1;
+    pc.rho = rho;
+    pc.PM = ctx->table.p;
+    pc.f_rows = ctx->f_rows.p;
+    pc.f_fsum = static_cast<const u64*>(ctx->f_fsum.p);
+    pc.f_count = &ctr->nf;
+    pc.f_max = (uint32_t)pf_max;
+    pc.out_rows = ctx->s2_rows.p;
+    pc.out_ids = static_cast<uint32_t*>(ctx->s2_ids.p);
+    pc.out_fsum = static_cast<u64*>(ctx->s2_fsum.p);
+    pc.status = static_cast<u64*>(at(sl_cand.status_off));
+    pc.claim = static_cast<u64*>(at(sl_cand.claim_off));
+    pc.out_count = &ctr->s2;
+    pc.examined = &ctr->examined;
+    const unsigned gc = (unsigned)std::max<u64>(1, std::min<u64>(tilesc, (u64)nsm * 4));
+    if (wide) {
+      auto kc = sk::k_candidates<TOut, D, uint32_t, kThreads, PPTc>;
+      ck(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pf), "smem attr");
+      kc<<<gc, kThreads, smem_pf, s>>>(pc);
+    } else {
+      auto kc = sk::k_candidates<TOut, D, uint8_t, kThreads, PPTc>;
+      ck(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pf), "smem attr");
+      kc<<<gc, kThreads, smem_pf, s>>>(pc);
+    }
+    ++ctx->launches;
+  }
+
+  // ---- K5: exact sort-first pass over the remaining points
+  const u64* final_count = nullptr;
+  const int cur = run_levels<TOut, D>(ctx, s, R, ctr, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
+                                      static_cast<const u64*>(ctx->s2_fsum.p), &ctr->s2, bounds, mls, ctr->zmid,
+                                      ctr->znext, f_max, smem_f, &final_count);
   ck(cudaGetLastError(), "kernel launch");
   if (q.timed) ck(cudaEventRecord(ctx->ev[3], s), "event");
+  ck(cudaStreamWaitEvent(s, ctx->ev_join, 0), "join");
 
   // ---- results
   ck(cudaMemcpyAsync(ctx->host_ctr, ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s), "counters D2H");
   ck(cudaStreamSynchronize(s), "query");
-  // The skyline ids are in z_ids[cur]; their count is znext[levels - 1].
   ctx->result_buf = cur;
-  ctx->result_level = levels - 1;
+  ctx->result_level = (int)bounds.size() - 1;
   const DevCounters& hc = *ctx->host_ctr;
   if (q.stats) {
     q.stats->n_layers = rho;
@@ -442,7 +572,7 @@ void run_pipeline(Query& q) {
     }
     q.stats->points_examined = hc.examined;
     q.stats->survivors_stream = hc.s1;
-    q.stats->survivors_filter = hc.zmid[levels - 1];
+    q.stats->survivors_filter = hc.s2;
   }
 }
 
@@ -551,7 +681,7 @@ int run_query(skycell_gpu_ctx* ctx, const TIn* coords, u64 n, int d, const doubl
       put_err(err, err_len, "normalize: non-finite coordinate in record " + std::to_string(~hc.nonfinite));
       return SKYCELL_INPUT;
     }
-    const u64 count = hc.znext[ctx->result_level];
+    const u64 count = hc.znext[ctx->result_level];  // K5's last level
     const int cur = ctx->result_buf;
     *n_out = count;
     cudaPointerAttributes oattr{};
@@ -574,6 +704,9 @@ int run_query(skycell_gpu_ctx* ctx, const TIn* coords, u64 n, int d, const doubl
       stats->refine_ms = c;
       stats->total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_begin).count();
       stats->kernel_launches = ctx->launches;
+      float k1 = 0;
+      cudaEventElapsedTime(&k1, ctx->ev[4], ctx->ev[5]);
+      stats->stream_kernel_ms = k1;
     }
     return SKYCELL_OK;
   } catch (const CudaFail& f) {
@@ -603,6 +736,9 @@ int skycell_gpu_create(int device, skycell_gpu_ctx** out, char* err, size_t err_
     ctx->device = device;
     ck(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device), "attr");
     ck(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming), "event");
     ck(cudaMallocHost(reinterpret_cast<void**>(&ctx->host_ctr), sizeof(DevCounters)), "pinned");
     for (auto& e : ctx->ev) ck(cudaEventCreate(&e), "event");
     *out = ctx;
@@ -616,7 +752,8 @@ int skycell_gpu_create(int device, skycell_gpu_ctx** out, char* err, size_t err_
 void skycell_gpu_destroy(skycell_gpu_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
-  DevBuf* bufs[] = {&ctx->reset, &ctx->slabs, &ctx->H, &ctx->table, &ctx->staging, &ctx->s1_rows, &ctx->s1_ids,
+  DevBuf* bufs[] = {&ctx->reset, &ctx->slabs, &ctx->H, &ctx->table, &ctx->table2, &ctx->table_s, &ctx->staging,
+                    &ctx->smp_rows, &ctx->smp_ids, &ctx->smp_fsum, &ctx->f_rows, &ctx->f_fsum, &ctx->s1_rows, &ctx->s1_ids,
                     &ctx->s2_rows, &ctx->s2_ids, &ctx->s2_fsum, &ctx->flags, &ctx->z_rows[0], &ctx->z_rows[1],
                     &ctx->z_ids[0], &ctx->z_ids[1], &ctx->z_fsum[0], &ctx->z_fsum[1]};
   for (DevBuf* b : bufs)
@@ -624,6 +761,9 @@ void skycell_gpu_destroy(skycell_gpu_ctx* ctx) {
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   if (ctx->host_ctr) cudaFreeHost(ctx->host_ctr);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }

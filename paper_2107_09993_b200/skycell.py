@@ -131,6 +131,7 @@ class SkylineResult:
     survivors_stream: int = 0
     survivors_filter: int = 0
     kernel_launches: int = 0
+    stream_kernel_ms: float = 0.0
 
 
 class _Stats(C.Structure):
@@ -140,6 +141,7 @@ class _Stats(C.Structure):
         ("points_examined", C.c_uint64), ("n_layers", C.c_int32), ("pad_", C.c_int32),
         ("keys", C.c_uint64 * 64), ("candidates", C.c_int64 * 64),
         ("survivors_stream", C.c_uint64), ("survivors_filter", C.c_uint64), ("kernel_launches", C.c_uint64),
+        ("stream_kernel_ms", C.c_double),
     ]
 
 
@@ -312,6 +314,7 @@ def _to_result(ids, st) -> SkylineResult:
         r.survivors_stream = int(st.survivors_stream)
         r.survivors_filter = int(st.survivors_filter)
         r.kernel_launches = int(st.kernel_launches)
+        r.stream_kernel_ms = float(st.stream_kernel_ms)
     return r
 
 

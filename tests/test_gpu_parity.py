@@ -113,3 +113,12 @@ def test_gpu_repeat_deterministic(engine, oracle):
     for _ in range(3):
         b = engine.compute_skyline(ds, 3)
         assert np.array_equal(a.ids, b.ids) and a.points_examined == b.points_examined
+
+
+@pytest.mark.parametrize("rec", load_json("large.json")["records"], ids=lambda r: r["key"])
+def test_gpu_large_skyline_golden(engine, oracle, rec):
+    """Large-S anchors: anti-correlated d=6/8 where 59-99% of points are
+    skyline points (the reference needs 40-290 s for these)."""
+    x, mn, mx = inputs_for(oracle, rec)
+    r = engine.compute_skyline(sky.Dataset(x, mn, mx), rec["rho"])
+    check(r, load_ids("large_ids.npz")[rec["key"]], rec["points_examined"], rec["keys"], rec["candidates"])
