@@ -21,12 +21,16 @@ constexpr unsigned kFull = 0xffffffffu;
 typedef unsigned long long u64;
 
 // ---------------------------------------------------------------- memory order
-__device__ __forceinline__ void st_release(u64* p, u64 v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// Look-back status words are self-contained (flag and value in one 64-bit
+// word) and publish nothing else, so relaxed gpu-scope accesses suffice.  An
+// acquire load would compile to CCTL.IVALL (a full L1 invalidate) per spin
+// iteration -- measured at 45% of K1's stall samples before this change.
+__device__ __forceinline__ void st_status(u64* p, u64 v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ u64 ld_acquire(const u64* p) {
+__device__ __forceinline__ u64 ld_status(const u64* p) {
   u64 v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 
@@ -42,17 +46,17 @@ constexpr u64 kValMask = (1ull << 62) - 1;
 __device__ __forceinline__ u64 warp_lookback(u64* status, u64 tile, u64 agg) {
   const int lane = threadIdx.x & 31;
   if (tile == 0) {
-    if (lane == 0) st_release(&status[0], kFlagInc | agg);
+    if (lane == 0) st_status(&status[0], kFlagInc | agg);
     return 0;
   }
-  if (lane == 0) st_release(&status[tile], kFlagAgg | agg);
+  if (lane == 0) st_status(&status[tile], kFlagAgg | agg);
   u64 excl = 0;
   long long base = (long long)tile - 1;
   while (true) {
     const long long t = base - lane;
     u64 s;
     if (t >= 0) {
-      do { s = ld_acquire(&status[t]); } while ((s >> 62) == 0);
+      do { s = ld_status(&status[t]); } while ((s >> 62) == 0);
     } else {
       s = kFlagInc;  // virtual predecessor with inclusive prefix 0
     }
@@ -65,8 +69,47 @@ __device__ __forceinline__ u64 warp_lookback(u64* status, u64 tile, u64 agg) {
     if (inc) break;
     base -= 32;
   }
-  if (lane == 0) st_release(&status[tile], kFlagInc | (excl + agg));
+  if (lane == 0) st_status(&status[tile], kFlagInc | (excl + agg));
   return excl;
+}
+
+// ------------------------------------------------ unordered warp output
+// Survivor streams that need no order are written through per-warp output
+// chunks reserved with one atomicAdd per chunk of slots (not per survivor: a
+// single global counter would serialise ~10^6 atomics).  Slots a warp does
+// not fill are stamped with kNoId, which every consumer skips; the record ids
+// are put back in ascending order once, at the end, through an id bitmap.
+constexpr uint32_t kNoId = 0xffffffffu;
+
+struct WarpOut {
+  u64 base;        // first slot of the current chunk (lane-uniform)
+  unsigned fill;   // slots used in it
+  unsigned chunk;  // chunk size (>= 32); fill starts at chunk so the first use reserves
+};
+
+// Reserve positions for the lanes with `flag` set; returns this lane's slot.
+// Call with all 32 lanes.  `stamp(slot)` writes kNoId into abandoned slots.
+template <typename Stamp>
+__device__ __forceinline__ u64 warp_reserve(WarpOut& wo, bool flag, u64* counter, Stamp stamp) {
+  const int lane = threadIdx.x & 31;
+  const unsigned m = __ballot_sync(kFull, flag);
+  const unsigned cnt = __popc(m);
+  if (wo.fill + cnt > wo.chunk) {
+    for (unsigned s = wo.fill + lane; s < wo.chunk; s += 32) stamp(wo.base + s);
+    u64 b = 0;
+    if (lane == 0) b = atomicAdd(counter, (u64)wo.chunk);
+    wo.base = __shfl_sync(kFull, b, 0);
+    wo.fill = 0;
+  }
+  const u64 slot = wo.base + wo.fill + __popc(m & ((1u << lane) - 1));
+  wo.fill += cnt;
+  return slot;
+}
+
+template <typename Stamp>
+__device__ __forceinline__ void warp_close(WarpOut& wo, Stamp stamp) {
+  const int lane = threadIdx.x & 31;
+  for (unsigned s = wo.fill + lane; s < wo.chunk; s += 32) stamp(wo.base + s);
 }
 
 // Block-wide stable ranks for PPT flags per thread laid out point-major:

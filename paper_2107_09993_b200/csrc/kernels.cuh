@@ -127,7 +127,7 @@ struct Coord;
 template <>
 struct Coord<float, float, true> {
   __device__ __forceinline__ static float value(float v, const Norm&, int) {
-    return v < 0.0f ? 0.0f : (v >= 1.0f ? 1.0f : v);  // NaN passes through; reported separately
+    return fminf(fmaxf(v, 0.0f), 1.0f);  // NaN -> 0; non-finite records are reported separately
   }
   __device__ __forceinline__ static int col(float u, float fscale, double, int top) {
     return cell_col(u, fscale, top);
@@ -274,8 +274,10 @@ __device__ __forceinline__ bool strictly_dominated_cols(const TT* __restrict__ P
 // key/candidate sets only at layers < L, so its occupancy is
 // recorded at layer L-1: a shared-memory bitmap for A (tiny), a global
 // check-before-set bitmap for B.  Survivors (about the candidate-cell
-// fraction: 6.1% at the headline config) are compacted in input order and set
-// their bit in the layer-rho occupancy.  Every coordinate is read once.
+// fraction: 6.1% at the headline config) go to per-warp output chunks and set
+// their bit in the layer-rho occupancy.  Every coordinate is read once; the
+// kernel has no block barrier in its main loop (warp-centric, static
+// round-robin warp tiles).
 struct StreamParams {
   const void* coords;
   u64 n;
@@ -291,106 +293,103 @@ struct StreamParams {
   uint32_t* slabs;         // per-CTA copies of the layer la-1 bitmap
   void* out_rows;
   uint32_t* out_ids;
-  u64* status;
-  u64* claim;
-  u64* out_count;
+  u64* out_reserved;       // slots handed out (multiple of chunk)
+  unsigned chunk;          // output chunk per warp reservation
+  u64* kept;               // exact number of survivors
   u64* nonfinite;          // max of (~record) over non-finite records: 0 = none
 };
 
 template <typename TIn, typename TOut, int D, bool IDENT, int THREADS, int PPT>
-__global__ void __launch_bounds__(THREADS) k_stream(StreamParams p) {
+__global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
   extern __shared__ __align__(16) uint8_t sm[];
   uint32_t* occ_s = reinterpret_cast<uint32_t*>(sm);
   uint8_t* H_s = sm + p.lo_words * 4;
-  unsigned* scratch = reinterpret_cast<unsigned*>(sm + p.lo_words * 4 + ((p.h_entries + 15) & ~15u));
-  __shared__ u64 s_tile, s_excl;
-
   for (uint32_t w = threadIdx.x; w < p.lo_words; w += THREADS) occ_s[w] = 0;
   for (uint32_t e = threadIdx.x; e < p.h_entries; e += THREADS) H_s[e] = p.H[e];
   __syncthreads();
 
   const TIn* coords = static_cast<const TIn*>(p.coords);
   TOut* out_rows = static_cast<TOut*>(p.out_rows);
-  constexpr u64 TILE = (u64)THREADS * PPT;
-  const u64 ntiles = (p.n + TILE - 1) / TILE;
-  const int rho = p.rho, la = p.la, sh = rho - la, lo_sh = rho - la + 1;
+  const int lane = threadIdx.x & 31;
+  const uint32_t n = (uint32_t)p.n;
+  constexpr uint32_t WT = 32u * PPT;
+  const uint32_t ntiles = (uint32_t)((p.n + WT - 1) / WT);
+  const uint32_t gw = (blockIdx.x * THREADS + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * THREADS) >> 5;
+  const int rho = p.rho, la = p.la, sh = rho - la;
   const int top = (1 << rho) - 1;
   const float fscale = ldexpf(1.0f, rho);
   const double dscale = ldexp(1.0, rho);
   const bool test_b = p.PMs != nullptr;
+  WarpOut wo{0, p.chunk, p.chunk};
+  auto stamp = [&](u64 slot) { p.out_ids[slot] = kNoId; };
+  unsigned kept = 0;
 
-  while (true) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(p.claim, 1ull);
-    __syncthreads();
-    const u64 tile = s_tile;
-    if (tile >= ntiles) break;
-    const u64 base = tile * TILE;
-
+  for (uint32_t t = gw; t < ntiles; t += nw) {
+    const uint32_t base = t * WT + lane;
     TIn raw[PPT][D];
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
-      const u64 i = base + (u64)j * THREADS + threadIdx.x;
-      if (i < p.n) load_row<TIn, D>(coords, i, raw[j]);
+      const uint32_t i = base + j * 32;
+      if (i < n) load_row<TIn, D>(coords, i, raw[j]);
     }
-
-    bool keep[PPT];
-    unsigned rank[PPT];
-    TOut val[PPT][D];
-    u64 lin[PPT];
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
-      const u64 i = base + (u64)j * THREADS + threadIdx.x;
-      const bool valid = i < p.n;
+      const uint32_t i = base + j * 32;
+      const bool valid = i < n;
       bool fin = true;
-      u64 l = 0, pl = 0;
-      uint32_t hidx = 0, lo = 0;
       int col[D];
 #pragma unroll
-      for (int k = D - 1; k >= 0; --k) {
+      for (int k = 0; k < D; ++k) {
         fin &= finite_v(raw[j][k]);
-        const TOut u = Coord<TIn, TOut, IDENT>::value(raw[j][k], p.nm, k);
-        val[j][k] = u;
-        const int c = Coord<TIn, TOut, IDENT>::col(u, fscale, dscale, top);
-        col[k] = c;
-        l = (l << rho) | (u64)c;
-        pl = (pl << (rho - 1)) | (u64)(c >> 1);
-        lo = (lo << (la - 1)) | (uint32_t)(c >> lo_sh);
-        if (k >= 1) hidx = (hidx << la) | (uint32_t)(c >> sh);
+        col[k] = Coord<TIn, TOut, IDENT>::col(Coord<TIn, TOut, IDENT>::value(raw[j][k], p.nm, k), fscale, dscale, top);
       }
-      if (valid && !fin) atomicMax(p.nonfinite, ~i);
+      uint32_t hidx = 0;
+#pragma unroll
+      for (int k = D - 1; k >= 1; --k) hidx = (hidx << la) | (uint32_t)(col[k] >> sh);
       const bool fail_a = (col[0] >> sh) > (int)H_s[hidx];
+      if (valid && !fin) atomicMax(p.nonfinite, ~(u64)i);
       bool fail_b = false;
-      if (valid && !fail_a && test_b) {
+      if (valid && fail_a) {
+        if (la >= 2) {
+          uint32_t lo = 0;
+#pragma unroll
+          for (int k = D - 1; k >= 0; --k) lo = (lo << (la - 1)) | (uint32_t)(col[k] >> (sh + 1));
+          set_bit_shared(occ_s, lo);
+        }
+      } else if (valid && test_b) {
         fail_b = p.pms_wide ? strictly_dominated_cols<uint32_t, D>(static_cast<const uint32_t*>(p.PMs), col, rho)
                             : strictly_dominated_cols<uint8_t, D>(static_cast<const uint8_t*>(p.PMs), col, rho);
-      }
-      if (valid && fail_a && la >= 2) set_bit_shared(occ_s, lo);
-      if (valid && fail_b) set_bit_global(p.occ_rm1, pl);
-      keep[j] = valid && !fail_a && !fail_b;
-      lin[j] = l;
-    }
-
-    const unsigned total = block_ranks<THREADS, PPT>(keep, rank, scratch);
-    if (threadIdx.x < 32) {
-      const u64 excl = warp_lookback(p.status, tile, total);
-      if (threadIdx.x == 0) {
-        s_excl = excl;
-        if (tile == ntiles - 1) *p.out_count = excl + total;
-      }
-    }
-    __syncthreads();
-    const u64 excl = s_excl;
+        if (fail_b) {
+          u64 pl = 0;
 #pragma unroll
-    for (int j = 0; j < PPT; ++j) {
-      if (keep[j]) {
-        const u64 i = base + (u64)j * THREADS + threadIdx.x;
-        const u64 o = excl + rank[j];
-        store_row<TOut, D>(out_rows, o, val[j]);
-        p.out_ids[o] = (uint32_t)i;
-        set_bit_global(p.occ_rho, lin[j]);
+          for (int k = D - 1; k >= 0; --k) pl = (pl << (rho - 1)) | (u64)(col[k] >> 1);
+          set_bit_global(p.occ_rm1, pl);
+        }
+      }
+      const bool keep = valid && !fail_a && !fail_b;
+      kept += keep;
+      if (__any_sync(kFull, keep)) {
+        const u64 o = warp_reserve(wo, keep, p.out_reserved, stamp);
+        if (keep) {
+          TOut u[D];
+          u64 l = 0;
+#pragma unroll
+          for (int k = D - 1; k >= 0; --k) {
+            u[k] = Coord<TIn, TOut, IDENT>::value(raw[j][k], p.nm, k);
+            l = (l << rho) | (u64)col[k];
+          }
+          store_row<TOut, D>(out_rows, o, u);
+          p.out_ids[o] = i;
+          set_bit_global(p.occ_rho, l);
+        }
       }
     }
   }
+  warp_close(wo, stamp);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) kept += __shfl_xor_sync(kFull, kept, o);
+  if (lane == 0 && kept) atomicAdd(p.kept, (u64)kept);
   if (p.lo_words) {
     __syncthreads();
     uint32_t* slab = p.slabs + (u64)blockIdx.x * p.lo_words;
@@ -547,6 +546,19 @@ __global__ void k_downsample(const uint32_t* __restrict__ src, int L, int d, u64
   }
 }
 
+// ------------------------------------------------- per-dimension lists
+// Dominance pruning index: for every dimension k, the points of a set ordered
+// by their column at a fixed fine level (kListLevel), with column starts.  A
+// dominator q of p satisfies q_k <= p_k, hence col(q_k) <= col(p_k) (floor of
+// a power-of-two scaling is monotone), so the candidates for p are a prefix of
+// each list and the shortest of the d prefixes suffices.  Near-face points --
+// the hard cases of independent/correlated data -- have one tiny coordinate
+// and therefore a tiny prefix.
+constexpr int kListLevel = 10;
+constexpr int kListCols = 1 << kListLevel;
+__device__ __forceinline__ int list_col(float v) { return cell_col(v, (float)kListCols, kListCols - 1); }
+__device__ __forceinline__ int list_col(double v) { return cell_col(v, (double)kListCols, kListCols - 1); }
+
 // ------------------------------------------------ K4: candidate-cell filter
 // Survivors of the stream that lie in layer-rho candidate cells (refine.cpp:
 // 78-96; their count is points_examined), minus those a filter point f
@@ -557,114 +569,124 @@ __global__ void k_downsample(const uint32_t* __restrict__ src, int L, int d, u64
 // reference drops p in phase 2 (refine.cpp:98-99).  Output keeps input order.
 struct CandParams {
   const void* rows;
-  const uint32_t* ids;
-  const u64* count;      // |S1|
+  const uint32_t* ids;    // kNoId marks an empty slot
+  const u64* count;       // slots to scan (device), or nullptr to use count_const
+  u64 count_const;
   int rho;
   const void* PM;        // layer-rho prefix-min table (u8 or u32), nullptr: no cell test
   const void* f_rows;    // filter points (strength order), may be empty
   const u64* f_fsum;
   const u64* f_count;
   uint32_t f_max;
+  const uint16_t* f_lists;  // D x f_max filter indices, column-ordered per dimension
+  const uint16_t* f_offs;   // D x (kListCols + 1) column starts
   void* out_rows;
   uint32_t* out_ids;
   u64* out_fsum;
-  u64* status;
-  u64* claim;
-  u64* out_count;
+  u64* out_reserved;
+  unsigned chunk;        // output chunk per warp reservation
+  u64* kept;             // exact number of points written
   u64* examined;         // points_examined (refine.cpp:90-96), may be null
 };
 
-template <typename T, int D, typename TT, int THREADS, int PPT>
+template <typename T, int D, typename TT, int THREADS>
 __global__ void __launch_bounds__(THREADS) k_candidates(CandParams p) {
   extern __shared__ __align__(16) uint8_t smc[];
-  __shared__ unsigned scratch[PPT * (THREADS / 32) + 1];
-  __shared__ u64 s_tile, s_excl;
-  const u64 n = *p.count;
-  constexpr u64 TILE = (u64)THREADS * PPT;
-  const u64 ntiles = (n + TILE - 1) / TILE;
-  if (ntiles == 0) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) *p.out_count = 0;
-    return;
-  }
+  const u64 n = p.count ? *p.count : p.count_const;
   uint32_t nf = 0;
+  const uint32_t fm = p.f_max;
   T* f_rows = reinterpret_cast<T*>(smc);
-  u64* f_sum = reinterpret_cast<u64*>(smc + (((u64)p.f_max * D * sizeof(T) + 15) & ~15ull));
+  u64* f_sum = reinterpret_cast<u64*>(smc + (((u64)fm * D * sizeof(T) + 15) & ~15ull));
+  uint16_t* f_list = reinterpret_cast<uint16_t*>(f_sum + fm);           // D x fm
+  uint16_t* f_off = f_list + (u64)D * fm;                              // D x (kListCols + 1)
   if (p.f_count) {
     const u64 fc = *p.f_count;
-    nf = (uint32_t)(fc < p.f_max ? fc : p.f_max);
+    nf = (uint32_t)(fc < fm ? fc : fm);
     const T* fr = static_cast<const T*>(p.f_rows);
     for (uint32_t e = threadIdx.x; e < nf * D; e += THREADS) f_rows[e] = fr[e];
     for (uint32_t e = threadIdx.x; e < nf; e += THREADS) f_sum[e] = p.f_fsum[e];
-    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < (uint32_t)D * fm; e += THREADS) f_list[e] = p.f_lists[e];
+    for (uint32_t e = threadIdx.x; e < (uint32_t)D * (kListCols + 1); e += THREADS) f_off[e] = p.f_offs[e];
   }
+  __syncthreads();
   const T* rows = static_cast<const T*>(p.rows);
   T* out_rows = static_cast<T*>(p.out_rows);
   const TT* PM = static_cast<const TT*>(p.PM);
   const int rho = p.rho, top = (1 << rho) - 1;
   const float fscale = ldexpf(1.0f, rho);
   const double dscale = ldexp(1.0, rho);
-  u64 examined = 0;
-  while (true) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(p.claim, 1ull);
-    __syncthreads();
-    const u64 tile = s_tile;
-    if (tile >= ntiles) break;
-    const u64 base = tile * TILE;
-    T v[PPT][D];
-    u64 ps[PPT];
-    bool keep[PPT];
-    unsigned rank[PPT];
+  const u64 gw = (blockIdx.x * (u64)THREADS + threadIdx.x) >> 5;
+  const u64 nw = ((u64)gridDim.x * THREADS) >> 5;
+  const int lane = threadIdx.x & 31;
+  WarpOut wo{0, p.chunk, p.chunk};
+  auto stamp = [&](u64 slot) { p.out_ids[slot] = kNoId; };
+  u64 examined = 0, kept = 0;
+  for (u64 wbase = gw * 32; wbase < n; wbase += nw * 32) {
+    const u64 i = wbase + lane;
+    bool keep = false;
+    T v[D];
+    u64 ps = 0;
+    uint32_t pid = kNoId;
+    if (i < n) pid = p.ids[i];
+    if (pid != kNoId) {
+      load_row_cached<T, D>(rows, i, v);
+      bool cand = true;
+      if (PM) {
+        int col[D];
 #pragma unroll
-    for (int j = 0; j < PPT; ++j) {
-      const u64 i = base + (u64)j * THREADS + threadIdx.x;
-      keep[j] = false;
-      if (i < n) {
-        load_row_cached<T, D>(rows, i, v[j]);
-        bool cand = true;
-        if (PM) {
-          int col[D];
-#pragma unroll
-          for (int k = 0; k < D; ++k) {
-            if constexpr (sizeof(T) == 4) col[k] = cell_col(v[j][k], fscale, top);
-            else col[k] = cell_col(v[j][k], dscale, top);
-          }
-          cand = !strictly_dominated_cols<TT, D>(PM, col, rho);
+        for (int k = 0; k < D; ++k) {
+          if constexpr (sizeof(T) == 4) col[k] = cell_col(v[k], fscale, top);
+          else col[k] = cell_col(v[k], dscale, top);
         }
-        examined += cand;
-        ps[j] = fsum_bits<T, D>(v[j]);
-        bool dom = false;
-        if (cand) {
-          for (uint32_t f = 0; f < nf && !dom; ++f)
-            dom = f_sum[f] < ps[j] && dominates<T, D>(f_rows + (u64)f * D, v[j]);
-        }
-        keep[j] = cand && !dom;
+        cand = !strictly_dominated_cols<TT, D>(PM, col, rho);
       }
-    }
-    const unsigned total = block_ranks<THREADS, PPT>(keep, rank, scratch);
-    if (threadIdx.x < 32) {
-      const u64 excl = warp_lookback(p.status, tile, total);
-      if (threadIdx.x == 0) {
-        s_excl = excl;
-        if (tile == ntiles - 1) *p.out_count = excl + total;
+      examined += cand;
+      ps = fsum_bits<T, D>(v);
+      bool dom = false;
+      if (cand && nf) {
+        // strongest filter points first (strength order): most points fall
+        // to one of them (median 1 test at the headline config)
+        const uint32_t head = nf < 32 ? nf : 32;
+        for (uint32_t f = 0; f < head && !dom; ++f)
+          dom = f_sum[f] < ps && dominates<T, D>(f_rows + (u64)f * D, v);
       }
-    }
-    __syncthreads();
-    const u64 excl = s_excl;
+      if (cand && nf && !dom) {
+        // a dominator f has col_k(f) <= col_k(p) in every dimension: scan
+        // the shortest such column prefix of the per-dimension lists
+        int bk = 0;
+        unsigned end = 0xffffffffu;
 #pragma unroll
-    for (int j = 0; j < PPT; ++j) {
-      if (keep[j]) {
-        const u64 i = base + (u64)j * THREADS + threadIdx.x;
-        const u64 o = excl + rank[j];
-        store_row<T, D>(out_rows, o, v[j]);
-        p.out_ids[o] = p.ids[i];
-        p.out_fsum[o] = ps[j];
+        for (int k = 0; k < D; ++k) {
+          const unsigned e = f_off[k * (kListCols + 1) + list_col(v[k]) + 1];
+          if (e < end) { end = e; bk = k; }
+        }
+        const uint16_t* lst = f_list + (u64)bk * fm;
+        for (unsigned e = 0; e < end && !dom; ++e) {
+          const unsigned f = lst[e];
+          dom = f_sum[f] < ps && dominates<T, D>(f_rows + (u64)f * D, v);
+        }
+      }
+      keep = cand && !dom;
+      kept += keep;
+    }
+    if (__any_sync(kFull, keep)) {
+      const u64 o = warp_reserve(wo, keep, p.out_reserved, stamp);
+      if (keep) {
+        store_row<T, D>(out_rows, o, v);
+        p.out_ids[o] = pid;
+        p.out_fsum[o] = ps;
       }
     }
   }
-  if (p.examined) {
+  warp_close(wo, stamp);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) examined += __shfl_xor_sync(kFull, examined, o);
-    if ((threadIdx.x & 31) == 0 && examined) atomicAdd(p.examined, examined);
+  for (int o = 16; o > 0; o >>= 1) {
+    examined += __shfl_xor_sync(kFull, examined, o);
+    kept += __shfl_xor_sync(kFull, kept, o);
+  }
+  if (lane == 0) {
+    if (p.examined && examined) atomicAdd(p.examined, examined);
+    if (kept) atomicAdd(p.kept, kept);
   }
 }
 
@@ -674,14 +696,19 @@ __global__ void __launch_bounds__(THREADS) k_candidates(CandParams p) {
 // k_candidates happen after ~1 test for most points (median 1, p90 18 at the
 // headline config).
 template <typename T, int D>
-__global__ void __launch_bounds__(1024) k_strength_order(const T* __restrict__ rows, const u64* __restrict__ fsum,
+__global__ void __launch_bounds__(1024) k_strength_order(const T* __restrict__ rows, const uint32_t* __restrict__ ids,
+                                                          const uint8_t* __restrict__ flag,
+                                                          const u64* __restrict__ fsum,
                                                           const u64* __restrict__ count, uint32_t f_max,
                                                           T* __restrict__ out_rows, u64* __restrict__ out_fsum,
-                                                          u64* __restrict__ out_count) {
+                                                          u64* __restrict__ out_count, uint16_t* __restrict__ f_lists,
+                                                          uint16_t* __restrict__ f_offs) {
   __shared__ unsigned hist[65];
   __shared__ unsigned offs[65];
-  const u64 n = *count;
+  __shared__ unsigned total;
+  const u64 slots = *count;
   if (threadIdx.x < 65) hist[threadIdx.x] = 0;
+  if (threadIdx.x == 0) total = 0;
   __syncthreads();
   auto bucket = [&](u64 i) {
     double vol = 1.0;
@@ -690,8 +717,14 @@ __global__ void __launch_bounds__(1024) k_strength_order(const T* __restrict__ r
     const double l = vol > 0 ? -log2(vol) * 2.0 : 1e9;
     return (int)(l < 63.0 ? l : 63.0);
   };
-  for (u64 i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&hist[bucket(i)], 1u);
+  auto live = [&](u64 i) { return ids[i] != kNoId && flag[i]; };
+  for (u64 i = threadIdx.x; i < slots; i += blockDim.x)
+    if (live(i)) {
+      atomicAdd(&hist[bucket(i)], 1u);
+      atomicAdd(&total, 1u);
+    }
   __syncthreads();
+  const u64 n = total;
   if (threadIdx.x == 0) {
     unsigned run = 0;
     for (int b = 0; b < 64; ++b) {
@@ -701,7 +734,8 @@ __global__ void __launch_bounds__(1024) k_strength_order(const T* __restrict__ r
     *out_count = n < f_max ? n : f_max;
   }
   __syncthreads();
-  for (u64 i = threadIdx.x; i < n; i += blockDim.x) {
+  for (u64 i = threadIdx.x; i < slots; i += blockDim.x) {
+    if (!live(i)) continue;
     const unsigned o = atomicAdd(&offs[bucket(i)], 1u);
     if (o < f_max) {
 #pragma unroll
@@ -709,235 +743,251 @@ __global__ void __launch_bounds__(1024) k_strength_order(const T* __restrict__ r
       out_fsum[o] = fsum[i];
     }
   }
+  // per-dimension column lists of the kept filter points
+  __shared__ unsigned cnt[kListCols + 1];
+  __syncthreads();
+  const unsigned nf = (unsigned)(n < f_max ? n : f_max);
+  for (int k = 0; k < D; ++k) {
+    for (unsigned c = threadIdx.x; c <= kListCols; c += blockDim.x) cnt[c] = 0;
+    __syncthreads();
+    for (unsigned f = threadIdx.x; f < nf; f += blockDim.x) atomicAdd(&cnt[list_col(out_rows[(u64)f * D + k]) + 1], 1u);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned run = 0;
+      for (int c = 0; c <= kListCols; ++c) {
+        run += cnt[c];
+        cnt[c] = run;  // cnt[c] = number of points with column < c
+        f_offs[k * (kListCols + 1) + c] = (uint16_t)run;
+      }
+    }
+    __syncthreads();
+    for (unsigned f = threadIdx.x; f < nf; f += blockDim.x) {
+      const unsigned pos = atomicAdd(&cnt[list_col(out_rows[(u64)f * D + k])], 1u);
+      f_lists[(u64)k * f_max + pos] = (uint16_t)f;
+    }
+    __syncthreads();
+  }
 }
 
 // ------------------------------------------- K5: exact sort-first dominance
-// A point set in ascending-id order: rows (T[D]), record ids, FP64 sum bits.
-template <typename T>
-struct PointBuf {
-  T* rows;
-  uint32_t* ids;
-  u64* fsum;
-};
-
-// Append the points of src[begin, end) (end clamped to *src_count) that no
-// filter point f (the first nf of F, f preceding p and f dominating p)
-// eliminates, to dst at offset *dst_count_in; writes the new count.
-struct FilterParams {
-  const void* src_rows;
-  const uint32_t* src_ids;
-  const u64* src_fsum;
-  const u64* src_count;
-  u64 begin, end;
-  const void* f_rows;
-  const uint32_t* f_ids;
-  const u64* f_fsum;
-  const u64* f_count;
-  uint32_t f_max;
-  void* dst_rows;
-  uint32_t* dst_ids;
-  u64* dst_fsum;
-  const u64* dst_count_in;
-  u64* dst_count_out;
-  u64* status;
-  u64* claim;
-};
-
-template <typename T, int D, int THREADS, int PPT>
-__global__ void __launch_bounds__(THREADS) k_filter_append(FilterParams p) {
-  extern __shared__ __align__(16) uint8_t sm[];
-  __shared__ unsigned scratch[PPT * (THREADS / 32) + 1];
-  __shared__ u64 s_tile, s_excl;
-  const u64 total_src = *p.src_count;
-  const u64 end = p.end < total_src ? p.end : total_src;
-  const u64 begin = p.begin;
-  const u64 nsrc = end > begin ? end - begin : 0;
-  const u64 off = *p.dst_count_in;
-  constexpr u64 TILE = (u64)THREADS * PPT;
-  const u64 ntiles = (nsrc + TILE - 1) / TILE;
-  if (ntiles == 0) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) *p.dst_count_out = off;
-    return;
-  }
-  const u64 fc = *p.f_count;
-  const uint32_t nf = (uint32_t)(fc < p.f_max ? fc : p.f_max);
-  T* f_rows = reinterpret_cast<T*>(sm);
-  u64* f_sum = reinterpret_cast<u64*>(sm + (((u64)p.f_max * D * sizeof(T) + 15) & ~15ull));
-  uint32_t* f_id = reinterpret_cast<uint32_t*>(f_sum + p.f_max);
-  const T* frows_g = static_cast<const T*>(p.f_rows);
-  for (uint32_t e = threadIdx.x; e < nf * D; e += THREADS) f_rows[e] = frows_g[e];
-  for (uint32_t e = threadIdx.x; e < nf; e += THREADS) {
-    f_sum[e] = p.f_fsum[e];
-    f_id[e] = p.f_ids[e];
-  }
-  __syncthreads();
-  const T* src_rows = static_cast<const T*>(p.src_rows);
-  T* dst_rows = static_cast<T*>(p.dst_rows);
-  while (true) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(p.claim, 1ull);
-    __syncthreads();
-    const u64 tile = s_tile;
-    if (tile >= ntiles) break;
-    const u64 base = begin + tile * TILE;
-    T v[PPT][D];
-    u64 ps[PPT];
-    uint32_t pid[PPT];
-    bool keep[PPT];
-    unsigned rank[PPT];
-#pragma unroll
-    for (int j = 0; j < PPT; ++j) {
-      const u64 i = base + (u64)j * THREADS + threadIdx.x;
-      keep[j] = false;
-      if (i < end) {
-        load_row_cached<T, D>(src_rows, i, v[j]);
-        ps[j] = p.src_fsum[i];
-        pid[j] = p.src_ids[i];
-        bool dom = false;
-        for (uint32_t f = 0; f < nf && !dom; ++f) {
-          dom = precedes(f_sum[f], f_id[f], ps[j], pid[j]) && dominates<T, D>(f_rows + (u64)f * D, v[j]);
-        }
-        keep[j] = !dom;
-      }
-    }
-    const unsigned total = block_ranks<THREADS, PPT>(keep, rank, scratch);
-    if (threadIdx.x < 32) {
-      const u64 excl = warp_lookback(p.status, tile, total);
-      if (threadIdx.x == 0) {
-        s_excl = excl;
-        if (tile == ntiles - 1) *p.dst_count_out = off + excl + total;
-      }
-    }
-    __syncthreads();
-    const u64 excl = s_excl;
-#pragma unroll
-    for (int j = 0; j < PPT; ++j) {
-      if (keep[j]) {
-        const u64 o = off + excl + rank[j];
-        store_row<T, D>(dst_rows, o, v[j]);
-        p.dst_ids[o] = pid[j];
-        p.dst_fsum[o] = ps[j];
-      }
-    }
-  }
-}
-
-// flag[i] is cleared iff some point of the set precedes point i and
-// dominates it (flags start at 1).  2-D decomposition: blockIdx.x picks a
-// block of THREADS points p, blockIdx.y a chunk of QCHUNK candidate
-// dominators q, so small sets still fill the GPU.
-template <typename T, int D, int THREADS, int QCHUNK>
-__global__ void __launch_bounds__(THREADS) k_allpairs(const T* __restrict__ rows, const uint32_t* __restrict__ ids,
-                                                      const u64* __restrict__ fsum, const u64* __restrict__ count,
-                                                      uint8_t* __restrict__ flag) {
-  __shared__ T q_rows[THREADS * D];
-  __shared__ u64 q_sum[THREADS];
-  __shared__ uint32_t q_id[THREADS];
+// Per-dimension column lists of a point set with a device-side count:
+// histogram, exclusive scan, scatter (non-stable within a column; the order
+// inside a column only affects how soon a dominator is met, never the result).
+template <typename T, int D>
+__global__ void k_list_hist(const T* __restrict__ rows, const uint32_t* __restrict__ ids, const u64* __restrict__ count,
+                            unsigned* __restrict__ hist) {
   const u64 n = *count;
-  const u64 q0 = (u64)blockIdx.y * QCHUNK;
-  if (q0 >= n) return;
-  const u64 q1 = q0 + QCHUNK < n ? q0 + QCHUNK : n;
-  for (u64 pb = blockIdx.x; pb * THREADS < n; pb += gridDim.x) {
-    const u64 i = pb * THREADS + threadIdx.x;
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    if (ids[i] == kNoId) continue;
     T v[D];
-    u64 ps = 0;
-    uint32_t pid = 0;
-    bool alive = i < n && flag[i];
-    if (alive) {
-      load_row_cached<T, D>(rows, i, v);
-      ps = fsum[i];
-      pid = ids[i];
-    }
-    bool dominated = false;
-    for (u64 qt = q0; qt < q1; qt += THREADS) {
-      if (!__syncthreads_or(alive)) break;
-      const u64 qi = qt + threadIdx.x;
-      if (qi < q1) {
-        T q[D];
-        load_row_cached<T, D>(rows, qi, q);
+    load_row_cached<T, D>(rows, i, v);
 #pragma unroll
-        for (int k = 0; k < D; ++k) q_rows[threadIdx.x * D + k] = q[k];
-        q_sum[threadIdx.x] = fsum[qi];
-        q_id[threadIdx.x] = ids[qi];
-      }
-      __syncthreads();
-      const u64 rem = q1 - qt;
-      const int m = rem < THREADS ? (int)rem : THREADS;
-      if (alive) {
-        for (int j = 0; j < m; ++j) {
-          if (precedes(q_sum[j], q_id[j], ps, pid) && dominates<T, D>(q_rows + j * D, v)) {
-            alive = false;
-            dominated = true;
-            break;
-          }
-        }
-      }
-    }
-    __syncthreads();
-    if (dominated) flag[i] = 0;
+    for (int k = 0; k < D; ++k) atomicAdd(&hist[k * (kListCols + 1) + list_col(v[k]) + 1], 1u);
   }
 }
 
-struct CompactParams {
-  const void* src_rows;
-  const uint32_t* src_ids;
-  const u64* src_fsum;
-  const u64* count;
-  const uint8_t* flag;
-  void* dst_rows;
-  uint32_t* dst_ids;
-  u64* dst_fsum;
-  u64* dst_count;
-  u64* status;
-  u64* claim;
-};
-
-template <typename T, int D, int THREADS, int PPT>
-__global__ void __launch_bounds__(THREADS) k_compact(CompactParams p) {
-  __shared__ unsigned scratch[PPT * (THREADS / 32) + 1];
-  __shared__ u64 s_tile, s_excl;
-  const u64 n = *p.count;
-  constexpr u64 TILE = (u64)THREADS * PPT;
-  const u64 ntiles = (n + TILE - 1) / TILE;
-  if (ntiles == 0) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) *p.dst_count = 0;
-    return;
+// One CTA per dimension: inclusive scan of (count shifted by one) = column starts.
+__global__ void __launch_bounds__(1024) k_list_scan(unsigned* __restrict__ hist, unsigned* __restrict__ cursor) {
+  __shared__ unsigned part[1024];
+  unsigned* h = hist + blockIdx.x * (kListCols + 1);
+  constexpr int PER = (kListCols + 1 + 1023) / 1024;
+  unsigned loc[PER], sum = 0;
+#pragma unroll
+  for (int e = 0; e < PER; ++e) {
+    const int c = threadIdx.x * PER + e;
+    loc[e] = c <= kListCols ? h[c] : 0;
+    sum += loc[e];
   }
-  const T* src_rows = static_cast<const T*>(p.src_rows);
-  T* dst_rows = static_cast<T*>(p.dst_rows);
-  while (true) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(p.claim, 1ull);
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const unsigned y = threadIdx.x >= (unsigned)o ? part[threadIdx.x - o] : 0;
     __syncthreads();
-    const u64 tile = s_tile;
-    if (tile >= ntiles) break;
-    const u64 base = tile * TILE;
-    bool keep[PPT];
-    unsigned rank[PPT];
+    part[threadIdx.x] += y;
+    __syncthreads();
+  }
+  unsigned run = part[threadIdx.x] - sum;
 #pragma unroll
-    for (int j = 0; j < PPT; ++j) {
-      const u64 i = base + (u64)j * THREADS + threadIdx.x;
-      keep[j] = i < n && p.flag[i];
+  for (int e = 0; e < PER; ++e) {
+    const int c = threadIdx.x * PER + e;
+    run += loc[e];
+    if (c <= kListCols) {
+      h[c] = run;
+      cursor[blockIdx.x * (kListCols + 1) + c] = run;
     }
-    const unsigned total = block_ranks<THREADS, PPT>(keep, rank, scratch);
-    if (threadIdx.x < 32) {
-      const u64 excl = warp_lookback(p.status, tile, total);
-      if (threadIdx.x == 0) {
-        s_excl = excl;
-        if (tile == ntiles - 1) *p.dst_count = excl + total;
+  }
+}
+
+template <typename T, int D>
+__global__ void k_list_scatter(const T* __restrict__ rows, const uint32_t* __restrict__ ids,
+                               const u64* __restrict__ count, unsigned* __restrict__ cursor,
+                               uint32_t* __restrict__ lists, u64 cap) {
+  const u64 n = *count;
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    if (ids[i] == kNoId) continue;
+    T v[D];
+    load_row_cached<T, D>(rows, i, v);
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const unsigned pos = atomicAdd(&cursor[k * (kListCols + 1) + list_col(v[k])], 1u);
+      lists[(u64)k * cap + pos] = (uint32_t)i;
+    }
+  }
+}
+
+// flag[i] = 1 iff no point q of the set precedes i (sort-first order,
+// refine.cpp:38-41) and dominates it.  Candidates q come from the shortest
+// per-dimension column prefix.  One warp per point: the 32 lanes test 32
+// candidates per step (independent gathers in flight) and stop at the first
+// step with a dominator, so a skyline point's scan is prefix/32 steps long.
+template <typename T, int D>
+__global__ void __launch_bounds__(256) k_allpairs_lists(const T* __restrict__ rows, const uint32_t* __restrict__ ids,
+                                                        const u64* __restrict__ fsum, const u64* __restrict__ count,
+                                                        const uint32_t* __restrict__ lists, const unsigned* __restrict__ offs,
+                                                        u64 cap, uint8_t* __restrict__ flag) {
+  const u64 n = *count;
+  const int lane = threadIdx.x & 31;
+  const u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
+  const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 i = warp; i < n; i += nwarps) {
+    const uint32_t pid = ids[i];
+    if (pid == kNoId) {
+      if (lane == 0) flag[i] = 0;
+      continue;
+    }
+    T v[D];
+    load_row_cached<T, D>(rows, i, v);
+    const u64 ps = fsum[i];
+    int bk = 0;
+    unsigned end = 0xffffffffu;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const unsigned e = __ldg(offs + k * (kListCols + 1) + list_col(v[k]) + 1);
+      if (e < end) { end = e; bk = k; }
+    }
+    const uint32_t* lst = lists + (u64)bk * cap;
+    bool dom = false;
+    for (unsigned base = 0; base < end; base += 32) {
+      const unsigned e = base + lane;
+      bool d_l = false;
+      if (e < end) {
+        const uint32_t q = __ldg(lst + e);
+        if (precedes(__ldg(fsum + q), __ldg(ids + q), ps, pid)) {
+          T w[D];
+          load_row_cached<T, D>(rows, q, w);
+          d_l = dominates<T, D>(w, v);
+        }
+      }
+      if (__any_sync(kFull, d_l)) {
+        dom = true;
+        break;
       }
     }
-    __syncthreads();
-    const u64 excl = s_excl;
+    if (lane == 0) flag[i] = dom ? 0 : 1;
+  }
+}
+
+// ----------------------------------------------- K6: ascending record ids
+// Skyline members set their record id in an n-bit bitmap; the ids are then
+// written in ascending order by a two-pass popcount scan over the bitmap
+// (refine.cpp:101-103 sorts instead).  kBitsBlock words per block.
+constexpr int kBitsThreads = 256;
+constexpr int kBitsPer = 8;
+constexpr u64 kBitsBlock = (u64)kBitsThreads * kBitsPer;
+
+__global__ void k_mark_ids(const uint32_t* __restrict__ ids, const uint8_t* __restrict__ flag,
+                           const u64* __restrict__ count, uint32_t* __restrict__ bits) {
+  const u64 n = *count;
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    const uint32_t id = ids[i];
+    if (id != kNoId && flag[i]) atomicOr(bits + (id >> 5), 1u << (id & 31));
+  }
+}
+
+__global__ void __launch_bounds__(kBitsThreads) k_bits_count(const uint32_t* __restrict__ bits, u64 words,
+                                                             unsigned* __restrict__ block_counts) {
+  const u64 b0 = blockIdx.x * kBitsBlock;
+  unsigned c = 0;
 #pragma unroll
-    for (int j = 0; j < PPT; ++j) {
-      if (keep[j]) {
-        const u64 i = base + (u64)j * THREADS + threadIdx.x;
-        const u64 o = excl + rank[j];
-        T v[D];
-        load_row_cached<T, D>(src_rows, i, v);
-        store_row<T, D>(dst_rows, o, v);
-        p.dst_ids[o] = p.src_ids[i];
-        p.dst_fsum[o] = p.src_fsum[i];
-      }
+  for (int e = 0; e < kBitsPer; ++e) {
+    const u64 w = b0 + (u64)e * kBitsThreads + threadIdx.x;
+    if (w < words) c += __popc(bits[w]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+  __shared__ unsigned ws[kBitsThreads / 32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+    for (int w = 0; w < kBitsThreads / 32; ++w) t += ws[w];
+    block_counts[blockIdx.x] = t;
+  }
+}
+
+// Single CTA: exclusive scan of the block counts; total -> *out_count.
+__global__ void __launch_bounds__(1024) k_bits_scan(unsigned* __restrict__ block_counts, unsigned nblocks,
+                                                    u64* __restrict__ out_count) {
+  __shared__ unsigned part[1024];
+  const unsigned per = (nblocks + 1023) / 1024;
+  unsigned sum = 0;
+  for (unsigned e = 0; e < per; ++e) {
+    const unsigned b = threadIdx.x * per + e;
+    if (b < nblocks) sum += block_counts[b];
+  }
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const unsigned y = threadIdx.x >= (unsigned)o ? part[threadIdx.x - o] : 0;
+    __syncthreads();
+    part[threadIdx.x] += y;
+    __syncthreads();
+  }
+  unsigned run = part[threadIdx.x] - sum;
+  for (unsigned e = 0; e < per; ++e) {
+    const unsigned b = threadIdx.x * per + e;
+    if (b < nblocks) {
+      const unsigned c = block_counts[b];
+      block_counts[b] = run;
+      run += c;
+    }
+  }
+  if (threadIdx.x == 1023) *out_count = part[1023];
+}
+
+__global__ void __launch_bounds__(kBitsThreads) k_bits_write(const uint32_t* __restrict__ bits, u64 words,
+                                                             const unsigned* __restrict__ block_offs,
+                                                             uint32_t* __restrict__ out_ids) {
+  // thread t owns words b0 + t*kBitsPer .. +kBitsPer-1 (contiguous, so the
+  // block-local exclusive scan over threads preserves id order)
+  const u64 w0 = blockIdx.x * kBitsBlock + (u64)threadIdx.x * kBitsPer;
+  uint32_t x[kBitsPer];
+  unsigned c = 0;
+#pragma unroll
+  for (int e = 0; e < kBitsPer; ++e) {
+    x[e] = (w0 + e < words) ? bits[w0 + e] : 0u;
+    c += __popc(x[e]);
+  }
+  __shared__ unsigned ws[kBitsThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) ws[warp] = incl;
+  __syncthreads();
+  unsigned wbase = 0;
+  for (int w = 0; w < warp; ++w) wbase += ws[w];
+  unsigned pos = block_offs[blockIdx.x] + wbase + incl - c;
+#pragma unroll
+  for (int e = 0; e < kBitsPer; ++e) {
+    uint32_t v = x[e];
+    while (v) {
+      const int b = __ffs(v) - 1;
+      v &= v - 1;
+      out_ids[pos++] = (uint32_t)((w0 + e) * 32 + b);
     }
   }
 }

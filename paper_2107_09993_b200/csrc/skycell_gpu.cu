@@ -26,17 +26,12 @@ using sk::u64;
 namespace {
 
 constexpr int kMaxLayers = 64;
-constexpr int kMaxLevels = 16;
 
 struct DevCounters {
   u64 nonfinite;
   u64 s1, s2, examined;
   u64 zero;
-  u64 m, xs, nf;
-  u64 zmid[kMaxLevels];
-  u64 znext[kMaxLevels];
-  u64 szmid[kMaxLevels];
-  u64 sznext[kMaxLevels];
+  u64 m, xs, xs_kept, nf, fs, fin, s1_kept, s2_kept;
   u64 cand[kMaxLayers];
   u64 key[kMaxLayers];
 };
@@ -79,14 +74,11 @@ struct skycell_gpu_ctx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   DevBuf reset, slabs, H, table, table2, table_s, staging;
-  DevBuf smp_rows, smp_ids, smp_fsum, f_rows, f_fsum;
+  DevBuf smp_rows, smp_ids, smp_fsum, f_rows, f_fsum, f_lists, f_offs, lists, ids_dev;
   DevBuf s1_rows, s1_ids, s2_rows, s2_ids, s2_fsum, flags;
-  DevBuf z_rows[2], z_ids[2], z_fsum[2];
   DevCounters* host_ctr = nullptr;  // pinned
   cudaEvent_t ev[8] = {};
   u64 launches = 0;
-  int result_buf = 0;     // z buffer holding the last query's ids
-  int result_level = 0;   // level whose znext counter is the skyline size
 };
 
 namespace {
@@ -107,9 +99,6 @@ struct Carver {
   }
 };
 
-struct Slot {
-  size_t claim_off, status_off;
-};
 
 // Validation in the reference's order: normalize() first (dataset.cpp:23-24),
 // then the grid budget (grid.cpp:38-43).
@@ -141,14 +130,10 @@ int default_rho(u64 n, int d) {
   return std::max(1, std::min(6, (bw - 1) / d));
 }
 
-template <typename TIn, typename TOut, bool IDENT>
-struct Pipeline;
 
 // ------------------------------------------------------------------ config
-constexpr int kStreamThreads = 512;
+constexpr int kStreamThreads = 256;
 constexpr int kThreads = 256;
-constexpr u64 kLevel0 = 4096;
-constexpr int kLevelGrowthLog2 = 4;
 
 template <typename T, int D>
 constexpr int ppt_for() {
@@ -165,6 +150,7 @@ struct Query {
   bool ident;
   sk::Norm nm;
   const void* dev_coords;  // device-resident input (user's or staged)
+  uint32_t* ids_dev;       // caller's device output buffer, or nullptr (use ctx->ids_dev)
   bool in_f32;
   bool out_f32;
   skycell_gpu_stats* stats;
@@ -196,102 +182,24 @@ void launch_count(skycell_gpu_ctx* ctx, cudaStream_t s, const uint32_t* bits, in
   ++ctx->launches;
 }
 
-// Per-query device bookkeeping carved out of one zeroed region.
-struct Layout {
-  Carver cv;
-  size_t o_ctr = 0;
-};
-
-// Block-recursive exact sort-first pass over src (ascending ids) -- refine.cpp:
-// 31-59 applied as in phase 2 (refine.cpp:98-99):
-//   Z_0 = src[0, b0);  F_0 = {p in Z_0 : no q in Z_0 precedes and dominates p}
-//   Z_k = F_{k-1} ++ {p in src[b_{k-1}, b_k) : no f in F_{k-1}[:f_max] precedes
-//         and dominates p};  F_k = skyline of Z_k
-// A point removed by a filter point is removed by the reference too, and every
-// dominator of a surviving point that the reference would use is itself in
-// Z_k (minimal-key argument), so F_last is exactly the
-// reference's output.  Returns the z buffer index holding F_last; *count_out
-// points at its device-side size.
-struct LevelSlots {
-  std::vector<Slot> filter, compact;
-};
-
+// Exact sort-first pass (refine.cpp:31-59 as applied in phase 2, :98-99) over
+// a point set given as slots (ids == kNoId marks an empty slot): per-dimension
+// column lists, then the list-pruned dominance test; flags[i] = 1 for members
+// of the result.
 template <typename TOut, int D>
-int run_levels(skycell_gpu_ctx* ctx, cudaStream_t s, char* R, DevCounters* ctr, const void* src_rows,
-               const uint32_t* src_ids, const u64* src_fsum, const u64* src_count, const std::vector<u64>& bounds,
-               const LevelSlots& slots, u64* zmid, u64* znext, int f_max, size_t smem_f, const u64** count_out) {
-  constexpr int PPTc = ppt_for<TOut, D>();
-  constexpr u64 TILEc = (u64)kThreads * PPTc;
-  constexpr int QCHUNK = 512;
+void run_exact(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint32_t* ids, const u64* fsum,
+               const u64* count, u64 cap, unsigned* hist, unsigned* cursor) {
   const int nsm = ctx->num_sms;
-  auto at = [&](size_t off) { return reinterpret_cast<void*>(R + off); };
-  auto kfilter = sk::k_filter_append<TOut, D, kThreads, PPTc>;
-  ck(cudaFuncSetAttribute(kfilter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f), "smem attr");
-  int cur = 0;
-  const u64* cnt_prev = &ctr->zero;
-  for (size_t k = 0; k < bounds.size(); ++k) {
-    const u64 b0 = k == 0 ? 0 : bounds[k - 1];
-    const u64 b1 = bounds[k];
-    sk::FilterParams pf{};
-    pf.src_rows = src_rows;
-    pf.src_ids = src_ids;
-    pf.src_fsum = src_fsum;
-    pf.src_count = src_count;
-    pf.begin = b0;
-    pf.end = b1;
-    pf.f_rows = ctx->z_rows[cur].p;
-    pf.f_ids = static_cast<const uint32_t*>(ctx->z_ids[cur].p);
-    pf.f_fsum = static_cast<const u64*>(ctx->z_fsum[cur].p);
-    pf.f_count = cnt_prev;
-    pf.f_max = (uint32_t)f_max;
-    pf.dst_rows = ctx->z_rows[cur].p;
-    pf.dst_ids = static_cast<uint32_t*>(ctx->z_ids[cur].p);
-    pf.dst_fsum = static_cast<u64*>(ctx->z_fsum[cur].p);
-    pf.dst_count_in = cnt_prev;
-    pf.dst_count_out = &zmid[k];
-    pf.status = static_cast<u64*>(at(slots.filter[k].status_off));
-    pf.claim = static_cast<u64*>(at(slots.filter[k].claim_off));
-    const u64 span = b1 - b0;
-    const unsigned gf = (unsigned)std::max<u64>(1, std::min<u64>((span + TILEc - 1) / TILEc, (u64)nsm * 2));
-    kfilter<<<gf, kThreads, smem_f, s>>>(pf);
-
-    const u64 zmax = b1;
-    ck(cudaMemsetAsync(ctx->flags.p, 1, zmax, s), "flags");
-    dim3 ga((unsigned)std::max<u64>(1, std::min<u64>((zmax + kThreads - 1) / kThreads, 128)),
-            (unsigned)std::max<u64>(1, std::min<u64>((zmax + QCHUNK - 1) / QCHUNK, 32)));
-    sk::k_allpairs<TOut, D, kThreads, QCHUNK><<<ga, kThreads, 0, s>>>(
-        static_cast<const TOut*>(ctx->z_rows[cur].p), static_cast<const uint32_t*>(ctx->z_ids[cur].p),
-        static_cast<const u64*>(ctx->z_fsum[cur].p), &zmid[k], static_cast<uint8_t*>(ctx->flags.p));
-
-    sk::CompactParams pk{};
-    pk.src_rows = ctx->z_rows[cur].p;
-    pk.src_ids = static_cast<const uint32_t*>(ctx->z_ids[cur].p);
-    pk.src_fsum = static_cast<const u64*>(ctx->z_fsum[cur].p);
-    pk.count = &zmid[k];
-    pk.flag = static_cast<const uint8_t*>(ctx->flags.p);
-    pk.dst_rows = ctx->z_rows[cur ^ 1].p;
-    pk.dst_ids = static_cast<uint32_t*>(ctx->z_ids[cur ^ 1].p);
-    pk.dst_fsum = static_cast<u64*>(ctx->z_fsum[cur ^ 1].p);
-    pk.dst_count = &znext[k];
-    pk.status = static_cast<u64*>(at(slots.compact[k].status_off));
-    pk.claim = static_cast<u64*>(at(slots.compact[k].claim_off));
-    const unsigned gk = (unsigned)std::max<u64>(1, std::min<u64>((zmax + TILEc - 1) / TILEc, (u64)nsm * 4));
-    sk::k_compact<TOut, D, kThreads, PPTc><<<gk, kThreads, 0, s>>>(pk);
-    ctx->launches += 3;
-    cur ^= 1;
-    cnt_prev = &znext[k];
-  }
-  *count_out = cnt_prev;
-  return cur;
-}
-
-std::vector<u64> level_bounds(u64 n) {
-  std::vector<u64> b;
-  for (u64 x = kLevel0;; x <<= kLevelGrowthLog2) {
-    b.push_back(std::min(x, n));
-    if (x >= n) break;
-  }
-  return b;
+  const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((cap + 255) / 256, (u64)nsm * 8));
+  const TOut* trows = static_cast<const TOut*>(rows);
+  uint32_t* lists = static_cast<uint32_t*>(ctx->lists.p);
+  sk::k_list_hist<TOut, D><<<g, 256, 0, s>>>(trows, ids, count, hist);
+  sk::k_list_scan<<<D, 1024, 0, s>>>(hist, cursor);
+  sk::k_list_scatter<TOut, D><<<g, 256, 0, s>>>(trows, ids, count, cursor, lists, cap);
+  const unsigned gw = (unsigned)std::max<u64>(1, std::min<u64>((cap * 32 + 255) / 256, (u64)nsm * 8));
+  sk::k_allpairs_lists<TOut, D><<<gw, 256, 0, s>>>(trows, ids, fsum, count, lists, hist, cap,
+                                                   static_cast<uint8_t*>(ctx->flags.p));
+  ctx->launches += 4;
 }
 
 template <typename TIn, typename TOut, bool IDENT, int D>
@@ -320,30 +228,30 @@ void run_pipeline(Query& q) {
   const size_t tt = wide ? 4 : 1;
   const u64 table_entries = 1ull << (u64)(rho * (D - 1));
 
-  // ---- K1 geometry
-  constexpr int PPT1 = ppt_for<TIn, D>();
-  constexpr u64 TILE1 = (u64)kStreamThreads * PPT1;
-  const u64 tiles1 = (n + TILE1 - 1) / TILE1;
-  const size_t smem1 = (size_t)lo_words * 4 + ((h_entries + 15) & ~15u) + (PPT1 * (kStreamThreads / 32) + 1) * 4 + 16;
+  // ---- K1 geometry: persistent warps over static round-robin warp tiles
+  constexpr int PPT1 = (ppt_for<TIn, D>() + 1) / 2;
+  const size_t smem1 = (size_t)lo_words * 4 + ((h_entries + 15) & ~15u) + 16;
   auto kstream = sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1>;
   ck(cudaFuncSetAttribute(kstream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1), "smem attr");
   int occ_blocks = 0;
   ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_blocks, kstream, kStreamThreads, smem1), "occupancy");
   occ_blocks = std::max(1, occ_blocks);
-  const int grid1 = (int)std::max<u64>(1, std::min<u64>(tiles1, (u64)nsm * occ_blocks));
+  const u64 wtiles = (n + 32 * PPT1 - 1) / (32 * PPT1);
+  const int grid1 = (int)std::max<u64>(1, std::min<u64>((wtiles + 7) / 8, (u64)nsm * occ_blocks));
+  constexpr unsigned kChunk1 = 256, kChunk4 = 64;
+  const u64 slack1 = (u64)grid1 * (kStreamThreads / 32) * kChunk1;
+  const u64 cap1 = n + slack1;
 
-  // ---- K4/K5 geometry
-  constexpr int PPTc = ppt_for<TOut, D>();
-  constexpr u64 TILEc = (u64)kThreads * PPTc;
-  const u64 tilesc = (n + TILEc - 1) / TILEc + 1;
-  const std::vector<u64> bounds = level_bounds(n);
-  const std::vector<u64> sbounds = level_bounds(m);
-  if (bounds.size() > (size_t)kMaxLevels) throw CudaFail{cudaErrorInvalidValue, "too many levels"};
-  const size_t rec = D * sizeof(TOut) + 12;
-  const int f_max = (int)std::min<u64>(4096, (64 * 1024) / rec);
-  const size_t smem_f = (((u64)f_max * D * sizeof(TOut) + 15) & ~15ull) + (u64)f_max * 12;
+  // ---- K4 geometry
+  const int grid4 = nsm * 4;
+  const u64 slack4 = (u64)grid4 * (kThreads / 32) * kChunk4;
+  const u64 cap4 = std::max(cap1, m) + slack4;
   const int pf_max = (int)std::min<u64>(1024, (32 * 1024) / (D * sizeof(TOut) + 8));  // K4 point filter
-  const size_t smem_pf = (((u64)pf_max * D * sizeof(TOut) + 15) & ~15ull) + (u64)pf_max * 8;
+  const size_t smem_pf = (((u64)pf_max * D * sizeof(TOut) + 15) & ~15ull) + (u64)pf_max * 8 +
+                         (u64)D * pf_max * 2 + (u64)D * (sk::kListCols + 1) * 2 + 16;
+  const size_t list_words = (size_t)D * (sk::kListCols + 1);
+  const u64 id_words = (n + 31) / 32;
+  const unsigned bit_blocks = (unsigned)((id_words + sk::kBitsBlock - 1) / sk::kBitsBlock);
 
   // ---- zeroed region
   Carver cv;
@@ -352,24 +260,10 @@ void run_pipeline(Query& q) {
   for (int L = 1; L <= rho; ++L) o_occ[L] = cv.take(words_at(L) * 4);
   const size_t o_sla = cv.take(words_at(la) * 4);
   const size_t o_srho = test_b ? cv.take(words_at(rho) * 4) : 0;
-  auto slot = [&](u64 tiles) {
-    Slot sl;
-    sl.claim_off = cv.take(8);
-    sl.status_off = cv.take(tiles * 8);
-    return sl;
-  };
-  const Slot sl_stream = slot(tiles1 + 1);
-  const Slot sl_scand = slot((m + TILEc - 1) / TILEc + 1);
-  const Slot sl_cand = slot(tilesc);
-  LevelSlots sls, mls;
-  for (size_t k = 0; k < sbounds.size(); ++k) {
-    sls.filter.push_back(slot((m + TILEc - 1) / TILEc + 1));
-    sls.compact.push_back(slot((m + TILEc - 1) / TILEc + 1));
-  }
-  for (size_t k = 0; k < bounds.size(); ++k) {
-    mls.filter.push_back(slot(tilesc));
-    mls.compact.push_back(slot(tilesc));
-  }
+  const size_t o_shist = cv.take(list_words * 4), o_scur = cv.take(list_words * 4);
+  const size_t o_hist = cv.take(list_words * 4), o_cur = cv.take(list_words * 4);
+  const size_t o_idbits = cv.take(id_words * 4);
+  const size_t o_bcount = cv.take((size_t)bit_blocks * 4);
   ensure(ctx->reset, cv.off);
   char* R = static_cast<char*>(ctx->reset.p);
   auto at = [&](size_t off) { return reinterpret_cast<void*>(R + off); };
@@ -387,22 +281,21 @@ void run_pipeline(Query& q) {
   ensure(ctx->smp_fsum, m * 8);
   ensure(ctx->f_rows, (size_t)pf_max * D * sizeof(TOut));
   ensure(ctx->f_fsum, (size_t)pf_max * 8);
-  ensure(ctx->s1_rows, n * D * sizeof(TOut));
-  ensure(ctx->s1_ids, n * 4);
-  ensure(ctx->s2_rows, n * D * sizeof(TOut));
-  ensure(ctx->s2_ids, n * 4);
-  ensure(ctx->s2_fsum, n * 8);
-  ensure(ctx->flags, n);
-  for (int b = 0; b < 2; ++b) {
-    ensure(ctx->z_rows[b], n * D * sizeof(TOut));
-    ensure(ctx->z_ids[b], n * 4);
-    ensure(ctx->z_fsum[b], n * 8);
-  }
+  ensure(ctx->f_lists, (size_t)D * pf_max * 2);
+  ensure(ctx->f_offs, list_words * 2);
+  ensure(ctx->s1_rows, cap1 * D * sizeof(TOut));
+  ensure(ctx->s1_ids, cap1 * 4);
+  ensure(ctx->s2_rows, cap4 * D * sizeof(TOut));
+  ensure(ctx->s2_ids, cap4 * 4);
+  ensure(ctx->s2_fsum, cap4 * 8);
+  ensure(ctx->flags, cap4);
+  ensure(ctx->lists, (size_t)D * cap4 * 4);
+  ensure(ctx->ids_dev, n * 4);
 
   if (q.timed) ck(cudaEventRecord(ctx->ev[0], s), "event");
   ck(cudaMemsetAsync(ctx->reset.p, 0, cv.off, s), "memset");
 
-  // ---- K0: sample occupancy, filter tables, sample skyline
+  // ---- K0: sample occupancy, filter tables, sample skyline -> filter points F
   {
     sk::SampleParams sp{};
     sp.coords = q.dev_coords;
@@ -424,35 +317,33 @@ void run_pipeline(Query& q) {
       if (wide) launch_tables<uint32_t>(ctx, s, static_cast<uint32_t*>(at(o_srho)), rho, D, static_cast<uint32_t*>(ctx->table_s.p));
       else launch_tables<uint8_t>(ctx, s, static_cast<uint32_t*>(at(o_srho)), rho, D, static_cast<uint8_t*>(ctx->table_s.p));
     }
-    // sample points not strictly dominated at layer rho -> X (in the s2 buffers)
+    // sample points not strictly dominated at layer rho -> X (s2 buffers)
     sk::CandParams pc{};
     pc.rows = ctx->smp_rows.p;
     pc.ids = static_cast<const uint32_t*>(ctx->smp_ids.p);
-    pc.count = &ctr->m;
+    pc.count = nullptr;
+    pc.count_const = m;
     pc.rho = rho;
     pc.PM = test_b ? ctx->table_s.p : nullptr;
     pc.f_max = 0;
     pc.out_rows = ctx->s2_rows.p;
     pc.out_ids = static_cast<uint32_t*>(ctx->s2_ids.p);
     pc.out_fsum = static_cast<u64*>(ctx->s2_fsum.p);
-    pc.status = static_cast<u64*>(at(sl_scand.status_off));
-    pc.claim = static_cast<u64*>(at(sl_scand.claim_off));
-    pc.out_count = &ctr->xs;
+    pc.out_reserved = &ctr->xs;
+    pc.chunk = kChunk4;
+    pc.kept = &ctr->xs_kept;
     pc.examined = nullptr;
-    ctx->host_ctr->m = m;  // staged through pinned memory
-    ck(cudaMemcpyAsync(&ctr->m, &ctx->host_ctr->m, 8, cudaMemcpyHostToDevice, s), "m");
-    const unsigned gs = (unsigned)std::max<u64>(1, std::min<u64>((m + TILEc - 1) / TILEc, (u64)nsm * 4));
-    if (wide) sk::k_candidates<TOut, D, uint32_t, kThreads, PPTc><<<gs, kThreads, 0, s>>>(pc);
-    else sk::k_candidates<TOut, D, uint8_t, kThreads, PPTc><<<gs, kThreads, 0, s>>>(pc);
+    if (wide) sk::k_candidates<TOut, D, uint32_t, kThreads><<<grid4, kThreads, 16, s>>>(pc);
+    else sk::k_candidates<TOut, D, uint8_t, kThreads><<<grid4, kThreads, 16, s>>>(pc);
     ++ctx->launches;
-    const u64* fcount = nullptr;
-    const int fb = run_levels<TOut, D>(ctx, s, R, ctr, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
-                                       static_cast<const u64*>(ctx->s2_fsum.p), &ctr->xs, sbounds, sls, ctr->szmid,
-                                       ctr->sznext, f_max, smem_f, &fcount);
-    sk::k_strength_order<TOut, D><<<1, 1024, 0, s>>>(static_cast<const TOut*>(ctx->z_rows[fb].p),
-                                                     static_cast<const u64*>(ctx->z_fsum[fb].p), fcount,
-                                                     (uint32_t)pf_max, static_cast<TOut*>(ctx->f_rows.p),
-                                                     static_cast<u64*>(ctx->f_fsum.p), &ctr->nf);
+    run_exact<TOut, D>(ctx, s, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
+                       static_cast<const u64*>(ctx->s2_fsum.p), &ctr->xs, cap4, static_cast<unsigned*>(at(o_shist)),
+                       static_cast<unsigned*>(at(o_scur)));
+    sk::k_strength_order<TOut, D><<<1, 1024, 0, s>>>(
+        static_cast<const TOut*>(ctx->s2_rows.p), static_cast<const uint32_t*>(ctx->s2_ids.p),
+        static_cast<const uint8_t*>(ctx->flags.p), static_cast<const u64*>(ctx->s2_fsum.p), &ctr->xs,
+        (uint32_t)pf_max, static_cast<TOut*>(ctx->f_rows.p), static_cast<u64*>(ctx->f_fsum.p), &ctr->nf,
+        static_cast<uint16_t*>(ctx->f_lists.p), static_cast<uint16_t*>(ctx->f_offs.p));
     ++ctx->launches;
   }
 
@@ -473,9 +364,9 @@ void run_pipeline(Query& q) {
   p1.slabs = static_cast<uint32_t*>(ctx->slabs.p);
   p1.out_rows = ctx->s1_rows.p;
   p1.out_ids = static_cast<uint32_t*>(ctx->s1_ids.p);
-  p1.status = static_cast<u64*>(at(sl_stream.status_off));
-  p1.claim = static_cast<u64*>(at(sl_stream.claim_off));
-  p1.out_count = &ctr->s1;
+  p1.out_reserved = &ctr->s1;
+  p1.chunk = kChunk1;
+  p1.kept = &ctr->s1_kept;
   p1.nonfinite = &ctr->nonfinite;
   if (q.timed) ck(cudaEventRecord(ctx->ev[4], s), "event");
   kstream<<<grid1, kStreamThreads, smem1, s>>>(p1);
@@ -529,31 +420,44 @@ void run_pipeline(Query& q) {
     pc.f_fsum = static_cast<const u64*>(ctx->f_fsum.p);
     pc.f_count = &ctr->nf;
     pc.f_max = (uint32_t)pf_max;
+    pc.f_lists = static_cast<const uint16_t*>(ctx->f_lists.p);
+    pc.f_offs = static_cast<const uint16_t*>(ctx->f_offs.p);
     pc.out_rows = ctx->s2_rows.p;
     pc.out_ids = static_cast<uint32_t*>(ctx->s2_ids.p);
     pc.out_fsum = static_cast<u64*>(ctx->s2_fsum.p);
-    pc.status = static_cast<u64*>(at(sl_cand.status_off));
-    pc.claim = static_cast<u64*>(at(sl_cand.claim_off));
-    pc.out_count = &ctr->s2;
+    pc.out_reserved = &ctr->s2;
+    pc.chunk = kChunk4;
+    pc.kept = &ctr->s2_kept;
     pc.examined = &ctr->examined;
-    const unsigned gc = (unsigned)std::max<u64>(1, std::min<u64>(tilesc, (u64)nsm * 4));
     if (wide) {
-      auto kc = sk::k_candidates<TOut, D, uint32_t, kThreads, PPTc>;
+      auto kc = sk::k_candidates<TOut, D, uint32_t, kThreads>;
       ck(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pf), "smem attr");
-      kc<<<gc, kThreads, smem_pf, s>>>(pc);
+      kc<<<grid4, kThreads, smem_pf, s>>>(pc);
     } else {
-      auto kc = sk::k_candidates<TOut, D, uint8_t, kThreads, PPTc>;
+      auto kc = sk::k_candidates<TOut, D, uint8_t, kThreads>;
       ck(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pf), "smem attr");
-      kc<<<gc, kThreads, smem_pf, s>>>(pc);
+      kc<<<grid4, kThreads, smem_pf, s>>>(pc);
     }
     ++ctx->launches;
   }
 
   // ---- K5: exact sort-first pass over the remaining points
-  const u64* final_count = nullptr;
-  const int cur = run_levels<TOut, D>(ctx, s, R, ctr, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
-                                      static_cast<const u64*>(ctx->s2_fsum.p), &ctr->s2, bounds, mls, ctr->zmid,
-                                      ctr->znext, f_max, smem_f, &final_count);
+  run_exact<TOut, D>(ctx, s, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
+                     static_cast<const u64*>(ctx->s2_fsum.p), &ctr->s2, cap4, static_cast<unsigned*>(at(o_hist)),
+                     static_cast<unsigned*>(at(o_cur)));
+  // ---- K6: ids in ascending order through the id bitmap
+  {
+    uint32_t* idbits = static_cast<uint32_t*>(at(o_idbits));
+    unsigned* bcount = static_cast<unsigned*>(at(o_bcount));
+    const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((cap4 + 255) / 256, (u64)nsm * 8));
+    sk::k_mark_ids<<<g, 256, 0, s>>>(static_cast<const uint32_t*>(ctx->s2_ids.p),
+                                     static_cast<const uint8_t*>(ctx->flags.p), &ctr->s2, idbits);
+    sk::k_bits_count<<<bit_blocks, sk::kBitsThreads, 0, s>>>(idbits, id_words, bcount);
+    sk::k_bits_scan<<<1, 1024, 0, s>>>(bcount, bit_blocks, &ctr->fin);
+    sk::k_bits_write<<<bit_blocks, sk::kBitsThreads, 0, s>>>(idbits, id_words, bcount,
+                                                              q.ids_dev ? q.ids_dev : static_cast<uint32_t*>(ctx->ids_dev.p));
+    ctx->launches += 4;
+  }
   ck(cudaGetLastError(), "kernel launch");
   if (q.timed) ck(cudaEventRecord(ctx->ev[3], s), "event");
   ck(cudaStreamWaitEvent(s, ctx->ev_join, 0), "join");
@@ -561,8 +465,6 @@ void run_pipeline(Query& q) {
   // ---- results
   ck(cudaMemcpyAsync(ctx->host_ctr, ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s), "counters D2H");
   ck(cudaStreamSynchronize(s), "query");
-  ctx->result_buf = cur;
-  ctx->result_level = (int)bounds.size() - 1;
   const DevCounters& hc = *ctx->host_ctr;
   if (q.stats) {
     q.stats->n_layers = rho;
@@ -571,8 +473,8 @@ void run_pipeline(Query& q) {
       q.stats->candidates[L - 1] = (q.mode == SKYCELL_SEQUENTIAL && L != rho) ? -1 : (int64_t)hc.cand[L - 1];
     }
     q.stats->points_examined = hc.examined;
-    q.stats->survivors_stream = hc.s1;
-    q.stats->survivors_filter = hc.s2;
+    q.stats->survivors_stream = hc.s1_kept;
+    q.stats->survivors_filter = hc.s2_kept;
   }
 }
 
@@ -647,6 +549,11 @@ int run_query(skycell_gpu_ctx* ctx, const TIn* coords, u64 n, int d, const doubl
     q.stats = stats;
     q.timed = stats != nullptr;
     q.dev_coords = dev_coords;
+    cudaPointerAttributes oattr{};
+    const bool out_dev = cudaPointerGetAttributes(&oattr, ids_out) == cudaSuccess &&
+                         (oattr.type == cudaMemoryTypeDevice || oattr.type == cudaMemoryTypeManaged);
+    cudaGetLastError();
+    q.ids_dev = out_dev ? ids_out : nullptr;
     // scale[k] = range > 0 ? 1/range : 0, dataset.cpp:32-36 (host, FP64).
     bool ident = true;
     for (int k = 0; k < d; ++k) {
@@ -681,18 +588,12 @@ int run_query(skycell_gpu_ctx* ctx, const TIn* coords, u64 n, int d, const doubl
       put_err(err, err_len, "normalize: non-finite coordinate in record " + std::to_string(~hc.nonfinite));
       return SKYCELL_INPUT;
     }
-    const u64 count = hc.znext[ctx->result_level];  // K5's last level
-    const int cur = ctx->result_buf;
+    const u64 count = hc.fin;
     *n_out = count;
-    cudaPointerAttributes oattr{};
-    const bool out_dev = cudaPointerGetAttributes(&oattr, ids_out) == cudaSuccess &&
-                         (oattr.type == cudaMemoryTypeDevice || oattr.type == cudaMemoryTypeManaged);
-    cudaGetLastError();
-    if (count)
-      ck(cudaMemcpyAsync(ids_out, ctx->z_ids[cur].p, count * 4, out_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
-                         s),
-         "ids copy");
-    ck(cudaStreamSynchronize(s), "sync");
+    if (count && !out_dev) {
+      ck(cudaMemcpyAsync(ids_out, ctx->ids_dev.p, count * 4, cudaMemcpyDeviceToHost, s), "ids copy");
+      ck(cudaStreamSynchronize(s), "sync");
+    }
     if (stats) {
       float a = 0, b = 0, c = 0;
       cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
@@ -753,9 +654,9 @@ void skycell_gpu_destroy(skycell_gpu_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   DevBuf* bufs[] = {&ctx->reset, &ctx->slabs, &ctx->H, &ctx->table, &ctx->table2, &ctx->table_s, &ctx->staging,
-                    &ctx->smp_rows, &ctx->smp_ids, &ctx->smp_fsum, &ctx->f_rows, &ctx->f_fsum, &ctx->s1_rows, &ctx->s1_ids,
-                    &ctx->s2_rows, &ctx->s2_ids, &ctx->s2_fsum, &ctx->flags, &ctx->z_rows[0], &ctx->z_rows[1],
-                    &ctx->z_ids[0], &ctx->z_ids[1], &ctx->z_fsum[0], &ctx->z_fsum[1]};
+                    &ctx->smp_rows, &ctx->smp_ids, &ctx->smp_fsum, &ctx->f_rows, &ctx->f_fsum, &ctx->f_lists, &ctx->f_offs,
+                    &ctx->lists, &ctx->ids_dev, &ctx->s1_rows, &ctx->s1_ids,
+                    &ctx->s2_rows, &ctx->s2_ids, &ctx->s2_fsum, &ctx->flags};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (auto& e : ctx->ev)
