@@ -556,6 +556,10 @@ __global__ void k_downsample(const uint32_t* __restrict__ src, int L, int d, u64
 // and therefore a tiny prefix.
 constexpr int kListLevel = 10;
 constexpr int kListCols = 1 << kListLevel;
+// Point-set lists additionally order each column by FP64 sum (64 buckets over
+// [0, d)), so the strongest candidate dominators of a column come first.
+constexpr int kSumBuckets = 64;
+constexpr int kListBins = kListCols * kSumBuckets;
 __device__ __forceinline__ int list_col(float v) { return cell_col(v, (float)kListCols, kListCols - 1); }
 __device__ __forceinline__ int list_col(double v) { return cell_col(v, (double)kListCols, kListCols - 1); }
 
@@ -650,25 +654,40 @@ __global__ void __launch_bounds__(THREADS) k_candidates(CandParams p) {
         for (uint32_t f = 0; f < head && !dom; ++f)
           dom = f_sum[f] < ps && dominates<T, D>(f_rows + (u64)f * D, v);
       }
-      if (cand && nf && !dom) {
-        // a dominator f has col_k(f) <= col_k(p) in every dimension: scan
-        // the shortest such column prefix of the per-dimension lists
-        int bk = 0;
-        unsigned end = 0xffffffffu;
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-          const unsigned e = f_off[k * (kListCols + 1) + list_col(v[k]) + 1];
-          if (e < end) { end = e; bk = k; }
-        }
-        const uint16_t* lst = f_list + (u64)bk * fm;
-        for (unsigned e = 0; e < end && !dom; ++e) {
-          const unsigned f = lst[e];
-          dom = f_sum[f] < ps && dominates<T, D>(f_rows + (u64)f * D, v);
-        }
-      }
       keep = cand && !dom;
-      kept += keep;
     }
+    // Points the 32 strongest filter points missed: the warp scans each one's
+    // shortest column prefix of F cooperatively, 32 entries per step
+    // (a dominator f has col_k(f) <= col_k(p) in every dimension).
+    unsigned pend = __ballot_sync(kFull, keep && nf > 32);
+    while (pend) {
+      const int src = __ffs(pend) - 1;
+      pend &= pend - 1;
+      T pv[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) pv[k] = __shfl_sync(kFull, v[k], src);
+      const u64 pps = __shfl_sync(kFull, ps, src);
+      int bk = 0;
+      unsigned end = 0xffffffffu;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const unsigned e = f_off[k * (kListCols + 1) + list_col(pv[k]) + 1];
+        if (e < end) { end = e; bk = k; }
+      }
+      const uint16_t* lst = f_list + (u64)bk * fm;
+      bool found = false;
+      for (unsigned base = 0; base < end && !found; base += 32) {
+        const unsigned e = base + lane;
+        bool d_l = false;
+        if (e < end) {
+          const unsigned f = lst[e];
+          d_l = f_sum[f] < pps && dominates<T, D>(f_rows + (u64)f * D, pv);
+        }
+        found = __any_sync(kFull, d_l);
+      }
+      if (found && lane == src) keep = false;
+    }
+    kept += keep;
     if (__any_sync(kFull, keep)) {
       const u64 o = warp_reserve(wo, keep, p.out_reserved, stamp);
       if (keep) {
@@ -690,25 +709,52 @@ __global__ void __launch_bounds__(THREADS) k_candidates(CandParams p) {
   }
 }
 
+// Compact the members (flag set, id != kNoId) of a slot array: rows and sums.
+template <typename T, int D>
+__global__ void k_compact_members(const T* __restrict__ rows, const uint32_t* __restrict__ ids,
+                                  const uint8_t* __restrict__ flag, const u64* __restrict__ fsum,
+                                  const u64* __restrict__ count, T* __restrict__ out_rows, u64* __restrict__ out_fsum,
+                                  u64* __restrict__ out_count) {
+  const u64 n = *count;
+  const int lane = threadIdx.x & 31;
+  for (u64 wb = ((blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5) * 32; wb < n;
+       wb += ((u64)gridDim.x * blockDim.x >> 5) * 32) {
+    const u64 i = wb + lane;
+    const bool live = i < n && ids[i] != kNoId && flag[i];
+    const unsigned m = __ballot_sync(kFull, live);
+    if (!m) continue;
+    u64 b = 0;
+    if (lane == 0) b = atomicAdd(out_count, (u64)__popc(m));
+    b = __shfl_sync(kFull, b, 0);
+    if (live) {
+      const u64 o = b + __popc(m & ((1u << lane) - 1));
+      T v[D];
+      load_row_cached<T, D>(rows, i, v);
+      store_row<T, D>(out_rows, o, v);
+      out_fsum[o] = fsum[i];
+    }
+  }
+}
+
 // Single CTA: order a point set by descending "strength" -- the volume it
 // dominates in the unit cube, prod(1 - u_k) -- in 64 log-spaced buckets, and
 // keep the first f_max.  Strong filter points first make the early exit in
 // k_candidates happen after ~1 test for most points (median 1, p90 18 at the
-// headline config).
+// headline config).  Then, per dimension, a stable column
+// order of the kept points (bitonic sort of (column, strength rank) keys), so
+// each column prefix is scanned strongest first.
 template <typename T, int D>
-__global__ void __launch_bounds__(1024) k_strength_order(const T* __restrict__ rows, const uint32_t* __restrict__ ids,
-                                                          const uint8_t* __restrict__ flag,
-                                                          const u64* __restrict__ fsum,
+__global__ void __launch_bounds__(1024) k_strength_order(const T* __restrict__ rows, const u64* __restrict__ fsum,
                                                           const u64* __restrict__ count, uint32_t f_max,
                                                           T* __restrict__ out_rows, u64* __restrict__ out_fsum,
                                                           u64* __restrict__ out_count, uint16_t* __restrict__ f_lists,
                                                           uint16_t* __restrict__ f_offs) {
   __shared__ unsigned hist[65];
   __shared__ unsigned offs[65];
-  __shared__ unsigned total;
-  const u64 slots = *count;
+  __shared__ uint32_t keys[1024];
+  __shared__ unsigned cnt[kListCols + 1];
+  const u64 n = *count;
   if (threadIdx.x < 65) hist[threadIdx.x] = 0;
-  if (threadIdx.x == 0) total = 0;
   __syncthreads();
   auto bucket = [&](u64 i) {
     double vol = 1.0;
@@ -717,14 +763,8 @@ __global__ void __launch_bounds__(1024) k_strength_order(const T* __restrict__ r
     const double l = vol > 0 ? -log2(vol) * 2.0 : 1e9;
     return (int)(l < 63.0 ? l : 63.0);
   };
-  auto live = [&](u64 i) { return ids[i] != kNoId && flag[i]; };
-  for (u64 i = threadIdx.x; i < slots; i += blockDim.x)
-    if (live(i)) {
-      atomicAdd(&hist[bucket(i)], 1u);
-      atomicAdd(&total, 1u);
-    }
+  for (u64 i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&hist[bucket(i)], 1u);
   __syncthreads();
-  const u64 n = total;
   if (threadIdx.x == 0) {
     unsigned run = 0;
     for (int b = 0; b < 64; ++b) {
@@ -734,8 +774,7 @@ __global__ void __launch_bounds__(1024) k_strength_order(const T* __restrict__ r
     *out_count = n < f_max ? n : f_max;
   }
   __syncthreads();
-  for (u64 i = threadIdx.x; i < slots; i += blockDim.x) {
-    if (!live(i)) continue;
+  for (u64 i = threadIdx.x; i < n; i += blockDim.x) {
     const unsigned o = atomicAdd(&offs[bucket(i)], 1u);
     if (o < f_max) {
 #pragma unroll
@@ -743,27 +782,39 @@ __global__ void __launch_bounds__(1024) k_strength_order(const T* __restrict__ r
       out_fsum[o] = fsum[i];
     }
   }
-  // per-dimension column lists of the kept filter points
-  __shared__ unsigned cnt[kListCols + 1];
   __syncthreads();
   const unsigned nf = (unsigned)(n < f_max ? n : f_max);
   for (int k = 0; k < D; ++k) {
-    for (unsigned c = threadIdx.x; c <= kListCols; c += blockDim.x) cnt[c] = 0;
+    // keys = column << 10 | strength rank, padded with 0xffffffff; f_max <= 1024
+    const unsigned t = threadIdx.x;
+    keys[t] = t < nf ? ((uint32_t)list_col(out_rows[(u64)t * D + k]) << 10) | t : 0xffffffffu;
+    for (unsigned c = t; c <= kListCols; c += blockDim.x) cnt[c] = 0;
     __syncthreads();
-    for (unsigned f = threadIdx.x; f < nf; f += blockDim.x) atomicAdd(&cnt[list_col(out_rows[(u64)f * D + k]) + 1], 1u);
+    for (unsigned size = 2; size <= 1024; size <<= 1) {
+      for (unsigned stride = size >> 1; stride > 0; stride >>= 1) {
+        const unsigned partner = t ^ stride;
+        if (partner > t) {
+          const bool up = (t & size) == 0;
+          const uint32_t a = keys[t], b = keys[partner];
+          if ((a > b) == up) {
+            keys[t] = b;
+            keys[partner] = a;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (t < nf) {
+      f_lists[(u64)k * f_max + t] = (uint16_t)(keys[t] & 1023);
+      atomicAdd(&cnt[(keys[t] >> 10) + 1], 1u);
+    }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (t == 0) {
       unsigned run = 0;
       for (int c = 0; c <= kListCols; ++c) {
         run += cnt[c];
-        cnt[c] = run;  // cnt[c] = number of points with column < c
-        f_offs[k * (kListCols + 1) + c] = (uint16_t)run;
+        f_offs[k * (kListCols + 1) + c] = (uint16_t)run;  // points with column < c
       }
-    }
-    __syncthreads();
-    for (unsigned f = threadIdx.x; f < nf; f += blockDim.x) {
-      const unsigned pos = atomicAdd(&cnt[list_col(out_rows[(u64)f * D + k])], 1u);
-      f_lists[(u64)k * f_max + pos] = (uint16_t)f;
     }
     __syncthreads();
   }
@@ -773,63 +824,83 @@ __global__ void __launch_bounds__(1024) k_strength_order(const T* __restrict__ r
 // Per-dimension column lists of a point set with a device-side count:
 // histogram, exclusive scan, scatter (non-stable within a column; the order
 // inside a column only affects how soon a dominator is met, never the result).
+template <int D>
+__device__ __forceinline__ int sum_bucket(u64 fsum_bits) {
+  const double f = __longlong_as_double((long long)fsum_bits);
+  if (!(f > 0.0)) return 0;  // also NaN sums of non-finite records (reported separately)
+  const int b = (int)(f * (kSumBuckets / (double)D));
+  return b < kSumBuckets - 1 ? b : kSumBuckets - 1;
+}
+
 template <typename T, int D>
-__global__ void k_list_hist(const T* __restrict__ rows, const uint32_t* __restrict__ ids, const u64* __restrict__ count,
-                            unsigned* __restrict__ hist) {
+__global__ void k_list_hist(const T* __restrict__ rows, const uint32_t* __restrict__ ids, const u64* __restrict__ fsum,
+                            const u64* __restrict__ count, unsigned* __restrict__ hist) {
   const u64 n = *count;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
     if (ids[i] == kNoId) continue;
     T v[D];
     load_row_cached<T, D>(rows, i, v);
+    const int sb = sum_bucket<D>(fsum[i]);
 #pragma unroll
-    for (int k = 0; k < D; ++k) atomicAdd(&hist[k * (kListCols + 1) + list_col(v[k]) + 1], 1u);
+    for (int k = 0; k < D; ++k) atomicAdd(&hist[k * (kListBins + 1) + list_col(v[k]) * kSumBuckets + sb + 1], 1u);
   }
 }
 
-// One CTA per dimension: inclusive scan of (count shifted by one) = column starts.
+// One CTA per dimension: inclusive scan of the shifted histogram = bin starts.
+// Chunks of 1024 bins, coalesced, with a running total.
 __global__ void __launch_bounds__(1024) k_list_scan(unsigned* __restrict__ hist, unsigned* __restrict__ cursor) {
-  __shared__ unsigned part[1024];
-  unsigned* h = hist + blockIdx.x * (kListCols + 1);
-  constexpr int PER = (kListCols + 1 + 1023) / 1024;
-  unsigned loc[PER], sum = 0;
-#pragma unroll
-  for (int e = 0; e < PER; ++e) {
-    const int c = threadIdx.x * PER + e;
-    loc[e] = c <= kListCols ? h[c] : 0;
-    sum += loc[e];
-  }
-  part[threadIdx.x] = sum;
+  __shared__ unsigned warp_tot[32];
+  __shared__ unsigned carry;
+  unsigned* h = hist + blockIdx.x * (u64)(kListBins + 1);
+  unsigned* cur = cursor + blockIdx.x * (u64)(kListBins + 1);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {
-    const unsigned y = threadIdx.x >= (unsigned)o ? part[threadIdx.x - o] : 0;
-    __syncthreads();
-    part[threadIdx.x] += y;
-    __syncthreads();
-  }
-  unsigned run = part[threadIdx.x] - sum;
+  for (int c0 = 0; c0 <= kListBins; c0 += 1024) {
+    const int c = c0 + threadIdx.x;
+    const unsigned v = c <= kListBins ? h[c] : 0;
+    unsigned incl = v;
 #pragma unroll
-  for (int e = 0; e < PER; ++e) {
-    const int c = threadIdx.x * PER + e;
-    run += loc[e];
-    if (c <= kListCols) {
-      h[c] = run;
-      cursor[blockIdx.x * (kListCols + 1) + c] = run;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
     }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      unsigned t = warp_tot[lane], ti = t;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(kFull, ti, o);
+        if (lane >= o) ti += y;
+      }
+      warp_tot[lane] = ti - t;
+    }
+    __syncthreads();
+    const unsigned out = carry + warp_tot[warp] + incl;
+    if (c <= kListBins) {
+      h[c] = out;
+      cur[c] = out;
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = out;
+    __syncthreads();
   }
 }
 
 template <typename T, int D>
 __global__ void k_list_scatter(const T* __restrict__ rows, const uint32_t* __restrict__ ids,
-                               const u64* __restrict__ count, unsigned* __restrict__ cursor,
-                               uint32_t* __restrict__ lists, u64 cap) {
+                               const u64* __restrict__ fsum, const u64* __restrict__ count,
+                               unsigned* __restrict__ cursor, uint32_t* __restrict__ lists, u64 cap) {
   const u64 n = *count;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
     if (ids[i] == kNoId) continue;
     T v[D];
     load_row_cached<T, D>(rows, i, v);
+    const int sb = sum_bucket<D>(fsum[i]);
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-      const unsigned pos = atomicAdd(&cursor[k * (kListCols + 1) + list_col(v[k])], 1u);
+      const unsigned pos = atomicAdd(&cursor[k * (kListBins + 1) + list_col(v[k]) * kSumBuckets + sb], 1u);
       lists[(u64)k * cap + pos] = (uint32_t)i;
     }
   }
@@ -862,25 +933,33 @@ __global__ void __launch_bounds__(256) k_allpairs_lists(const T* __restrict__ ro
     unsigned end = 0xffffffffu;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-      const unsigned e = __ldg(offs + k * (kListCols + 1) + list_col(v[k]) + 1);
+      const unsigned e = __ldg(offs + k * (kListBins + 1) + (list_col(v[k]) + 1) * kSumBuckets);
       if (e < end) { end = e; bk = k; }
     }
+    // per column c <= col(p): only sum buckets <= bucket(p) can hold a
+    // dominator (sums are monotone under dominance)
     const uint32_t* lst = lists + (u64)bk * cap;
+    const unsigned* ob = offs + bk * (kListBins + 1);
+    const int pc = list_col(v[bk]);
+    const int sb = sum_bucket<D>(ps);
     bool dom = false;
-    for (unsigned base = 0; base < end; base += 32) {
-      const unsigned e = base + lane;
-      bool d_l = false;
-      if (e < end) {
-        const uint32_t q = __ldg(lst + e);
-        if (precedes(__ldg(fsum + q), __ldg(ids + q), ps, pid)) {
+    for (int c = 0; c <= pc && !dom; ++c) {
+      const unsigned s0 = __ldg(ob + c * kSumBuckets), s1 = __ldg(ob + c * kSumBuckets + sb + 1);
+      for (unsigned base = s0; base < s1; base += 32) {
+        const unsigned e = base + lane;
+        bool d_l = false;
+        if (e < s1) {
+          const uint32_t q = __ldg(lst + e);
+          const u64 qs = __ldg(fsum + q);
+          const uint32_t qi = __ldg(ids + q);
           T w[D];
           load_row_cached<T, D>(rows, q, w);
-          d_l = dominates<T, D>(w, v);
+          d_l = precedes(qs, qi, ps, pid) && dominates<T, D>(w, v);
         }
-      }
-      if (__any_sync(kFull, d_l)) {
-        dom = true;
-        break;
+        if (__any_sync(kFull, d_l)) {
+          dom = true;
+          break;
+        }
       }
     }
     if (lane == 0) flag[i] = dom ? 0 : 1;

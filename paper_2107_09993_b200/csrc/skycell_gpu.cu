@@ -193,9 +193,9 @@ void run_exact(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uin
   const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((cap + 255) / 256, (u64)nsm * 8));
   const TOut* trows = static_cast<const TOut*>(rows);
   uint32_t* lists = static_cast<uint32_t*>(ctx->lists.p);
-  sk::k_list_hist<TOut, D><<<g, 256, 0, s>>>(trows, ids, count, hist);
+  sk::k_list_hist<TOut, D><<<g, 256, 0, s>>>(trows, ids, fsum, count, hist);
   sk::k_list_scan<<<D, 1024, 0, s>>>(hist, cursor);
-  sk::k_list_scatter<TOut, D><<<g, 256, 0, s>>>(trows, ids, count, cursor, lists, cap);
+  sk::k_list_scatter<TOut, D><<<g, 256, 0, s>>>(trows, ids, fsum, count, cursor, lists, cap);
   const unsigned gw = (unsigned)std::max<u64>(1, std::min<u64>((cap * 32 + 255) / 256, (u64)nsm * 8));
   sk::k_allpairs_lists<TOut, D><<<gw, 256, 0, s>>>(trows, ids, fsum, count, lists, hist, cap,
                                                    static_cast<uint8_t*>(ctx->flags.p));
@@ -250,6 +250,7 @@ void run_pipeline(Query& q) {
   const size_t smem_pf = (((u64)pf_max * D * sizeof(TOut) + 15) & ~15ull) + (u64)pf_max * 8 +
                          (u64)D * pf_max * 2 + (u64)D * (sk::kListCols + 1) * 2 + 16;
   const size_t list_words = (size_t)D * (sk::kListCols + 1);
+  const size_t bin_words = (size_t)D * (sk::kListBins + 1);
   const u64 id_words = (n + 31) / 32;
   const unsigned bit_blocks = (unsigned)((id_words + sk::kBitsBlock - 1) / sk::kBitsBlock);
 
@@ -260,8 +261,8 @@ void run_pipeline(Query& q) {
   for (int L = 1; L <= rho; ++L) o_occ[L] = cv.take(words_at(L) * 4);
   const size_t o_sla = cv.take(words_at(la) * 4);
   const size_t o_srho = test_b ? cv.take(words_at(rho) * 4) : 0;
-  const size_t o_shist = cv.take(list_words * 4), o_scur = cv.take(list_words * 4);
-  const size_t o_hist = cv.take(list_words * 4), o_cur = cv.take(list_words * 4);
+  const size_t o_shist = cv.take(bin_words * 4), o_scur = cv.take(bin_words * 4);
+  const size_t o_hist = cv.take(bin_words * 4), o_cur = cv.take(bin_words * 4);
   const size_t o_idbits = cv.take(id_words * 4);
   const size_t o_bcount = cv.take((size_t)bit_blocks * 4);
   ensure(ctx->reset, cv.off);
@@ -339,11 +340,15 @@ void run_pipeline(Query& q) {
     run_exact<TOut, D>(ctx, s, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
                        static_cast<const u64*>(ctx->s2_fsum.p), &ctr->xs, cap4, static_cast<unsigned*>(at(o_shist)),
                        static_cast<unsigned*>(at(o_scur)));
-    sk::k_strength_order<TOut, D><<<1, 1024, 0, s>>>(
+    sk::k_compact_members<TOut, D><<<nsm * 4, 256, 0, s>>>(
         static_cast<const TOut*>(ctx->s2_rows.p), static_cast<const uint32_t*>(ctx->s2_ids.p),
         static_cast<const uint8_t*>(ctx->flags.p), static_cast<const u64*>(ctx->s2_fsum.p), &ctr->xs,
+        static_cast<TOut*>(ctx->smp_rows.p), static_cast<u64*>(ctx->smp_fsum.p), &ctr->fs);
+    sk::k_strength_order<TOut, D><<<1, 1024, 0, s>>>(
+        static_cast<const TOut*>(ctx->smp_rows.p), static_cast<const u64*>(ctx->smp_fsum.p), &ctr->fs,
         (uint32_t)pf_max, static_cast<TOut*>(ctx->f_rows.p), static_cast<u64*>(ctx->f_fsum.p), &ctr->nf,
         static_cast<uint16_t*>(ctx->f_lists.p), static_cast<uint16_t*>(ctx->f_offs.p));
+    ++ctx->launches;
     ++ctx->launches;
   }
 
