@@ -302,8 +302,13 @@ struct StreamParams {
 template <typename TIn, typename TOut, int D, bool IDENT, int THREADS, int PPT>
 __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
   extern __shared__ __align__(16) uint8_t sm[];
-  uint32_t* occ_s = reinterpret_cast<uint32_t*>(sm);
-  uint8_t* H_s = sm + p.lo_words * 4;
+  constexpr int NW = THREADS / 32;
+  constexpr int QCAP = 32 * PPT;
+  // [warp queues: lin (u64) x QCAP | record (u32) x QCAP] [occ layer la-1] [H]
+  u64* q_lin_all = reinterpret_cast<u64*>(sm);
+  uint32_t* q_id_all = reinterpret_cast<uint32_t*>(sm + (size_t)NW * QCAP * 8);
+  uint32_t* occ_s = reinterpret_cast<uint32_t*>(sm + (size_t)NW * QCAP * 12);
+  uint8_t* H_s = reinterpret_cast<uint8_t*>(occ_s + p.lo_words);
   for (uint32_t w = threadIdx.x; w < p.lo_words; w += THREADS) occ_s[w] = 0;
   for (uint32_t e = threadIdx.x; e < p.h_entries; e += THREADS) H_s[e] = p.H[e];
   __syncthreads();
@@ -311,6 +316,9 @@ __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
   const TIn* coords = static_cast<const TIn*>(p.coords);
   TOut* out_rows = static_cast<TOut*>(p.out_rows);
   const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1;
+  u64* q_lin = q_lin_all + (threadIdx.x >> 5) * QCAP;
+  uint32_t* q_id = q_id_all + (threadIdx.x >> 5) * QCAP;
   const uint32_t n = (uint32_t)p.n;
   constexpr uint32_t WT = 32u * PPT;
   const uint32_t ntiles = (uint32_t)((p.n + WT - 1) / WT);
@@ -318,6 +326,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
   const uint32_t nw = (gridDim.x * THREADS) >> 5;
   const int rho = p.rho, la = p.la, sh = rho - la;
   const int top = (1 << rho) - 1;
+  const u64 cmask = (u64)top;
   const float fscale = ldexpf(1.0f, rho);
   const double dscale = ldexp(1.0, rho);
   const bool test_b = p.PMs != nullptr;
@@ -333,58 +342,94 @@ __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
       const uint32_t i = base + j * 32;
       if (i < n) load_row<TIn, D>(coords, i, raw[j]);
     }
+    // ---- phase 1: every point -- finiteness, level-la filter, occupancy of
+    // filtered points at layer la-1; passing points join the warp queue
+    unsigned qn = 0;
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
       const uint32_t i = base + j * 32;
       const bool valid = i < n;
-      bool fin = true;
+      TIn sum = raw[j][0];
+#pragma unroll
+      for (int k = 1; k < D; ++k) sum += raw[j][k];
+      if (valid && !finite_v(sum)) {  // rare: NaN/Inf somewhere (or overflow of the probe sum)
+        bool fin = true;
+#pragma unroll
+        for (int k = 0; k < D; ++k) fin &= finite_v(raw[j][k]);
+        if (!fin) atomicMax(p.nonfinite, ~(u64)i);
+      }
       int col[D];
 #pragma unroll
-      for (int k = 0; k < D; ++k) {
-        fin &= finite_v(raw[j][k]);
+      for (int k = 0; k < D; ++k)
         col[k] = Coord<TIn, TOut, IDENT>::col(Coord<TIn, TOut, IDENT>::value(raw[j][k], p.nm, k), fscale, dscale, top);
-      }
       uint32_t hidx = 0;
+      u64 lin = 0;
 #pragma unroll
-      for (int k = D - 1; k >= 1; --k) hidx = (hidx << la) | (uint32_t)(col[k] >> sh);
+      for (int k = D - 1; k >= 1; --k) {
+        hidx = (hidx << la) | (uint32_t)(col[k] >> sh);
+        lin = (lin << rho) | (u64)col[k];
+      }
+      lin = (lin << rho) | (u64)col[0];
       const bool fail_a = (col[0] >> sh) > (int)H_s[hidx];
-      if (valid && !fin) atomicMax(p.nonfinite, ~(u64)i);
-      bool fail_b = false;
-      if (valid && fail_a) {
-        if (la >= 2) {
-          uint32_t lo = 0;
+      if (valid && fail_a && la >= 2) {
+        uint32_t lo = 0;
 #pragma unroll
-          for (int k = D - 1; k >= 0; --k) lo = (lo << (la - 1)) | (uint32_t)(col[k] >> (sh + 1));
-          set_bit_shared(occ_s, lo);
-        }
-      } else if (valid && test_b) {
-        fail_b = p.pms_wide ? strictly_dominated_cols<uint32_t, D>(static_cast<const uint32_t*>(p.PMs), col, rho)
-                            : strictly_dominated_cols<uint8_t, D>(static_cast<const uint8_t*>(p.PMs), col, rho);
-        if (fail_b) {
-          u64 pl = 0;
+        for (int k = D - 1; k >= 0; --k) lo = (lo << (la - 1)) | (uint32_t)(col[k] >> (sh + 1));
+        set_bit_shared(occ_s, lo);
+      }
+      const bool pass = valid && !fail_a;
+      const unsigned m = __ballot_sync(kFull, pass);
+      if (pass) {
+        const unsigned pos = qn + __popc(m & lt);
+        q_lin[pos] = lin;
+        q_id[pos] = i;
+      }
+      qn += __popc(m);
+    }
+    __syncwarp();
+    // ---- phase 2: queued points with full warps -- layer-rho test against
+    // the sample table, occupancy, output
+    for (unsigned r = 0; r < qn; r += 32) {
+      const unsigned e = r + lane;
+      bool keep = false;
+      u64 lin = 0;
+      uint32_t i = 0;
+      if (e < qn) {
+        lin = q_lin[e];
+        i = q_id[e];
+        keep = true;
+        if (test_b) {
+          int col[D];
 #pragma unroll
-          for (int k = D - 1; k >= 0; --k) pl = (pl << (rho - 1)) | (u64)(col[k] >> 1);
-          set_bit_global(p.occ_rm1, pl);
+          for (int k = 0; k < D; ++k) col[k] = (int)((lin >> (rho * k)) & cmask);
+          const bool fail_b =
+              p.pms_wide ? strictly_dominated_cols<uint32_t, D>(static_cast<const uint32_t*>(p.PMs), col, rho)
+                         : strictly_dominated_cols<uint8_t, D>(static_cast<const uint8_t*>(p.PMs), col, rho);
+          if (fail_b) {
+            u64 pl = 0;
+#pragma unroll
+            for (int k = D - 1; k >= 0; --k) pl = (pl << (rho - 1)) | (u64)(col[k] >> 1);
+            set_bit_global(p.occ_rm1, pl);
+            keep = false;
+          }
         }
       }
-      const bool keep = valid && !fail_a && !fail_b;
       kept += keep;
       if (__any_sync(kFull, keep)) {
         const u64 o = warp_reserve(wo, keep, p.out_reserved, stamp);
         if (keep) {
+          TIn rr[D];
+          load_row_cached<TIn, D>(coords, i, rr);
           TOut u[D];
-          u64 l = 0;
 #pragma unroll
-          for (int k = D - 1; k >= 0; --k) {
-            u[k] = Coord<TIn, TOut, IDENT>::value(raw[j][k], p.nm, k);
-            l = (l << rho) | (u64)col[k];
-          }
+          for (int k = 0; k < D; ++k) u[k] = Coord<TIn, TOut, IDENT>::value(rr[k], p.nm, k);
           store_row<TOut, D>(out_rows, o, u);
           p.out_ids[o] = i;
-          set_bit_global(p.occ_rho, l);
+          set_bit_global(p.occ_rho, lin);
         }
       }
     }
+    __syncwarp();
   }
   warp_close(wo, stamp);
 #pragma unroll
