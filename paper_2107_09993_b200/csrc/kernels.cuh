@@ -299,15 +299,34 @@ struct StreamParams {
   u64* nonfinite;          // max of (~record) over non-finite records: 0 = none
 };
 
+// Column of a coordinate at an arbitrary level L <= rho: floor(u * 2^L) is
+// the layer-rho column shifted right by rho - L (power-of-two scalings are
+// exact), computed directly to keep the per-point path short.
+template <typename TIn, typename TOut, bool IDENT>
+__device__ __forceinline__ int col_at(TIn raw, const Norm& nm, int k, float fs, double ds, int top);
+template <>
+__device__ __forceinline__ int col_at<float, float, true>(float raw, const Norm&, int, float fs, double, int top) {
+  // saturate to [0, 1] (NaN -> 0), scale, truncate; only the top needs a clamp
+  return min(__float2int_rz(__fmul_rn(__saturatef(raw), fs)), top);
+}
+template <>
+__device__ __forceinline__ int col_at<float, double, false>(float raw, const Norm& nm, int k, float, double ds, int top) {
+  return cell_col(Coord<float, double, false>::value(raw, nm, k), ds, top);
+}
+template <>
+__device__ __forceinline__ int col_at<double, double, false>(double raw, const Norm& nm, int k, float, double ds, int top) {
+  return cell_col(Coord<double, double, false>::value(raw, nm, k), ds, top);
+}
+
 template <typename TIn, typename TOut, int D, bool IDENT, int THREADS, int PPT>
-__global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
+__global__ void __launch_bounds__(THREADS, 3) k_stream(StreamParams p) {
   extern __shared__ __align__(16) uint8_t sm[];
   constexpr int NW = THREADS / 32;
   constexpr int QCAP = 32 * PPT;
-  // [warp queues: lin (u64) x QCAP | record (u32) x QCAP] [occ layer la-1] [H]
-  u64* q_lin_all = reinterpret_cast<u64*>(sm);
-  uint32_t* q_id_all = reinterpret_cast<uint32_t*>(sm + (size_t)NW * QCAP * 8);
-  uint32_t* occ_s = reinterpret_cast<uint32_t*>(sm + (size_t)NW * QCAP * 12);
+  // [warp queues: raw rows (TIn[D]) x QCAP | record (u32) x QCAP] [occ layer la-1] [H]
+  TIn* q_row_all = reinterpret_cast<TIn*>(sm);
+  uint32_t* q_id_all = reinterpret_cast<uint32_t*>(sm + (size_t)NW * QCAP * D * sizeof(TIn));
+  uint32_t* occ_s = q_id_all + NW * QCAP;
   uint8_t* H_s = reinterpret_cast<uint8_t*>(occ_s + p.lo_words);
   for (uint32_t w = threadIdx.x; w < p.lo_words; w += THREADS) occ_s[w] = 0;
   for (uint32_t e = threadIdx.x; e < p.h_entries; e += THREADS) H_s[e] = p.H[e];
@@ -317,19 +336,20 @@ __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
   TOut* out_rows = static_cast<TOut*>(p.out_rows);
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1;
-  u64* q_lin = q_lin_all + (threadIdx.x >> 5) * QCAP;
+  TIn* q_row = q_row_all + (threadIdx.x >> 5) * QCAP * D;
   uint32_t* q_id = q_id_all + (threadIdx.x >> 5) * QCAP;
   const uint32_t n = (uint32_t)p.n;
   constexpr uint32_t WT = 32u * PPT;
   const uint32_t ntiles = (uint32_t)((p.n + WT - 1) / WT);
   const uint32_t gw = (blockIdx.x * THREADS + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * THREADS) >> 5;
-  const int rho = p.rho, la = p.la, sh = rho - la;
-  const int top = (1 << rho) - 1;
-  const u64 cmask = (u64)top;
-  const float fscale = ldexpf(1.0f, rho);
-  const double dscale = ldexp(1.0, rho);
+  const int rho = p.rho, la = p.la;
+  const int top = (1 << rho) - 1, top_a = (1 << la) - 1;
+  const float fs_r = ldexpf(1.0f, rho), fs_a = ldexpf(1.0f, la);
+  const double ds_r = ldexp(1.0, rho), ds_a = ldexp(1.0, la);
+  const uint32_t mul_a = 1u << la, mul_lo = 1u << (la > 1 ? la - 1 : 0);
   const bool test_b = p.PMs != nullptr;
+  const bool rec_lo = la >= 2;
   WarpOut wo{0, p.chunk, p.chunk};
   auto stamp = [&](u64 slot) { p.out_ids[slot] = kNoId; };
   unsigned kept = 0;
@@ -342,8 +362,8 @@ __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
       const uint32_t i = base + j * 32;
       if (i < n) load_row<TIn, D>(coords, i, raw[j]);
     }
-    // ---- phase 1: every point -- finiteness, level-la filter, occupancy of
-    // filtered points at layer la-1; passing points join the warp queue
+    // ---- phase 1: every point -- finiteness probe, level-la filter,
+    // occupancy of filtered points at layer la-1; others join the warp queue
     unsigned qn = 0;
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
@@ -358,30 +378,25 @@ __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
         for (int k = 0; k < D; ++k) fin &= finite_v(raw[j][k]);
         if (!fin) atomicMax(p.nonfinite, ~(u64)i);
       }
-      int col[D];
+      int ca[D];
 #pragma unroll
-      for (int k = 0; k < D; ++k)
-        col[k] = Coord<TIn, TOut, IDENT>::col(Coord<TIn, TOut, IDENT>::value(raw[j][k], p.nm, k), fscale, dscale, top);
+      for (int k = 0; k < D; ++k) ca[k] = col_at<TIn, TOut, IDENT>(raw[j][k], p.nm, k, fs_a, ds_a, top_a);
       uint32_t hidx = 0;
-      u64 lin = 0;
 #pragma unroll
-      for (int k = D - 1; k >= 1; --k) {
-        hidx = (hidx << la) | (uint32_t)(col[k] >> sh);
-        lin = (lin << rho) | (u64)col[k];
-      }
-      lin = (lin << rho) | (u64)col[0];
-      const bool fail_a = (col[0] >> sh) > (int)H_s[hidx];
-      if (valid && fail_a && la >= 2) {
+      for (int k = D - 1; k >= 1; --k) hidx = hidx * mul_a + (uint32_t)ca[k];
+      const bool fail_a = ca[0] > (int)H_s[hidx];
+      if (valid && fail_a && rec_lo) {
         uint32_t lo = 0;
 #pragma unroll
-        for (int k = D - 1; k >= 0; --k) lo = (lo << (la - 1)) | (uint32_t)(col[k] >> (sh + 1));
+        for (int k = D - 1; k >= 0; --k) lo = lo * mul_lo + (uint32_t)(ca[k] >> 1);
         set_bit_shared(occ_s, lo);
       }
       const bool pass = valid && !fail_a;
       const unsigned m = __ballot_sync(kFull, pass);
       if (pass) {
         const unsigned pos = qn + __popc(m & lt);
-        q_lin[pos] = lin;
+#pragma unroll
+        for (int k = 0; k < D; ++k) q_row[pos * D + k] = raw[j][k];
         q_id[pos] = i;
       }
       qn += __popc(m);
@@ -392,16 +407,18 @@ __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
     for (unsigned r = 0; r < qn; r += 32) {
       const unsigned e = r + lane;
       bool keep = false;
-      u64 lin = 0;
+      int col[D];
+      TIn rr[D];
       uint32_t i = 0;
       if (e < qn) {
-        lin = q_lin[e];
         i = q_id[e];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          rr[k] = q_row[e * D + k];
+          col[k] = col_at<TIn, TOut, IDENT>(rr[k], p.nm, k, fs_r, ds_r, top);
+        }
         keep = true;
         if (test_b) {
-          int col[D];
-#pragma unroll
-          for (int k = 0; k < D; ++k) col[k] = (int)((lin >> (rho * k)) & cmask);
           const bool fail_b =
               p.pms_wide ? strictly_dominated_cols<uint32_t, D>(static_cast<const uint32_t*>(p.PMs), col, rho)
                          : strictly_dominated_cols<uint8_t, D>(static_cast<const uint8_t*>(p.PMs), col, rho);
@@ -418,11 +435,13 @@ __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
       if (__any_sync(kFull, keep)) {
         const u64 o = warp_reserve(wo, keep, p.out_reserved, stamp);
         if (keep) {
-          TIn rr[D];
-          load_row_cached<TIn, D>(coords, i, rr);
           TOut u[D];
+          u64 lin = 0;
 #pragma unroll
-          for (int k = 0; k < D; ++k) u[k] = Coord<TIn, TOut, IDENT>::value(rr[k], p.nm, k);
+          for (int k = D - 1; k >= 0; --k) {
+            u[k] = Coord<TIn, TOut, IDENT>::value(rr[k], p.nm, k);
+            lin = (lin << rho) | (u64)col[k];
+          }
           store_row<TOut, D>(out_rows, o, u);
           p.out_ids[o] = i;
           set_bit_global(p.occ_rho, lin);

@@ -229,8 +229,8 @@ void run_pipeline(Query& q) {
   const u64 table_entries = 1ull << (u64)(rho * (D - 1));
 
   // ---- K1 geometry: persistent warps over static round-robin warp tiles
-  constexpr int PPT1 = ppt_for<TIn, D>();
-  const size_t smem1 = (size_t)(kStreamThreads / 32) * 32 * PPT1 * 12 + (size_t)lo_words * 4 +
+  constexpr int PPT1 = (ppt_for<TIn, D>() + 1) / 2;
+  const size_t smem1 = (size_t)(kStreamThreads / 32) * 32 * PPT1 * (D * sizeof(TIn) + 4) + (size_t)lo_words * 4 +
                        ((h_entries + 15) & ~15u) + 16;
   auto kstream = sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1>;
   ck(cudaFuncSetAttribute(kstream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1), "smem attr");
