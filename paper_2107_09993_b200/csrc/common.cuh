@@ -34,6 +34,40 @@ __device__ __forceinline__ u64 ld_status(const u64* p) {
   return v;
 }
 
+// --------------------------------------------------------- mbarrier / TMA
+// Thin wrappers over the Hopper+/Blackwell async-copy primitives used by the
+// streaming kernel: a 1-D bulk copy global -> shared (cp.async.bulk, SASS
+// UBLKCP) that completes a transaction count on an mbarrier.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
 // ------------------------------------------------------- decoupled look-back
 // Status word per tile: bits 62-63 flag (0 empty, 1 aggregate, 2 inclusive
 // prefix), bits 0-61 value.  Status arrays are zeroed once per query.
@@ -222,10 +256,16 @@ __device__ __forceinline__ void set_bit_global(uint32_t* bits, u64 idx) {
   uint32_t* w = bits + (idx >> 5);
   if (!(__ldcg(w) & m)) atomicOr(w, m);
 }
+// Fire-and-forget (red.global.or): no result to wait for.
+__device__ __forceinline__ void red_or_global(uint32_t* bits, u64 idx) {
+  asm volatile("red.global.or.b32 [%0], %1;" ::"l"(bits + (idx >> 5)), "r"(1u << (idx & 31)) : "memory");
+}
 __device__ __forceinline__ void set_bit_shared(uint32_t* bits, uint32_t idx) {
   const uint32_t m = 1u << (idx & 31);
-  uint32_t* w = bits + (idx >> 5);
-  if (!(*w & m)) atomicOr(w, m);
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bits) + ((idx >> 5) << 2);
+  uint32_t w;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(a));
+  if (!(w & m)) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(m) : "memory");
 }
 
 }  // namespace sk

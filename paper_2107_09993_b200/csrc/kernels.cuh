@@ -265,19 +265,14 @@ __device__ __forceinline__ bool strictly_dominated_cols(const TT* __restrict__ P
 }
 
 // -------------------------------------------------------- K1: the stream
-// Two-level cell filter (SURVEY §0.3 applied to a sample):
-//   A: level la (<= 7, table H in shared memory): the point's level-la cell
-//      is strictly dominated by an occupied sample cell -> not a candidate.
-//   B: layer rho (global prefix-min table of the sample, only for points
-//      passing A): same test at the reference's own layer.
-// A point filtered at level L can influence the reference's per-layer
-// key/candidate sets only at layers < L, so its occupancy is
-// recorded at layer L-1: a shared-memory bitmap for A (tiny), a global
-// check-before-set bitmap for B.  Survivors (about the candidate-cell
-// fraction: 6.1% at the headline config) go to per-warp output chunks and set
-// their bit in the layer-rho occupancy.  Every coordinate is read once; the
-// kernel has no block barrier in its main loop (warp-centric, static
-// round-robin warp tiles).
+// Cell filter from a sample (SURVEY §0.3 applied to a sample): a point whose
+// level-la cell (la <= 7, table H in shared memory) is strictly dominated by
+// an occupied sample cell cannot lie in a layer-rho candidate cell.  Such a
+// point can influence the reference's per-layer key/candidate sets only at
+// layers < la, so its occupancy is recorded at layer la-1 in
+// a small shared-memory bitmap.  Survivors (11.9% at the headline config) go
+// to per-warp output chunks and mark their layer-rho cell.  Every coordinate
+// is read once; the main loop has no block barrier.
 struct StreamParams {
   const void* coords;
   u64 n;
@@ -318,15 +313,35 @@ __device__ __forceinline__ int col_at<double, double, false>(double raw, const N
   return cell_col(Coord<double, double, false>::value(raw, nm, k), ds, top);
 }
 
-template <typename TIn, typename TOut, int D, bool IDENT, int THREADS, int PPT>
-__global__ void __launch_bounds__(THREADS, 3) k_stream(StreamParams p) {
+// Level of the shared-memory filter table for (d, rho): the largest L <=
+// min(rho, 7) whose table (2^(L(d-1)) bytes) fits 32 KB.
+__host__ __device__ constexpr int filter_level(int rho, int d) {
+  int best = 1;
+  for (int L = 1; L <= (rho < 7 ? rho : 7); ++L)
+    if ((1ull << (L * (d - 1))) <= 32768ull && L * d <= 30) best = L;
+  return best;
+}
+
+// Per-dimension digit index with the magic-number trick: for u in [0, 1),
+// fma.rz(u, 2^L, 2^23) is the float 2^23 + trunc(u * 2^L) exactly, whose bit
+// pattern is 0x4B000000 + col.  Summing bit patterns with power-of-two digit
+// weights and subtracting the constant sum of 0x4B000000 digits yields the
+// packed index (mod 2^32).
+__device__ __forceinline__ uint32_t mag_col(float u, float scale) {
+  return __float_as_uint(__fmaf_rz(u, scale, 8388608.0f));
+}
+
+// Warp-centric persistent kernel: each warp walks tiles of 32*PPT
+// consecutive points round-robin, with the next tile's loads issued before
+// the current tile is processed (register double buffering).  Survivors of
+// the level-la test go straight to per-warp output chunks (one reservation
+// per tile); their layer-rho cells are marked with fire-and-forget red.or.
+// RHO > 0 (f32 identity path) fixes rho and la at compile time so every index
+// is a constant-weight IMAD chain; RHO == 0 is the general runtime path.
+template <typename TIn, typename TOut, int D, bool IDENT, int THREADS, int PPT, int RHO>
+__global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
   extern __shared__ __align__(16) uint8_t sm[];
-  constexpr int NW = THREADS / 32;
-  constexpr int QCAP = 32 * PPT;
-  // [warp queues: raw rows (TIn[D]) x QCAP | record (u32) x QCAP] [occ layer la-1] [H]
-  TIn* q_row_all = reinterpret_cast<TIn*>(sm);
-  uint32_t* q_id_all = reinterpret_cast<uint32_t*>(sm + (size_t)NW * QCAP * D * sizeof(TIn));
-  uint32_t* occ_s = q_id_all + NW * QCAP;
+  uint32_t* occ_s = reinterpret_cast<uint32_t*>(sm);
   uint8_t* H_s = reinterpret_cast<uint8_t*>(occ_s + p.lo_words);
   for (uint32_t w = threadIdx.x; w < p.lo_words; w += THREADS) occ_s[w] = 0;
   for (uint32_t e = threadIdx.x; e < p.h_entries; e += THREADS) H_s[e] = p.H[e];
@@ -336,123 +351,159 @@ __global__ void __launch_bounds__(THREADS, 3) k_stream(StreamParams p) {
   TOut* out_rows = static_cast<TOut*>(p.out_rows);
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1;
-  TIn* q_row = q_row_all + (threadIdx.x >> 5) * QCAP * D;
-  uint32_t* q_id = q_id_all + (threadIdx.x >> 5) * QCAP;
   const uint32_t n = (uint32_t)p.n;
   constexpr uint32_t WT = 32u * PPT;
-  const uint32_t ntiles = (uint32_t)((p.n + WT - 1) / WT);
+  const uint32_t ntiles = (n + WT - 1) / WT;
+  const uint32_t nfull = n / WT;
   const uint32_t gw = (blockIdx.x * THREADS + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * THREADS) >> 5;
-  const int rho = p.rho, la = p.la;
+  constexpr bool kFixed = RHO > 0;
+  constexpr int kLa = kFixed ? filter_level(RHO, D) : 1;
+  const int rho = kFixed ? RHO : p.rho;
+  const int la = kFixed ? kLa : p.la;
   const int top = (1 << rho) - 1, top_a = (1 << la) - 1;
   const float fs_r = ldexpf(1.0f, rho), fs_a = ldexpf(1.0f, la);
   const double ds_r = ldexp(1.0, rho), ds_a = ldexp(1.0, la);
-  const uint32_t mul_a = 1u << la, mul_lo = 1u << (la > 1 ? la - 1 : 0);
-  const bool test_b = p.PMs != nullptr;
+  const uint32_t mul_a = 1u << la, mul_lo = 1u << (la > 1 ? la - 1 : 0), mul_r = 1u << rho;
+  const float fs_lo = ldexpf(1.0f, la > 1 ? la - 1 : 0);
+  uint32_t hcorr = 0, locorr = 0, rcorr = 0;
+  for (int k = D - 1; k >= 1; --k) hcorr = hcorr * mul_a + 0x4B000000u;
+  for (int k = D - 1; k >= 0; --k) locorr = locorr * mul_lo + 0x4B000000u;
+  for (int k = D - 1; k >= 0; --k) rcorr = rcorr * mul_r + 0x4B000000u;
   const bool rec_lo = la >= 2;
+  const bool lin32 = rho * D <= 32;
   WarpOut wo{0, p.chunk, p.chunk};
   auto stamp = [&](u64 slot) { p.out_ids[slot] = kNoId; };
   unsigned kept = 0;
 
-  for (uint32_t t = gw; t < ntiles; t += nw) {
-    const uint32_t base = t * WT + lane;
-    TIn raw[PPT][D];
+  TIn raw[PPT][D];
+  auto load_tile = [&](uint32_t t) {
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
-      const uint32_t i = base + j * 32;
-      if (i < n) load_row<TIn, D>(coords, i, raw[j]);
+      const uint32_t i = t * WT + j * 32 + lane;
+      if (t < nfull || i < n) load_row<TIn, D>(coords, i, raw[j]);
     }
-    // ---- phase 1: every point -- finiteness probe, level-la filter,
-    // occupancy of filtered points at layer la-1; others join the warp queue
-    unsigned qn = 0;
+  };
+  uint32_t t = gw;
+  if (t < ntiles) load_tile(t);
+  while (t < ntiles) {
+    TIn cur[PPT][D];
+#pragma unroll
+    for (int j = 0; j < PPT; ++j)
+#pragma unroll
+      for (int k = 0; k < D; ++k) cur[j][k] = raw[j][k];
+    const uint32_t tn = t + nw;
+    if (tn < ntiles) load_tile(tn);  // prefetch: in flight while this tile is processed
+    const bool full = t < nfull;
+    const uint32_t base = t * WT + lane;
+    bool keep[PPT];
+    bool bad = false;
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
-      const uint32_t i = base + j * 32;
-      const bool valid = i < n;
-      TIn sum = raw[j][0];
+      const bool valid = full || base + j * 32 < n;
+      bool fail_a;
+      if constexpr (IDENT) {
+        // u = min(max(v, 0), 1 - 2^-24): every column stays below 2^L (the
+        // reference clamps to 1 - 2^-32, whose column is also 2^L - 1); NaN -> 0
+        float probe = 0.0f;
+        uint32_t hidx = 0, lo = 0;
 #pragma unroll
-      for (int k = 1; k < D; ++k) sum += raw[j][k];
-      if (valid && !finite_v(sum)) {  // rare: NaN/Inf somewhere (or overflow of the probe sum)
-        bool fin = true;
+        for (int k = D - 1; k >= 1; --k) {
+          probe += cur[j][k];
+          const float u = fminf(fmaxf(cur[j][k], 0.0f), 0x1.fffffep-1f);
+          hidx = hidx * mul_a + mag_col(u, fs_a);
+          if (rec_lo) lo = lo * mul_lo + mag_col(u, fs_lo);
+        }
+        probe += cur[j][0];
+        const float u0 = fminf(fmaxf(cur[j][0], 0.0f), 0x1.fffffep-1f);
+        const int c0 = (int)(mag_col(u0, fs_a) - 0x4B000000u);
+        bad |= !isfinite(probe);
+        fail_a = c0 > (int)H_s[hidx - hcorr];
+        if (valid && fail_a && rec_lo) set_bit_shared(occ_s, lo * mul_lo + mag_col(u0, fs_lo) - locorr);
+      } else {
+        TIn sum = cur[j][0];
 #pragma unroll
-        for (int k = 0; k < D; ++k) fin &= finite_v(raw[j][k]);
-        if (!fin) atomicMax(p.nonfinite, ~(u64)i);
-      }
-      int ca[D];
+        for (int k = 1; k < D; ++k) sum += cur[j][k];
+        bad |= valid && !finite_v(sum);
+        int ca[D];
 #pragma unroll
-      for (int k = 0; k < D; ++k) ca[k] = col_at<TIn, TOut, IDENT>(raw[j][k], p.nm, k, fs_a, ds_a, top_a);
-      uint32_t hidx = 0;
+        for (int k = 0; k < D; ++k) ca[k] = col_at<TIn, TOut, IDENT>(cur[j][k], p.nm, k, fs_a, ds_a, top_a);
+        uint32_t hidx = 0, lo = 0;
 #pragma unroll
-      for (int k = D - 1; k >= 1; --k) hidx = hidx * mul_a + (uint32_t)ca[k];
-      const bool fail_a = ca[0] > (int)H_s[hidx];
-      if (valid && fail_a && rec_lo) {
-        uint32_t lo = 0;
+        for (int k = D - 1; k >= 1; --k) hidx = hidx * mul_a + (uint32_t)ca[k];
+        fail_a = ca[0] > (int)H_s[hidx];
 #pragma unroll
         for (int k = D - 1; k >= 0; --k) lo = lo * mul_lo + (uint32_t)(ca[k] >> 1);
-        set_bit_shared(occ_s, lo);
+        if (valid && fail_a && rec_lo) set_bit_shared(occ_s, lo);
       }
-      const bool pass = valid && !fail_a;
-      const unsigned m = __ballot_sync(kFull, pass);
-      if (pass) {
-        const unsigned pos = qn + __popc(m & lt);
-#pragma unroll
-        for (int k = 0; k < D; ++k) q_row[pos * D + k] = raw[j][k];
-        q_id[pos] = i;
-      }
-      qn += __popc(m);
+      keep[j] = valid && !fail_a;
     }
-    __syncwarp();
-    // ---- phase 2: queued points with full warps -- layer-rho test against
-    // the sample table, occupancy, output
-    for (unsigned r = 0; r < qn; r += 32) {
-      const unsigned e = r + lane;
-      bool keep = false;
-      int col[D];
-      TIn rr[D];
-      uint32_t i = 0;
-      if (e < qn) {
-        i = q_id[e];
+    // one output reservation per tile
+    unsigned mk[PPT], tot = 0;
 #pragma unroll
-        for (int k = 0; k < D; ++k) {
-          rr[k] = q_row[e * D + k];
-          col[k] = col_at<TIn, TOut, IDENT>(rr[k], p.nm, k, fs_r, ds_r, top);
-        }
-        keep = true;
-        if (test_b) {
-          const bool fail_b =
-              p.pms_wide ? strictly_dominated_cols<uint32_t, D>(static_cast<const uint32_t*>(p.PMs), col, rho)
-                         : strictly_dominated_cols<uint8_t, D>(static_cast<const uint8_t*>(p.PMs), col, rho);
-          if (fail_b) {
-            u64 pl = 0;
-#pragma unroll
-            for (int k = D - 1; k >= 0; --k) pl = (pl << (rho - 1)) | (u64)(col[k] >> 1);
-            set_bit_global(p.occ_rm1, pl);
-            keep = false;
-          }
-        }
+    for (int j = 0; j < PPT; ++j) {
+      mk[j] = __ballot_sync(kFull, keep[j]);
+      tot += __popc(mk[j]);
+    }
+    if (tot) {
+      if (wo.fill + tot > wo.chunk) {  // host guarantees chunk >= 32 * PPT >= tot
+        for (unsigned sl = wo.fill + lane; sl < wo.chunk; sl += 32) stamp(wo.base + sl);
+        u64 bb = 0;
+        if (lane == 0) bb = atomicAdd(p.out_reserved, (u64)wo.chunk);
+        wo.base = __shfl_sync(kFull, bb, 0);
+        wo.fill = 0;
       }
-      kept += keep;
-      if (__any_sync(kFull, keep)) {
-        const u64 o = warp_reserve(wo, keep, p.out_reserved, stamp);
-        if (keep) {
+      u64 o = wo.base + wo.fill;
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) {
+        if (keep[j]) {
+          const u64 slot = o + __popc(mk[j] & lt);
           TOut u[D];
-          u64 lin = 0;
+          if constexpr (IDENT) {
+            uint32_t l = 0;
 #pragma unroll
-          for (int k = D - 1; k >= 0; --k) {
-            u[k] = Coord<TIn, TOut, IDENT>::value(rr[k], p.nm, k);
-            lin = (lin << rho) | (u64)col[k];
+            for (int k = D - 1; k >= 0; --k) {
+              u[k] = __saturatef(cur[j][k]);  // the stored proxy (dataset.cpp:45 clamp, 1.0f = 1 - 2^-32)
+              l = l * mul_r + mag_col(fminf(u[k], 0x1.fffffep-1f), fs_r);
+            }
+            if (lin32) red_or_global(p.occ_rho, (u64)(l - rcorr));
+            else {
+              u64 lin = 0;
+#pragma unroll
+              for (int k = D - 1; k >= 0; --k)
+                lin = (lin << rho) | (u64)(mag_col(fminf(u[k], 0x1.fffffep-1f), fs_r) - 0x4B000000u);
+              red_or_global(p.occ_rho, lin);
+            }
+          } else {
+            u64 lin = 0;
+#pragma unroll
+            for (int k = D - 1; k >= 0; --k) {
+              u[k] = Coord<TIn, TOut, IDENT>::value(cur[j][k], p.nm, k);
+              lin = (lin << rho) | (u64)col_at<TIn, TOut, IDENT>(cur[j][k], p.nm, k, fs_r, ds_r, top);
+            }
+            red_or_global(p.occ_rho, lin);
           }
-          store_row<TOut, D>(out_rows, o, u);
-          p.out_ids[o] = i;
-          set_bit_global(p.occ_rho, lin);
+          store_row<TOut, D>(out_rows, slot, u);
+          p.out_ids[slot] = base + j * 32;
         }
+        o += __popc(mk[j]);
+      }
+      wo.fill += tot;
+      kept += tot;
+    }
+    if (__any_sync(kFull, bad)) {  // rare: NaN/Inf (or overflow of the probe sum)
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) {
+        const uint32_t i = base + j * 32;
+        bool fin = true;
+#pragma unroll
+        for (int k = 0; k < D; ++k) fin &= finite_v(cur[j][k]);
+        if (i < n && !fin) atomicMax(p.nonfinite, ~(u64)i);
       }
     }
-    __syncwarp();
+    t = tn;
   }
   warp_close(wo, stamp);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) kept += __shfl_xor_sync(kFull, kept, o);
   if (lane == 0 && kept) atomicAdd(p.kept, (u64)kept);
   if (p.lo_words) {
     __syncthreads();

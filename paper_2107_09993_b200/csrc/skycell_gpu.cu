@@ -132,7 +132,6 @@ int default_rho(u64 n, int d) {
 
 
 // ------------------------------------------------------------------ config
-constexpr int kStreamThreads = 256;
 constexpr int kThreads = 256;
 
 template <typename T, int D>
@@ -212,13 +211,7 @@ void run_pipeline(Query& q) {
   const int nsm = ctx->num_sms;
 
   // ---- levels and sizes
-  int la = 1;
-  for (int L = std::min(rho, 7); L >= 1; --L) {
-    if ((1ull << (u64)(L * (D - 1))) <= 32768 && L * D <= 30) {
-      la = L;
-      break;
-    }
-  }
+  const int la = sk::filter_level(rho, D);
   const bool test_b = rho > la;
   const u64 m = std::min<u64>(n, 1ull << 20);
   const uint32_t h_entries = (uint32_t)(1ull << (u64)(la * (D - 1)));
@@ -228,11 +221,27 @@ void run_pipeline(Query& q) {
   const size_t tt = wide ? 4 : 1;
   const u64 table_entries = 1ull << (u64)(rho * (D - 1));
 
-  // ---- K1 geometry: persistent warps over static round-robin warp tiles
-  constexpr int PPT1 = (ppt_for<TIn, D>() + 1) / 2;
-  const size_t smem1 = (size_t)(kStreamThreads / 32) * 32 * PPT1 * (D * sizeof(TIn) + 4) + (size_t)lo_words * 4 +
-                       ((h_entries + 15) & ~15u) + 16;
-  auto kstream = sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1>;
+  // ---- K1 geometry: persistent warps over round-robin warp tiles
+  constexpr int kStreamThreads = 256;
+  constexpr int PPT1 = std::max(1, ppt_for<TIn, D>() / 2);
+  const size_t smem1 = (size_t)lo_words * 4 + ((h_entries + 15) & ~15u) + 16;
+  // f32 identity inputs with D <= 8 and rho <= 7 get a compile-time (rho, la) instance
+  auto pick = [&]() {
+    if constexpr (IDENT && D <= 8) {
+      switch (rho) {
+        case 1: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 1>;
+        case 2: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 2>;
+        case 3: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 3>;
+        case 4: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 4>;
+        case 5: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 5>;
+        case 6: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 6>;
+        case 7: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 7>;
+        default: break;
+      }
+    }
+    return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 0>;
+  };
+  auto kstream = pick();
   ck(cudaFuncSetAttribute(kstream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1), "smem attr");
   int occ_blocks = 0;
   ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_blocks, kstream, kStreamThreads, smem1), "occupancy");
@@ -240,6 +249,7 @@ void run_pipeline(Query& q) {
   const u64 wtiles = (n + 32 * PPT1 - 1) / (32 * PPT1);
   const int grid1 = (int)std::max<u64>(1, std::min<u64>((wtiles + 7) / 8, (u64)nsm * occ_blocks));
   constexpr unsigned kChunk1 = 256, kChunk4 = 64;
+  static_assert(kChunk1 >= 32 * PPT1, "a stream tile's survivors must fit one output chunk");
   const u64 slack1 = (u64)grid1 * (kStreamThreads / 32) * kChunk1;
   const u64 cap1 = n + slack1;
 
