@@ -175,22 +175,19 @@ def run_ours(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dist_id, n_gpu, d, desc = CONFIGS[args.config]
+    eng = sky.Engine(local)
     if world > 1:
         import torch.distributed as tdist
         tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-        from paper_2107_09993_b200 import dist as skydist
-        runner = skydist.ShardedSkyline(local, rank, world)
+        from paper_2107_09993_b200.dist import ShardedSkyline
+        runner = ShardedSkyline(eng, device=torch.device(f"cuda:{local}"))
     else:
         runner = None
-    eng = sky.Engine(local)
     n_total = n_gpu * world
     rho = args.rho or sky.default_rho(n_total, d)
-    # per-rank shard of the global dataset: rank r owns ids [r*n_gpu, (r+1)*n_gpu)
-    x = eng.generate(dist_id, n_total, d, 42, quantized=True) if world == 1 else None
-    if world > 1:
-        full = eng.generate(dist_id, n_total, d, 42, quantized=True)
-        x = full[rank * n_gpu:(rank + 1) * n_gpu].contiguous()
-        del full
+    # rank r owns records [r*n_gpu, (r+1)*n_gpu) of the global dataset and
+    # generates exactly those (same streams as the single-device dataset)
+    x = eng.generate(dist_id, n_total, d, 42, quantized=True, begin=rank * n_gpu, count=n_gpu)
     ids_dev = torch.empty(n_gpu, dtype=torch.int32, device=f"cuda:{local}")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
     mn, mx = np.zeros(d), np.ones(d)
@@ -199,7 +196,7 @@ def run_ours(args):
     def step(with_stats=True):
         if runner is None:
             return eng.skyline_raw(x, n_gpu, d, mn, mx, rho, 1, True, ids_out=ids_dev, with_stats=with_stats)
-        return runner.skyline(eng, x, n_gpu, d, mn, mx, rho, ids_out=ids_dev)
+        return runner.skyline(x, n_gpu, d, mn, mx, rho, rank * n_gpu, ids_out=ids_dev)
 
     for _ in range(max(3, args.warmup)):
         res = step()
@@ -230,23 +227,38 @@ def run_ours(args):
     sky_size = int(len(res.ids))
 
     # ---- e2e through the public API: pinned host coords -> ids on host
-    e2e = None
-    if world == 1:
-        hx = torch.empty((n_gpu, d), dtype=torch.float32, pin_memory=True)
-        hx.copy_(x)
-        hx_np = hx.numpy()
-        ids_host = torch.empty(n_gpu, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
-        for _ in range(2):
-            eng.skyline_raw(hx_np, n_gpu, d, mn, mx, rho, 1, True, ids_out=ids_host, with_stats=False)
-        e2e_ms = []
-        for _ in range(max(1, min(args.steps, 5))):
-            t0 = time.perf_counter()
-            r2 = eng.skyline_raw(hx_np, n_gpu, d, mn, mx, rho, 1, True, ids_out=ids_host, with_stats=False)
-            e2e_ms.append(1000.0 * (time.perf_counter() - t0))
+    # (H2D of the shard and D2H of the ids inside the timed region; under
+    # torchrun every rank stages its own shard, max over ranks)
+    hx = torch.empty((n_gpu, d), dtype=torch.float32, pin_memory=True)
+    hx.copy_(x)
+    hx_np = hx.numpy()
+    ids_host = torch.empty(n_gpu, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+
+    def e2e_step():
+        if runner is None:
+            return eng.skyline_raw(hx_np, n_gpu, d, mn, mx, rho, 1, True, ids_out=ids_host, with_stats=False)
+        return runner.skyline(hx_np, n_gpu, d, mn, mx, rho, rank * n_gpu, ids_out=ids_host)
+
+    for _ in range(2):
+        e2e_step()
+    e2e_ms = []
+    for _ in range(max(1, min(args.steps, 5))):
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r2 = e2e_step()
+        torch.cuda.synchronize()
+        e2e_ms.append(1000.0 * (time.perf_counter() - t0))
+    e2e_mean = statistics.mean(e2e_ms)
+    if world > 1:
+        t = torch.tensor([e2e_mean], device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_mean = float(t.item())
+    if rank == 0:
         assert len(r2.ids) == sky_size
-        e2e = {"value": n_gpu / (statistics.mean(e2e_ms) / 1000.0) / 1e9, "unit": UNIT,
-               "ms_per_step": statistics.mean(e2e_ms), "h2d_bytes_per_step": n_gpu * d * 4,
-               "d2h_bytes_per_step": sky_size * 4 + 8 * 1024}
+    e2e = {"value": n_total / (e2e_mean / 1000.0) / 1e9, "unit": UNIT, "ms_per_step": e2e_mean,
+           "h2d_bytes_per_step": n_total * d * 4, "d2h_bytes_per_step": sky_size * 4}
 
     # ---- roofline of the dominant kernel (K1 streaming pass)
     peak, peak_src = measured_peaks()

@@ -99,6 +99,48 @@ int skycell_gpu_quadrant_f64(skycell_gpu_ctx* ctx, const double* coords, uint64_
                              uint32_t* ids_out, uint64_t* n_out, skycell_gpu_stats* stats,
                              char* err, size_t err_len);
 
+/* Bind the context to a caller's CUDA stream (a cudaStream_t; NULL restores
+ * the context's own stream).  Every kernel and copy of later calls is
+ * enqueued on it, so collectives the caller issues on the same stream (the
+ * sharded query below) are ordered without host synchronisation. */
+int skycell_gpu_set_stream(skycell_gpu_ctx* ctx, void* stream);
+
+/* ---- Sharded query over G devices (one process / context per device).
+ * No reference equivalent: the reference is single-process
+ * (SURVEY.md §8(e)); the result equals compute_skyline over the
+ * concatenation of all shards.  Rank g holds records [id_base, id_base + n)
+ * of the global dataset.  The caller performs the two exchanges (NCCL over
+ * NVLink in paper_2107_09993_b200/dist.py):
+ *
+ *   shard_begin        K0 + K1 on the shard; *occ_bytes = size of the
+ *                      occupancy region to exchange
+ *   shard_export_occ   copy this rank's occupancy region to dev_dst
+ *      -- caller: all-gather the regions (rank order) into one buffer --
+ *   shard_prune        OR the world regions (K2), prune against the global
+ *                      occupancy (K3, K4), local skyline (K5);
+ *                      *local_count = its size
+ *      -- caller: all-gather the counts; max_count = their maximum --
+ *   shard_block_bytes  bytes of one rank's padded local-skyline block
+ *   shard_pack         write this rank's block (padded to max_count)
+ *      -- caller: all-gather the blocks (rank order) --
+ *   shard_finish       this rank's local-skyline points against the union;
+ *                      writes this rank's part of the global skyline
+ *                      (global ids, ascending) to ids_out; stats hold the
+ *                      global per-layer counts and the LOCAL points_examined.
+ * coords_f32 selects float (1) or double (0) coordinates.  dim_min/dim_max are
+ * the GLOBAL declared range (identical on every rank). */
+int skycell_gpu_shard_begin(skycell_gpu_ctx* ctx, const void* coords, int coords_f32, uint64_t n, int d,
+                            const double* dim_min, const double* dim_max, int rho, int mode, uint64_t id_base,
+                            uint64_t* occ_bytes, char* err, size_t err_len);
+int skycell_gpu_shard_export_occ(skycell_gpu_ctx* ctx, void* dev_dst, char* err, size_t err_len);
+int skycell_gpu_shard_prune(skycell_gpu_ctx* ctx, const void* dev_gathered, int world, uint64_t* local_count,
+                            char* err, size_t err_len);
+uint64_t skycell_gpu_shard_block_bytes(skycell_gpu_ctx* ctx, uint64_t max_count);
+int skycell_gpu_shard_pack(skycell_gpu_ctx* ctx, void* dev_dst, uint64_t max_count, char* err, size_t err_len);
+int skycell_gpu_shard_finish(skycell_gpu_ctx* ctx, const void* dev_recv, int world, uint64_t max_count, int rank,
+                             uint64_t own_count, uint32_t* ids_out, uint64_t* n_out, skycell_gpu_stats* stats,
+                             char* err, size_t err_len);
+
 /* On-device synthetic data with the reference generator's streams
  * (skycell::generate, datagen.cpp:62-87): dist 0 independent, 1 correlated,
  * 2 anti-correlated.  kind 0 writes n*d raw doubles, kind 1 writes n*d floats
@@ -106,6 +148,9 @@ int skycell_gpu_quadrant_f64(skycell_gpu_ctx* ctx, const double* coords, uint64_
  * benchmark input rule of BASELINE.md §2).  dev_out is a device pointer. */
 int skycell_gpu_generate(skycell_gpu_ctx* ctx, int dist, uint64_t n, int d, uint64_t seed, int kind,
                          void* dev_out, char* err, size_t err_len);
+/* Records [begin, begin + count) of the same n-record dataset (a shard). */
+int skycell_gpu_generate_range(skycell_gpu_ctx* ctx, int dist, uint64_t n, int d, uint64_t seed, int kind,
+                               uint64_t begin, uint64_t count, void* dev_out, char* err, size_t err_len);
 
 /* MultiLayerGrid::default_rho (grid.cpp:30-33). */
 int skycell_default_rho(uint64_t n, int d);

@@ -50,16 +50,21 @@ __device__ __forceinline__ double clamp_unit(double v) {
 }
 
 // kind 0: raw f64; kind 1: f32 quantised to the 2^-24 grid.
+// Writes records [rbegin, rbegin + rcount) of the n-record dataset to out
+// (record rbegin at out[0]): a shard generates only its own index range.
 template <int D>
-__global__ void k_generate(int dist, u64 n, u64 seed, int kind, void* out) {
-  const u64 blocks = (n + 65535) / 65536;
-  for (u64 b = blockIdx.x * (u64)blockDim.x + threadIdx.x; b < blocks; b += (u64)gridDim.x * blockDim.x) {
+__global__ void k_generate(int dist, u64 n, u64 seed, int kind, u64 rbegin, u64 rcount, void* out) {
+  const u64 b0 = rbegin / 65536, b1 = (rbegin + rcount + 65535) / 65536;
+  for (u64 b = b0 + blockIdx.x * (u64)blockDim.x + threadIdx.x; b < b1; b += (u64)gridDim.x * blockDim.x) {
     Xo rng;
     u64 st = seed ^ ((b + 1) * 0x9e3779b97f4a7c15ull);
     for (int i = 0; i < 4; ++i) rng.s[i] = splitmix(st);
     const u64 begin = b * 65536;
     const u64 count = (n - begin < 65536) ? n - begin : 65536;
+    const u64 rend = rbegin + rcount;
     for (u64 p = 0; p < count; ++p) {
+      const u64 rec = begin + p;
+      if (rec >= rend) break;
       double row[D];
       if (dist == 0) {
 #pragma unroll
@@ -79,7 +84,8 @@ __global__ void k_generate(int dist, u64 n, u64 seed, int kind, void* out) {
 #pragma unroll
         for (int k = 0; k < D; ++k) row[k] = clamp_unit(__dadd_rn(__dadd_rn(row[k], shift), rng.normal(0.0, 0.05)));
       }
-      const u64 o = (begin + p) * D;
+      if (rec < rbegin) continue;  // the stream still advances
+      const u64 o = (rec - rbegin) * D;
       if (kind == 0) {
 #pragma unroll
         for (int k = 0; k < D; ++k) static_cast<double*>(out)[o + k] = row[k];

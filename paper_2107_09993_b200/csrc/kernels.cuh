@@ -164,6 +164,7 @@ struct SampleParams {
   void* rows;
   uint32_t* ids;
   u64* fsum;
+  uint32_t id_base;   // global id of local record 0 (shard offset)
 };
 
 template <typename TIn, typename TOut, int D, bool IDENT>
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(256) k_sample(SampleParams p) {
     set_bit_global(p.occ_la, la_lin);
     if (p.occ_rho) set_bit_global(p.occ_rho, lin);
     store_row<TOut, D>(static_cast<TOut*>(p.rows), i, u);
-    p.ids[i] = (uint32_t)i;
+    p.ids[i] = p.id_base + (uint32_t)i;
     p.fsum[i] = fsum_bits<TOut, D>(u);
   }
 }
@@ -292,6 +293,7 @@ struct StreamParams {
   unsigned chunk;          // output chunk per warp reservation
   u64* kept;               // exact number of survivors
   u64* nonfinite;          // max of (~record) over non-finite records: 0 = none
+  uint32_t id_base;        // global id of local record 0 (shard offset)
 };
 
 // Column of a coordinate at an arbitrary level L <= rho: floor(u * 2^L) is
@@ -484,7 +486,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
             red_or_global(p.occ_rho, lin);
           }
           store_row<TOut, D>(out_rows, slot, u);
-          p.out_ids[slot] = base + j * 32;
+          p.out_ids[slot] = p.id_base + base + j * 32;
         }
         o += __popc(mk[j]);
       }
@@ -1027,15 +1029,26 @@ __global__ void k_list_scatter(const T* __restrict__ rows, const uint32_t* __res
 // candidates per step (independent gathers in flight) and stop at the first
 // step with a dominator, so a skyline point's scan is prefix/32 steps long.
 template <typename T, int D>
+__device__ __forceinline__ bool same_cell(const T* q, const T* p, int L, int top) {
+  const T scale = (T)(1u << L);
+  bool eq = true;
+#pragma unroll
+  for (int k = 0; k < D; ++k) eq &= cell_col(q[k], scale, top) == cell_col(p[k], scale, top);
+  return eq;
+}
+
+template <typename T, int D>
 __global__ void __launch_bounds__(256) k_allpairs_lists(const T* __restrict__ rows, const uint32_t* __restrict__ ids,
                                                         const u64* __restrict__ fsum, const u64* __restrict__ count,
                                                         const uint32_t* __restrict__ lists, const unsigned* __restrict__ offs,
-                                                        u64 cap, uint8_t* __restrict__ flag) {
-  const u64 n = *count;
+                                                        u64 cap, uint8_t* __restrict__ flag, u64 q_begin,
+                                                        const u64* __restrict__ q_end, int cell_level) {
+  const u64 n = q_end ? *q_end : *count;
   const int lane = threadIdx.x & 31;
   const u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
   const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
-  for (u64 i = warp; i < n; i += nwarps) {
+  const int ctop = (1 << cell_level) - 1;
+  for (u64 i = q_begin + warp; i < n; i += nwarps) {
     const uint32_t pid = ids[i];
     if (pid == kNoId) {
       if (lane == 0) flag[i] = 0;
@@ -1070,6 +1083,9 @@ __global__ void __launch_bounds__(256) k_allpairs_lists(const T* __restrict__ ro
           T w[D];
           load_row_cached<T, D>(rows, q, w);
           d_l = precedes(qs, qi, ps, pid) && dominates<T, D>(w, v);
+          // merge_cross_cell = false (refine.cpp:98): phase-1 semantics only,
+          // a dominator must share p's layer-rho cell
+          if (cell_level && d_l) d_l = same_cell<T, D>(w, v, cell_level, ctop);
         }
         if (__any_sync(kFull, d_l)) {
           dom = true;
@@ -1090,11 +1106,14 @@ constexpr int kBitsPer = 8;
 constexpr u64 kBitsBlock = (u64)kBitsThreads * kBitsPer;
 
 __global__ void k_mark_ids(const uint32_t* __restrict__ ids, const uint8_t* __restrict__ flag,
-                           const u64* __restrict__ count, uint32_t* __restrict__ bits) {
+                           const u64* __restrict__ count, uint32_t* __restrict__ bits, uint32_t base) {
   const u64 n = *count;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
     const uint32_t id = ids[i];
-    if (id != kNoId && flag[i]) atomicOr(bits + (id >> 5), 1u << (id & 31));
+    if (id != kNoId && flag[i]) {
+      const uint32_t b = id - base;
+      atomicOr(bits + (b >> 5), 1u << (b & 31));
+    }
   }
 }
 
@@ -1151,7 +1170,7 @@ __global__ void __launch_bounds__(1024) k_bits_scan(unsigned* __restrict__ block
 
 __global__ void __launch_bounds__(kBitsThreads) k_bits_write(const uint32_t* __restrict__ bits, u64 words,
                                                              const unsigned* __restrict__ block_offs,
-                                                             uint32_t* __restrict__ out_ids) {
+                                                             uint32_t* __restrict__ out_ids, uint32_t base) {
   // thread t owns words b0 + t*kBitsPer .. +kBitsPer-1 (contiguous, so the
   // block-local exclusive scan over threads preserves id order)
   const u64 w0 = blockIdx.x * kBitsBlock + (u64)threadIdx.x * kBitsPer;
@@ -1181,7 +1200,7 @@ __global__ void __launch_bounds__(kBitsThreads) k_bits_write(const uint32_t* __r
     while (v) {
       const int b = __ffs(v) - 1;
       v &= v - 1;
-      out_ids[pos++] = (uint32_t)((w0 + e) * 32 + b);
+      out_ids[pos++] = base + (uint32_t)((w0 + e) * 32 + b);
     }
   }
 }
@@ -1193,6 +1212,131 @@ __global__ void k_check_finite(const TIn* __restrict__ coords, u64 total, int d,
   for (u64 e = blockIdx.x * (u64)blockDim.x + threadIdx.x; e < total; e += (u64)gridDim.x * blockDim.x) {
     if (!finite_v(coords[e])) atomicMax(nonfinite, ~(e / d));
   }
+}
+
+// ------------------------------------------- K2: occupancy OR across shards
+// dst[w] = OR over g < world of gathered[g * words + w]: the bitwise-OR
+// reduction NCCL lacks (nccl.h:260-275), applied to the all-gathered
+// occupancy region of every rank.  uint4 words: 16 B per load.
+__global__ void k_or_gather(const uint4* __restrict__ gathered, int world, u64 words4, uint4* __restrict__ dst) {
+  for (u64 w = blockIdx.x * (u64)blockDim.x + threadIdx.x; w < words4; w += (u64)gridDim.x * blockDim.x) {
+    uint4 x = gathered[w];
+    for (int g = 1; g < world; ++g) {
+      const uint4 y = gathered[(u64)g * words4 + w];
+      x.x |= y.x;
+      x.y |= y.y;
+      x.z |= y.z;
+      x.w |= y.w;
+    }
+    dst[w] = x;
+  }
+}
+
+// Members (flag set, id != kNoId) of a slot array -> dense rows / sums / ids
+// (order irrelevant: the final ids are ordered through the id bitmap).
+template <typename T, int D>
+__global__ void k_pack_members(const T* __restrict__ rows, const uint32_t* __restrict__ ids,
+                               const uint8_t* __restrict__ flag, const u64* __restrict__ fsum,
+                               const u64* __restrict__ count, T* __restrict__ out_rows, u64* __restrict__ out_fsum,
+                               uint32_t* __restrict__ out_ids, u64* __restrict__ out_count) {
+  const u64 n = *count;
+  const int lane = threadIdx.x & 31;
+  for (u64 wb = ((blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5) * 32; wb < n;
+       wb += ((u64)gridDim.x * blockDim.x >> 5) * 32) {
+    const u64 i = wb + lane;
+    const bool live = i < n && ids[i] != kNoId && flag[i];
+    const unsigned m = __ballot_sync(kFull, live);
+    if (!m) continue;
+    u64 b = 0;
+    if (lane == 0) b = atomicAdd(out_count, (u64)__popc(m));
+    b = __shfl_sync(kFull, b, 0);
+    if (live) {
+      const u64 o = b + __popc(m & ((1u << lane) - 1));
+      T v[D];
+      load_row_cached<T, D>(rows, i, v);
+      store_row<T, D>(out_rows, o, v);
+      out_fsum[o] = fsum[i];
+      out_ids[o] = ids[i];
+    }
+  }
+}
+
+__global__ void k_fill_u32(uint32_t* __restrict__ p, u64 count, uint32_t v) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < count; i += (u64)gridDim.x * blockDim.x) p[i] = v;
+}
+
+// ------------------------------------------------ quadrant_skyline (f1)
+// refine.cpp:166-174: record i is inside iff p[k] >= origin[k] for every k
+// (NaN compares false, so NaN records are outside).  Inside records set their
+// bit in an n-bit bitmap; the K6 scan then lists them in ascending order,
+// which is the reference's original_ids vector.
+template <int D>
+__global__ void k_quadrant_mark(const double* __restrict__ coords, u64 n, Norm origin, uint32_t* __restrict__ bits) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    double v[D];
+    load_row_cached<double, D>(coords, i, v);
+    bool inside = true;
+#pragma unroll
+    for (int k = 0; k < D; ++k) inside &= v[k] >= origin.mn[k];
+    if (inside) atomicOr(bits + (i >> 5), 1u << (i & 31));
+  }
+}
+
+// Order-preserving u64 image of a double (for atomic min/max).
+__device__ __forceinline__ u64 dkey(double x) {
+  const u64 b = (u64)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__host__ __device__ inline double dkey_inv(u64 k) {
+  const u64 b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  double x;
+  memcpy(&x, &b, 8);
+  return x;
+}
+
+// sub.coords[j] = coords[orig[j]] and the per-dimension min / max of the
+// subset (Dataset::compute_minmax, dataset.cpp:10-20; exact, order-free).
+// mm[2k] = min key, mm[2k+1] = max key, pre-set to (~0, 0).
+template <int D>
+__global__ void k_quadrant_gather(const double* __restrict__ coords, const uint32_t* __restrict__ orig,
+                                  const u64* __restrict__ count, double* __restrict__ sub, u64* __restrict__ mm) {
+  const u64 n = *count;
+  u64 lo[D], hi[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    lo[k] = ~0ull;
+    hi[k] = 0;
+  }
+  for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x) {
+    double v[D];
+    load_row_cached<double, D>(coords, orig[j], v);
+    store_row<double, D>(sub, j, v);
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const u64 key = dkey(v[k]);
+      lo[k] = key < lo[k] ? key : lo[k];
+      hi[k] = key > hi[k] ? key : hi[k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    u64 a = lo[k], b = hi[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const u64 x = __shfl_xor_sync(kFull, a, o), y = __shfl_xor_sync(kFull, b, o);
+      a = x < a ? x : a;
+      b = y > b ? y : b;
+    }
+    if ((threadIdx.x & 31) == 0) {
+      if (a != ~0ull) atomicMin(mm + 2 * k, a);
+      if (b != 0) atomicMax(mm + 2 * k + 1, b);
+    }
+  }
+}
+
+// ids[j] = orig[ids[j]] (refine.cpp:182): ascending stays ascending.
+__global__ void k_map_ids(uint32_t* __restrict__ ids, const uint32_t* __restrict__ orig, u64 n) {
+  for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x) ids[j] = orig[ids[j]];
 }
 
 }  // namespace sk

@@ -3,10 +3,18 @@
 // One query = one pass of compute_skyline (refine.cpp:108-158) on one device:
 //   validate (dataset.cpp:23-24, grid.cpp:38-43) -> K0 sample filter -> K1
 //   streaming pass -> K3 cell tables + per-layer counts -> K4 candidate
-//   filter -> K5 block-recursive exact dominance -> ids (ascending) + stats.
+//   filter -> K5 exact sort-first dominance -> K6 ids (ascending) + stats.
 // Every data-dependent size stays on the device (kernels read their input
 // counts from device memory), so the whole query is enqueued without a host
 // round trip; the only synchronisation is the final read of the counters.
+//
+// The same pipeline object runs the sharded (multi-GPU) query in phases
+// (DESIGN.md §4): local (K0+K1) | occupancy exchange (K2) | prune + local
+// skyline (K3-K5) | local-skyline exchange | finish (K5 over the union, K6).
+// The collectives themselves are issued by the caller (NCCL through
+// torch.distributed in paper_2107_09993_b200/dist.py) on the stream the
+// context is bound to (skycell_gpu_set_stream), so no phase needs a host
+// synchronisation except where a count must reach the host.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -14,6 +22,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -32,6 +41,8 @@ struct DevCounters {
   u64 s1, s2, examined;
   u64 zero;
   u64 m, xs, xs_kept, nf, fs, fin, s1_kept, s2_kept;
+  u64 lsky;       // local skyline size (sharded)
+  u64 un, qend;   // union slots and own-slice end (sharded finish)
   u64 cand[kMaxLayers];
   u64 key[kMaxLayers];
 };
@@ -51,6 +62,11 @@ struct CudaFail {
   const char* what;
 };
 
+struct ApiFail {
+  int code;
+  std::string msg;
+};
+
 inline void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw CudaFail{e, what};
 }
@@ -65,20 +81,38 @@ void ensure(DevBuf& b, size_t bytes) {
   b.cap = bytes;
 }
 
+struct PipeBase {
+  virtual ~PipeBase() = default;
+  virtual void local() = 0;
+  virtual u64 occ_bytes() const = 0;
+  virtual void export_occ(void* dst) = 0;
+  virtual void or_gathered(const void* gathered, int world) = 0;
+  virtual u64 prune_local_skyline() = 0;
+  virtual u64 block_bytes(u64 maxc) const = 0;
+  virtual void pack(void* dst, u64 maxc) = 0;
+  virtual void finish(const void* recv, int world, u64 maxc, int rank, u64 own_count, uint32_t* ids_out,
+                      uint64_t* n_out, skycell_gpu_stats* stats) = 0;
+};
+
 }  // namespace
 
 struct skycell_gpu_ctx {
   int device = 0;
   int num_sms = 148;
-  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;  // the stream every kernel is enqueued on
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   DevBuf reset, slabs, H, table, table2, table_s, staging;
   DevBuf smp_rows, smp_ids, smp_fsum, f_rows, f_fsum, f_lists, f_offs, lists, ids_dev;
   DevBuf s1_rows, s1_ids, s2_rows, s2_ids, s2_fsum, flags;
+  DevBuf sky_rows, sky_ids, sky_fsum;  // local skyline (sharded)
+  DevBuf q_bits, q_orig, q_sub, q_ids, q_mm;  // quadrant_skyline
   DevCounters* host_ctr = nullptr;  // pinned
+  u64* host_param = nullptr;        // pinned H2D staging
   cudaEvent_t ev[8] = {};
   u64 launches = 0;
+  std::unique_ptr<PipeBase> shard;  // sharded query in flight
 };
 
 namespace {
@@ -98,7 +132,6 @@ struct Carver {
     return o;
   }
 };
-
 
 // Validation in the reference's order: normalize() first (dataset.cpp:23-24),
 // then the grid budget (grid.cpp:38-43).
@@ -130,7 +163,6 @@ int default_rho(u64 n, int d) {
   return std::max(1, std::min(6, (bw - 1) / d));
 }
 
-
 // ------------------------------------------------------------------ config
 constexpr int kThreads = 256;
 
@@ -146,14 +178,12 @@ struct Query {
   skycell_gpu_ctx* ctx;
   u64 n;
   int d, rho, mode, merge;
-  bool ident;
   sk::Norm nm;
   const void* dev_coords;  // device-resident input (user's or staged)
   uint32_t* ids_dev;       // caller's device output buffer, or nullptr (use ctx->ids_dev)
-  bool in_f32;
-  bool out_f32;
   skycell_gpu_stats* stats;
   bool timed;
+  uint32_t id_base;        // global id of local record 0 (sharded: the shard offset)
 };
 
 template <typename TT>
@@ -184,10 +214,13 @@ void launch_count(skycell_gpu_ctx* ctx, cudaStream_t s, const uint32_t* bits, in
 // Exact sort-first pass (refine.cpp:31-59 as applied in phase 2, :98-99) over
 // a point set given as slots (ids == kNoId marks an empty slot): per-dimension
 // column lists, then the list-pruned dominance test; flags[i] = 1 for members
-// of the result.
+// of the result, for the query slots [q_begin, *q_end) (all slots when q_end
+// is null).  cell_level > 0 restricts dominators to p's own layer-rho cell
+// (merge_cross_cell = false, refine.cpp:98).
 template <typename TOut, int D>
 void run_exact(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint32_t* ids, const u64* fsum,
-               const u64* count, u64 cap, unsigned* hist, unsigned* cursor) {
+               const u64* count, u64 cap, unsigned* hist, unsigned* cursor, u64 q_begin = 0,
+               const u64* q_end = nullptr, int cell_level = 0) {
   const int nsm = ctx->num_sms;
   const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((cap + 255) / 256, (u64)nsm * 8));
   const TOut* trows = static_cast<const TOut*>(rows);
@@ -197,36 +230,49 @@ void run_exact(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uin
   sk::k_list_scatter<TOut, D><<<g, 256, 0, s>>>(trows, ids, fsum, count, cursor, lists, cap);
   const unsigned gw = (unsigned)std::max<u64>(1, std::min<u64>((cap * 32 + 255) / 256, (u64)nsm * 8));
   sk::k_allpairs_lists<TOut, D><<<gw, 256, 0, s>>>(trows, ids, fsum, count, lists, hist, cap,
-                                                   static_cast<uint8_t*>(ctx->flags.p));
+                                                   static_cast<uint8_t*>(ctx->flags.p), q_begin, q_end, cell_level);
   ctx->launches += 4;
 }
 
 template <typename TIn, typename TOut, bool IDENT, int D>
-void run_pipeline(Query& q) {
-  skycell_gpu_ctx* ctx = q.ctx;
-  cudaStream_t s = ctx->stream;
-  cudaStream_t s2 = ctx->side;
-  const u64 n = q.n;
-  const int rho = q.rho;
-  const int nsm = ctx->num_sms;
+struct Pipe final : PipeBase {
+  Query q;
+  skycell_gpu_ctx* ctx;
+  cudaStream_t s, s2;
+  u64 n;
+  int rho, nsm;
 
-  // ---- levels and sizes
-  const int la = sk::filter_level(rho, D);
-  const bool test_b = rho > la;
-  const u64 m = std::min<u64>(n, 1ull << 20);
-  const uint32_t h_entries = (uint32_t)(1ull << (u64)(la * (D - 1)));
-  auto words_at = [&](int L) { return std::max<u64>(1, (1ull << (u64)(L * D)) / 32); };
-  const uint32_t lo_words = la >= 2 ? (uint32_t)words_at(la - 1) : 0;
-  const bool wide = rho > 7;
-  const size_t tt = wide ? 4 : 1;
-  const u64 table_entries = 1ull << (u64)(rho * (D - 1));
+  // ---- geometry
+  int la;
+  bool test_b, wide;
+  u64 m;
+  uint32_t h_entries, lo_words;
+  size_t tt;
+  u64 table_entries;
+  static constexpr int kStreamThreads = 256;
+  static constexpr int PPT1 = std::max(1, ppt_for<TIn, D>() / 2);
+  static constexpr unsigned kChunk1 = 256, kChunk4 = 64;
+  static_assert(kChunk1 >= 32 * PPT1, "a stream tile's survivors must fit one output chunk");
+  size_t smem1;
+  void (*kstream)(sk::StreamParams);
+  int grid1, grid4, pf_max;
+  u64 cap1, cap4;
+  size_t smem_pf;
+  u64 id_words;
+  unsigned bit_blocks;
 
-  // ---- K1 geometry: persistent warps over round-robin warp tiles
-  constexpr int kStreamThreads = 256;
-  constexpr int PPT1 = std::max(1, ppt_for<TIn, D>() / 2);
-  const size_t smem1 = (size_t)lo_words * 4 + ((h_entries + 15) & ~15u) + 16;
-  // f32 identity inputs with D <= 8 and rho <= 7 get a compile-time (rho, la) instance
-  auto pick = [&]() {
+  // ---- zeroed region
+  size_t o_ctr, o_sla, o_srho, o_shist, o_scur, o_hist, o_cur, o_fhist, o_fcur, o_idbits, o_bcount, o_end, o_total;
+  std::vector<size_t> o_occ;
+
+  u64 words_at(int L) const { return std::max<u64>(1, (1ull << (u64)(L * D)) / 32); }
+  void* at(size_t off) const { return static_cast<char*>(ctx->reset.p) + off; }
+  uint32_t* occ(int L) const { return static_cast<uint32_t*>(at(o_occ[L])); }
+  DevCounters* ctr() const { return static_cast<DevCounters*>(at(o_ctr)); }
+  unsigned* U(size_t off) const { return static_cast<unsigned*>(at(off)); }
+  int cell_level() const { return q.merge ? 0 : rho; }
+
+  static auto pick_stream(int rho) {
     if constexpr (IDENT && D <= 8) {
       switch (rho) {
         case 1: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 1>;
@@ -240,174 +286,208 @@ void run_pipeline(Query& q) {
       }
     }
     return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 0>;
-  };
-  auto kstream = pick();
-  ck(cudaFuncSetAttribute(kstream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1), "smem attr");
-  int occ_blocks = 0;
-  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_blocks, kstream, kStreamThreads, smem1), "occupancy");
-  occ_blocks = std::max(1, occ_blocks);
-  const u64 wtiles = (n + 32 * PPT1 - 1) / (32 * PPT1);
-  const int grid1 = (int)std::max<u64>(1, std::min<u64>((wtiles + 7) / 8, (u64)nsm * occ_blocks));
-  constexpr unsigned kChunk1 = 256, kChunk4 = 64;
-  static_assert(kChunk1 >= 32 * PPT1, "a stream tile's survivors must fit one output chunk");
-  const u64 slack1 = (u64)grid1 * (kStreamThreads / 32) * kChunk1;
-  const u64 cap1 = n + slack1;
+  }
 
-  // ---- K4 geometry
-  const int grid4 = nsm * 4;
-  const u64 slack4 = (u64)grid4 * (kThreads / 32) * kChunk4;
-  const u64 cap4 = std::max(cap1, m) + slack4;
-  const int pf_max = (int)std::min<u64>(1024, (32 * 1024) / (D * sizeof(TOut) + 8));  // K4 point filter
-  const size_t smem_pf = (((u64)pf_max * D * sizeof(TOut) + 15) & ~15ull) + (u64)pf_max * 8 +
-                         (u64)D * pf_max * 2 + (u64)D * (sk::kListCols + 1) * 2 + 16;
-  const size_t list_words = (size_t)D * (sk::kListCols + 1);
-  const size_t bin_words = (size_t)D * (sk::kListBins + 1);
-  const u64 id_words = (n + 31) / 32;
-  const unsigned bit_blocks = (unsigned)((id_words + sk::kBitsBlock - 1) / sk::kBitsBlock);
+  explicit Pipe(const Query& qq) : q(qq), ctx(qq.ctx), s(qq.ctx->stream), s2(qq.ctx->side), n(qq.n), rho(qq.rho) {
+    nsm = ctx->num_sms;
+    la = sk::filter_level(rho, D);
+    test_b = rho > la;
+    m = std::min<u64>(n, 1ull << 20);
+    h_entries = (uint32_t)(1ull << (u64)(la * (D - 1)));
+    lo_words = la >= 2 ? (uint32_t)words_at(la - 1) : 0;
+    wide = rho > 7;
+    tt = wide ? 4 : 1;
+    table_entries = 1ull << (u64)(rho * (D - 1));
 
-  // ---- zeroed region
-  Carver cv;
-  const size_t o_ctr = cv.take(sizeof(DevCounters));
-  std::vector<size_t> o_occ(rho + 1, 0);
-  for (int L = 1; L <= rho; ++L) o_occ[L] = cv.take(words_at(L) * 4);
-  const size_t o_sla = cv.take(words_at(la) * 4);
-  const size_t o_srho = test_b ? cv.take(words_at(rho) * 4) : 0;
-  const size_t o_shist = cv.take(bin_words * 4), o_scur = cv.take(bin_words * 4);
-  const size_t o_hist = cv.take(bin_words * 4), o_cur = cv.take(bin_words * 4);
-  const size_t o_idbits = cv.take(id_words * 4);
-  const size_t o_bcount = cv.take((size_t)bit_blocks * 4);
-  ensure(ctx->reset, cv.off);
-  char* R = static_cast<char*>(ctx->reset.p);
-  auto at = [&](size_t off) { return reinterpret_cast<void*>(R + off); };
-  auto occ = [&](int L) { return static_cast<uint32_t*>(at(o_occ[L])); };
-  DevCounters* ctr = static_cast<DevCounters*>(at(o_ctr));
+    // K1 geometry: persistent warps over round-robin warp tiles
+    smem1 = (size_t)lo_words * 4 + ((h_entries + 15) & ~15u) + 16;
+    kstream = pick_stream(rho);
+    ck(cudaFuncSetAttribute(kstream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1), "smem attr");
+    int occ_blocks = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_blocks, kstream, kStreamThreads, smem1), "occupancy");
+    occ_blocks = std::max(1, occ_blocks);
+    const u64 wtiles = (n + 32 * PPT1 - 1) / (32 * PPT1);
+    grid1 = (int)std::max<u64>(1, std::min<u64>((wtiles + 7) / 8, (u64)nsm * occ_blocks));
+    cap1 = n + (u64)grid1 * (kStreamThreads / 32) * kChunk1;
 
-  // ---- working buffers
-  ensure(ctx->H, std::max<u64>(h_entries, 16));
-  if (lo_words) ensure(ctx->slabs, (size_t)grid1 * lo_words * 4);
-  ensure(ctx->table, table_entries * tt);
-  ensure(ctx->table2, table_entries * tt);
-  if (test_b) ensure(ctx->table_s, table_entries * tt);
-  ensure(ctx->smp_rows, m * D * sizeof(TOut));
-  ensure(ctx->smp_ids, m * 4);
-  ensure(ctx->smp_fsum, m * 8);
-  ensure(ctx->f_rows, (size_t)pf_max * D * sizeof(TOut));
-  ensure(ctx->f_fsum, (size_t)pf_max * 8);
-  ensure(ctx->f_lists, (size_t)D * pf_max * 2);
-  ensure(ctx->f_offs, list_words * 2);
-  ensure(ctx->s1_rows, cap1 * D * sizeof(TOut));
-  ensure(ctx->s1_ids, cap1 * 4);
-  ensure(ctx->s2_rows, cap4 * D * sizeof(TOut));
-  ensure(ctx->s2_ids, cap4 * 4);
-  ensure(ctx->s2_fsum, cap4 * 8);
-  ensure(ctx->flags, cap4);
-  ensure(ctx->lists, (size_t)D * cap4 * 4);
-  ensure(ctx->ids_dev, n * 4);
+    // K4 geometry
+    grid4 = nsm * 4;
+    cap4 = std::max(cap1, m) + (u64)grid4 * (kThreads / 32) * kChunk4;
+    pf_max = (int)std::min<u64>(1024, (32 * 1024) / (D * sizeof(TOut) + 8));
+    smem_pf = (((u64)pf_max * D * sizeof(TOut) + 15) & ~15ull) + (u64)pf_max * 8 + (u64)D * pf_max * 2 +
+              (u64)D * (sk::kListCols + 1) * 2 + 16;
+    const size_t bin_words = (size_t)D * (sk::kListBins + 1);
+    id_words = (n + 31) / 32;
+    bit_blocks = (unsigned)((id_words + sk::kBitsBlock - 1) / sk::kBitsBlock);
 
-  if (q.timed) ck(cudaEventRecord(ctx->ev[0], s), "event");
-  ck(cudaMemsetAsync(ctx->reset.p, 0, cv.off, s), "memset");
+    // zeroed region: counters, occupancy layers 1..rho (contiguous: the
+    // sharded exchange ships [o_occ[1], o_occ[rho] + words) as one block)
+    Carver cv;
+    o_ctr = cv.take(sizeof(DevCounters));
+    o_occ.assign(rho + 1, 0);
+    for (int L = 1; L <= rho; ++L) o_occ[L] = cv.take(words_at(L) * 4);
+    o_end = cv.off;
+    o_sla = cv.take(words_at(la) * 4);
+    o_srho = test_b ? cv.take(words_at(rho) * 4) : 0;
+    o_shist = cv.take(bin_words * 4);
+    o_scur = cv.take(bin_words * 4);
+    o_hist = cv.take(bin_words * 4);
+    o_cur = cv.take(bin_words * 4);
+    o_fhist = cv.take(bin_words * 4);
+    o_fcur = cv.take(bin_words * 4);
+    o_idbits = cv.take(id_words * 4);
+    o_bcount = cv.take((size_t)bit_blocks * 4);
+    o_total = cv.off;
+    ensure(ctx->reset, o_total);
 
-  // ---- K0: sample occupancy, filter tables, sample skyline -> filter points F
-  {
-    sk::SampleParams sp{};
-    sp.coords = q.dev_coords;
-    sp.m = m;
-    sp.rho = rho;
-    sp.la = la;
-    sp.nm = q.nm;
-    sp.occ_la = static_cast<uint32_t*>(at(o_sla));
-    sp.occ_rho = test_b ? static_cast<uint32_t*>(at(o_srho)) : nullptr;
-    sp.rows = ctx->smp_rows.p;
-    sp.ids = static_cast<uint32_t*>(ctx->smp_ids.p);
-    sp.fsum = static_cast<u64*>(ctx->smp_fsum.p);
-    const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((m + 255) / 256, (u64)nsm * 8));
-    sk::k_sample<TIn, TOut, D, IDENT><<<g, 256, 0, s>>>(sp);
-    sk::k_build_filter<<<1, 1024, h_entries, s>>>(static_cast<uint32_t*>(at(o_sla)), la, D,
-                                                  static_cast<uint8_t*>(ctx->H.p));
-    ctx->launches += 2;
-    if (test_b) {
-      if (wide) launch_tables<uint32_t>(ctx, s, static_cast<uint32_t*>(at(o_srho)), rho, D, static_cast<uint32_t*>(ctx->table_s.p));
-      else launch_tables<uint8_t>(ctx, s, static_cast<uint32_t*>(at(o_srho)), rho, D, static_cast<uint8_t*>(ctx->table_s.p));
+    // working buffers
+    ensure(ctx->H, std::max<u64>(h_entries, 16));
+    if (lo_words) ensure(ctx->slabs, (size_t)grid1 * lo_words * 4);
+    ensure(ctx->table, table_entries * tt);
+    ensure(ctx->table2, table_entries * tt);
+    if (test_b) ensure(ctx->table_s, table_entries * tt);
+    ensure(ctx->smp_rows, m * D * sizeof(TOut));
+    ensure(ctx->smp_ids, m * 4);
+    ensure(ctx->smp_fsum, m * 8);
+    ensure(ctx->f_rows, (size_t)pf_max * D * sizeof(TOut));
+    ensure(ctx->f_fsum, (size_t)pf_max * 8);
+    ensure(ctx->f_lists, (size_t)D * pf_max * 2);
+    ensure(ctx->f_offs, (size_t)D * (sk::kListCols + 1) * 2);
+    ensure(ctx->s1_rows, cap1 * D * sizeof(TOut));
+    ensure(ctx->s1_ids, cap1 * 4);
+    ensure(ctx->s2_rows, cap4 * D * sizeof(TOut));
+    ensure(ctx->s2_ids, cap4 * 4);
+    ensure(ctx->s2_fsum, cap4 * 8);
+    ensure(ctx->flags, cap4);
+    ensure(ctx->lists, (size_t)D * cap4 * 4);
+    ensure(ctx->ids_dev, n * 4);
+  }
+
+  // ---- K0 + K1 (+ slab reduction): everything that reads the input
+  void local() override {
+    DevCounters* c = ctr();
+    if (q.timed) ck(cudaEventRecord(ctx->ev[0], s), "event");
+    ck(cudaMemsetAsync(ctx->reset.p, 0, o_total, s), "memset");
+
+    // K0: sample occupancy, filter tables, sample skyline -> filter points F
+    {
+      sk::SampleParams sp{};
+      sp.coords = q.dev_coords;
+      sp.m = m;
+      sp.rho = rho;
+      sp.la = la;
+      sp.nm = q.nm;
+      sp.occ_la = U(o_sla);
+      sp.occ_rho = test_b ? U(o_srho) : nullptr;
+      sp.rows = ctx->smp_rows.p;
+      sp.ids = static_cast<uint32_t*>(ctx->smp_ids.p);
+      sp.fsum = static_cast<u64*>(ctx->smp_fsum.p);
+      sp.id_base = q.id_base;
+      const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((m + 255) / 256, (u64)nsm * 8));
+      sk::k_sample<TIn, TOut, D, IDENT><<<g, 256, 0, s>>>(sp);
+      sk::k_build_filter<<<1, 1024, h_entries, s>>>(U(o_sla), la, D, static_cast<uint8_t*>(ctx->H.p));
+      ctx->launches += 2;
+      if (q.merge) {
+        // The sample skyline only serves as K4's point filter, which phase-1
+        // only semantics (merge_cross_cell = false) cannot use.
+        if (test_b) {
+          if (wide) launch_tables<uint32_t>(ctx, s, U(o_srho), rho, D, static_cast<uint32_t*>(ctx->table_s.p));
+          else launch_tables<uint8_t>(ctx, s, U(o_srho), rho, D, static_cast<uint8_t*>(ctx->table_s.p));
+        }
+        // sample points not strictly dominated at layer rho -> X (s2 buffers)
+        sk::CandParams pc{};
+        pc.rows = ctx->smp_rows.p;
+        pc.ids = static_cast<const uint32_t*>(ctx->smp_ids.p);
+        pc.count = nullptr;
+        pc.count_const = m;
+        pc.rho = rho;
+        pc.PM = test_b ? ctx->table_s.p : nullptr;
+        pc.f_max = 0;
+        pc.out_rows = ctx->s2_rows.p;
+        pc.out_ids = static_cast<uint32_t*>(ctx->s2_ids.p);
+        pc.out_fsum = static_cast<u64*>(ctx->s2_fsum.p);
+        pc.out_reserved = &c->xs;
+        pc.chunk = kChunk4;
+        pc.kept = &c->xs_kept;
+        pc.examined = nullptr;
+        if (wide) sk::k_candidates<TOut, D, uint32_t, kThreads><<<grid4, kThreads, 16, s>>>(pc);
+        else sk::k_candidates<TOut, D, uint8_t, kThreads><<<grid4, kThreads, 16, s>>>(pc);
+        ++ctx->launches;
+        run_exact<TOut, D>(ctx, s, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
+                           static_cast<const u64*>(ctx->s2_fsum.p), &c->xs, cap4, U(o_shist), U(o_scur));
+        sk::k_compact_members<TOut, D><<<nsm * 4, 256, 0, s>>>(
+            static_cast<const TOut*>(ctx->s2_rows.p), static_cast<const uint32_t*>(ctx->s2_ids.p),
+            static_cast<const uint8_t*>(ctx->flags.p), static_cast<const u64*>(ctx->s2_fsum.p), &c->xs,
+            static_cast<TOut*>(ctx->smp_rows.p), static_cast<u64*>(ctx->smp_fsum.p), &c->fs);
+        sk::k_strength_order<TOut, D><<<1, 1024, 0, s>>>(
+            static_cast<const TOut*>(ctx->smp_rows.p), static_cast<const u64*>(ctx->smp_fsum.p), &c->fs,
+            (uint32_t)pf_max, static_cast<TOut*>(ctx->f_rows.p), static_cast<u64*>(ctx->f_fsum.p), &c->nf,
+            static_cast<uint16_t*>(ctx->f_lists.p), static_cast<uint16_t*>(ctx->f_offs.p));
+        ctx->launches += 2;
+      }
     }
-    // sample points not strictly dominated at layer rho -> X (s2 buffers)
-    sk::CandParams pc{};
-    pc.rows = ctx->smp_rows.p;
-    pc.ids = static_cast<const uint32_t*>(ctx->smp_ids.p);
-    pc.count = nullptr;
-    pc.count_const = m;
-    pc.rho = rho;
-    pc.PM = test_b ? ctx->table_s.p : nullptr;
-    pc.f_max = 0;
-    pc.out_rows = ctx->s2_rows.p;
-    pc.out_ids = static_cast<uint32_t*>(ctx->s2_ids.p);
-    pc.out_fsum = static_cast<u64*>(ctx->s2_fsum.p);
-    pc.out_reserved = &ctr->xs;
-    pc.chunk = kChunk4;
-    pc.kept = &ctr->xs_kept;
-    pc.examined = nullptr;
-    if (wide) sk::k_candidates<TOut, D, uint32_t, kThreads><<<grid4, kThreads, 16, s>>>(pc);
-    else sk::k_candidates<TOut, D, uint8_t, kThreads><<<grid4, kThreads, 16, s>>>(pc);
+
+    // K1: the streaming pass
+    sk::StreamParams p1{};
+    p1.coords = q.dev_coords;
+    p1.n = n;
+    p1.rho = rho;
+    p1.la = la;
+    p1.lo_words = lo_words;
+    p1.h_entries = h_entries;
+    p1.nm = q.nm;
+    p1.H = static_cast<const uint8_t*>(ctx->H.p);
+    p1.PMs = test_b ? ctx->table_s.p : nullptr;
+    p1.pms_wide = wide;
+    p1.occ_rho = occ(rho);
+    p1.occ_rm1 = rho >= 2 ? occ(rho - 1) : nullptr;
+    p1.slabs = static_cast<uint32_t*>(ctx->slabs.p);
+    p1.out_rows = ctx->s1_rows.p;
+    p1.out_ids = static_cast<uint32_t*>(ctx->s1_ids.p);
+    p1.out_reserved = &c->s1;
+    p1.chunk = kChunk1;
+    p1.kept = &c->s1_kept;
+    p1.nonfinite = &c->nonfinite;
+    p1.id_base = q.id_base;
+    if (q.timed) ck(cudaEventRecord(ctx->ev[4], s), "event");
+    kstream<<<grid1, kStreamThreads, smem1, s>>>(p1);
     ++ctx->launches;
-    run_exact<TOut, D>(ctx, s, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
-                       static_cast<const u64*>(ctx->s2_fsum.p), &ctr->xs, cap4, static_cast<unsigned*>(at(o_shist)),
-                       static_cast<unsigned*>(at(o_scur)));
-    sk::k_compact_members<TOut, D><<<nsm * 4, 256, 0, s>>>(
-        static_cast<const TOut*>(ctx->s2_rows.p), static_cast<const uint32_t*>(ctx->s2_ids.p),
-        static_cast<const uint8_t*>(ctx->flags.p), static_cast<const u64*>(ctx->s2_fsum.p), &ctr->xs,
-        static_cast<TOut*>(ctx->smp_rows.p), static_cast<u64*>(ctx->smp_fsum.p), &ctr->fs);
-    sk::k_strength_order<TOut, D><<<1, 1024, 0, s>>>(
-        static_cast<const TOut*>(ctx->smp_rows.p), static_cast<const u64*>(ctx->smp_fsum.p), &ctr->fs,
-        (uint32_t)pf_max, static_cast<TOut*>(ctx->f_rows.p), static_cast<u64*>(ctx->f_fsum.p), &ctr->nf,
-        static_cast<uint16_t*>(ctx->f_lists.p), static_cast<uint16_t*>(ctx->f_offs.p));
-    ++ctx->launches;
+    if (q.timed) ck(cudaEventRecord(ctx->ev[5], s), "event");
+    if (lo_words) {
+      const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((lo_words + 255) / 256, (u64)nsm * 8));
+      sk::k_reduce_slabs<<<g, 256, 0, s>>>(static_cast<uint32_t*>(ctx->slabs.p), grid1, lo_words, occ(la - 1));
+      ++ctx->launches;
+    }
+    if (q.timed) ck(cudaEventRecord(ctx->ev[1], s), "event");
+  }
+
+  // ---- sharded exchange 1: the occupancy region of every layer
+  u64 occ_bytes() const override { return o_end - o_occ[1]; }
+  void export_occ(void* dst) override {
+    ck(cudaMemcpyAsync(dst, at(o_occ[1]), occ_bytes(), cudaMemcpyDeviceToDevice, s), "occ export");
+  }
+  void or_gathered(const void* gathered, int world) override {
+    const u64 w4 = occ_bytes() / 16;
+    const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((w4 + 255) / 256, (u64)nsm * 8));
+    sk::k_or_gather<<<g, 256, 0, s>>>(static_cast<const uint4*>(gathered), world, w4,
+                                      static_cast<uint4*>(at(o_occ[1])));
     ++ctx->launches;
   }
 
-  // ---- K1: the streaming pass
-  sk::StreamParams p1{};
-  p1.coords = q.dev_coords;
-  p1.n = n;
-  p1.rho = rho;
-  p1.la = la;
-  p1.lo_words = lo_words;
-  p1.h_entries = h_entries;
-  p1.nm = q.nm;
-  p1.H = static_cast<const uint8_t*>(ctx->H.p);
-  p1.PMs = test_b ? ctx->table_s.p : nullptr;
-  p1.pms_wide = wide;
-  p1.occ_rho = occ(rho);
-  p1.occ_rm1 = rho >= 2 ? occ(rho - 1) : nullptr;
-  p1.slabs = static_cast<uint32_t*>(ctx->slabs.p);
-  p1.out_rows = ctx->s1_rows.p;
-  p1.out_ids = static_cast<uint32_t*>(ctx->s1_ids.p);
-  p1.out_reserved = &ctr->s1;
-  p1.chunk = kChunk1;
-  p1.kept = &ctr->s1_kept;
-  p1.nonfinite = &ctr->nonfinite;
-  if (q.timed) ck(cudaEventRecord(ctx->ev[4], s), "event");
-  kstream<<<grid1, kStreamThreads, smem1, s>>>(p1);
-  ++ctx->launches;
-  if (q.timed) ck(cudaEventRecord(ctx->ev[5], s), "event");
-  if (lo_words) {
-    const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((lo_words + 255) / 256, (u64)nsm * 8));
-    sk::k_reduce_slabs<<<g, 256, 0, s>>>(static_cast<uint32_t*>(ctx->slabs.p), grid1, lo_words, occ(la - 1));
-    ++ctx->launches;
-  }
-  if (q.timed) ck(cudaEventRecord(ctx->ev[1], s), "event");
+  // ---- K3 (tables + per-layer counts on the side stream) + K4
+  void prune() {
+    DevCounters* c = ctr();
+    if (wide) launch_tables<uint32_t>(ctx, s, occ(rho), rho, D, static_cast<uint32_t*>(ctx->table.p));
+    else launch_tables<uint8_t>(ctx, s, occ(rho), rho, D, static_cast<uint8_t*>(ctx->table.p));
+    if (q.timed) ck(cudaEventRecord(ctx->ev[2], s), "event");
 
-  // ---- K3: layer-rho prefix-min table of the survivors' occupancy
-  if (wide) launch_tables<uint32_t>(ctx, s, occ(rho), rho, D, static_cast<uint32_t*>(ctx->table.p));
-  else launch_tables<uint8_t>(ctx, s, occ(rho), rho, D, static_cast<uint8_t*>(ctx->table.p));
-  if (q.timed) ck(cudaEventRecord(ctx->ev[2], s), "event");
-
-  // ---- side stream: per-layer |KS_i|, |CS_i| (refine.cpp:125-147), overlapped with K4/K5.
-  // Layer rho from O'_rho; below, O'_rho is OR-ed down into the partial
-  // occupancies recorded by the filter.
-  ck(cudaEventRecord(ctx->ev_fork, s), "event");
-  ck(cudaStreamWaitEvent(s2, ctx->ev_fork, 0), "wait");
-  {
-    if (wide) launch_count<uint32_t>(ctx, s2, occ(rho), rho, D, static_cast<const uint32_t*>(ctx->table.p), &ctr->cand[rho - 1], &ctr->key[rho - 1]);
-    else launch_count<uint8_t>(ctx, s2, occ(rho), rho, D, static_cast<const uint8_t*>(ctx->table.p), &ctr->cand[rho - 1], &ctr->key[rho - 1]);
+    // Per-layer |KS_i|, |CS_i| (refine.cpp:125-147), overlapped with K4/K5.
+    // Layer rho from O'_rho; below, O'_rho is OR-ed down into the partial
+    // occupancies recorded by the filter.
+    ck(cudaEventRecord(ctx->ev_fork, s), "event");
+    ck(cudaStreamWaitEvent(s2, ctx->ev_fork, 0), "wait");
+    if (wide) launch_count<uint32_t>(ctx, s2, occ(rho), rho, D, static_cast<const uint32_t*>(ctx->table.p), &c->cand[rho - 1], &c->key[rho - 1]);
+    else launch_count<uint8_t>(ctx, s2, occ(rho), rho, D, static_cast<const uint8_t*>(ctx->table.p), &c->cand[rho - 1], &c->key[rho - 1]);
     for (int L = rho - 1; L >= 1; --L) {
       const u64 src_words = words_at(L + 1);
       const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((src_words + 255) / 256, (u64)nsm * 8));
@@ -415,36 +495,34 @@ void run_pipeline(Query& q) {
       ++ctx->launches;
       if (L > 7) {
         launch_tables<uint32_t>(ctx, s2, occ(L), L, D, static_cast<uint32_t*>(ctx->table2.p));
-        launch_count<uint32_t>(ctx, s2, occ(L), L, D, static_cast<const uint32_t*>(ctx->table2.p), &ctr->cand[L - 1], &ctr->key[L - 1]);
+        launch_count<uint32_t>(ctx, s2, occ(L), L, D, static_cast<const uint32_t*>(ctx->table2.p), &c->cand[L - 1], &c->key[L - 1]);
       } else {
         launch_tables<uint8_t>(ctx, s2, occ(L), L, D, static_cast<uint8_t*>(ctx->table2.p));
-        launch_count<uint8_t>(ctx, s2, occ(L), L, D, static_cast<const uint8_t*>(ctx->table2.p), &ctr->cand[L - 1], &ctr->key[L - 1]);
+        launch_count<uint8_t>(ctx, s2, occ(L), L, D, static_cast<const uint8_t*>(ctx->table2.p), &c->cand[L - 1], &c->key[L - 1]);
       }
     }
-  }
-  ck(cudaEventRecord(ctx->ev_join, s2), "event");
+    ck(cudaEventRecord(ctx->ev_join, s2), "event");
 
-  // ---- K4: candidate cells + sample-skyline point filter
-  {
+    // K4: candidate cells + sample-skyline point filter
     sk::CandParams pc{};
     pc.rows = ctx->s1_rows.p;
     pc.ids = static_cast<const uint32_t*>(ctx->s1_ids.p);
-    pc.count = &ctr->s1;
+    pc.count = &c->s1;
     pc.rho = rho;
     pc.PM = ctx->table.p;
     pc.f_rows = ctx->f_rows.p;
     pc.f_fsum = static_cast<const u64*>(ctx->f_fsum.p);
-    pc.f_count = &ctr->nf;
-    pc.f_max = (uint32_t)pf_max;
+    pc.f_count = q.merge ? &c->nf : nullptr;
+    pc.f_max = q.merge ? (uint32_t)pf_max : 0;
     pc.f_lists = static_cast<const uint16_t*>(ctx->f_lists.p);
     pc.f_offs = static_cast<const uint16_t*>(ctx->f_offs.p);
     pc.out_rows = ctx->s2_rows.p;
     pc.out_ids = static_cast<uint32_t*>(ctx->s2_ids.p);
     pc.out_fsum = static_cast<u64*>(ctx->s2_fsum.p);
-    pc.out_reserved = &ctr->s2;
+    pc.out_reserved = &c->s2;
     pc.chunk = kChunk4;
-    pc.kept = &ctr->s2_kept;
-    pc.examined = &ctr->examined;
+    pc.kept = &c->s2_kept;
+    pc.examined = &c->examined;
     if (wide) {
       auto kc = sk::k_candidates<TOut, D, uint32_t, kThreads>;
       ck(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pf), "smem attr");
@@ -457,175 +535,283 @@ void run_pipeline(Query& q) {
     ++ctx->launches;
   }
 
-  // ---- K5: exact sort-first pass over the remaining points
-  run_exact<TOut, D>(ctx, s, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
-                     static_cast<const u64*>(ctx->s2_fsum.p), &ctr->s2, cap4, static_cast<unsigned*>(at(o_hist)),
-                     static_cast<unsigned*>(at(o_cur)));
-  // ---- K6: ids in ascending order through the id bitmap
-  {
-    uint32_t* idbits = static_cast<uint32_t*>(at(o_idbits));
-    unsigned* bcount = static_cast<unsigned*>(at(o_bcount));
-    const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((cap4 + 255) / 256, (u64)nsm * 8));
-    sk::k_mark_ids<<<g, 256, 0, s>>>(static_cast<const uint32_t*>(ctx->s2_ids.p),
-                                     static_cast<const uint8_t*>(ctx->flags.p), &ctr->s2, idbits);
+  // ---- K5 over S2 (the local point set)
+  void exact_local() {
+    DevCounters* c = ctr();
+    run_exact<TOut, D>(ctx, s, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
+                       static_cast<const u64*>(ctx->s2_fsum.p), &c->s2, cap4, U(o_hist), U(o_cur), 0, nullptr,
+                       cell_level());
+  }
+
+  // ---- K6: members' ids in ascending order through the id bitmap
+  void ids_out(const uint32_t* ids, const u64* count, u64 cap, uint32_t* dst) {
+    DevCounters* c = ctr();
+    uint32_t* idbits = U(o_idbits);
+    unsigned* bcount = U(o_bcount);
+    const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((cap + 255) / 256, (u64)nsm * 8));
+    sk::k_mark_ids<<<g, 256, 0, s>>>(ids, static_cast<const uint8_t*>(ctx->flags.p), count, idbits, q.id_base);
     sk::k_bits_count<<<bit_blocks, sk::kBitsThreads, 0, s>>>(idbits, id_words, bcount);
-    sk::k_bits_scan<<<1, 1024, 0, s>>>(bcount, bit_blocks, &ctr->fin);
-    sk::k_bits_write<<<bit_blocks, sk::kBitsThreads, 0, s>>>(idbits, id_words, bcount,
-                                                              q.ids_dev ? q.ids_dev : static_cast<uint32_t*>(ctx->ids_dev.p));
+    sk::k_bits_scan<<<1, 1024, 0, s>>>(bcount, bit_blocks, &c->fin);
+    sk::k_bits_write<<<bit_blocks, sk::kBitsThreads, 0, s>>>(idbits, id_words, bcount, dst, q.id_base);
     ctx->launches += 4;
   }
-  ck(cudaGetLastError(), "kernel launch");
-  if (q.timed) ck(cudaEventRecord(ctx->ev[3], s), "event");
-  ck(cudaStreamWaitEvent(s, ctx->ev_join, 0), "join");
 
-  // ---- results
-  ck(cudaMemcpyAsync(ctx->host_ctr, ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s), "counters D2H");
-  ck(cudaStreamSynchronize(s), "query");
-  const DevCounters& hc = *ctx->host_ctr;
-  if (q.stats) {
-    q.stats->n_layers = rho;
-    for (int L = 1; L <= rho; ++L) {
-      q.stats->keys[L - 1] = hc.key[L - 1] + (u64)D;
-      q.stats->candidates[L - 1] = (q.mode == SKYCELL_SEQUENTIAL && L != rho) ? -1 : (int64_t)hc.cand[L - 1];
-    }
-    q.stats->points_examined = hc.examined;
-    q.stats->survivors_stream = hc.s1_kept;
-    q.stats->survivors_filter = hc.s2_kept;
+  uint32_t* id_dst() const { return q.ids_dev ? q.ids_dev : static_cast<uint32_t*>(ctx->ids_dev.p); }
+
+  void read_counters() {
+    ck(cudaStreamWaitEvent(s, ctx->ev_join, 0), "join");
+    ck(cudaMemcpyAsync(ctx->host_ctr, ctr(), sizeof(DevCounters), cudaMemcpyDeviceToHost, s), "counters D2H");
+    ck(cudaStreamSynchronize(s), "query");
   }
+
+  void fill_stats(skycell_gpu_stats* st) const {
+    if (!st) return;
+    const DevCounters& hc = *ctx->host_ctr;
+    st->n_layers = rho;
+    for (int L = 1; L <= rho; ++L) {
+      st->keys[L - 1] = hc.key[L - 1] + (u64)D;
+      st->candidates[L - 1] = (q.mode == SKYCELL_SEQUENTIAL && L != rho) ? -1 : (int64_t)hc.cand[L - 1];
+    }
+    st->points_examined = hc.examined;
+    st->survivors_stream = hc.s1_kept;
+    st->survivors_filter = hc.s2_kept;
+  }
+
+  void check_finite() const {
+    const DevCounters& hc = *ctx->host_ctr;
+    if (hc.nonfinite)
+      throw ApiFail{SKYCELL_INPUT,
+                    "normalize: non-finite coordinate in record " + std::to_string((u64)q.id_base + ~hc.nonfinite)};
+  }
+
+  // ---- the single-device query
+  void run_single() {
+    DevCounters* c = ctr();
+    local();
+    prune();
+    exact_local();
+    ids_out(static_cast<const uint32_t*>(ctx->s2_ids.p), &c->s2, cap4, id_dst());
+    ck(cudaGetLastError(), "kernel launch");
+    if (q.timed) ck(cudaEventRecord(ctx->ev[3], s), "event");
+    read_counters();
+    fill_stats(q.stats);
+  }
+
+  // ---- sharded phase 2: prune against the global occupancy, local skyline
+  u64 prune_local_skyline() override {
+    DevCounters* c = ctr();
+    prune();
+    exact_local();
+    ensure(ctx->sky_rows, cap4 * D * sizeof(TOut));
+    ensure(ctx->sky_fsum, cap4 * 8);
+    ensure(ctx->sky_ids, cap4 * 4);
+    sk::k_pack_members<TOut, D><<<nsm * 4, 256, 0, s>>>(
+        static_cast<const TOut*>(ctx->s2_rows.p), static_cast<const uint32_t*>(ctx->s2_ids.p),
+        static_cast<const uint8_t*>(ctx->flags.p), static_cast<const u64*>(ctx->s2_fsum.p), &c->s2,
+        static_cast<TOut*>(ctx->sky_rows.p), static_cast<u64*>(ctx->sky_fsum.p),
+        static_cast<uint32_t*>(ctx->sky_ids.p), &c->lsky);
+    ++ctx->launches;
+    ck(cudaGetLastError(), "kernel launch");
+    read_counters();
+    check_finite();
+    return ctx->host_ctr->lsky;
+  }
+
+  // Block layout of one rank's local skyline in the exchange buffer:
+  // [rows maxc x D x TOut][fsum maxc x u64][ids maxc x u32], 256-B aligned.
+  static u64 al(u64 b) { return (b + 255) & ~255ull; }
+  u64 rows_bytes(u64 maxc) const { return al(maxc * D * sizeof(TOut)); }
+  u64 block_bytes(u64 maxc) const override { return rows_bytes(maxc) + al(maxc * 8) + al(maxc * 4); }
+
+  void pack(void* dst, u64 maxc) override {
+    const u64 cnt = ctx->host_ctr->lsky;
+    char* b = static_cast<char*>(dst);
+    if (cnt) {
+      ck(cudaMemcpyAsync(b, ctx->sky_rows.p, cnt * D * sizeof(TOut), cudaMemcpyDeviceToDevice, s), "pack");
+      ck(cudaMemcpyAsync(b + rows_bytes(maxc), ctx->sky_fsum.p, cnt * 8, cudaMemcpyDeviceToDevice, s), "pack");
+      ck(cudaMemcpyAsync(b + rows_bytes(maxc) + al(maxc * 8), ctx->sky_ids.p, cnt * 4, cudaMemcpyDeviceToDevice, s),
+         "pack");
+    }
+    if (maxc > cnt) {
+      uint32_t* ids = reinterpret_cast<uint32_t*>(b + rows_bytes(maxc) + al(maxc * 8));
+      sk::k_fill_u32<<<nsm, 256, 0, s>>>(ids + cnt, maxc - cnt, sk::kNoId);
+      ++ctx->launches;
+    }
+  }
+
+  // ---- sharded phase 3: own local skyline against the union -> ids
+  void finish(const void* recv, int world, u64 maxc, int rank, u64 own_count, uint32_t* ids_dst, uint64_t* n_out,
+              skycell_gpu_stats* st) override {
+    DevCounters* c = ctr();
+    const u64 un = (u64)world * maxc;
+    const u64 cap = std::max<u64>(un, 1);
+    // the union, unpacked into flat slot arrays (S2's buffers are free now)
+    ensure(ctx->s2_rows, cap * D * sizeof(TOut));
+    ensure(ctx->s2_fsum, cap * 8);
+    ensure(ctx->s2_ids, cap * 4);
+    ensure(ctx->flags, cap);
+    ensure(ctx->lists, (size_t)D * cap * 4);
+    const char* r = static_cast<const char*>(recv);
+    const u64 bb = block_bytes(maxc);
+    if (maxc) {
+      ck(cudaMemcpy2DAsync(ctx->s2_rows.p, maxc * D * sizeof(TOut), r, bb, maxc * D * sizeof(TOut), world,
+                           cudaMemcpyDeviceToDevice, s), "unpack rows");
+      ck(cudaMemcpy2DAsync(ctx->s2_fsum.p, maxc * 8, r + rows_bytes(maxc), bb, maxc * 8, world,
+                           cudaMemcpyDeviceToDevice, s), "unpack sums");
+      ck(cudaMemcpy2DAsync(ctx->s2_ids.p, maxc * 4, r + rows_bytes(maxc) + al(maxc * 8), bb, maxc * 4, world,
+                           cudaMemcpyDeviceToDevice, s), "unpack ids");
+    }
+    ctx->host_param[0] = un;
+    ctx->host_param[1] = (u64)rank * maxc + own_count;
+    ck(cudaMemcpyAsync(&c->un, ctx->host_param, 16, cudaMemcpyHostToDevice, s), "params");
+    ck(cudaMemsetAsync(ctx->flags.p, 0, cap, s), "flags");
+    run_exact<TOut, D>(ctx, s, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
+                       static_cast<const u64*>(ctx->s2_fsum.p), &c->un, cap, U(o_fhist), U(o_fcur),
+                       (u64)rank * maxc, &c->qend, cell_level());
+    ids_out(static_cast<const uint32_t*>(ctx->s2_ids.p), &c->un, cap, ids_dst ? ids_dst : id_dst());
+    ck(cudaGetLastError(), "kernel launch");
+    if (q.timed) ck(cudaEventRecord(ctx->ev[3], s), "event");
+    read_counters();
+    *n_out = ctx->host_ctr->fin;
+    fill_stats(st);
+  }
+};
+
+// --------------------------------------------------------- query plumbing
+template <typename TIn>
+const void* stage_input(skycell_gpu_ctx* ctx, const TIn* coords, u64 n, int d) {
+  // Input residency: device pointers are used in place when 16-byte
+  // aligned; host pointers (and misaligned device pointers) are staged.
+  cudaPointerAttributes attr{};
+  const bool on_device = cudaPointerGetAttributes(&attr, coords) == cudaSuccess &&
+                         (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged);
+  cudaGetLastError();
+  if (on_device && !(reinterpret_cast<uintptr_t>(coords) & 15)) return coords;
+  const size_t bytes = n * (size_t)d * sizeof(TIn);
+  ensure(ctx->staging, bytes);
+  ck(cudaMemcpyAsync(ctx->staging.p, coords, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                     ctx->stream),
+     "input copy");
+  return ctx->staging.p;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a{};
+  const bool dev = p && cudaPointerGetAttributes(&a, p) == cudaSuccess &&
+                   (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged);
+  cudaGetLastError();
+  return dev;
+}
+
+// normalize() runs before the grid checks (refine.cpp:113 then :117): with an
+// invalid rho a non-finite record still wins.
+template <typename TIn>
+void reject_rho(skycell_gpu_ctx* ctx, const void* dev_coords, u64 n, int d, const Status& rs, u64 id_base) {
+  ensure(ctx->reset, 256);
+  ck(cudaMemsetAsync(ctx->reset.p, 0, 8, ctx->stream), "memset");
+  sk::k_check_finite<TIn><<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(static_cast<const TIn*>(dev_coords), n * d, d,
+                                                                      static_cast<u64*>(ctx->reset.p));
+  u64 nf = 0;
+  ck(cudaMemcpyAsync(&nf, ctx->reset.p, 8, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+  ck(cudaStreamSynchronize(ctx->stream), "sync");
+  if (nf) throw ApiFail{SKYCELL_INPUT, "normalize: non-finite coordinate in record " + std::to_string(id_base + ~nf)};
+  throw ApiFail{rs.code, rs.msg};
+}
+
+// Builds the Query (validation, staging, normalisation constants).
+template <typename TIn>
+Query make_query(skycell_gpu_ctx* ctx, const TIn* coords, u64 n, int d, const double* dmin, const double* dmax,
+                 int rho, int mode, int merge, uint32_t* ids_out, skycell_gpu_stats* stats, u64 id_base) {
+  Status st = validate_shape(n, d);
+  if (st.code) throw ApiFail{st.code, st.msg};
+  if (!ctx) throw ApiFail{SKYCELL_USAGE, "skycell_gpu: null context"};
+  if (!coords || !dmin || !dmax) throw ApiFail{SKYCELL_USAGE, "skycell_gpu: null coordinate or range pointer"};
+  ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+  ctx->launches = 0;
+  const void* dev_coords = stage_input<TIn>(ctx, coords, n, d);
+  Status rs = validate_rho(rho, d);
+  if (rs.code) reject_rho<TIn>(ctx, dev_coords, n, d, rs, id_base);
+  if ((u64)rho * d > 36 || (u64)rho * (d - 1) > 30)
+    throw ApiFail{SKYCELL_UNSUPPORTED, "skycell_gpu: rho*d = " + std::to_string(rho * d) +
+                                           " needs the sparse cell index (dense bitmaps are limited to 2^36 cells)"};
+  Query q{};
+  q.ctx = ctx;
+  q.n = n;
+  q.d = d;
+  q.rho = rho;
+  q.mode = mode;
+  q.merge = merge;
+  q.stats = stats;
+  q.timed = stats != nullptr;
+  q.dev_coords = dev_coords;
+  q.ids_dev = is_device_ptr(ids_out) ? ids_out : nullptr;
+  q.id_base = (uint32_t)id_base;
+  // scale[k] = range > 0 ? 1/range : 0, dataset.cpp:32-36 (host, FP64).
+  for (int k = 0; k < d; ++k) {
+    const double range = dmax[k] - dmin[k];
+    q.nm.mn[k] = dmin[k];
+    q.nm.sc[k] = range > 0 ? 1.0 / range : 0.0;
+  }
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  return q;
 }
 
 template <typename TIn>
-int run_query(skycell_gpu_ctx* ctx, const TIn* coords, u64 n, int d, const double* dmin, const double* dmax,
-              int rho, int mode, int merge, uint32_t* ids_out, uint64_t* n_out, skycell_gpu_stats* stats, char* err,
-              size_t err_len) {
-  try {
-    Status st = validate_shape(n, d);
-    if (st.code) {
-      put_err(err, err_len, st.msg);
-      return st.code;
-    }
-    if (!ctx) {
-      put_err(err, err_len, "skycell_gpu: null context");
-      return SKYCELL_USAGE;
-    }
-    if (!merge) {
-      put_err(err, err_len, "skycell_gpu: merge_cross_cell=false is not implemented on the GPU path yet");
-      return SKYCELL_UNSUPPORTED;
-    }
-    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
-    const auto t_begin = std::chrono::steady_clock::now();
-    cudaStream_t s = ctx->stream;
-    ctx->launches = 0;
+bool identity_range(const Query& q, const double* dmin, const double* dmax) {
+  if (sizeof(TIn) != 4) return false;
+  for (int k = 0; k < q.d; ++k)
+    if (!(dmin[k] == 0.0 && dmax[k] == 1.0)) return false;
+  return true;
+}
 
-    // Input residency: device pointers are used in place when 16-byte
-    // aligned; host pointers (and misaligned device pointers) are staged.
-    cudaPointerAttributes attr{};
-    const bool on_device = cudaPointerGetAttributes(&attr, coords) == cudaSuccess &&
-                           (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged);
-    cudaGetLastError();
-    const size_t bytes = n * (size_t)d * sizeof(TIn);
-    const void* dev_coords = coords;
-    if (!on_device || (reinterpret_cast<uintptr_t>(coords) & 15)) {
-      ensure(ctx->staging, bytes);
-      ck(cudaMemcpyAsync(ctx->staging.p, coords, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s),
-         "input copy");
-      dev_coords = ctx->staging.p;
-    }
-
-    Status rs = validate_rho(rho, d);
-    if (rs.code) {
-      // normalize() runs before the grid checks: a non-finite record wins.
-      ensure(ctx->reset, 256);
-      ck(cudaMemsetAsync(ctx->reset.p, 0, 8, s), "memset");
-      sk::k_check_finite<TIn><<<ctx->num_sms * 4, 256, 0, s>>>(static_cast<const TIn*>(dev_coords), n * d, d,
-                                                               static_cast<u64*>(ctx->reset.p));
-      u64 nf = 0;
-      ck(cudaMemcpyAsync(&nf, ctx->reset.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
-      ck(cudaStreamSynchronize(s), "sync");
-      if (nf) {
-        put_err(err, err_len, "normalize: non-finite coordinate in record " + std::to_string(~nf));
-        return SKYCELL_INPUT;
-      }
-      put_err(err, err_len, rs.msg);
-      return rs.code;
-    }
-    if ((u64)rho * d > 36 || (u64)rho * (d - 1) > 30) {
-      put_err(err, err_len, "skycell_gpu: rho*d = " + std::to_string(rho * d) +
-                                " needs the sparse cell index (dense bitmaps are limited to 2^36 cells)");
-      return SKYCELL_UNSUPPORTED;
-    }
-
-    Query q{};
-    q.ctx = ctx;
-    q.n = n;
-    q.d = d;
-    q.rho = rho;
-    q.mode = mode;
-    q.merge = merge;
-    q.stats = stats;
-    q.timed = stats != nullptr;
-    q.dev_coords = dev_coords;
-    cudaPointerAttributes oattr{};
-    const bool out_dev = cudaPointerGetAttributes(&oattr, ids_out) == cudaSuccess &&
-                         (oattr.type == cudaMemoryTypeDevice || oattr.type == cudaMemoryTypeManaged);
-    cudaGetLastError();
-    q.ids_dev = out_dev ? ids_out : nullptr;
-    // scale[k] = range > 0 ? 1/range : 0, dataset.cpp:32-36 (host, FP64).
-    bool ident = true;
-    for (int k = 0; k < d; ++k) {
-      const double range = dmax[k] - dmin[k];
-      q.nm.mn[k] = dmin[k];
-      q.nm.sc[k] = range > 0 ? 1.0 / range : 0.0;
-      ident &= dmin[k] == 0.0 && dmax[k] == 1.0;
-    }
-    if (stats) std::memset(stats, 0, sizeof(*stats));
-
-    constexpr bool kF32 = sizeof(TIn) == 4;
-#define SKYCELL_CASE(DD)                                              \
-  case DD:                                                            \
-    if constexpr (kF32) {                                             \
-      if (ident) run_pipeline<float, float, true, DD>(q);             \
-      else run_pipeline<float, double, false, DD>(q);                 \
-    } else {                                                          \
-      run_pipeline<double, double, false, DD>(q);                     \
-    }                                                                 \
+// Dispatch on (input type, identity range, d) to a Pipe instance.
+template <typename TIn, template <typename, typename, bool, int> class F, typename... A>
+void dispatch(const Query& q, bool ident, A&&... a) {
+  constexpr bool kF32 = sizeof(TIn) == 4;
+#define SKYCELL_CASE(DD)                                                \
+  case DD:                                                              \
+    if constexpr (kF32) {                                               \
+      if (ident) F<float, float, true, DD>::run(q, a...);               \
+      else F<float, double, false, DD>::run(q, a...);                   \
+    } else {                                                            \
+      F<double, double, false, DD>::run(q, a...);                       \
+    }                                                                   \
     break;
-    switch (d) {
-      SKYCELL_CASE(2) SKYCELL_CASE(3) SKYCELL_CASE(4) SKYCELL_CASE(5) SKYCELL_CASE(6) SKYCELL_CASE(7)
-      SKYCELL_CASE(8) SKYCELL_CASE(9) SKYCELL_CASE(10) SKYCELL_CASE(11) SKYCELL_CASE(12) SKYCELL_CASE(13)
-      SKYCELL_CASE(14) SKYCELL_CASE(15) SKYCELL_CASE(16)
-      default:
-        put_err(err, err_len, "normalize: dimensionality must be at most 16");
-        return SKYCELL_INPUT;
-    }
+  switch (q.d) {
+    SKYCELL_CASE(2) SKYCELL_CASE(3) SKYCELL_CASE(4) SKYCELL_CASE(5) SKYCELL_CASE(6) SKYCELL_CASE(7)
+    SKYCELL_CASE(8) SKYCELL_CASE(9) SKYCELL_CASE(10) SKYCELL_CASE(11) SKYCELL_CASE(12) SKYCELL_CASE(13)
+    SKYCELL_CASE(14) SKYCELL_CASE(15) SKYCELL_CASE(16)
+    default:
+      throw ApiFail{SKYCELL_INPUT, "normalize: dimensionality must be at most 16"};
+  }
 #undef SKYCELL_CASE
-    const DevCounters& hc = *ctx->host_ctr;
-    if (hc.nonfinite) {
-      put_err(err, err_len, "normalize: non-finite coordinate in record " + std::to_string(~hc.nonfinite));
-      return SKYCELL_INPUT;
-    }
-    const u64 count = hc.fin;
-    *n_out = count;
-    if (count && !out_dev) {
-      ck(cudaMemcpyAsync(ids_out, ctx->ids_dev.p, count * 4, cudaMemcpyDeviceToHost, s), "ids copy");
-      ck(cudaStreamSynchronize(s), "sync");
-    }
-    if (stats) {
-      float a = 0, b = 0, c = 0;
-      cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
-      cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]);
-      cudaEventElapsedTime(&c, ctx->ev[2], ctx->ev[3]);
-      stats->normalize_ms = 0.0;  // fused into the streaming pass (grid_ms)
-      stats->grid_ms = a;
-      stats->shrink_ms = b;
-      stats->refine_ms = c;
-      stats->total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_begin).count();
-      stats->kernel_launches = ctx->launches;
-      float k1 = 0;
-      cudaEventElapsedTime(&k1, ctx->ev[4], ctx->ev[5]);
-      stats->stream_kernel_ms = k1;
-    }
+}
+
+template <typename TIn, typename TOut, bool IDENT, int D>
+struct RunSingle {
+  static void run(const Query& q) {
+    Pipe<TIn, TOut, IDENT, D> p(q);
+    p.run_single();
+  }
+};
+
+template <typename TIn, typename TOut, bool IDENT, int D>
+struct MakeShard {
+  static void run(const Query& q, std::unique_ptr<PipeBase>* out) {
+    auto p = std::make_unique<Pipe<TIn, TOut, IDENT, D>>(q);
+    p->local();
+    *out = std::move(p);
+  }
+};
+
+template <typename F>
+int guarded(char* err, size_t err_len, F&& body) {
+  try {
+    body();
     return SKYCELL_OK;
+  } catch (const ApiFail& f) {
+    put_err(err, err_len, f.msg);
+    return f.code;
   } catch (const CudaFail& f) {
     put_err(err, err_len, std::string("CUDA error in ") + f.what + ": " + cudaGetErrorString(f.e));
     cudaGetLastError();
@@ -636,53 +822,110 @@ int run_query(skycell_gpu_ctx* ctx, const TIn* coords, u64 n, int d, const doubl
   }
 }
 
+template <typename TIn>
+int run_query(skycell_gpu_ctx* ctx, const TIn* coords, u64 n, int d, const double* dmin, const double* dmax,
+              int rho, int mode, int merge, uint32_t* ids_out, uint64_t* n_out, skycell_gpu_stats* stats, char* err,
+              size_t err_len) {
+  return guarded(err, err_len, [&] {
+    const auto t_begin = std::chrono::steady_clock::now();
+    if (!n_out || !ids_out) throw ApiFail{SKYCELL_USAGE, "skycell_gpu: null output pointer"};
+    Query q = make_query<TIn>(ctx, coords, n, d, dmin, dmax, rho, mode, merge, ids_out, stats, 0);
+    dispatch<TIn, RunSingle>(q, identity_range<TIn>(q, dmin, dmax));
+    const DevCounters& hc = *ctx->host_ctr;
+    if (hc.nonfinite)
+      throw ApiFail{SKYCELL_INPUT, "normalize: non-finite coordinate in record " + std::to_string(~hc.nonfinite)};
+    const u64 count = hc.fin;
+    *n_out = count;
+    if (count && !q.ids_dev) {
+      ck(cudaMemcpyAsync(ids_out, ctx->ids_dev.p, count * 4, cudaMemcpyDeviceToHost, ctx->stream), "ids copy");
+      ck(cudaStreamSynchronize(ctx->stream), "sync");
+    }
+    if (stats) {
+      float a = 0, b = 0, c = 0, k1 = 0;
+      cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
+      cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]);
+      cudaEventElapsedTime(&c, ctx->ev[2], ctx->ev[3]);
+      cudaEventElapsedTime(&k1, ctx->ev[4], ctx->ev[5]);
+      stats->normalize_ms = 0.0;  // fused into the streaming pass (grid_ms)
+      stats->grid_ms = a;
+      stats->shrink_ms = b;
+      stats->refine_ms = c;
+      stats->total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_begin).count();
+      stats->kernel_launches = ctx->launches;
+      stats->stream_kernel_ms = k1;
+    }
+  });
+}
+
+template <int D>
+void quadrant_launch(skycell_gpu_ctx* ctx, const double* dev, u64 n, const sk::Norm& org, u64 id_words,
+                     unsigned blocks, u64* d_count) {
+  cudaStream_t s = ctx->stream;
+  const int nsm = ctx->num_sms;
+  uint32_t* bits = static_cast<uint32_t*>(ctx->q_bits.p);
+  unsigned* bcount = reinterpret_cast<unsigned*>(bits + id_words);
+  const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((n + 255) / 256, (u64)nsm * 8));
+  sk::k_quadrant_mark<D><<<g, 256, 0, s>>>(dev, n, org, bits);
+  sk::k_bits_count<<<blocks, sk::kBitsThreads, 0, s>>>(bits, id_words, bcount);
+  sk::k_bits_scan<<<1, 1024, 0, s>>>(bcount, blocks, d_count);
+  sk::k_bits_write<<<blocks, sk::kBitsThreads, 0, s>>>(bits, id_words, bcount, static_cast<uint32_t*>(ctx->q_orig.p), 0);
+  sk::k_quadrant_gather<D><<<g, 256, 0, s>>>(dev, static_cast<const uint32_t*>(ctx->q_orig.p), d_count,
+                                             static_cast<double*>(ctx->q_sub.p), static_cast<u64*>(ctx->q_mm.p) + 2);
+  ctx->launches += 5;
+}
+
 }  // namespace
 
 extern "C" {
 
 int skycell_gpu_create(int device, skycell_gpu_ctx** out, char* err, size_t err_len) {
-  try {
+  return guarded(err, err_len, [&] {
+    if (!out) throw ApiFail{SKYCELL_USAGE, "skycell_gpu: null output handle"};
     int count = 0;
     ck(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
-    if (device < 0 || device >= count) {
-      put_err(err, err_len, "skycell_gpu: no CUDA device " + std::to_string(device));
-      return SKYCELL_CUDA;
-    }
+    if (device < 0 || device >= count) throw ApiFail{SKYCELL_CUDA, "skycell_gpu: no CUDA device " + std::to_string(device)};
     ck(cudaSetDevice(device), "cudaSetDevice");
     auto* ctx = new skycell_gpu_ctx();
     ctx->device = device;
     ck(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device), "attr");
-    ck(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking), "stream");
+    ctx->stream = ctx->own_stream;
     ck(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming), "event");
     ck(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming), "event");
     ck(cudaMallocHost(reinterpret_cast<void**>(&ctx->host_ctr), sizeof(DevCounters)), "pinned");
+    ck(cudaMallocHost(reinterpret_cast<void**>(&ctx->host_param), 64), "pinned");
     for (auto& e : ctx->ev) ck(cudaEventCreate(&e), "event");
     *out = ctx;
-    return SKYCELL_OK;
-  } catch (const CudaFail& f) {
-    put_err(err, err_len, std::string("CUDA error in ") + f.what + ": " + cudaGetErrorString(f.e));
-    return SKYCELL_CUDA;
-  }
+  });
 }
 
 void skycell_gpu_destroy(skycell_gpu_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
+  ctx->shard.reset();
   DevBuf* bufs[] = {&ctx->reset, &ctx->slabs, &ctx->H, &ctx->table, &ctx->table2, &ctx->table_s, &ctx->staging,
-                    &ctx->smp_rows, &ctx->smp_ids, &ctx->smp_fsum, &ctx->f_rows, &ctx->f_fsum, &ctx->f_lists, &ctx->f_offs,
-                    &ctx->lists, &ctx->ids_dev, &ctx->s1_rows, &ctx->s1_ids,
-                    &ctx->s2_rows, &ctx->s2_ids, &ctx->s2_fsum, &ctx->flags};
+                    &ctx->smp_rows, &ctx->smp_ids, &ctx->smp_fsum, &ctx->f_rows, &ctx->f_fsum, &ctx->f_lists,
+                    &ctx->f_offs, &ctx->lists, &ctx->ids_dev, &ctx->s1_rows, &ctx->s1_ids, &ctx->s2_rows,
+                    &ctx->s2_ids, &ctx->s2_fsum, &ctx->flags, &ctx->sky_rows, &ctx->sky_ids, &ctx->sky_fsum,
+                    &ctx->q_bits, &ctx->q_orig, &ctx->q_sub, &ctx->q_ids, &ctx->q_mm};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   if (ctx->host_ctr) cudaFreeHost(ctx->host_ctr);
+  if (ctx->host_param) cudaFreeHost(ctx->host_param);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->side) cudaStreamDestroy(ctx->side);
-  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
+}
+
+int skycell_gpu_set_stream(skycell_gpu_ctx* ctx, void* stream) {
+  if (!ctx) return SKYCELL_USAGE;
+  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  return SKYCELL_OK;
 }
 
 int skycell_gpu_skyline_f64(skycell_gpu_ctx* ctx, const double* coords, uint64_t n, int d, const double* dim_min,
@@ -699,28 +942,185 @@ int skycell_gpu_skyline_f32(skycell_gpu_ctx* ctx, const float* coords, uint64_t 
                           err, err_len);
 }
 
-int skycell_gpu_quadrant_f64(skycell_gpu_ctx*, const double*, uint64_t, int, const double*, int, int, int, uint32_t*,
-                             uint64_t*, skycell_gpu_stats*, char* err, size_t err_len) {
-  put_err(err, err_len, "skycell_gpu: quadrant_skyline not implemented yet");
-  return SKYCELL_UNSUPPORTED;
+int skycell_gpu_quadrant_f64(skycell_gpu_ctx* ctx, const double* coords, uint64_t n, int d, const double* origin,
+                             int origin_len, int rho, int mode, uint32_t* ids_out, uint64_t* n_out,
+                             skycell_gpu_stats* stats, char* err, size_t err_len) {
+  return guarded(err, err_len, [&] {
+    if (!ctx) throw ApiFail{SKYCELL_USAGE, "skycell_gpu: null context"};
+    if (!n_out || !ids_out) throw ApiFail{SKYCELL_USAGE, "skycell_gpu: null output pointer"};
+    // refine.cpp:162-163
+    if (origin_len != d)
+      throw ApiFail{SKYCELL_USAGE, "quadrant_skyline: origin arity does not match the dataset dimensionality"};
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    *n_out = 0;
+    if (n == 0) return;  // empty quadrant -> empty result (refine.cpp:176)
+    if (d < 1 || d > sk::kMaxD) throw ApiFail{SKYCELL_INPUT, "normalize: dimensionality must be at most 16"};
+    if (d < 2) throw ApiFail{SKYCELL_INPUT, "normalize: dimensionality must be at least 2"};
+    if (n > 0xffffffffull) throw ApiFail{SKYCELL_INPUT, "normalize: more than 2^32 - 1 records"};
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    ctx->launches = 0;
+    cudaStream_t s = ctx->stream;
+    const double* dev = static_cast<const double*>(stage_input<double>(ctx, coords, n, d));
+    const u64 id_words = (n + 31) / 32;
+    const unsigned blocks = (unsigned)((id_words + sk::kBitsBlock - 1) / sk::kBitsBlock);
+    ensure(ctx->q_bits, id_words * 4 + (u64)blocks * 4);
+    ensure(ctx->q_orig, n * 4);
+    ensure(ctx->q_sub, n * (u64)d * 8);
+    ensure(ctx->q_mm, (2 + 2 * (u64)d) * 8);
+    ck(cudaMemsetAsync(ctx->q_bits.p, 0, id_words * 4, s), "memset");
+    // q_mm = [count, pad, (min key, max key) x d]
+    ck(cudaMemsetAsync(ctx->q_mm.p, 0, 16, s), "memset");
+    std::vector<u64> init(2 * d);
+    for (int k = 0; k < d; ++k) {
+      init[2 * k] = ~0ull;
+      init[2 * k + 1] = 0;
+    }
+    ck(cudaMemcpyAsync(static_cast<u64*>(ctx->q_mm.p) + 2, init.data(), 16 * (u64)d, cudaMemcpyHostToDevice, s),
+       "mm init");
+    sk::Norm org{};
+    for (int k = 0; k < d; ++k) org.mn[k] = origin[k];
+    u64* d_count = static_cast<u64*>(ctx->q_mm.p);
+#define SKYCELL_Q(DD) \
+  case DD: quadrant_launch<DD>(ctx, dev, n, org, id_words, blocks, d_count); break;
+    switch (d) {
+      SKYCELL_Q(2) SKYCELL_Q(3) SKYCELL_Q(4) SKYCELL_Q(5) SKYCELL_Q(6) SKYCELL_Q(7) SKYCELL_Q(8) SKYCELL_Q(9)
+      SKYCELL_Q(10) SKYCELL_Q(11) SKYCELL_Q(12) SKYCELL_Q(13) SKYCELL_Q(14) SKYCELL_Q(15) SKYCELL_Q(16)
+    }
+#undef SKYCELL_Q
+    ck(cudaGetLastError(), "kernel launch");
+    std::vector<u64> mm(2 + 2 * d);
+    ck(cudaMemcpyAsync(mm.data(), ctx->q_mm.p, mm.size() * 8, cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "sync");
+    const u64 sub_n = mm[0];
+    if (sub_n == 0) return;  // refine.cpp:176
+    std::vector<double> mn(d), mx(d);
+    for (int k = 0; k < d; ++k) {
+      mn[k] = sk::dkey_inv(mm[2 + 2 * k]);
+      mx[k] = sk::dkey_inv(mm[2 + 2 * k + 1]);
+    }
+    // refine.cpp:179: sub_rho = min(rho, max(1, default_rho(sub.n, d)))
+    const int sub_rho = std::min(rho, std::max(1, default_rho(sub_n, d)));
+    ensure(ctx->q_ids, sub_n * 4);
+    uint32_t* sub_ids = static_cast<uint32_t*>(ctx->q_ids.p);
+    const u64 prior = ctx->launches;
+    uint64_t k = 0;
+    const int rc = run_query<double>(ctx, static_cast<const double*>(ctx->q_sub.p), sub_n, d, mn.data(), mx.data(),
+                                     sub_rho, mode, 1, sub_ids, &k, stats, err, err_len);
+    if (rc != SKYCELL_OK) throw ApiFail{rc, std::string(err ? err : "")};
+    ctx->launches += prior;
+    if (k) {
+      const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((k + 255) / 256, (u64)ctx->num_sms * 8));
+      sk::k_map_ids<<<g, 256, 0, s>>>(sub_ids, static_cast<const uint32_t*>(ctx->q_orig.p), k);
+      ++ctx->launches;
+      ck(cudaGetLastError(), "kernel launch");
+      if (is_device_ptr(ids_out)) ck(cudaMemcpyAsync(ids_out, sub_ids, k * 4, cudaMemcpyDeviceToDevice, s), "ids");
+      else ck(cudaMemcpyAsync(ids_out, sub_ids, k * 4, cudaMemcpyDeviceToHost, s), "ids");
+      ck(cudaStreamSynchronize(s), "sync");
+    }
+    *n_out = k;
+    if (stats) stats->kernel_launches = ctx->launches;
+  });
+}
+
+// ------------------------------------------------------ sharded query (§4)
+int skycell_gpu_shard_begin(skycell_gpu_ctx* ctx, const void* coords, int coords_f32, uint64_t n, int d,
+                            const double* dim_min, const double* dim_max, int rho, int mode, uint64_t id_base,
+                            uint64_t* occ_bytes, char* err, size_t err_len) {
+  return guarded(err, err_len, [&] {
+    if (!ctx || !occ_bytes) throw ApiFail{SKYCELL_USAGE, "skycell_gpu: null context or output pointer"};
+    ctx->shard.reset();
+    if (id_base + n > 0xffffffffull + 1) throw ApiFail{SKYCELL_INPUT, "normalize: more than 2^32 - 1 records"};
+    if (coords_f32) {
+      Query q = make_query<float>(ctx, static_cast<const float*>(coords), n, d, dim_min, dim_max, rho, mode, 1,
+                                  nullptr, nullptr, id_base);
+      q.timed = true;  // K1 events: stream_kernel_ms of the finish stats
+      dispatch<float, MakeShard>(q, identity_range<float>(q, dim_min, dim_max), &ctx->shard);
+    } else {
+      Query q = make_query<double>(ctx, static_cast<const double*>(coords), n, d, dim_min, dim_max, rho, mode, 1,
+                                   nullptr, nullptr, id_base);
+      q.timed = true;
+      dispatch<double, MakeShard>(q, false, &ctx->shard);
+    }
+    ck(cudaGetLastError(), "kernel launch");
+    *occ_bytes = ctx->shard->occ_bytes();
+  });
+}
+
+int skycell_gpu_shard_export_occ(skycell_gpu_ctx* ctx, void* dev_dst, char* err, size_t err_len) {
+  return guarded(err, err_len, [&] {
+    if (!ctx || !ctx->shard) throw ApiFail{SKYCELL_USAGE, "skycell_gpu: no sharded query in flight"};
+    ctx->shard->export_occ(dev_dst);
+  });
+}
+
+int skycell_gpu_shard_prune(skycell_gpu_ctx* ctx, const void* dev_gathered, int world, uint64_t* local_count,
+                            char* err, size_t err_len) {
+  return guarded(err, err_len, [&] {
+    if (!ctx || !ctx->shard) throw ApiFail{SKYCELL_USAGE, "skycell_gpu: no sharded query in flight"};
+    if (world < 1 || !dev_gathered || !local_count) throw ApiFail{SKYCELL_USAGE, "skycell_gpu: bad exchange buffer"};
+    ctx->shard->or_gathered(dev_gathered, world);
+    *local_count = ctx->shard->prune_local_skyline();
+  });
+}
+
+uint64_t skycell_gpu_shard_block_bytes(skycell_gpu_ctx* ctx, uint64_t max_count) {
+  if (!ctx || !ctx->shard) return 0;
+  return ctx->shard->block_bytes(max_count);
+}
+
+int skycell_gpu_shard_pack(skycell_gpu_ctx* ctx, void* dev_dst, uint64_t max_count, char* err, size_t err_len) {
+  return guarded(err, err_len, [&] {
+    if (!ctx || !ctx->shard) throw ApiFail{SKYCELL_USAGE, "skycell_gpu: no sharded query in flight"};
+    ctx->shard->pack(dev_dst, max_count);
+  });
+}
+
+int skycell_gpu_shard_finish(skycell_gpu_ctx* ctx, const void* dev_recv, int world, uint64_t max_count, int rank,
+                             uint64_t own_count, uint32_t* ids_out, uint64_t* n_out, skycell_gpu_stats* stats,
+                             char* err, size_t err_len) {
+  return guarded(err, err_len, [&] {
+    if (!ctx || !ctx->shard) throw ApiFail{SKYCELL_USAGE, "skycell_gpu: no sharded query in flight"};
+    if (rank < 0 || rank >= world || !n_out) throw ApiFail{SKYCELL_USAGE, "skycell_gpu: bad rank or output pointer"};
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    const bool dev_out = is_device_ptr(ids_out);
+    ctx->shard->finish(dev_recv, world, max_count, rank, own_count, dev_out ? ids_out : nullptr, n_out, stats);
+    if (!dev_out && *n_out) {
+      if (!ids_out) throw ApiFail{SKYCELL_USAGE, "skycell_gpu: null output pointer"};
+      ck(cudaMemcpyAsync(ids_out, ctx->ids_dev.p, *n_out * 4, cudaMemcpyDeviceToHost, ctx->stream), "ids copy");
+      ck(cudaStreamSynchronize(ctx->stream), "sync");
+    }
+    if (stats) {
+      stats->kernel_launches = ctx->launches;
+      float k1 = 0;
+      cudaEventElapsedTime(&k1, ctx->ev[4], ctx->ev[5]);
+      stats->stream_kernel_ms = k1;
+    }
+    ctx->shard.reset();
+  });
 }
 
 int skycell_gpu_generate(skycell_gpu_ctx* ctx, int dist, uint64_t n, int d, uint64_t seed, int kind, void* dev_out,
                          char* err, size_t err_len) {
+  return skycell_gpu_generate_range(ctx, dist, n, d, seed, kind, 0, n, dev_out, err, err_len);
+}
+
+int skycell_gpu_generate_range(skycell_gpu_ctx* ctx, int dist, uint64_t n, int d, uint64_t seed, int kind,
+                               uint64_t begin, uint64_t count, void* dev_out, char* err, size_t err_len) {
   // generate(): ConfigError on n < 1, d < 2, d > kMaxDims (datagen.cpp:63-65)
   if (n < 1) { put_err(err, err_len, "generate: n must be at least 1"); return SKYCELL_CONFIG; }
   if (d < 2) { put_err(err, err_len, "generate: d must be at least 2"); return SKYCELL_CONFIG; }
   if (d > sk::kMaxD) { put_err(err, err_len, "generate: d must be at most 16"); return SKYCELL_CONFIG; }
-  if (dist < 0 || dist > 2 || kind < 0 || kind > 1 || !ctx) {
-    put_err(err, err_len, "generate: bad distribution or output kind");
+  if (dist < 0 || dist > 2 || kind < 0 || kind > 1 || !ctx || begin > n || count > n - begin) {
+    put_err(err, err_len, "generate: bad distribution, output kind or record range");
     return SKYCELL_USAGE;
   }
-  try {
+  return guarded(err, err_len, [&] {
     ck(cudaSetDevice(ctx->device), "cudaSetDevice");
-    const u64 blocks = (n + 65535) / 65536;
-    const unsigned g = (unsigned)std::max<u64>(1, (blocks + 127) / 128);
+    if (count == 0) return;
+    const u64 b0 = begin / 65536, b1 = (begin + count + 65535) / 65536;
+    const unsigned g = (unsigned)std::max<u64>(1, (b1 - b0 + 127) / 128);
 #define SKYCELL_GEN(DD) \
-  case DD: sk::k_generate<DD><<<g, 128, 0, ctx->stream>>>(dist, n, seed, kind, dev_out); break;
+  case DD: sk::k_generate<DD><<<g, 128, 0, ctx->stream>>>(dist, n, seed, kind, begin, count, dev_out); break;
     switch (d) {
       SKYCELL_GEN(2) SKYCELL_GEN(3) SKYCELL_GEN(4) SKYCELL_GEN(5) SKYCELL_GEN(6) SKYCELL_GEN(7) SKYCELL_GEN(8)
       SKYCELL_GEN(9) SKYCELL_GEN(10) SKYCELL_GEN(11) SKYCELL_GEN(12) SKYCELL_GEN(13) SKYCELL_GEN(14)
@@ -729,12 +1129,7 @@ int skycell_gpu_generate(skycell_gpu_ctx* ctx, int dist, uint64_t n, int d, uint
 #undef SKYCELL_GEN
     ck(cudaGetLastError(), "generate launch");
     ck(cudaStreamSynchronize(ctx->stream), "generate");
-    return SKYCELL_OK;
-  } catch (const CudaFail& f) {
-    put_err(err, err_len, std::string("CUDA error in ") + f.what + ": " + cudaGetErrorString(f.e));
-    cudaGetLastError();
-    return SKYCELL_CUDA;
-  }
+  });
 }
 
 int skycell_default_rho(uint64_t n, int d) { return default_rho(n, d); }
@@ -746,6 +1141,6 @@ int skycell_validate(uint64_t n, int d, int rho, char* err, size_t err_len) {
   return st.code;
 }
 
-const char* skycell_gpu_version(void) { return "skycell-b200 0.1 (sm_100a)"; }
+const char* skycell_gpu_version(void) { return "skycell-b200 0.2 (sm_100a)"; }
 
 }  // extern "C"

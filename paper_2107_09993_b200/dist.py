@@ -1,0 +1,145 @@
+"""Sharded skyline query over G devices: one process per GPU, points sharded
+by index, NCCL over NVLink for the two exchanges (SURVEY.md
+§8(e)).  No reference equivalent: the reference is single-process; the result
+equals ``compute_skyline`` (refine.cpp:108-158) over the concatenation of all
+shards, ids and per-layer counts included.
+
+Protocol (each arrow is one collective on the engine's stream):
+
+    shard_begin (K0+K1 on the local shard)
+      -> all_gather(occupancy regions)         NCCL has no bitwise OR
+    shard_prune (K2 OR, K3, K4, local K5)      (nccl.h:260-275), so the OR
+      -> all_gather(local skyline counts)      is fused into the library
+    shard_pack                                 after an all-gather
+      -> all_gather(padded local skylines)
+    shard_finish (own points vs the union, K6)
+      -> all_gather(counts), all_gather(padded ids) -> rank 0 concatenates
+         in rank order (ids are global and ascending per rank)
+
+The engine only needs the ``shard_*`` methods of
+:class:`paper_2107_09993_b200.skycell.Engine`; the collectives are plain
+``torch.distributed`` calls, so the same code runs over NCCL on B200s and
+over gloo on CPU tensors (tests/test_dist.py drives it with a CPU stand-in
+engine at world_size 2).
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .skycell import InputError, SkycellError, SkylineResult
+
+
+def shard_range(n_total: int, rank: int, world: int) -> tuple[int, int]:
+    """Records [begin, end) owned by `rank`: contiguous index ranges, the
+    first n_total % world ranks one record longer."""
+    base, extra = divmod(n_total, world)
+    begin = rank * base + min(rank, extra)
+    return begin, begin + base + (1 if rank < extra else 0)
+
+
+class ShardedSkyline:
+    """Runs the phase API of one engine against the other ranks of `group`."""
+
+    def __init__(self, engine, group=None, device=None):
+        self.eng = engine
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu")
+        self.device = torch.device(device)
+        self._bufs: dict[str, torch.Tensor] = {}
+
+    def _buf(self, name: str, nbytes: int) -> torch.Tensor:
+        b = self._bufs.get(name)
+        if b is None or b.numel() < nbytes:
+            b = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=self.device)
+            self._bufs[name] = b
+        return b[:nbytes]
+
+    def _gather_counts(self, value: int) -> list[int]:
+        t = torch.tensor([value], dtype=torch.int64, device=self.device)
+        out = torch.empty(self.world, dtype=torch.int64, device=self.device)
+        dist.all_gather_into_tensor(out, t, group=self.group)
+        return [int(v) for v in out.cpu().tolist()]
+
+    def skyline(self, coords, n_local: int, d: int, dim_min, dim_max, rho: int, id_base: int, mode: int = 1,
+                ids_out=None, gather_to: int | None = 0) -> SkylineResult:
+        """Skyline of the global dataset of which this rank holds records
+        [id_base, id_base + n_local).  Returns, on rank `gather_to`, the whole
+        skyline (ascending global ids) with global stats; on other ranks this
+        rank's part.  With gather_to=None every rank returns its own part."""
+        world, rank = self.world, self.rank
+        if self.device.type == "cuda" and hasattr(self.eng, "set_stream"):
+            # kernels and NCCL collectives share torch's current stream
+            self.eng.set_stream(torch.cuda.current_stream(self.device))
+        # phase 1: local streaming pass.  A failing rank still takes part in
+        # the collectives (count -1) so that every rank raises, none hangs.
+        err = None
+        try:
+            occ_bytes = self.eng.shard_begin(coords, n_local, d, dim_min, dim_max, rho, mode, id_base)
+        except SkycellError as e:
+            err, occ_bytes = e, 0
+        sizes = self._gather_counts(occ_bytes if err is None else -1)
+        self._reraise(err, sizes)
+        occ = self._buf("occ", occ_bytes)
+        self.eng.shard_export_occ(occ)
+        gathered = self._buf("occ_all", world * occ_bytes)
+        dist.all_gather_into_tensor(gathered, occ, group=self.group)
+
+        # phase 2: prune against the global occupancy, local skyline
+        try:
+            cnt = self.eng.shard_prune(gathered, world)
+        except SkycellError as e:
+            err, cnt = e, 0
+        counts = self._gather_counts(cnt if err is None else -1)
+        self._reraise(err, counts)
+        maxc = max(counts)
+        bb = self.eng.shard_block_bytes(maxc)
+        send = self._buf("send", bb)
+        self.eng.shard_pack(send, maxc)
+        recv = self._buf("recv", world * bb)
+        dist.all_gather_into_tensor(recv, send, group=self.group)
+
+        # phase 3: own local skyline against the union
+        if ids_out is None:
+            ids_out = np.empty(max(n_local, 1), dtype=np.uint32)
+        res = self.eng.shard_finish(recv, world, maxc, rank, counts[rank], ids_out)
+        examined = self._gather_counts(res.points_examined)
+        res.points_examined = sum(examined)
+        for f in ("survivors_stream", "survivors_filter"):
+            setattr(res, f, sum(self._gather_counts(getattr(res, f))))
+        if gather_to is None:
+            return res
+        res.ids = self._gather_ids(res.ids, gather_to)
+        return res
+
+    def _reraise(self, err, values) -> None:
+        if err is not None:
+            raise err
+        if any(v < 0 for v in values):
+            raise InputError("sharded skyline: another rank rejected its shard")
+
+    def _gather_ids(self, ids, root: int):
+        """Concatenate every rank's ids on `root`, in rank order."""
+        if isinstance(ids, torch.Tensor):
+            local = ids.to(self.device).view(torch.int32)
+        else:
+            local = torch.from_numpy(np.ascontiguousarray(ids, dtype=np.uint32).view(np.int32)).to(self.device)
+        counts = self._gather_counts(int(local.numel()))
+        maxk = max(counts)
+        pad = torch.full((max(maxk, 1),), -1, dtype=torch.int32, device=self.device)
+        pad[: local.numel()] = local
+        allp = torch.empty(self.world * pad.numel(), dtype=torch.int32, device=self.device)
+        dist.all_gather_into_tensor(allp, pad, group=self.group)
+        if self.rank != root:
+            return ids
+        allp = allp.view(self.world, -1)
+        parts = [allp[g, : counts[g]] for g in range(self.world)]
+        out = torch.cat(parts).cpu().numpy().view(np.uint32)
+        return out
+
+
+__all__ = ["ShardedSkyline", "shard_range"]

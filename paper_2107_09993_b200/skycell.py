@@ -150,8 +150,10 @@ _lib = None
 _lib_lock = threading.Lock()
 
 EXPORTS = (
-    "skycell_gpu_create", "skycell_gpu_destroy", "skycell_gpu_skyline_f64", "skycell_gpu_skyline_f32",
-    "skycell_gpu_quadrant_f64", "skycell_gpu_generate", "skycell_default_rho", "skycell_validate",
+    "skycell_gpu_create", "skycell_gpu_destroy", "skycell_gpu_set_stream", "skycell_gpu_skyline_f64",
+    "skycell_gpu_skyline_f32", "skycell_gpu_quadrant_f64", "skycell_gpu_shard_begin", "skycell_gpu_shard_export_occ",
+    "skycell_gpu_shard_prune", "skycell_gpu_shard_block_bytes", "skycell_gpu_shard_pack", "skycell_gpu_shard_finish",
+    "skycell_gpu_generate", "skycell_gpu_generate_range", "skycell_default_rho", "skycell_validate",
     "skycell_gpu_version",
 )
 
@@ -175,6 +177,16 @@ def load_library(path: str = LIB_PATH):
         lib.skycell_gpu_quadrant_f64.argtypes = [vp, fp, u64, i32, dp, i32, i32, i32, u32p, C.POINTER(C.c_uint64),
                                                  C.POINTER(_Stats), C.c_char_p, C.c_size_t]
         lib.skycell_gpu_generate.argtypes = [vp, i32, u64, i32, u64, i32, vp, C.c_char_p, C.c_size_t]
+        lib.skycell_gpu_generate_range.argtypes = [vp, i32, u64, i32, u64, i32, u64, u64, vp, C.c_char_p, C.c_size_t]
+        lib.skycell_gpu_set_stream.argtypes = [vp, vp]
+        u64p, cp, sz = C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t
+        lib.skycell_gpu_shard_begin.argtypes = [vp, vp, i32, u64, i32, dp, dp, i32, i32, u64, u64p, cp, sz]
+        lib.skycell_gpu_shard_export_occ.argtypes = [vp, vp, cp, sz]
+        lib.skycell_gpu_shard_prune.argtypes = [vp, vp, i32, u64p, cp, sz]
+        lib.skycell_gpu_shard_block_bytes.argtypes = [vp, u64]
+        lib.skycell_gpu_shard_block_bytes.restype = C.c_uint64
+        lib.skycell_gpu_shard_pack.argtypes = [vp, vp, u64, cp, sz]
+        lib.skycell_gpu_shard_finish.argtypes = [vp, vp, i32, u64, i32, u64, u32p, u64p, C.POINTER(_Stats), cp, sz]
         lib.skycell_default_rho.argtypes = [u64, i32]
         lib.skycell_validate.argtypes = [u64, i32, i32, C.c_char_p, C.c_size_t]
         lib.skycell_gpu_version.restype = C.c_char_p
@@ -247,17 +259,67 @@ class Engine:
         ids = ids_out[:k].copy() if own else ids_out[:k]
         return _to_result(ids, st if with_stats else None)
 
-    def generate(self, dist: int, n: int, d: int, seed: int, quantized: bool = True, out=None):
-        """Synthetic data on the device (skycell_gpu_generate).  Returns a CUDA
-        tensor of shape (n, d): float32 on the 2^-24 grid, or raw float64."""
+    def generate(self, dist: int, n: int, d: int, seed: int, quantized: bool = True, out=None,
+                 begin: int = 0, count: int | None = None):
+        """Synthetic data on the device (skycell_gpu_generate_range).  Returns a
+        CUDA tensor of shape (count, d) holding records [begin, begin + count)
+        of the n-record dataset: float32 on the 2^-24 grid, or raw float64."""
         import torch
+        count = n - begin if count is None else count
         if out is None:
-            out = torch.empty((n, d), dtype=torch.float32 if quantized else torch.float64,
+            out = torch.empty((count, d), dtype=torch.float32 if quantized else torch.float64,
                               device=f"cuda:{self.device}")
         err = C.create_string_buffer(512)
-        _raise(self.lib.skycell_gpu_generate(self._ctx, int(dist), n, d, seed, 1 if quantized else 0,
-                                             C.c_void_p(out.data_ptr()), err, 512), err)
+        _raise(self.lib.skycell_gpu_generate_range(self._ctx, int(dist), n, d, seed, 1 if quantized else 0, begin,
+                                                   count, C.c_void_p(out.data_ptr()), err, 512), err)
         return out
+
+    def set_stream(self, stream) -> None:
+        """Enqueue all later work on `stream` (a torch.cuda.Stream, a raw
+        cudaStream_t int, or None for the context's own stream)."""
+        h = getattr(stream, "cuda_stream", stream)
+        self.lib.skycell_gpu_set_stream(self._ctx, C.c_void_p(h) if h else None)
+
+    # ---- sharded query phases (include/skycell_gpu.h, DESIGN.md §4); the
+    # exchanges between them are issued by paper_2107_09993_b200.dist.
+    def shard_begin(self, coords, n: int, d: int, dim_min, dim_max, rho: int, mode: int, id_base: int) -> int:
+        ptr, is_f32 = _data_ptr(coords)
+        mn = np.ascontiguousarray(dim_min, dtype=np.float64)
+        mx = np.ascontiguousarray(dim_max, dtype=np.float64)
+        occ = C.c_uint64(0)
+        err = C.create_string_buffer(512)
+        _raise(self.lib.skycell_gpu_shard_begin(self._ctx, ptr, int(is_f32), n, d,
+                                                mn.ctypes.data_as(C.POINTER(C.c_double)),
+                                                mx.ctypes.data_as(C.POINTER(C.c_double)), rho, int(mode), id_base,
+                                                C.byref(occ), err, 512), err)
+        return int(occ.value)
+
+    def shard_export_occ(self, dst) -> None:
+        err = C.create_string_buffer(512)
+        _raise(self.lib.skycell_gpu_shard_export_occ(self._ctx, C.c_void_p(dst.data_ptr()), err, 512), err)
+
+    def shard_prune(self, gathered, world: int) -> int:
+        cnt = C.c_uint64(0)
+        err = C.create_string_buffer(512)
+        _raise(self.lib.skycell_gpu_shard_prune(self._ctx, C.c_void_p(gathered.data_ptr()), world, C.byref(cnt),
+                                                err, 512), err)
+        return int(cnt.value)
+
+    def shard_block_bytes(self, max_count: int) -> int:
+        return int(self.lib.skycell_gpu_shard_block_bytes(self._ctx, max_count))
+
+    def shard_pack(self, dst, max_count: int) -> None:
+        err = C.create_string_buffer(512)
+        _raise(self.lib.skycell_gpu_shard_pack(self._ctx, C.c_void_p(dst.data_ptr()), max_count, err, 512), err)
+
+    def shard_finish(self, recv, world: int, max_count: int, rank: int, own_count: int, ids_out):
+        out_ptr, _ = _data_ptr(ids_out)
+        n_out = C.c_uint64(0)
+        st = _Stats()
+        err = C.create_string_buffer(512)
+        _raise(self.lib.skycell_gpu_shard_finish(self._ctx, C.c_void_p(recv.data_ptr()), world, max_count, rank,
+                                                 own_count, out_ptr, C.byref(n_out), C.byref(st), err, 512), err)
+        return _to_result(ids_out[: n_out.value], st)
 
     def compute_skyline(self, ds: Dataset, rho: int, mode: Mode = Mode.kParallel, pool=None,
                         merge_cross_cell: bool = True) -> SkylineResult:

@@ -22,14 +22,14 @@ def check(res, ids=None, examined=None, keys=None, cands=None):
         assert res.layers.candidates == list(cands)
 
 
-@pytest.mark.parametrize("case", [c for c in load_json("kat.json")["cases"] if c["merge"]], ids=lambda c: c["name"])
+@pytest.mark.parametrize("case", load_json("kat.json")["cases"], ids=lambda c: c["name"])
 def test_gpu_kats(engine, case):
     x = np.asarray(case["rows"], dtype=np.float64)
     ds = sky.Dataset(x, np.asarray(case["dim_min"], float), np.asarray(case["dim_max"], float))
     for mode, key in MODES.items():
         w = case[key]
-        check(engine.compute_skyline(ds, case["rho"], sky.Mode(mode)), w["ids"], w["points_examined"], w["keys"],
-              w["candidates"])
+        check(engine.compute_skyline(ds, case["rho"], sky.Mode(mode), merge_cross_cell=case["merge"]), w["ids"],
+              w["points_examined"], w["keys"], w["candidates"])
 
 
 @pytest.mark.parametrize("case", load_json("kat.json")["errors"], ids=lambda c: c["name"])
@@ -122,3 +122,53 @@ def test_gpu_large_skyline_golden(engine, oracle, rec):
     x, mn, mx = inputs_for(oracle, rec)
     r = engine.compute_skyline(sky.Dataset(x, mn, mx), rec["rho"])
     check(r, load_ids("large_ids.npz")[rec["key"]], rec["points_examined"], rec["keys"], rec["candidates"])
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_gpu_phase1_only_vs_oracle(engine, oracle, seed):
+    """merge_cross_cell = false (refine.hpp:50-56): union of per-cell SFS."""
+    from oracle.oracle import quantize_f32
+    rng = np.random.default_rng(100 + seed)
+    dist, d = seed % 3, int(rng.integers(2, 6))
+    n = int(rng.integers(50, 4000))
+    rho = int(rng.integers(1, 4))
+    v = oracle.generate(dist, n, d, 300 + seed)
+    for x, mn, mx in ((quantize_f32(v), np.zeros(d), np.ones(d)), (v * 2 - 1, (v * 2 - 1).min(0), (v * 2 - 1).max(0))):
+        want = oracle.compute_skyline(x.astype(np.float64), mn, mx, rho, 1, False)
+        got = engine.compute_skyline(sky.Dataset(np.ascontiguousarray(x), mn, mx), rho, merge_cross_cell=False)
+        check(got, want.ids, want.points_examined, want.keys, want.candidates)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_gpu_quadrant_vs_oracle(engine, oracle, seed):
+    """quadrant_skyline (refine.cpp:160-184): filter, renormalise, sub_rho."""
+    rng = np.random.default_rng(seed)
+    d = 2 + seed % 4
+    v = oracle.generate(seed % 3, 3000 + 500 * seed, d, 40 + seed)
+    for _ in range(4):
+        origin = rng.uniform(-0.1, 0.7, d)
+        want = oracle.quadrant_skyline(v, origin, 4)
+        got = engine.quadrant_skyline(sky.Dataset(v, v.min(0), v.max(0)), origin, 4)
+        check(got, want.ids, want.points_examined, want.keys, want.candidates)
+
+
+def test_gpu_quadrant_edges(engine, oracle):
+    v = oracle.generate(0, 500, 3, 1)
+    ds = sky.Dataset(v, v.min(0), v.max(0))
+    # empty quadrant -> empty result, no layers (refine.cpp:176)
+    r = engine.quadrant_skyline(ds, np.full(3, 2.0), 3)
+    assert r.ids.size == 0 and r.layers.keys == []
+    # arity mismatch -> UsageError with the reference's message (refine.cpp:162-163)
+    with pytest.raises(sky.UsageError, match="origin arity does not match"):
+        engine.quadrant_skyline(ds, np.zeros(2), 3)
+    # NaN records are outside every quadrant (the >= test is false)
+    w = v.copy()
+    w[7, 1] = np.nan
+    want = oracle.quadrant_skyline(w, np.zeros(3), 3)
+    got = engine.quadrant_skyline(sky.Dataset(w, np.zeros(3), np.ones(3)), np.zeros(3), 3)
+    check(got, want.ids, want.points_examined)
+    # a single record inside
+    o = v[np.argmax(v.sum(1))]
+    want = oracle.quadrant_skyline(v, o, 3)
+    got = engine.quadrant_skyline(ds, o, 3)
+    check(got, want.ids, want.points_examined)

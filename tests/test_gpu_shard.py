@@ -1,0 +1,112 @@
+"""Device phases of the sharded query on one B200: G shards,
+each with its own context, exchanging through an in-process loopback (the
+same byte buffers the NCCL all-gathers carry), must reproduce the
+single-device query and the oracle bit-exactly -- ids, points_examined and
+per-layer key/candidate counts.  Plus the real NCCL path at world_size 1."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2107_09993_b200 as sky
+from paper_2107_09993_b200.dist import ShardedSkyline, shard_range
+
+pytestmark = pytest.mark.gpu
+
+
+def loopback_query(engines, x, d, mn, mx, rho, mode=1):
+    G = len(engines)
+    n = x.shape[0]
+    stream = torch.cuda.current_stream()
+    spans = [shard_range(n, g, G) for g in range(G)]
+    occ = []
+    for eng, (b, e) in zip(engines, spans):
+        eng.set_stream(stream)
+        nb = eng.shard_begin(x[b:e], e - b, d, mn, mx, rho, mode, b)
+        t = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        eng.shard_export_occ(t)
+        occ.append(t)
+    gathered = torch.cat(occ)
+    counts = [eng.shard_prune(gathered, G) for eng in engines]
+    maxc = max(counts)
+    blocks = []
+    for eng in engines:
+        t = torch.empty(eng.shard_block_bytes(maxc), dtype=torch.uint8, device="cuda")
+        eng.shard_pack(t, maxc)
+        blocks.append(t)
+    recv = torch.cat(blocks)
+    ids, examined, res0 = [], 0, None
+    for g, (eng, (b, e)) in enumerate(zip(engines, spans)):
+        out = np.empty(max(e - b, 1), dtype=np.uint32)
+        r = eng.shard_finish(recv, G, maxc, g, counts[g], out)
+        ids.append(np.asarray(r.ids).copy())
+        examined += r.points_examined
+        if res0 is None:
+            res0 = r
+        else:
+            assert r.layers.keys == res0.layers.keys and r.layers.candidates == res0.layers.candidates
+    return np.concatenate(ids), examined, res0
+
+
+@pytest.fixture(scope="module")
+def engines():
+    es = [sky.Engine(0) for _ in range(4)]
+    yield es
+    for e in es:
+        e.close()
+
+
+CASES = [(0, 200_000, 4, None), (1, 150_000, 4, None), (2, 60_000, 3, None), (2, 20_000, 6, 3), (0, 5_000, 2, None),
+         (1, 30_000, 8, 2), (0, 3, 3, 1)]
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"dist{c[0]}-n{c[1]}-d{c[2]}")
+@pytest.mark.parametrize("G", [1, 2, 3, 4])
+def test_loopback_shards_match_single(engines, oracle, case, G):
+    from oracle.oracle import quantize_f32
+    dist_id, n, d, rho = case
+    x = quantize_f32(oracle.generate(dist_id, n, d, 99 + n))
+    rho = rho or sky.default_rho(n, d)
+    mn, mx = np.zeros(d), np.ones(d)
+    single = engines[0].compute_skyline(sky.Dataset(x, mn, mx), rho)
+    want = oracle.compute_skyline(x.astype(np.float64), mn, mx, rho)
+    assert np.array_equal(single.ids, want.ids)
+    xd = torch.from_numpy(x).cuda()
+    ids, examined, r0 = loopback_query(engines[:G], xd, d, mn, mx, rho)
+    assert np.array_equal(ids, want.ids), (G, len(ids), len(want.ids))
+    assert examined == want.points_examined
+    assert r0.layers.keys == want.keys and r0.layers.candidates == want.candidates
+
+
+def test_loopback_shards_f64_general_range(engines, oracle):
+    v = oracle.generate(2, 40_000, 4, 5)
+    x = v * 3.0 - 1.0
+    mn, mx = x.min(0), x.max(0)
+    want = oracle.compute_skyline(x, mn, mx, 4)
+    ids, examined, r0 = loopback_query(engines[:3], torch.from_numpy(x).cuda(), 4, mn, mx, 4)
+    assert np.array_equal(ids, want.ids)
+    assert examined == want.points_examined
+
+
+def test_nccl_world1(oracle):
+    import torch.distributed as dist
+    from oracle.oracle import quantize_f32
+    if dist.is_initialized():
+        pytest.skip("a process group already exists")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda:0"))
+    try:
+        eng = sky.Engine(0)
+        x = quantize_f32(oracle.generate(0, 300_000, 4, 3))
+        want = oracle.compute_skyline(x.astype(np.float64), np.zeros(4), np.ones(4), 4)
+        res = ShardedSkyline(eng).skyline(torch.from_numpy(x).cuda(), 300_000, 4, np.zeros(4), np.ones(4), 4, 0)
+        assert np.array_equal(res.ids, want.ids)
+        assert res.points_examined == want.points_examined
+        eng.close()
+    finally:
+        dist.destroy_process_group()
