@@ -99,11 +99,12 @@ int skycell_gpu_quadrant_f64(skycell_gpu_ctx* ctx, const double* coords, uint64_
                              uint32_t* ids_out, uint64_t* n_out, skycell_gpu_stats* stats,
                              char* err, size_t err_len);
 
-/* Bind the context to a caller's CUDA stream (a cudaStream_t; NULL restores
- * the context's own stream).  Every kernel and copy of later calls is
- * enqueued on it, so collectives the caller issues on the same stream (the
- * sharded query below) are ordered without host synchronisation. */
-int skycell_gpu_set_stream(skycell_gpu_ctx* ctx, void* stream);
+/* Bind the context to a caller's CUDA stream (a cudaStream_t; 0 is the
+ * legacy default stream), or back to its own stream with use_own = 1.  Every
+ * kernel and copy of later calls is enqueued on it, so collectives the caller
+ * issues on the same stream (the sharded query below) are ordered without
+ * host synchronisation. */
+int skycell_gpu_set_stream(skycell_gpu_ctx* ctx, void* stream, int use_own);
 
 /* ---- Sharded query over G devices (one process / context per device).
  * No reference equivalent: the reference is single-process

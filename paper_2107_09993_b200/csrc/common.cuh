@@ -256,6 +256,16 @@ __device__ __forceinline__ void set_bit_global(uint32_t* bits, u64 idx) {
   uint32_t* w = bits + (idx >> 5);
   if (!(__ldcg(w) & m)) atomicOr(w, m);
 }
+// Check-before-set through L1: a stale L1 copy can only cause a redundant
+// (harmless) red.or, and hot words -- correlated data piles ~1e-3 n points
+// into the origin cell -- stop reaching the L2 atomic unit after the first hit.
+__device__ __forceinline__ void set_bit_cached(uint32_t* bits, u64 idx) {
+  const uint32_t m = 1u << (idx & 31);
+  uint32_t* w = bits + (idx >> 5);
+  uint32_t v;
+  asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(v) : "l"(w));
+  if (!(v & m)) asm volatile("red.global.or.b32 [%0], %1;" ::"l"(w), "r"(m) : "memory");
+}
 // Fire-and-forget (red.global.or): no result to wait for.
 __device__ __forceinline__ void red_or_global(uint32_t* bits, u64 idx) {
   asm volatile("red.global.or.b32 [%0], %1;" ::"l"(bits + (idx >> 5)), "r"(1u << (idx & 31)) : "memory");

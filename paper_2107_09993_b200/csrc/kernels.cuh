@@ -468,13 +468,13 @@ __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
               u[k] = __saturatef(cur[j][k]);  // the stored proxy (dataset.cpp:45 clamp, 1.0f = 1 - 2^-32)
               l = l * mul_r + mag_col(fminf(u[k], 0x1.fffffep-1f), fs_r);
             }
-            if (lin32) red_or_global(p.occ_rho, (u64)(l - rcorr));
+            if (lin32) set_bit_cached(p.occ_rho, (u64)(l - rcorr));
             else {
               u64 lin = 0;
 #pragma unroll
               for (int k = D - 1; k >= 0; --k)
                 lin = (lin << rho) | (u64)(mag_col(fminf(u[k], 0x1.fffffep-1f), fs_r) - 0x4B000000u);
-              red_or_global(p.occ_rho, lin);
+              set_bit_cached(p.occ_rho, lin);
             }
           } else {
             u64 lin = 0;
@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
               u[k] = Coord<TIn, TOut, IDENT>::value(cur[j][k], p.nm, k);
               lin = (lin << rho) | (u64)col_at<TIn, TOut, IDENT>(cur[j][k], p.nm, k, fs_r, ds_r, top);
             }
-            red_or_global(p.occ_rho, lin);
+            set_bit_cached(p.occ_rho, lin);
           }
           store_row<TOut, D>(out_rows, slot, u);
           p.out_ids[slot] = p.id_base + base + j * 32;
@@ -938,9 +938,20 @@ __global__ void __launch_bounds__(1024) k_strength_order(const T* __restrict__ r
 }
 
 // ------------------------------------------- K5: exact sort-first dominance
-// Per-dimension column lists of a point set with a device-side count:
-// histogram, exclusive scan, scatter (non-stable within a column; the order
-// inside a column only affects how soon a dominator is met, never the result).
+// Per-dimension candidate lists of a point set with a device-side count.
+// For every dimension k the slots are counting-sorted by the bin
+// (sum bucket b, column c) in BUCKET-MAJOR order, so the candidate
+// dominators of p in dimension k -- col_k(q) <= col_k(p) and bucket(q) <=
+// bucket(p) (sums are monotone under dominance) -- form one contiguous range
+// per sum bucket: at most kSumBuckets ranges, visited in ascending sum order
+// (strongest dominators first).  A per-dimension column histogram picks the
+// dimension with the fewest candidates.  Layout per dimension:
+//   [0, kListBins]                          shifted bin counts -> bin starts
+//   [kListBins + 1, kListBins + kListCols + 1]  shifted column counts -> cumulative
+// Order inside a bin only affects how soon a dominator is met, never the result.
+constexpr int kColBase = kListBins + 1;
+constexpr int kListStride = kListBins + 1 + kListCols + 1;
+
 template <int D>
 __device__ __forceinline__ int sum_bucket(u64 fsum_bits) {
   const double f = __longlong_as_double((long long)fsum_bits);
@@ -948,6 +959,8 @@ __device__ __forceinline__ int sum_bucket(u64 fsum_bits) {
   const int b = (int)(f * (kSumBuckets / (double)D));
   return b < kSumBuckets - 1 ? b : kSumBuckets - 1;
 }
+
+__device__ __forceinline__ int list_bin(int b, int c) { return b * kListCols + c; }
 
 template <typename T, int D>
 __global__ void k_list_hist(const T* __restrict__ rows, const uint32_t* __restrict__ ids, const u64* __restrict__ fsum,
@@ -959,24 +972,42 @@ __global__ void k_list_hist(const T* __restrict__ rows, const uint32_t* __restri
     load_row_cached<T, D>(rows, i, v);
     const int sb = sum_bucket<D>(fsum[i]);
 #pragma unroll
-    for (int k = 0; k < D; ++k) atomicAdd(&hist[k * (kListBins + 1) + list_col(v[k]) * kSumBuckets + sb + 1], 1u);
+    for (int k = 0; k < D; ++k) {
+      const int c = list_col(v[k]);
+      atomicAdd(&hist[k * kListStride + list_bin(sb, c) + 1], 1u);
+      atomicAdd(&hist[k * kListStride + kColBase + c + 1], 1u);
+    }
   }
 }
 
-// One CTA per dimension: inclusive scan of the shifted histogram = bin starts.
-// Chunks of 1024 bins, coalesced, with a running total.
-__global__ void __launch_bounds__(1024) k_list_scan(unsigned* __restrict__ hist, unsigned* __restrict__ cursor) {
+// One CTA per (dimension, array): inclusive scan of a shifted histogram =
+// starts.  The array is processed in smem tiles of 1024 x kScanPer entries:
+// coalesced load, a serial sum over each thread's kScanPer consecutive
+// entries, one block scan of the 1024 run totals, coalesced write-back.
+// blockIdx.x < D: bin arrays (also copied to the scatter cursor);
+// blockIdx.x >= D: column arrays.
+constexpr int kScanPer = 8;
+__global__ void __launch_bounds__(1024) k_list_scan(unsigned* __restrict__ hist, unsigned* __restrict__ cursor, int D) {
+  __shared__ unsigned tile[1024 * kScanPer + 1024 * kScanPer / 32];  // one pad word per 32 entries
   __shared__ unsigned warp_tot[32];
-  __shared__ unsigned carry;
-  unsigned* h = hist + blockIdx.x * (u64)(kListBins + 1);
-  unsigned* cur = cursor + blockIdx.x * (u64)(kListBins + 1);
+  __shared__ unsigned carry_s;
+  const bool bins = (int)blockIdx.x < D;
+  const int k = bins ? blockIdx.x : blockIdx.x - D;
+  unsigned* h = hist + (u64)k * kListStride + (bins ? 0 : kColBase);
+  unsigned* cur = bins ? cursor + (u64)k * kListStride : nullptr;
+  const int len = bins ? kListBins + 1 : kListCols + 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int c0 = 0; c0 <= kListBins; c0 += 1024) {
-    const int c = c0 + threadIdx.x;
-    const unsigned v = c <= kListBins ? h[c] : 0;
-    unsigned incl = v;
+  constexpr int T = 1024 * kScanPer;
+  auto pad = [](int i) { return i + (i >> 5); };  // one pad word per 32: conflict-free strided runs
+  if (threadIdx.x == 0) carry_s = 0;
+  for (int t0 = 0; t0 < len; t0 += T) {
+    for (int i = threadIdx.x; i < T; i += 1024) tile[pad(i)] = (t0 + i < len) ? h[t0 + i] : 0u;
+    __syncthreads();
+    const int r0 = threadIdx.x * kScanPer;
+    unsigned run = 0;
+#pragma unroll
+    for (int e = 0; e < kScanPer; ++e) run += tile[pad(r0 + e)];
+    unsigned incl = run;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const unsigned y = __shfl_up_sync(kFull, incl, o);
@@ -985,7 +1016,8 @@ __global__ void __launch_bounds__(1024) k_list_scan(unsigned* __restrict__ hist,
     if (lane == 31) warp_tot[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-      unsigned t = warp_tot[lane], ti = t;
+      const unsigned t = warp_tot[lane];
+      unsigned ti = t;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const unsigned y = __shfl_up_sync(kFull, ti, o);
@@ -994,13 +1026,21 @@ __global__ void __launch_bounds__(1024) k_list_scan(unsigned* __restrict__ hist,
       warp_tot[lane] = ti - t;
     }
     __syncthreads();
-    const unsigned out = carry + warp_tot[warp] + incl;
-    if (c <= kListBins) {
-      h[c] = out;
-      cur[c] = out;
+    unsigned acc = carry_s + warp_tot[warp] + incl - run;
+#pragma unroll
+    for (int e = 0; e < kScanPer; ++e) {
+      acc += tile[pad(r0 + e)];
+      tile[pad(r0 + e)] = acc;
     }
     __syncthreads();
-    if (threadIdx.x == 1023) carry = out;
+    for (int i = threadIdx.x; i < T; i += 1024) {
+      if (t0 + i < len) {
+        const unsigned v = tile[pad(i)];
+        h[t0 + i] = v;
+        if (cur) cur[t0 + i] = v;
+      }
+    }
+    if (threadIdx.x == 1023) carry_s = acc;
     __syncthreads();
   }
 }
@@ -1017,17 +1057,12 @@ __global__ void k_list_scatter(const T* __restrict__ rows, const uint32_t* __res
     const int sb = sum_bucket<D>(fsum[i]);
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-      const unsigned pos = atomicAdd(&cursor[k * (kListBins + 1) + list_col(v[k]) * kSumBuckets + sb], 1u);
+      const unsigned pos = atomicAdd(&cursor[k * kListStride + list_bin(sb, list_col(v[k]))], 1u);
       lists[(u64)k * cap + pos] = (uint32_t)i;
     }
   }
 }
 
-// flag[i] = 1 iff no point q of the set precedes i (sort-first order,
-// refine.cpp:38-41) and dominates it.  Candidates q come from the shortest
-// per-dimension column prefix.  One warp per point: the 32 lanes test 32
-// candidates per step (independent gathers in flight) and stop at the first
-// step with a dominator, so a skyline point's scan is prefix/32 steps long.
 template <typename T, int D>
 __device__ __forceinline__ bool same_cell(const T* q, const T* p, int L, int top) {
   const T scale = (T)(1u << L);
@@ -1037,6 +1072,15 @@ __device__ __forceinline__ bool same_cell(const T* q, const T* p, int L, int top
   return eq;
 }
 
+// flag[i] = 1 iff no point q of the set precedes i (sort-first order,
+// refine.cpp:38-41) and dominates it, for query slots [q_begin, *q_end).
+// One warp per point: the candidate ranges of its sum buckets (<= 32 per
+// round) are concatenated by a warp scan of their lengths; the 32 lanes then
+// test 32 consecutive candidates per step (independent gathers in flight) and
+// stop at the first step with a dominator.  A point with sum 0 lies at the
+// origin and has no dominator (normalised coordinates are >= 0); skipping it
+// keeps correlated data's ~8.7e-4 n exact origin duplicates
+// from scanning each other.
 template <typename T, int D>
 __global__ void __launch_bounds__(256) k_allpairs_lists(const T* __restrict__ rows, const uint32_t* __restrict__ ids,
                                                         const u64* __restrict__ fsum, const u64* __restrict__ count,
@@ -1054,38 +1098,63 @@ __global__ void __launch_bounds__(256) k_allpairs_lists(const T* __restrict__ ro
       if (lane == 0) flag[i] = 0;
       continue;
     }
+    const u64 ps = fsum[i];
+    if (ps == 0) {  // the origin: nothing dominates it
+      if (lane == 0) flag[i] = 1;
+      continue;
+    }
     T v[D];
     load_row_cached<T, D>(rows, i, v);
-    const u64 ps = fsum[i];
-    int bk = 0;
-    unsigned end = 0xffffffffu;
+    int bk = 0, pc = 0;
+    unsigned best = 0xffffffffu;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-      const unsigned e = __ldg(offs + k * (kListBins + 1) + (list_col(v[k]) + 1) * kSumBuckets);
-      if (e < end) { end = e; bk = k; }
+      const int c = list_col(v[k]);
+      const unsigned e = __ldg(offs + k * kListStride + kColBase + c + 1);  // entries with col <= c
+      if (e < best) { best = e; bk = k; pc = c; }
     }
-    // per column c <= col(p): only sum buckets <= bucket(p) can hold a
-    // dominator (sums are monotone under dominance)
     const uint32_t* lst = lists + (u64)bk * cap;
-    const unsigned* ob = offs + bk * (kListBins + 1);
-    const int pc = list_col(v[bk]);
+    const unsigned* ob = offs + bk * kListStride;
     const int sb = sum_bucket<D>(ps);
     bool dom = false;
-    for (int c = 0; c <= pc && !dom; ++c) {
-      const unsigned s0 = __ldg(ob + c * kSumBuckets), s1 = __ldg(ob + c * kSumBuckets + sb + 1);
-      for (unsigned base = s0; base < s1; base += 32) {
+    for (int b0 = 0; b0 <= sb && !dom; b0 += 32) {
+      const int b = b0 + lane;
+      unsigned lo = 0, len = 0;
+      if (b <= sb) {
+        lo = __ldg(ob + list_bin(b, 0));
+        len = __ldg(ob + list_bin(b, pc + 1)) - lo;
+      }
+      unsigned incl = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const unsigned total = __shfl_sync(kFull, incl, 31);
+      for (unsigned base = 0; base < total; base += 32) {
         const unsigned e = base + lane;
+        // range j holding entry e: the first lane whose inclusive end exceeds e
+        int j = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const unsigned end_j = __shfl_sync(kFull, incl, j + step - 1);
+          if (end_j <= e) j += step;
+        }
+        const unsigned start_j = __shfl_sync(kFull, incl - len, j);
+        const unsigned lo_j = __shfl_sync(kFull, lo, j);
         bool d_l = false;
-        if (e < s1) {
-          const uint32_t q = __ldg(lst + e);
+        if (e < total) {
+          const uint32_t q = __ldg(lst + lo_j + (e - start_j));
           const u64 qs = __ldg(fsum + q);
-          const uint32_t qi = __ldg(ids + q);
-          T w[D];
-          load_row_cached<T, D>(rows, q, w);
-          d_l = precedes(qs, qi, ps, pid) && dominates<T, D>(w, v);
-          // merge_cross_cell = false (refine.cpp:98): phase-1 semantics only,
-          // a dominator must share p's layer-rho cell
-          if (cell_level && d_l) d_l = same_cell<T, D>(w, v, cell_level, ctop);
+          if (qs <= ps) {
+            const uint32_t qi = __ldg(ids + q);
+            T w[D];
+            load_row_cached<T, D>(rows, q, w);
+            d_l = precedes(qs, qi, ps, pid) && dominates<T, D>(w, v);
+            // merge_cross_cell = false (refine.cpp:98): phase-1 semantics
+            // only, a dominator must share p's layer-rho cell
+            if (cell_level && d_l) d_l = same_cell<T, D>(w, v, cell_level, ctop);
+          }
         }
         if (__any_sync(kFull, d_l)) {
           dom = true;

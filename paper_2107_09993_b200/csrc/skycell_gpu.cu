@@ -226,7 +226,7 @@ void run_exact(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uin
   const TOut* trows = static_cast<const TOut*>(rows);
   uint32_t* lists = static_cast<uint32_t*>(ctx->lists.p);
   sk::k_list_hist<TOut, D><<<g, 256, 0, s>>>(trows, ids, fsum, count, hist);
-  sk::k_list_scan<<<D, 1024, 0, s>>>(hist, cursor);
+  sk::k_list_scan<<<2 * D, 1024, 0, s>>>(hist, cursor, D);
   sk::k_list_scatter<TOut, D><<<g, 256, 0, s>>>(trows, ids, fsum, count, cursor, lists, cap);
   const unsigned gw = (unsigned)std::max<u64>(1, std::min<u64>((cap * 32 + 255) / 256, (u64)nsm * 8));
   sk::k_allpairs_lists<TOut, D><<<gw, 256, 0, s>>>(trows, ids, fsum, count, lists, hist, cap,
@@ -316,7 +316,7 @@ struct Pipe final : PipeBase {
     pf_max = (int)std::min<u64>(1024, (32 * 1024) / (D * sizeof(TOut) + 8));
     smem_pf = (((u64)pf_max * D * sizeof(TOut) + 15) & ~15ull) + (u64)pf_max * 8 + (u64)D * pf_max * 2 +
               (u64)D * (sk::kListCols + 1) * 2 + 16;
-    const size_t bin_words = (size_t)D * (sk::kListBins + 1);
+    const size_t bin_words = (size_t)D * sk::kListStride;
     id_words = (n + 31) / 32;
     bit_blocks = (unsigned)((id_words + sk::kBitsBlock - 1) / sk::kBitsBlock);
 
@@ -758,10 +758,13 @@ Query make_query(skycell_gpu_ctx* ctx, const TIn* coords, u64 n, int d, const do
 
 template <typename TIn>
 bool identity_range(const Query& q, const double* dmin, const double* dmax) {
-  if (sizeof(TIn) != 4) return false;
-  for (int k = 0; k < q.d; ++k)
-    if (!(dmin[k] == 0.0 && dmax[k] == 1.0)) return false;
-  return true;
+  if constexpr (sizeof(TIn) != 4) {
+    return false;
+  } else {
+    for (int k = 0; k < q.d; ++k)
+      if (!(dmin[k] == 0.0 && dmax[k] == 1.0)) return false;
+    return true;
+  }
 }
 
 // Dispatch on (input type, identity range, d) to a Pipe instance.
@@ -922,9 +925,9 @@ void skycell_gpu_destroy(skycell_gpu_ctx* ctx) {
   delete ctx;
 }
 
-int skycell_gpu_set_stream(skycell_gpu_ctx* ctx, void* stream) {
+int skycell_gpu_set_stream(skycell_gpu_ctx* ctx, void* stream, int use_own) {
   if (!ctx) return SKYCELL_USAGE;
-  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  ctx->stream = use_own ? ctx->own_stream : static_cast<cudaStream_t>(stream);  // 0 = the legacy default stream
   return SKYCELL_OK;
 }
 

@@ -178,7 +178,7 @@ def load_library(path: str = LIB_PATH):
                                                  C.POINTER(_Stats), C.c_char_p, C.c_size_t]
         lib.skycell_gpu_generate.argtypes = [vp, i32, u64, i32, u64, i32, vp, C.c_char_p, C.c_size_t]
         lib.skycell_gpu_generate_range.argtypes = [vp, i32, u64, i32, u64, i32, u64, u64, vp, C.c_char_p, C.c_size_t]
-        lib.skycell_gpu_set_stream.argtypes = [vp, vp]
+        lib.skycell_gpu_set_stream.argtypes = [vp, vp, i32]
         u64p, cp, sz = C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t
         lib.skycell_gpu_shard_begin.argtypes = [vp, vp, i32, u64, i32, dp, dp, i32, i32, u64, u64p, cp, sz]
         lib.skycell_gpu_shard_export_occ.argtypes = [vp, vp, cp, sz]
@@ -277,8 +277,11 @@ class Engine:
     def set_stream(self, stream) -> None:
         """Enqueue all later work on `stream` (a torch.cuda.Stream, a raw
         cudaStream_t int, or None for the context's own stream)."""
-        h = getattr(stream, "cuda_stream", stream)
-        self.lib.skycell_gpu_set_stream(self._ctx, C.c_void_p(h) if h else None)
+        if stream is None:
+            self.lib.skycell_gpu_set_stream(self._ctx, None, 1)
+        else:
+            h = int(getattr(stream, "cuda_stream", stream))  # 0 = legacy default stream
+            self.lib.skycell_gpu_set_stream(self._ctx, C.c_void_p(h), 0)
 
     # ---- sharded query phases (include/skycell_gpu.h, DESIGN.md §4); the
     # exchanges between them are issued by paper_2107_09993_b200.dist.

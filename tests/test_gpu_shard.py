@@ -67,6 +67,8 @@ CASES = [(0, 200_000, 4, None), (1, 150_000, 4, None), (2, 60_000, 3, None), (2,
 def test_loopback_shards_match_single(engines, oracle, case, G):
     from oracle.oracle import quantize_f32
     dist_id, n, d, rho = case
+    if n < G:
+        pytest.skip("every shard must hold at least one record")
     x = quantize_f32(oracle.generate(dist_id, n, d, 99 + n))
     rho = rho or sky.default_rho(n, d)
     mn, mx = np.zeros(d), np.ones(d)
