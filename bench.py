@@ -175,6 +175,8 @@ def run_ours(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dist_id, n_gpu, d, desc = CONFIGS[args.config]
+    if args.n:
+        n_gpu, desc = args.n, desc + f" [n overridden: {args.n} per GPU]"
     eng = sky.Engine(local)
     if world > 1:
         import torch.distributed as tdist
@@ -317,6 +319,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--rho", type=int, default=0)
+    ap.add_argument("--n", type=int, default=0, help="override the config's points per GPU (debugging)")
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

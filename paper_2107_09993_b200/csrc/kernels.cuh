@@ -342,9 +342,11 @@ __device__ __forceinline__ uint32_t mag_col(float u, float scale) {
 // is a constant-weight IMAD chain; RHO == 0 is the general runtime path.
 template <typename TIn, typename TOut, int D, bool IDENT, int THREADS, int PPT, int RHO>
 __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
+  static_assert(PPT <= 8, "survivor codes are (j * 32 + lane) in one byte");
   extern __shared__ __align__(16) uint8_t sm[];
   uint32_t* occ_s = reinterpret_cast<uint32_t*>(sm);
   uint8_t* H_s = reinterpret_cast<uint8_t*>(occ_s + p.lo_words);
+  uint8_t* code_w = H_s + ((p.h_entries + 15) & ~15u) + (threadIdx.x >> 5) * (32 * PPT);  // survivor codes
   for (uint32_t w = threadIdx.x; w < p.lo_words; w += THREADS) occ_s[w] = 0;
   for (uint32_t e = threadIdx.x; e < p.h_entries; e += THREADS) H_s[e] = p.H[e];
   __syncthreads();
@@ -455,17 +457,42 @@ __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
         wo.base = __shfl_sync(kFull, bb, 0);
         wo.fill = 0;
       }
-      u64 o = wo.base + wo.fill;
+      const u64 o = wo.base + wo.fill;
+      // Survivors (~12% of the tile at the headline config) are compacted
+      // onto consecutive lanes before any per-survivor work: their (j, lane)
+      // codes are staged in tile order, each lane pulls one survivor's
+      // coordinates by shuffle, and the row / id stores are coalesced.
+      {
+        unsigned cum = 0;
 #pragma unroll
-      for (int j = 0; j < PPT; ++j) {
-        if (keep[j]) {
-          const u64 slot = o + __popc(mk[j] & lt);
+        for (int j = 0; j < PPT; ++j) {
+          if (keep[j]) code_w[cum + __popc(mk[j] & lt)] = (uint8_t)(j * 32 + lane);
+          cum += __popc(mk[j]);
+        }
+      }
+      __syncwarp();
+      for (unsigned r = 0; r < tot; r += 32) {
+        const unsigned sidx = r + lane;
+        const bool act = sidx < tot;
+        const unsigned cd = act ? code_w[sidx] : 0u;
+        const int sj = (int)(cd >> 5), src = (int)(cd & 31);
+        TIn x[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) x[k] = cur[0][k];
+#pragma unroll
+        for (int jj = 0; jj < PPT; ++jj)
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            const TIn tv = __shfl_sync(kFull, cur[jj][k], src);
+            if (sj == jj) x[k] = tv;
+          }
+        if (act) {
           TOut u[D];
           if constexpr (IDENT) {
             uint32_t l = 0;
 #pragma unroll
             for (int k = D - 1; k >= 0; --k) {
-              u[k] = __saturatef(cur[j][k]);  // the stored proxy (dataset.cpp:45 clamp, 1.0f = 1 - 2^-32)
+              u[k] = __saturatef(x[k]);  // the stored proxy (dataset.cpp:45 clamp, 1.0f = 1 - 2^-32)
               l = l * mul_r + mag_col(fminf(u[k], 0x1.fffffep-1f), fs_r);
             }
             if (lin32) set_bit_cached(p.occ_rho, (u64)(l - rcorr));
@@ -480,16 +507,16 @@ __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
             u64 lin = 0;
 #pragma unroll
             for (int k = D - 1; k >= 0; --k) {
-              u[k] = Coord<TIn, TOut, IDENT>::value(cur[j][k], p.nm, k);
-              lin = (lin << rho) | (u64)col_at<TIn, TOut, IDENT>(cur[j][k], p.nm, k, fs_r, ds_r, top);
+              u[k] = Coord<TIn, TOut, IDENT>::value(x[k], p.nm, k);
+              lin = (lin << rho) | (u64)col_at<TIn, TOut, IDENT>(x[k], p.nm, k, fs_r, ds_r, top);
             }
             set_bit_cached(p.occ_rho, lin);
           }
-          store_row<TOut, D>(out_rows, slot, u);
-          p.out_ids[slot] = p.id_base + base + j * 32;
+          store_row<TOut, D>(out_rows, o + sidx, u);
+          p.out_ids[o + sidx] = p.id_base + t * WT + sj * 32 + src;
         }
-        o += __popc(mk[j]);
       }
+      __syncwarp();
       wo.fill += tot;
       kept += tot;
     }
@@ -746,6 +773,8 @@ __global__ void __launch_bounds__(THREADS) k_candidates(CandParams p) {
     const u64 i = wbase + lane;
     bool keep = false;
     T v[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) v[k] = (T)2;  // empty slot: dominated by nothing that matters (keep = false)
     u64 ps = 0;
     uint32_t pid = kNoId;
     if (i < n) pid = p.ids[i];
@@ -763,15 +792,25 @@ __global__ void __launch_bounds__(THREADS) k_candidates(CandParams p) {
       }
       examined += cand;
       ps = fsum_bits<T, D>(v);
+      keep = cand;
+    }
+    // Strongest filter points first (strength order): the first 8 remove
+    // ~87% of the candidates at the headline config, tested branch-free by
+    // every lane; only the rest continue (divergently) through 8..31.
+    if (nf) {
+      constexpr uint32_t kHead0 = 8;
+      const uint32_t h0 = nf < kHead0 ? nf : kHead0;
       bool dom = false;
-      if (cand && nf) {
-        // strongest filter points first (strength order): most points fall
-        // to one of them (median 1 test at the headline config)
-        const uint32_t head = nf < 32 ? nf : 32;
-        for (uint32_t f = 0; f < head && !dom; ++f)
+#pragma unroll
+      for (uint32_t f = 0; f < kHead0; ++f)
+        if (f < h0) dom |= dominates<T, D>(f_rows + (u64)f * D, v) && f_sum[f] < ps;
+      const uint32_t head = nf < 32 ? nf : 32;
+      if (keep && !dom)
+        for (uint32_t f = h0; f < head && !dom; ++f)
           dom = f_sum[f] < ps && dominates<T, D>(f_rows + (u64)f * D, v);
-      }
-      keep = cand && !dom;
+      keep = keep && !dom;
+    }
+    {
     }
     // Points the 32 strongest filter points missed: the warp scans each one's
     // shortest column prefix of F cooperatively, 32 entries per step
@@ -940,12 +979,12 @@ __global__ void __launch_bounds__(1024) k_strength_order(const T* __restrict__ r
 // ------------------------------------------- K5: exact sort-first dominance
 // Per-dimension candidate lists of a point set with a device-side count.
 // For every dimension k the slots are counting-sorted by the bin
-// (sum bucket b, column c) in BUCKET-MAJOR order, so the candidate
+// (column c, sum bucket b) in column-major order, so the candidate
 // dominators of p in dimension k -- col_k(q) <= col_k(p) and bucket(q) <=
 // bucket(p) (sums are monotone under dominance) -- form one contiguous range
-// per sum bucket: at most kSumBuckets ranges, visited in ascending sum order
-// (strongest dominators first).  A per-dimension column histogram picks the
-// dimension with the fewest candidates.  Layout per dimension:
+// per column, visited in ascending column order.  A per-dimension column
+// histogram picks the dimension with the fewest candidates.  Layout per
+// dimension:
 //   [0, kListBins]                          shifted bin counts -> bin starts
 //   [kListBins + 1, kListBins + kListCols + 1]  shifted column counts -> cumulative
 // Order inside a bin only affects how soon a dominator is met, never the result.
@@ -960,7 +999,7 @@ __device__ __forceinline__ int sum_bucket(u64 fsum_bits) {
   return b < kSumBuckets - 1 ? b : kSumBuckets - 1;
 }
 
-__device__ __forceinline__ int list_bin(int b, int c) { return b * kListCols + c; }
+__device__ __forceinline__ int list_bin(int b, int c) { return c * kSumBuckets + b; }
 
 template <typename T, int D>
 __global__ void k_list_hist(const T* __restrict__ rows, const uint32_t* __restrict__ ids, const u64* __restrict__ fsum,
@@ -1117,12 +1156,14 @@ __global__ void __launch_bounds__(256) k_allpairs_lists(const T* __restrict__ ro
     const unsigned* ob = offs + bk * kListStride;
     const int sb = sum_bucket<D>(ps);
     bool dom = false;
-    for (int b0 = 0; b0 <= sb && !dom; b0 += 32) {
-      const int b = b0 + lane;
+    // columns 0..pc of dimension bk, 32 per round; column c contributes its
+    // sum buckets 0..sb, one contiguous range (column-major bins)
+    for (int c0 = 0; c0 <= pc && !dom; c0 += 32) {
+      const int c = c0 + lane;
       unsigned lo = 0, len = 0;
-      if (b <= sb) {
-        lo = __ldg(ob + list_bin(b, 0));
-        len = __ldg(ob + list_bin(b, pc + 1)) - lo;
+      if (c <= pc) {
+        lo = __ldg(ob + list_bin(0, c));
+        len = __ldg(ob + list_bin(sb + 1, c)) - lo;
       }
       unsigned incl = len;
 #pragma unroll

@@ -21,13 +21,17 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
 #include <vector>
 
 #include "../../include/skycell_gpu.h"
+#include <cub/device/device_radix_sort.cuh>
+
 #include "kernels.cuh"
+#include "tree.cuh"
 #include "datagen.cuh"
 
 using sk::u64;
@@ -42,6 +46,7 @@ struct DevCounters {
   u64 zero;
   u64 m, xs, xs_kept, nf, fs, fin, s1_kept, s2_kept;
   u64 lsky;       // local skyline size (sharded)
+  u64 tvalid;     // valid slots of the set a dominance tree is built over
   u64 un, qend;   // union slots and own-slice end (sharded finish)
   u64 cand[kMaxLayers];
   u64 key[kMaxLayers];
@@ -108,6 +113,8 @@ struct skycell_gpu_ctx {
   DevBuf s1_rows, s1_ids, s2_rows, s2_ids, s2_fsum, flags;
   DevBuf sky_rows, sky_ids, sky_fsum;  // local skyline (sharded)
   DevBuf q_bits, q_orig, q_sub, q_ids, q_mm;  // quadrant_skyline
+  DevBuf t_keys, t_keys2, t_vals, t_vals2, t_cub, t_rows, t_ids, t_fsum, t_lo, t_hi, t_cs, t_ci;  // K5 tree
+  int k5_mode = -1;  // 0 lists, 1 tree, 2 auto (SKYCELL_K5)
   DevCounters* host_ctr = nullptr;  // pinned
   u64* host_param = nullptr;        // pinned H2D staging
   cudaEvent_t ev[8] = {};
@@ -234,6 +241,121 @@ void run_exact(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uin
   ctx->launches += 4;
 }
 
+// Exact sort-first pass through the dominance tree (tree.cuh).  Needs the
+// set's slot count on the host (CUB's item count), so it synchronises once.
+template <typename TOut, int D>
+void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint32_t* ids, const u64* fsum,
+              const u64* count, u64* valid_ctr, u64 q_begin, const u64* q_end, int cell_level) {
+  const int nsm = ctx->num_sms;
+  u64 hv[2];
+  ck(cudaMemcpyAsync(&hv[0], count, 8, cudaMemcpyDeviceToHost, s), "D2H");
+  ck(cudaStreamSynchronize(s), "sync");
+  const u64 nslots = hv[0];
+  if (nslots == 0) return;
+  ensure(ctx->t_keys, nslots * 8);
+  ensure(ctx->t_keys2, nslots * 8);
+  ensure(ctx->t_vals, nslots * 4);
+  ensure(ctx->t_vals2, nslots * 4);
+  ck(cudaMemsetAsync(valid_ctr, 0, 8, s), "memset");
+  const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((nslots + 255) / 256, (u64)nsm * 8));
+  sk::k_tree_keys<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, count,
+                                            static_cast<u64*>(ctx->t_keys.p), static_cast<uint32_t*>(ctx->t_vals.p),
+                                            valid_ctr);
+  size_t temp = 0;
+  ck(cub::DeviceRadixSort::SortPairs(nullptr, temp, static_cast<const u64*>(ctx->t_keys.p),
+                                     static_cast<u64*>(ctx->t_keys2.p), static_cast<const uint32_t*>(ctx->t_vals.p),
+                                     static_cast<uint32_t*>(ctx->t_vals2.p), (int)nslots, 0, 64, s),
+     "cub temp");
+  ensure(ctx->t_cub, temp);
+  ck(cub::DeviceRadixSort::SortPairs(ctx->t_cub.p, temp, static_cast<const u64*>(ctx->t_keys.p),
+                                     static_cast<u64*>(ctx->t_keys2.p), static_cast<const uint32_t*>(ctx->t_vals.p),
+                                     static_cast<uint32_t*>(ctx->t_vals2.p), (int)nslots, 0, 64, s),
+     "cub sort");
+  ck(cudaMemcpyAsync(&hv[1], valid_ctr, 8, cudaMemcpyDeviceToHost, s), "D2H");
+  ck(cudaStreamSynchronize(s), "sync");
+  const u64 m = hv[1];
+  ctx->launches += 2;
+  if (m == 0) return;
+  sk::TreeShape sh{};
+  sh.m = m;
+  sh.nleaf = (m + sk::kLeaf - 1) / sk::kLeaf;
+  u64 off = 0, cnt = sh.nleaf;
+  int L = 0;
+  while (true) {
+    sh.off[L] = off;
+    sh.cnt[L] = cnt;
+    off += cnt;
+    ++L;
+    if (cnt == 1) break;
+    cnt = (cnt + 1) / 2;
+  }
+  sh.levels = L;
+  const u64 nodes = off;
+  ensure(ctx->t_rows, m * D * sizeof(TOut));
+  ensure(ctx->t_ids, m * 4);
+  ensure(ctx->t_fsum, m * 8);
+  ensure(ctx->t_lo, nodes * D * sizeof(TOut));
+  ensure(ctx->t_hi, nodes * D * sizeof(TOut));
+  ensure(ctx->t_cs, nodes * 8);
+  ensure(ctx->t_ci, nodes * 4);
+  TOut* srows = static_cast<TOut*>(ctx->t_rows.p);
+  uint32_t* sids = static_cast<uint32_t*>(ctx->t_ids.p);
+  u64* sfsum = static_cast<u64*>(ctx->t_fsum.p);
+  const uint32_t* order = static_cast<const uint32_t*>(ctx->t_vals2.p);
+  const unsigned gm = (unsigned)std::max<u64>(1, std::min<u64>((m + 255) / 256, (u64)nsm * 8));
+  sk::k_tree_gather<TOut, D><<<gm, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, order, m, srows, sids, sfsum);
+  sk::TreeView<TOut, D> tv{static_cast<TOut*>(ctx->t_lo.p), static_cast<TOut*>(ctx->t_hi.p),
+                           static_cast<u64*>(ctx->t_cs.p), static_cast<uint32_t*>(ctx->t_ci.p)};
+  const unsigned gl = (unsigned)std::max<u64>(1, std::min<u64>((sh.nleaf * 32 + 255) / 256, (u64)nsm * 8));
+  sk::k_tree_leaves<TOut, D><<<gl, 256, 0, s>>>(srows, sids, sfsum, m, sh.nleaf, tv);
+  ctx->launches += 2;
+  for (int l = 1; l < sh.levels; ++l) {
+    const unsigned gn = (unsigned)std::max<u64>(1, std::min<u64>((sh.cnt[l] + 255) / 256, (u64)nsm * 8));
+    sk::k_tree_level<TOut, D><<<gn, 256, 0, s>>>(tv, sh.off[l - 1], sh.cnt[l - 1], sh.off[l], sh.cnt[l]);
+    ++ctx->launches;
+  }
+  const unsigned gq = (unsigned)std::max<u64>(1, std::min<u64>((m * 32 + 255) / 256, (u64)nsm * 8));
+  sk::k_tree_query<TOut, D><<<gq, 256, 0, s>>>(srows, sids, sfsum, order, tv, sh, q_begin, q_end, cell_level,
+                                              static_cast<uint8_t*>(ctx->flags.p));
+  ++ctx->launches;
+}
+
+// SKYCELL_K5 = lists | tree | auto (default): which K5 variant runs.
+int k5_mode(skycell_gpu_ctx* ctx) {
+  if (ctx->k5_mode < 0) {
+    const char* e = std::getenv("SKYCELL_K5");
+    ctx->k5_mode = (e && !std::strcmp(e, "lists")) ? 0 : (e && !std::strcmp(e, "tree")) ? 1 : 2;
+  }
+  return ctx->k5_mode;
+}
+
+// Sets up to this many slots go through the column lists; larger ones
+// (anti-correlated data: 8e6 at n=1e8 d=4, 5.4e7 at d=6) through the tree,
+// whose cost grows with the skyline boundary instead of the list prefixes.
+constexpr u64 kTreeMinSlots = 1ull << 20;
+
+// K5 dispatcher: flags[slot] for the query slots of the set.
+template <typename TOut, int D>
+void run_dominance(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint32_t* ids, const u64* fsum,
+                   const u64* count, u64 cap, unsigned* hist, unsigned* cursor, u64* valid_ctr, u64 q_begin = 0,
+                   const u64* q_end = nullptr, int cell_level = 0) {
+  int mode = k5_mode(ctx);
+  if (mode == 2) {
+    if (cap <= kTreeMinSlots) {
+      mode = 0;
+    } else {
+      u64 nslots = 0;
+      ck(cudaMemcpyAsync(&nslots, count, 8, cudaMemcpyDeviceToHost, s), "D2H");
+      ck(cudaStreamSynchronize(s), "sync");
+      mode = nslots > kTreeMinSlots ? 1 : 0;
+    }
+  }
+  if (mode == 0)
+    run_exact<TOut, D>(ctx, s, rows, ids, fsum, count, cap, hist, cursor, q_begin, q_end, cell_level);
+  else
+    run_tree<TOut, D>(ctx, s, rows, ids, fsum, count, valid_ctr, q_begin, q_end, cell_level);
+}
+
 template <typename TIn, typename TOut, bool IDENT, int D>
 struct Pipe final : PipeBase {
   Query q;
@@ -300,7 +422,7 @@ struct Pipe final : PipeBase {
     table_entries = 1ull << (u64)(rho * (D - 1));
 
     // K1 geometry: persistent warps over round-robin warp tiles
-    smem1 = (size_t)lo_words * 4 + ((h_entries + 15) & ~15u) + 16;
+    smem1 = (size_t)lo_words * 4 + ((h_entries + 15) & ~15u) + (size_t)kStreamThreads * PPT1 + 16;
     kstream = pick_stream(rho);
     ck(cudaFuncSetAttribute(kstream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1), "smem attr");
     int occ_blocks = 0;
@@ -413,8 +535,9 @@ struct Pipe final : PipeBase {
         if (wide) sk::k_candidates<TOut, D, uint32_t, kThreads><<<grid4, kThreads, 16, s>>>(pc);
         else sk::k_candidates<TOut, D, uint8_t, kThreads><<<grid4, kThreads, 16, s>>>(pc);
         ++ctx->launches;
-        run_exact<TOut, D>(ctx, s, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
-                           static_cast<const u64*>(ctx->s2_fsum.p), &c->xs, cap4, U(o_shist), U(o_scur));
+        run_dominance<TOut, D>(ctx, s, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
+                               static_cast<const u64*>(ctx->s2_fsum.p), &c->xs, cap4, U(o_shist), U(o_scur),
+                               &c->tvalid);
         sk::k_compact_members<TOut, D><<<nsm * 4, 256, 0, s>>>(
             static_cast<const TOut*>(ctx->s2_rows.p), static_cast<const uint32_t*>(ctx->s2_ids.p),
             static_cast<const uint8_t*>(ctx->flags.p), static_cast<const u64*>(ctx->s2_fsum.p), &c->xs,
@@ -538,9 +661,9 @@ struct Pipe final : PipeBase {
   // ---- K5 over S2 (the local point set)
   void exact_local() {
     DevCounters* c = ctr();
-    run_exact<TOut, D>(ctx, s, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
-                       static_cast<const u64*>(ctx->s2_fsum.p), &c->s2, cap4, U(o_hist), U(o_cur), 0, nullptr,
-                       cell_level());
+    run_dominance<TOut, D>(ctx, s, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
+                           static_cast<const u64*>(ctx->s2_fsum.p), &c->s2, cap4, U(o_hist), U(o_cur), &c->tvalid, 0,
+                           nullptr, cell_level());
   }
 
   // ---- K6: members' ids in ascending order through the id bitmap
@@ -665,9 +788,9 @@ struct Pipe final : PipeBase {
     ctx->host_param[1] = (u64)rank * maxc + own_count;
     ck(cudaMemcpyAsync(&c->un, ctx->host_param, 16, cudaMemcpyHostToDevice, s), "params");
     ck(cudaMemsetAsync(ctx->flags.p, 0, cap, s), "flags");
-    run_exact<TOut, D>(ctx, s, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
-                       static_cast<const u64*>(ctx->s2_fsum.p), &c->un, cap, U(o_fhist), U(o_fcur),
-                       (u64)rank * maxc, &c->qend, cell_level());
+    run_dominance<TOut, D>(ctx, s, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
+                           static_cast<const u64*>(ctx->s2_fsum.p), &c->un, cap, U(o_fhist), U(o_fcur), &c->tvalid,
+                           (u64)rank * maxc, &c->qend, cell_level());
     ids_out(static_cast<const uint32_t*>(ctx->s2_ids.p), &c->un, cap, ids_dst ? ids_dst : id_dst());
     ck(cudaGetLastError(), "kernel launch");
     if (q.timed) ck(cudaEventRecord(ctx->ev[3], s), "event");
@@ -911,7 +1034,9 @@ void skycell_gpu_destroy(skycell_gpu_ctx* ctx) {
                     &ctx->smp_rows, &ctx->smp_ids, &ctx->smp_fsum, &ctx->f_rows, &ctx->f_fsum, &ctx->f_lists,
                     &ctx->f_offs, &ctx->lists, &ctx->ids_dev, &ctx->s1_rows, &ctx->s1_ids, &ctx->s2_rows,
                     &ctx->s2_ids, &ctx->s2_fsum, &ctx->flags, &ctx->sky_rows, &ctx->sky_ids, &ctx->sky_fsum,
-                    &ctx->q_bits, &ctx->q_orig, &ctx->q_sub, &ctx->q_ids, &ctx->q_mm};
+                    &ctx->q_bits, &ctx->q_orig, &ctx->q_sub, &ctx->q_ids, &ctx->q_mm, &ctx->t_keys,
+                    &ctx->t_keys2, &ctx->t_vals, &ctx->t_vals2, &ctx->t_cub, &ctx->t_rows, &ctx->t_ids,
+                    &ctx->t_fsum, &ctx->t_lo, &ctx->t_hi, &ctx->t_cs, &ctx->t_ci};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (auto& e : ctx->ev)

@@ -172,3 +172,44 @@ def test_gpu_quadrant_edges(engine, oracle):
     want = oracle.quadrant_skyline(v, o, 3)
     got = engine.quadrant_skyline(ds, o, 3)
     check(got, want.ids, want.points_examined)
+
+
+@pytest.fixture(scope="module", params=["tree", "lists"])
+def forced_engine(request):
+    """An engine pinned to one K5 variant (SKYCELL_K5 is read once per context)."""
+    import os
+    old = os.environ.get("SKYCELL_K5")
+    os.environ["SKYCELL_K5"] = request.param
+    e = sky.Engine(0)
+    e.compute_skyline(sky.Dataset(np.zeros((1, 2)), np.zeros(2), np.ones(2)), 1)  # latch the mode
+    if old is None:
+        del os.environ["SKYCELL_K5"]
+    else:
+        os.environ["SKYCELL_K5"] = old
+    yield e
+    e.close()
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_gpu_k5_variants_vs_oracle(forced_engine, oracle, seed):
+    """Both K5 variants (column lists, dominance tree) on every path:
+    identity f32, general f64, merge_cross_cell = false."""
+    from oracle.oracle import quantize_f32
+    rng = np.random.default_rng(500 + seed)
+    dist, d = seed % 3, int(rng.integers(2, 9))
+    n = int(rng.integers(1, 8000))
+    rho = int(rng.integers(1, 4))
+    v = oracle.generate(dist, n, d, 900 + seed)
+    for x, mn, mx in ((quantize_f32(v), np.zeros(d), np.ones(d)), (v * 4 - 1, (v * 4 - 1).min(0), (v * 4 - 1).max(0))):
+        for merge in (True, False):
+            want = oracle.compute_skyline(x.astype(np.float64), mn, mx, rho, 1, merge)
+            got = forced_engine.compute_skyline(sky.Dataset(np.ascontiguousarray(x), mn, mx), rho,
+                                                merge_cross_cell=merge)
+            check(got, want.ids, want.points_examined, want.keys, want.candidates)
+
+
+@pytest.mark.parametrize("rec", load_json("large.json")["records"], ids=lambda r: r["key"])
+def test_gpu_k5_variants_large_golden(forced_engine, oracle, rec):
+    x, mn, mx = inputs_for(oracle, rec)
+    r = forced_engine.compute_skyline(sky.Dataset(x, mn, mx), rec["rho"])
+    check(r, load_ids("large_ids.npz")[rec["key"]], rec["points_examined"], rec["keys"], rec["candidates"])
