@@ -122,21 +122,29 @@ struct WarpOut {
 };
 
 // Reserve positions for the lanes with `flag` set; returns this lane's slot.
-// Call with all 32 lanes.  `stamp(slot)` writes kNoId into abandoned slots.
+// Call with all 32 lanes.  A batch that does not fit the current chunk
+// straddles into a freshly reserved one, so only each warp's last chunk can
+// hold unused slots (stamped with kNoId by warp_close): the output capacity
+// needed is count + warps * chunk whatever the survivor rate.
 template <typename Stamp>
-__device__ __forceinline__ u64 warp_reserve(WarpOut& wo, bool flag, u64* counter, Stamp stamp) {
+__device__ __forceinline__ u64 warp_reserve(WarpOut& wo, bool flag, u64* counter, Stamp) {
   const int lane = threadIdx.x & 31;
   const unsigned m = __ballot_sync(kFull, flag);
   const unsigned cnt = __popc(m);
-  if (wo.fill + cnt > wo.chunk) {
-    for (unsigned s = wo.fill + lane; s < wo.chunk; s += 32) stamp(wo.base + s);
-    u64 b = 0;
-    if (lane == 0) b = atomicAdd(counter, (u64)wo.chunk);
-    wo.base = __shfl_sync(kFull, b, 0);
-    wo.fill = 0;
+  const unsigned rank = __popc(m & ((1u << lane) - 1));
+  const unsigned rem = wo.chunk - wo.fill;
+  u64 nb = 0;
+  if (cnt > rem) {  // chunk >= 32 >= cnt: one new chunk always suffices
+    if (lane == 0) nb = atomicAdd(counter, (u64)wo.chunk);
+    nb = __shfl_sync(kFull, nb, 0);
   }
-  const u64 slot = wo.base + wo.fill + __popc(m & ((1u << lane) - 1));
-  wo.fill += cnt;
+  const u64 slot = rank < rem ? wo.base + wo.fill + rank : nb + (rank - rem);
+  if (cnt > rem) {
+    wo.base = nb;
+    wo.fill = cnt - rem;
+  } else {
+    wo.fill += cnt;
+  }
   return slot;
 }
 

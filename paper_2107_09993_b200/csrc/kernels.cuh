@@ -450,14 +450,16 @@ __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
       tot += __popc(mk[j]);
     }
     if (tot) {
-      if (wo.fill + tot > wo.chunk) {  // host guarantees chunk >= 32 * PPT >= tot
-        for (unsigned sl = wo.fill + lane; sl < wo.chunk; sl += 32) stamp(wo.base + sl);
-        u64 bb = 0;
-        if (lane == 0) bb = atomicAdd(p.out_reserved, (u64)wo.chunk);
-        wo.base = __shfl_sync(kFull, bb, 0);
-        wo.fill = 0;
+      // the tile's survivors fill the rest of the current chunk and straddle
+      // into a new one (host guarantees chunk >= 32 * PPT >= tot)
+      const unsigned rem = wo.chunk - wo.fill;
+      u64 nb = 0;
+      if (tot > rem) {
+        if (lane == 0) nb = atomicAdd(p.out_reserved, (u64)wo.chunk);
+        nb = __shfl_sync(kFull, nb, 0);
       }
       const u64 o = wo.base + wo.fill;
+      auto out_slot = [&](unsigned sidx) { return sidx < rem ? o + sidx : nb + (sidx - rem); };
       // Survivors (~12% of the tile at the headline config) are compacted
       // onto consecutive lanes before any per-survivor work: their (j, lane)
       // codes are staged in tile order, each lane pulls one survivor's
@@ -512,12 +514,18 @@ __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
             }
             set_bit_cached(p.occ_rho, lin);
           }
-          store_row<TOut, D>(out_rows, o + sidx, u);
-          p.out_ids[o + sidx] = p.id_base + t * WT + sj * 32 + src;
+          const u64 slot = out_slot(sidx);
+          store_row<TOut, D>(out_rows, slot, u);
+          p.out_ids[slot] = p.id_base + t * WT + sj * 32 + src;
         }
       }
       __syncwarp();
-      wo.fill += tot;
+      if (tot > rem) {
+        wo.base = nb;
+        wo.fill = tot - rem;
+      } else {
+        wo.fill += tot;
+      }
       kept += tot;
     }
     if (__any_sync(kFull, bad)) {  // rare: NaN/Inf (or overflow of the probe sum)
@@ -796,26 +804,22 @@ __global__ void __launch_bounds__(THREADS) k_candidates(CandParams p) {
     }
     // Strongest filter points first (strength order): the first 8 remove
     // ~87% of the candidates at the headline config, tested branch-free by
-    // every lane; only the rest continue (divergently) through 8..31.
+    // every lane.
+    constexpr uint32_t kHead0 = 8;
     if (nf) {
-      constexpr uint32_t kHead0 = 8;
       const uint32_t h0 = nf < kHead0 ? nf : kHead0;
       bool dom = false;
 #pragma unroll
       for (uint32_t f = 0; f < kHead0; ++f)
         if (f < h0) dom |= dominates<T, D>(f_rows + (u64)f * D, v) && f_sum[f] < ps;
-      const uint32_t head = nf < 32 ? nf : 32;
-      if (keep && !dom)
-        for (uint32_t f = h0; f < head && !dom; ++f)
-          dom = f_sum[f] < ps && dominates<T, D>(f_rows + (u64)f * D, v);
       keep = keep && !dom;
     }
-    {
-    }
-    // Points the 32 strongest filter points missed: the warp scans each one's
-    // shortest column prefix of F cooperatively, 32 entries per step
-    // (a dominator f has col_k(f) <= col_k(p) in every dimension).
-    unsigned pend = __ballot_sync(kFull, keep && nf > 32);
+    // The rest, one pending point at a time with the whole warp: first the
+    // next 32 strongest filter points (one per lane), then the point's
+    // shortest column prefix of F, 32 entries per step (a dominator f has
+    // col_k(f) <= col_k(p) in every dimension).  A per-lane loop here ran
+    // with ~5 of 32 lanes active (ncu: 68% of K4's instructions).
+    unsigned pend = __ballot_sync(kFull, keep && nf > kHead0);
     while (pend) {
       const int src = __ffs(pend) - 1;
       pend &= pend - 1;
@@ -823,6 +827,16 @@ __global__ void __launch_bounds__(THREADS) k_candidates(CandParams p) {
 #pragma unroll
       for (int k = 0; k < D; ++k) pv[k] = __shfl_sync(kFull, v[k], src);
       const u64 pps = __shfl_sync(kFull, ps, src);
+      bool found;
+      {
+        const uint32_t f = kHead0 + lane;
+        found = __any_sync(kFull, f < nf && f_sum[f] < pps && dominates<T, D>(f_rows + (u64)f * D, pv));
+      }
+      if (found) {
+        if (lane == src) keep = false;
+        continue;
+      }
+      if (nf <= kHead0 + 32) continue;
       int bk = 0;
       unsigned end = 0xffffffffu;
 #pragma unroll
@@ -831,7 +845,6 @@ __global__ void __launch_bounds__(THREADS) k_candidates(CandParams p) {
         if (e < end) { end = e; bk = k; }
       }
       const uint16_t* lst = f_list + (u64)bk * fm;
-      bool found = false;
       for (unsigned base = 0; base < end && !found; base += 32) {
         const unsigned e = base + lane;
         bool d_l = false;
@@ -1113,10 +1126,9 @@ __device__ __forceinline__ bool same_cell(const T* q, const T* p, int L, int top
 
 // flag[i] = 1 iff no point q of the set precedes i (sort-first order,
 // refine.cpp:38-41) and dominates it, for query slots [q_begin, *q_end).
-// One warp per point: the candidate ranges of its sum buckets (<= 32 per
-// round) are concatenated by a warp scan of their lengths; the 32 lanes then
-// test 32 consecutive candidates per step (independent gathers in flight) and
-// stop at the first step with a dominator.  A point with sum 0 lies at the
+// One warp per point: per column of its shortest prefix, the 32 lanes test
+// 32 candidates per step (independent gathers in flight) and stop at the
+// first step with a dominator.  A point with sum 0 lies at the
 // origin and has no dominator (normalised coordinates are >= 0); skipping it
 // keeps correlated data's ~8.7e-4 n exact origin duplicates
 // from scanning each other.
@@ -1156,36 +1168,15 @@ __global__ void __launch_bounds__(256) k_allpairs_lists(const T* __restrict__ ro
     const unsigned* ob = offs + bk * kListStride;
     const int sb = sum_bucket<D>(ps);
     bool dom = false;
-    // columns 0..pc of dimension bk, 32 per round; column c contributes its
-    // sum buckets 0..sb, one contiguous range (column-major bins)
-    for (int c0 = 0; c0 <= pc && !dom; c0 += 32) {
-      const int c = c0 + lane;
-      unsigned lo = 0, len = 0;
-      if (c <= pc) {
-        lo = __ldg(ob + list_bin(0, c));
-        len = __ldg(ob + list_bin(sb + 1, c)) - lo;
-      }
-      unsigned incl = len;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned y = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const unsigned total = __shfl_sync(kFull, incl, 31);
-      for (unsigned base = 0; base < total; base += 32) {
+    // columns 0..pc of dimension bk in ascending order; column c contributes
+    // its sum buckets 0..sb, one contiguous range (column-major bins)
+    for (int c = 0; c <= pc && !dom; ++c) {
+      const unsigned s0 = __ldg(ob + list_bin(0, c)), s1 = __ldg(ob + list_bin(sb + 1, c));
+      for (unsigned base = s0; base < s1; base += 32) {
         const unsigned e = base + lane;
-        // range j holding entry e: the first lane whose inclusive end exceeds e
-        int j = 0;
-#pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-          const unsigned end_j = __shfl_sync(kFull, incl, j + step - 1);
-          if (end_j <= e) j += step;
-        }
-        const unsigned start_j = __shfl_sync(kFull, incl - len, j);
-        const unsigned lo_j = __shfl_sync(kFull, lo, j);
         bool d_l = false;
-        if (e < total) {
-          const uint32_t q = __ldg(lst + lo_j + (e - start_j));
+        if (e < s1) {
+          const uint32_t q = __ldg(lst + e);
           const u64 qs = __ldg(fsum + q);
           if (qs <= ps) {
             const uint32_t qi = __ldg(ids + q);

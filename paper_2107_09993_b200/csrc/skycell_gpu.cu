@@ -170,6 +170,23 @@ int default_rho(u64 n, int d) {
   return std::max(1, std::min(6, (bw - 1) / d));
 }
 
+// SKYCELL_TRACE=1: synchronise and print the host time of each phase to
+// stderr (debugging only; it serialises the pipeline).
+struct Tracer {
+  bool on = std::getenv("SKYCELL_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(cudaStream_t s, const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    std::fprintf(stderr, "[skycell] %-24s %9.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
+};
+Tracer& tracer() {
+  static thread_local Tracer t;
+  return t;
+}
+
 // ------------------------------------------------------------------ config
 constexpr int kThreads = 256;
 
@@ -258,6 +275,7 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
   ensure(ctx->t_vals2, nslots * 4);
   ck(cudaMemsetAsync(valid_ctr, 0, 8, s), "memset");
   const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((nslots + 255) / 256, (u64)nsm * 8));
+  tracer().mark(s, "tree: count read");
   sk::k_tree_keys<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, count,
                                             static_cast<u64*>(ctx->t_keys.p), static_cast<uint32_t*>(ctx->t_vals.p),
                                             valid_ctr);
@@ -271,6 +289,7 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
                                      static_cast<u64*>(ctx->t_keys2.p), static_cast<const uint32_t*>(ctx->t_vals.p),
                                      static_cast<uint32_t*>(ctx->t_vals2.p), (int)nslots, 0, 64, s),
      "cub sort");
+  tracer().mark(s, "tree: keys + sort");
   ck(cudaMemcpyAsync(&hv[1], valid_ctr, 8, cudaMemcpyDeviceToHost, s), "D2H");
   ck(cudaStreamSynchronize(s), "sync");
   const u64 m = hv[1];
@@ -290,6 +309,7 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
     cnt = (cnt + 1) / 2;
   }
   sh.levels = L;
+  if (sh.nleaf >= (1ull << 27) || L > 31) throw ApiFail{SKYCELL_UNSUPPORTED, "skycell_gpu: dominance tree too large"};
   const u64 nodes = off;
   ensure(ctx->t_rows, m * D * sizeof(TOut));
   ensure(ctx->t_ids, m * 4);
@@ -314,10 +334,12 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
     sk::k_tree_level<TOut, D><<<gn, 256, 0, s>>>(tv, sh.off[l - 1], sh.cnt[l - 1], sh.off[l], sh.cnt[l]);
     ++ctx->launches;
   }
+  tracer().mark(s, "tree: build");
   const unsigned gq = (unsigned)std::max<u64>(1, std::min<u64>((m * 32 + 255) / 256, (u64)nsm * 8));
   sk::k_tree_query<TOut, D><<<gq, 256, 0, s>>>(srows, sids, sfsum, order, tv, sh, q_begin, q_end, cell_level,
                                               static_cast<uint8_t*>(ctx->flags.p));
   ++ctx->launches;
+  tracer().mark(s, "tree: query");
 }
 
 // SKYCELL_K5 = lists | tree | auto (default): which K5 variant runs.
@@ -506,8 +528,11 @@ struct Pipe final : PipeBase {
       sp.fsum = static_cast<u64*>(ctx->smp_fsum.p);
       sp.id_base = q.id_base;
       const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((m + 255) / 256, (u64)nsm * 8));
+      tracer().mark(s, "K0: memset");
       sk::k_sample<TIn, TOut, D, IDENT><<<g, 256, 0, s>>>(sp);
+      tracer().mark(s, "K0: sample");
       sk::k_build_filter<<<1, 1024, h_entries, s>>>(U(o_sla), la, D, static_cast<uint8_t*>(ctx->H.p));
+      tracer().mark(s, "K0: build_filter");
       ctx->launches += 2;
       if (q.merge) {
         // The sample skyline only serves as K4's point filter, which phase-1
@@ -516,6 +541,7 @@ struct Pipe final : PipeBase {
           if (wide) launch_tables<uint32_t>(ctx, s, U(o_srho), rho, D, static_cast<uint32_t*>(ctx->table_s.p));
           else launch_tables<uint8_t>(ctx, s, U(o_srho), rho, D, static_cast<uint8_t*>(ctx->table_s.p));
         }
+        tracer().mark(s, "K0: sample tables");
         // sample points not strictly dominated at layer rho -> X (s2 buffers)
         sk::CandParams pc{};
         pc.rows = ctx->smp_rows.p;
@@ -535,9 +561,11 @@ struct Pipe final : PipeBase {
         if (wide) sk::k_candidates<TOut, D, uint32_t, kThreads><<<grid4, kThreads, 16, s>>>(pc);
         else sk::k_candidates<TOut, D, uint8_t, kThreads><<<grid4, kThreads, 16, s>>>(pc);
         ++ctx->launches;
+        tracer().mark(s, "K0: sample X");
         run_dominance<TOut, D>(ctx, s, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
                                static_cast<const u64*>(ctx->s2_fsum.p), &c->xs, cap4, U(o_shist), U(o_scur),
                                &c->tvalid);
+        tracer().mark(s, "K0: sample skyline");
         sk::k_compact_members<TOut, D><<<nsm * 4, 256, 0, s>>>(
             static_cast<const TOut*>(ctx->s2_rows.p), static_cast<const uint32_t*>(ctx->s2_ids.p),
             static_cast<const uint8_t*>(ctx->flags.p), static_cast<const u64*>(ctx->s2_fsum.p), &c->xs,
@@ -710,10 +738,15 @@ struct Pipe final : PipeBase {
   // ---- the single-device query
   void run_single() {
     DevCounters* c = ctr();
+    tracer().t0 = std::chrono::steady_clock::now();
     local();
+    tracer().mark(s, "K0+K1");
     prune();
+    tracer().mark(s, "K3+K4");
     exact_local();
+    tracer().mark(s, "K5");
     ids_out(static_cast<const uint32_t*>(ctx->s2_ids.p), &c->s2, cap4, id_dst());
+    tracer().mark(s, "K6");
     ck(cudaGetLastError(), "kernel launch");
     if (q.timed) ck(cudaEventRecord(ctx->ev[3], s), "event");
     read_counters();

@@ -190,13 +190,15 @@ __global__ void __launch_bounds__(256) k_tree_query(const T* __restrict__ srows,
                                                     TreeView<T, D> tv, TreeShape sh, u64 q_begin,
                                                     const u64* __restrict__ q_end, int cell_level,
                                                     uint8_t* __restrict__ flag) {
-  constexpr int kStack = 96;
+  constexpr int kStack = 64;
+  // stack entries: level << 27 | index within the level (nleaf < 2^27)
   __shared__ uint32_t stack_s[8][kStack];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint32_t* stk = stack_s[wib];
   const u64 qend = q_end ? *q_end : ~0ull;
   const int ctop = (1 << cell_level) - 1;
-  const u64 root = sh.off[sh.levels - 1];
+  const int ch = lane / D, kd = lane % D;  // lanes [0, D): child 0 dims; [D, 2D): child 1 dims
+  const unsigned m0 = (1u << D) - 1;
   for (u64 j = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; j < sh.m; j += ((u64)gridDim.x * blockDim.x) >> 5) {
     const uint32_t slot = order[j];
     if (slot < q_begin || slot >= qend) continue;
@@ -208,22 +210,21 @@ __global__ void __launch_bounds__(256) k_tree_query(const T* __restrict__ srows,
     }
     T v[D];
     load_row_cached<T, D>(srows, j, v);
-    // the lane-th coordinate of p, for the per-dimension box tests
     T pk = v[0];
 #pragma unroll
     for (int k = 1; k < D; ++k)
-      if (lane % D == k) pk = v[k];
+      if (kd == k) pk = v[k];
     bool dom = false;
-    int top = 0;
-    if (lane == 0) stk[0] = (uint32_t)root;
-    top = 1;
+    if (lane == 0) stk[0] = (uint32_t)(sh.levels - 1) << 27;
+    int top = 1;
     __syncwarp();
     while (top > 0 && !dom) {
-      const uint32_t node = stk[--top];
+      const uint32_t e = stk[--top];
       __syncwarp();
-      // level of the node: leaves are nodes [0, nleaf)
-      if (node < sh.nleaf) {
-        const u64 q = (u64)node * kLeaf + lane;
+      const int lvl = (int)(e >> 27);
+      const u64 idx = e & ((1u << 27) - 1);
+      if (lvl == 0) {
+        const u64 q = idx * kLeaf + lane;
         bool d_l = false;
         if (q < sh.m) {
           const u64 qs = __ldg(sfsum + q);
@@ -237,46 +238,44 @@ __global__ void __launch_bounds__(256) k_tree_query(const T* __restrict__ srows,
         dom = __any_sync(kFull, d_l);
         continue;
       }
-      // internal node: children 2i, 2i+1 of the level below
-      int lvl = 1;
-      while (lvl < sh.levels - 1 && node >= sh.off[lvl + 1]) ++lvl;
-      const u64 idx = node - sh.off[lvl];
-      const u64 c0 = sh.off[lvl - 1] + 2 * idx;
-      const bool has1 = 2 * idx + 1 < sh.cnt[lvl - 1];
-      // lanes [0, D): child 0 dims; lanes [D, 2D): child 1 dims (D <= 16)
-      const int ch = lane / D, k = lane % D;
+      // internal node: children 2 idx, 2 idx + 1 of level lvl - 1
+      const u64 ci0 = 2 * idx;
+      const bool has1 = ci0 + 1 < sh.cnt[lvl - 1];
+      const u64 c0 = sh.off[lvl - 1] + ci0;
       bool lo_ok = true, hi_lt = true;
       if (ch < 2 && (ch == 0 || has1)) {
         const u64 c = c0 + ch;
-        lo_ok = __ldg(tv.lo + c * D + k) <= pk;
-        hi_lt = __ldg(tv.hi + c * D + k) < pk;
+        lo_ok = __ldg(tv.lo + c * D + kd) <= pk;
+        hi_lt = __ldg(tv.hi + c * D + kd) < pk;
       }
-      const unsigned lo_bad = __ballot_sync(kFull, !lo_ok), hi_ge = __ballot_sync(kFull, !hi_lt);
-      const unsigned m0 = (D == 32 ? kFull : ((1u << D) - 1));
-      u64 s0 = __ldg(tv.cs + c0), s1 = has1 ? __ldg(tv.cs + c0 + 1) : ~0ull;
+      const unsigned lo_bad = __ballot_sync(kFull, !lo_ok), hi_in = __ballot_sync(kFull, hi_lt && ch < 2);
+      const u64 s0 = __ldg(tv.cs + c0), s1 = has1 ? __ldg(tv.cs + c0 + 1) : ~0ull;
       const uint32_t i0 = __ldg(tv.ci + c0), i1 = has1 ? __ldg(tv.ci + c0 + 1) : kNoId;
-      bool want[2];
-      for (int c = 0; c < 2; ++c) {
-        const unsigned msk = m0 << (c * D);
-        const u64 cs = c ? s1 : s0;
-        const uint32_t ci = c ? i1 : i0;
-        want[c] = (c == 0 || has1) && !(lo_bad & msk) && cs <= ps;
-        if (want[c] && !cell_level && !(hi_ge & msk) && precedes(cs, ci, ps, pid)) dom = true;
+      const unsigned in0 = hi_in & m0, in1 = (hi_in >> D) & m0;
+      const bool want0 = !(lo_bad & m0) && s0 <= ps;
+      const bool want1 = has1 && !((lo_bad >> D) & m0) && s1 <= ps;
+      // a child strictly below p in every dimension: its champion decides
+      if (!cell_level && ((want0 && in0 == m0 && precedes(s0, i0, ps, pid)) ||
+                          (want1 && in1 == m0 && precedes(s1, i1, ps, pid)))) {
+        dom = true;
+        break;
       }
-      if (dom) break;
-      // push the weaker child first so the stronger one is visited next
-      const bool first1 = want[0] && want[1] ? (key_less(s1, i1, s0, i0)) : false;
+      // visit first the child lying below p in more dimensions (more likely
+      // to hold a dominator), ties: the stronger champion
+      const int n0 = __popc(in0), n1 = __popc(in1);
+      const bool first1 = want0 && want1 && (n1 > n0 || (n1 == n0 && key_less(s1, i1, s0, i0)));
+      const uint32_t e0 = ((uint32_t)(lvl - 1) << 27) | (uint32_t)ci0, e1 = e0 + 1;
       if (lane == 0) {
+        int t = top;
         if (first1) {
-          stk[top] = (uint32_t)c0;
-          stk[top + 1] = (uint32_t)(c0 + 1);
+          stk[t++] = e0;
+          stk[t++] = e1;
         } else {
-          int t = top;
-          if (want[1]) stk[t++] = (uint32_t)(c0 + 1);
-          if (want[0]) stk[t++] = (uint32_t)c0;
+          if (want1) stk[t++] = e1;
+          if (want0) stk[t++] = e0;
         }
       }
-      top += (int)want[0] + (int)want[1];
+      top += (int)want0 + (int)want1;
       __syncwarp();
     }
     if (lane == 0) flag[slot] = dom ? 0 : 1;
