@@ -267,19 +267,22 @@ def run_ours(args):
     k1 = statistics.mean(k1_ms)
     alg_bytes = 4 * d * n_gpu
     achieved = alg_bytes / (k1 / 1000.0) / 1e9
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "k_stream_ncu_summary.json")
-    if os.path.exists(prof):
+    # dram__bytes_read + dram__bytes_write of one K1 launch from the newest
+    # committed ncu --set full summary of this config (profiles/*_k1_kstream_<config>.json)
+    traffic, traffic_src = None, None
+    import glob
+    profs = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_k1_kstream_{args.config}.json")))
+    if profs and n_gpu == CONFIGS[args.config][1]:
         try:
-            with open(prof) as f:
-                pj = json.load(f)
-            if pj.get("config") == args.config:
-                traffic = pj.get("dram_bytes_per_launch")
+            with open(profs[-1]) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+            traffic_src = os.path.relpath(profs[-1], ROOT)
         except Exception:
             pass
     roofline = {"bound": "hbm", "kernel": "k_stream (K1)", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes_per_launch": alg_bytes,
                 "kernel_ms": k1, "kernel_share_of_step": k1 / statistics.mean(step_ms), "peak_source": peak_src,
+                "traffic_source": traffic_src,
                 "query_frac": (4 * d * n_gpu + 4 * sky_size) / (ms / 1000.0) / 1e9 / peak}
 
     cpu = None

@@ -345,8 +345,10 @@ __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
   static_assert(PPT <= 8, "survivor codes are (j * 32 + lane) in one byte");
   extern __shared__ __align__(16) uint8_t sm[];
   uint32_t* occ_s = reinterpret_cast<uint32_t*>(sm);
-  uint8_t* H_s = reinterpret_cast<uint8_t*>(occ_s + p.lo_words);
+  uint8_t* H_s = sm + ((p.lo_words * 4 + 15) & ~15u);
   uint8_t* code_w = H_s + ((p.h_entries + 15) & ~15u) + (threadIdx.x >> 5) * (32 * PPT);  // survivor codes
+  u64* occ_cache = reinterpret_cast<u64*>(H_s + ((p.h_entries + 15) & ~15u) + THREADS * PPT);  // kOccCache entries
+  for (int e = threadIdx.x; e < kOccCache; e += THREADS) occ_cache[e] = ~0ull;
   for (uint32_t w = threadIdx.x; w < p.lo_words; w += THREADS) occ_s[w] = 0;
   for (uint32_t e = threadIdx.x; e < p.h_entries; e += THREADS) H_s[e] = p.H[e];
   __syncthreads();
@@ -497,13 +499,13 @@ __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
               u[k] = __saturatef(x[k]);  // the stored proxy (dataset.cpp:45 clamp, 1.0f = 1 - 2^-32)
               l = l * mul_r + mag_col(fminf(u[k], 0x1.fffffep-1f), fs_r);
             }
-            if (lin32) set_bit_cached(p.occ_rho, (u64)(l - rcorr));
+            if (lin32) set_bit_smcache(p.occ_rho, (u64)(l - rcorr), occ_cache);
             else {
               u64 lin = 0;
 #pragma unroll
               for (int k = D - 1; k >= 0; --k)
                 lin = (lin << rho) | (u64)(mag_col(fminf(u[k], 0x1.fffffep-1f), fs_r) - 0x4B000000u);
-              set_bit_cached(p.occ_rho, lin);
+              set_bit_smcache(p.occ_rho, lin, occ_cache);
             }
           } else {
             u64 lin = 0;
@@ -512,7 +514,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
               u[k] = Coord<TIn, TOut, IDENT>::value(x[k], p.nm, k);
               lin = (lin << rho) | (u64)col_at<TIn, TOut, IDENT>(x[k], p.nm, k, fs_r, ds_r, top);
             }
-            set_bit_cached(p.occ_rho, lin);
+            set_bit_smcache(p.occ_rho, lin, occ_cache);
           }
           const u64 slot = out_slot(sidx);
           store_row<TOut, D>(out_rows, slot, u);
@@ -549,12 +551,16 @@ __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
   }
 }
 
+// OR of the per-CTA slabs: blockIdx.y picks a group of slabs, so the
+// (slabs x words) reduction runs on many CTAs; one red.or per word and group.
 __global__ void k_reduce_slabs(const uint32_t* __restrict__ slabs, int nslabs, uint32_t words,
                                uint32_t* __restrict__ out) {
+  const int per = (nslabs + gridDim.y - 1) / gridDim.y;
+  const int s0 = blockIdx.y * per, s1 = min(nslabs, s0 + per);
   for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x) {
     uint32_t x = 0;
-    for (int s = 0; s < nslabs; ++s) x |= slabs[(u64)s * words + w];
-    out[w] |= x;
+    for (int s = s0; s < s1; ++s) x |= slabs[(u64)s * words + w];
+    if (x) atomicOr(out + w, x);
   }
 }
 
@@ -678,6 +684,110 @@ __global__ void k_count_cells(const uint32_t* __restrict__ bits, int L, int d, u
   if ((threadIdx.x & 31) == 0) {
     if (nc) atomicAdd(cand_out, nc);
     if (nk) atomicAdd(key_out, nk);
+  }
+}
+
+// Row-parallel layer counts (same definitions as k_count_cells): one thread
+// per row x = (c_1..c_{d-1}) of layer L.  With PM the prefix-min table,
+//   candidate cells of the row:  c_0 <= PM[x - 1]       (all x_k >= 1; else every cell)
+//   key cells (no top in x):      c_0 < min(PM[x] + 1, top, min_{x_k>=1} PM[x - e_k])
+// so both are occupancy bits below a per-row threshold: d table lookups and
+// a popcount per row instead of d lookups per occupied cell.
+template <typename TT>
+__global__ void k_count_rows(const uint32_t* __restrict__ bits, int L, int d, u64 rows, const TT* __restrict__ PM,
+                             u64* cand_out, u64* key_out) {
+  const int n0 = 1 << L, top = n0 - 1;
+  const u64 mask = (u64)top;
+  const TT none = (TT)~(TT)0;
+  u64 nc = 0, nk = 0;
+  for (u64 r = blockIdx.x * (u64)blockDim.x + threadIdx.x; r < rows; r += (u64)gridDim.x * blockDim.x) {
+    bool all_pos = true, has_top = false;
+    u64 dm1 = 0;  // sum of the per-dimension strides (row index of x - 1)
+    for (int k = 1; k < d; ++k) {
+      const u64 xk = (r >> (L * (k - 1))) & mask;
+      all_pos &= xk >= 1;
+      has_top |= xk == (u64)top;
+      dm1 += 1ull << (L * (k - 1));
+    }
+    int tc = top;  // candidate cells: c_0 <= tc
+    if (all_pos) {
+      const TT v = __ldg(PM + (r - dm1));
+      tc = v == none ? top : min((int)v, top);
+      // PM[x - 1] <= c_0 - 1 means strictly dominated: candidates are c_0 <= PM
+    }
+    int tk = -1;  // key cells: c_0 <= tk
+    if (!has_top) {
+      const TT v0 = __ldg(PM + r);
+      int t = v0 == none ? top : min((int)v0 + 1, top);  // c_0 < PM[x] + 1 and c_0 < top
+      for (int k = 1; k < d; ++k) {
+        if (((r >> (L * (k - 1))) & mask) == 0) continue;
+        const TT v = __ldg(PM + (r - (1ull << (L * (k - 1)))));
+        if (v != none) t = min(t, (int)v);
+      }
+      tk = t - 1;
+    }
+    // count occupied c_0 <= threshold in the row
+    auto count_le = [&](int thr) -> u64 {
+      if (thr < 0) return 0;
+      if (L >= 5) {
+        const u64 wpr = (u64)n0 >> 5;
+        u64 c = 0;
+        for (u64 w = 0; w < wpr; ++w) {
+          const int base = (int)(w * 32);
+          if (base > thr) break;
+          uint32_t x = __ldg(bits + r * wpr + w);
+          if (thr - base < 31) x &= (2u << (thr - base)) - 1;
+          c += __popc(x);
+        }
+        return c;
+      }
+      const u64 bit0 = r * (u64)n0;
+      uint32_t x = (__ldg(bits + (bit0 >> 5)) >> (bit0 & 31)) & ((1u << n0) - 1);
+      if (thr < top) x &= (2u << thr) - 1;
+      return __popc(x);
+    };
+    nc += count_le(tc);
+    nk += count_le(tk);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    nc += __shfl_xor_sync(kFull, nc, o);
+    nk += __shfl_xor_sync(kFull, nk, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (nc) atomicAdd(cand_out, nc);
+    if (nk) atomicAdd(key_out, nk);
+  }
+}
+
+// Word-parallel child-OR for coarse layers L >= 5 (a coarse row spans whole
+// words): coarse word w covers c_0 in [32q, 32q + 32) of row x; its children
+// are the 64 fine bits [64q, 64q + 64) of the 2^(d-1) fine rows (2x_k + b_k).
+// OR them, fold bit pairs, gather the even bits: one 32-bit word, no atomics.
+__global__ void k_downsample_words(const uint32_t* __restrict__ src, int L, int d, u64 dst_words,
+                                   uint32_t* __restrict__ dst) {
+  const u64 wpr = (1ull << L) >> 5, wpr_f = wpr * 2;
+  const u64 mask = (1ull << L) - 1;
+  for (u64 w = blockIdx.x * (u64)blockDim.x + threadIdx.x; w < dst_words; w += (u64)gridDim.x * blockDim.x) {
+    const u64 r = w / wpr, q = w % wpr;
+    u64 acc = 0;
+    const int nchild = 1 << (d - 1);
+    for (int b = 0; b < nchild; ++b) {
+      u64 R = 0;
+      for (int k = d - 1; k >= 1; --k) {
+        const u64 xk = (r >> (L * (k - 1))) & mask;
+        R = (R << (L + 1)) | (2 * xk + ((b >> (k - 1)) & 1));
+      }
+      const u64 fw = R * wpr_f + 2 * q;
+      acc |= (u64)__ldg(src + fw) | ((u64)__ldg(src + fw + 1) << 32);
+    }
+    u64 x = (acc | (acc >> 1)) & 0x5555555555555555ull;
+    x = (x | (x >> 1)) & 0x3333333333333333ull;
+    x = (x | (x >> 2)) & 0x0f0f0f0f0f0f0f0full;
+    x = (x | (x >> 4)) & 0x00ff00ff00ff00ffull;
+    x = (x | (x >> 8)) & 0x0000ffff0000ffffull;
+    x = (x | (x >> 16)) & 0x00000000ffffffffull;
+    dst[w] |= (uint32_t)x;
   }
 }
 
@@ -1176,17 +1286,16 @@ __global__ void __launch_bounds__(256) k_allpairs_lists(const T* __restrict__ ro
         const unsigned e = base + lane;
         bool d_l = false;
         if (e < s1) {
+          // independent gathers: sum, id and row are all in flight at once
           const uint32_t q = __ldg(lst + e);
           const u64 qs = __ldg(fsum + q);
-          if (qs <= ps) {
-            const uint32_t qi = __ldg(ids + q);
-            T w[D];
-            load_row_cached<T, D>(rows, q, w);
-            d_l = precedes(qs, qi, ps, pid) && dominates<T, D>(w, v);
-            // merge_cross_cell = false (refine.cpp:98): phase-1 semantics
-            // only, a dominator must share p's layer-rho cell
-            if (cell_level && d_l) d_l = same_cell<T, D>(w, v, cell_level, ctop);
-          }
+          const uint32_t qi = __ldg(ids + q);
+          T w[D];
+          load_row_cached<T, D>(rows, q, w);
+          d_l = precedes(qs, qi, ps, pid) && dominates<T, D>(w, v);
+          // merge_cross_cell = false (refine.cpp:98): phase-1 semantics
+          // only, a dominator must share p's layer-rho cell
+          if (cell_level && d_l) d_l = same_cell<T, D>(w, v, cell_level, ctop);
         }
         if (__any_sync(kFull, d_l)) {
           dom = true;

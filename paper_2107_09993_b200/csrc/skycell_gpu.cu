@@ -229,9 +229,9 @@ void launch_tables(skycell_gpu_ctx* ctx, cudaStream_t s, const uint32_t* bits, i
 template <typename TT>
 void launch_count(skycell_gpu_ctx* ctx, cudaStream_t s, const uint32_t* bits, int L, int d, const TT* table, u64* cand,
                   u64* key) {
-  const u64 words = std::max<u64>(1, (1ull << (u64)(L * d)) / 32);
-  const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((words + 255) / 256, (u64)ctx->num_sms * 16));
-  sk::k_count_cells<TT><<<g, 256, 0, s>>>(bits, L, d, words, table, cand, key);
+  const u64 rows = 1ull << (u64)(L * (d - 1));
+  const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((rows + 255) / 256, (u64)ctx->num_sms * 16));
+  sk::k_count_rows<TT><<<g, 256, 0, s>>>(bits, L, d, rows, table, cand, key);
   ++ctx->launches;
 }
 
@@ -444,7 +444,7 @@ struct Pipe final : PipeBase {
     table_entries = 1ull << (u64)(rho * (D - 1));
 
     // K1 geometry: persistent warps over round-robin warp tiles
-    smem1 = (size_t)lo_words * 4 + ((h_entries + 15) & ~15u) + (size_t)kStreamThreads * PPT1 + 16;
+    smem1 = (((size_t)lo_words * 4 + 15) & ~(size_t)15) + ((h_entries + 15) & ~15u) + (size_t)kStreamThreads * PPT1 + sk::kOccCache * 8 + 16;
     kstream = pick_stream(rho);
     ck(cudaFuncSetAttribute(kstream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1), "smem attr");
     int occ_blocks = 0;
@@ -605,8 +605,9 @@ struct Pipe final : PipeBase {
     ++ctx->launches;
     if (q.timed) ck(cudaEventRecord(ctx->ev[5], s), "event");
     if (lo_words) {
-      const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((lo_words + 255) / 256, (u64)nsm * 8));
-      sk::k_reduce_slabs<<<g, 256, 0, s>>>(static_cast<uint32_t*>(ctx->slabs.p), grid1, lo_words, occ(la - 1));
+      const unsigned gx = (unsigned)std::max<u64>(1, std::min<u64>((lo_words + 255) / 256, (u64)nsm * 8));
+      const unsigned gy = (unsigned)std::max<u64>(1, std::min<u64>(32, (u64)nsm * 4 / gx));
+      sk::k_reduce_slabs<<<dim3(gx, gy), 256, 0, s>>>(static_cast<uint32_t*>(ctx->slabs.p), grid1, lo_words, occ(la - 1));
       ++ctx->launches;
     }
     if (q.timed) ck(cudaEventRecord(ctx->ev[1], s), "event");
@@ -642,7 +643,13 @@ struct Pipe final : PipeBase {
     for (int L = rho - 1; L >= 1; --L) {
       const u64 src_words = words_at(L + 1);
       const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((src_words + 255) / 256, (u64)nsm * 8));
-      sk::k_downsample<<<g, 256, 0, s2>>>(occ(L + 1), L, D, src_words, occ(L));
+      if (L >= 5) {
+        const u64 dst_words = words_at(L);
+        const unsigned gw = (unsigned)std::max<u64>(1, std::min<u64>((dst_words + 255) / 256, (u64)nsm * 8));
+        sk::k_downsample_words<<<gw, 256, 0, s2>>>(occ(L + 1), L, D, dst_words, occ(L));
+      } else {
+        sk::k_downsample<<<g, 256, 0, s2>>>(occ(L + 1), L, D, src_words, occ(L));
+      }
       ++ctx->launches;
       if (L > 7) {
         launch_tables<uint32_t>(ctx, s2, occ(L), L, D, static_cast<uint32_t*>(ctx->table2.p));

@@ -1,0 +1,7 @@
+TAG=r1i
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu_${TAG}.log 2>&1; echo "pytest rc=$?"; tail -4 gpurun_out/pytest_gpu_${TAG}.log
+for c in c2 c1 c4c c4i c5d2 c5d3 c5d4; do timeout 300 python bench.py --config $c --steps 5 --no-cpu > gpurun_out/bench_${c}_${TAG}.json 2>&1; echo "$c rc=$?"; done
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2_${TAG}.csv python bench.py --config c2 --steps 1 --warmup 3 --no-cpu > /dev/null 2>&1; echo "launch c2 rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_stream -s 3 -c 1 -o gpurun_out/prof_k1_${TAG} python bench.py --steps 1 --warmup 3 --no-cpu > /dev/null 2>&1; echo "ncu k1 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_tree_query -s 1 -c 1 -o gpurun_out/prof_tree_${TAG} python bench.py --config c5d4 --steps 1 --warmup 1 --no-cpu > /dev/null 2>&1; echo "ncu tree rc=$?"
