@@ -274,20 +274,6 @@ __device__ __forceinline__ void set_bit_cached(uint32_t* bits, u64 idx) {
   asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(v) : "l"(w));
   if (!(v & m)) asm volatile("red.global.or.b32 [%0], %1;" ::"l"(w), "r"(m) : "memory");
 }
-// Per-CTA direct-mapped shared-memory cache of recently set occupancy words
-// (entry = word index << 32 | bits this CTA has set in it).  A hit skips the
-// global red.or entirely -- correlated data sends ~1e-3 n points to the
-// origin word -- and a miss costs one shared load/store, no global round trip.
-constexpr int kOccCache = 512;
-__device__ __forceinline__ void set_bit_smcache(uint32_t* bits, u64 idx, u64* cache) {
-  const uint32_t w = (uint32_t)(idx >> 5), m = 1u << (idx & 31);
-  const uint32_t h = (w ^ (w >> 9) ^ (w >> 18)) & (kOccCache - 1);
-  const u64 e = cache[h];
-  const bool same = (uint32_t)(e >> 32) == w;
-  if (same && ((uint32_t)e & m)) return;
-  asm volatile("red.global.or.b32 [%0], %1;" ::"l"(bits + w), "r"(m) : "memory");
-  cache[h] = ((u64)w << 32) | ((same ? (uint32_t)e : 0u) | m);
-}
 // Fire-and-forget (red.global.or): no result to wait for.
 __device__ __forceinline__ void red_or_global(uint32_t* bits, u64 idx) {
   asm volatile("red.global.or.b32 [%0], %1;" ::"l"(bits + (idx >> 5)), "r"(1u << (idx & 31)) : "memory");

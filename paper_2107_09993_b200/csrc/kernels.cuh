@@ -27,6 +27,8 @@
 //   K6  ids leave K5 ascending (stable compaction everywhere).
 #pragma once
 
+#include <cub/block/block_radix_sort.cuh>
+
 #include "common.cuh"
 
 namespace sk {
@@ -347,8 +349,6 @@ __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
   uint32_t* occ_s = reinterpret_cast<uint32_t*>(sm);
   uint8_t* H_s = sm + ((p.lo_words * 4 + 15) & ~15u);
   uint8_t* code_w = H_s + ((p.h_entries + 15) & ~15u) + (threadIdx.x >> 5) * (32 * PPT);  // survivor codes
-  u64* occ_cache = reinterpret_cast<u64*>(H_s + ((p.h_entries + 15) & ~15u) + THREADS * PPT);  // kOccCache entries
-  for (int e = threadIdx.x; e < kOccCache; e += THREADS) occ_cache[e] = ~0ull;
   for (uint32_t w = threadIdx.x; w < p.lo_words; w += THREADS) occ_s[w] = 0;
   for (uint32_t e = threadIdx.x; e < p.h_entries; e += THREADS) H_s[e] = p.H[e];
   __syncthreads();
@@ -499,13 +499,13 @@ __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
               u[k] = __saturatef(x[k]);  // the stored proxy (dataset.cpp:45 clamp, 1.0f = 1 - 2^-32)
               l = l * mul_r + mag_col(fminf(u[k], 0x1.fffffep-1f), fs_r);
             }
-            if (lin32) set_bit_smcache(p.occ_rho, (u64)(l - rcorr), occ_cache);
+            if (lin32) set_bit_cached(p.occ_rho, (u64)(l - rcorr));
             else {
               u64 lin = 0;
 #pragma unroll
               for (int k = D - 1; k >= 0; --k)
                 lin = (lin << rho) | (u64)(mag_col(fminf(u[k], 0x1.fffffep-1f), fs_r) - 0x4B000000u);
-              set_bit_smcache(p.occ_rho, lin, occ_cache);
+              set_bit_cached(p.occ_rho, lin);
             }
           } else {
             u64 lin = 0;
@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
               u[k] = Coord<TIn, TOut, IDENT>::value(x[k], p.nm, k);
               lin = (lin << rho) | (u64)col_at<TIn, TOut, IDENT>(x[k], p.nm, k, fs_r, ds_r, top);
             }
-            set_bit_smcache(p.occ_rho, lin, occ_cache);
+            set_bit_cached(p.occ_rho, lin);
           }
           const u64 slot = out_slot(sidx);
           store_row<TOut, D>(out_rows, slot, u);
@@ -1017,21 +1017,15 @@ __global__ void k_compact_members(const T* __restrict__ rows, const uint32_t* __
 
 // Single CTA: order a point set by descending "strength" -- the volume it
 // dominates in the unit cube, prod(1 - u_k) -- in 64 log-spaced buckets, and
-// keep the first f_max.  Strong filter points first make the early exit in
-// k_candidates happen after ~1 test for most points (median 1, p90 18 at the
-// headline config).  Then, per dimension, a stable column
-// order of the kept points (bitonic sort of (column, strength rank) keys), so
-// each column prefix is scanned strongest first.
+// keep the first f_max.  Strong filter points first make K4's early exit
+// happen after ~1 test for most points.
 template <typename T, int D>
 __global__ void __launch_bounds__(1024) k_strength_order(const T* __restrict__ rows, const u64* __restrict__ fsum,
                                                           const u64* __restrict__ count, uint32_t f_max,
                                                           T* __restrict__ out_rows, u64* __restrict__ out_fsum,
-                                                          u64* __restrict__ out_count, uint16_t* __restrict__ f_lists,
-                                                          uint16_t* __restrict__ f_offs) {
+                                                          u64* __restrict__ out_count) {
   __shared__ unsigned hist[65];
   __shared__ unsigned offs[65];
-  __shared__ uint32_t keys[1024];
-  __shared__ unsigned cnt[kListCols + 1];
   const u64 n = *count;
   if (threadIdx.x < 65) hist[threadIdx.x] = 0;
   __syncthreads();
@@ -1061,41 +1055,35 @@ __global__ void __launch_bounds__(1024) k_strength_order(const T* __restrict__ r
       out_fsum[o] = fsum[i];
     }
   }
+}
+
+// One CTA per dimension k: the filter points' stable column order in
+// dimension k (key = column << 10 | strength rank, one block radix sort), so
+// each column prefix is scanned strongest first, plus the column starts.
+template <typename T, int D>
+__global__ void __launch_bounds__(1024) k_filter_lists(const T* __restrict__ f_rows, const u64* __restrict__ f_count,
+                                                        uint32_t f_max, uint16_t* __restrict__ f_lists,
+                                                        uint16_t* __restrict__ f_offs) {
+  using Sort = cub::BlockRadixSort<uint32_t, 1024, 1>;
+  __shared__ typename Sort::TempStorage tmp;
+  __shared__ unsigned cnt[kListCols + 1];
+  const int k = blockIdx.x;
+  const unsigned nf = (unsigned)(*f_count < f_max ? *f_count : f_max);  // f_max <= 1024
+  const unsigned t = threadIdx.x;
+  for (unsigned c = t; c <= kListCols; c += blockDim.x) cnt[c] = 0;
   __syncthreads();
-  const unsigned nf = (unsigned)(n < f_max ? n : f_max);
-  for (int k = 0; k < D; ++k) {
-    // keys = column << 10 | strength rank, padded with 0xffffffff; f_max <= 1024
-    const unsigned t = threadIdx.x;
-    keys[t] = t < nf ? ((uint32_t)list_col(out_rows[(u64)t * D + k]) << 10) | t : 0xffffffffu;
-    for (unsigned c = t; c <= kListCols; c += blockDim.x) cnt[c] = 0;
-    __syncthreads();
-    for (unsigned size = 2; size <= 1024; size <<= 1) {
-      for (unsigned stride = size >> 1; stride > 0; stride >>= 1) {
-        const unsigned partner = t ^ stride;
-        if (partner > t) {
-          const bool up = (t & size) == 0;
-          const uint32_t a = keys[t], b = keys[partner];
-          if ((a > b) == up) {
-            keys[t] = b;
-            keys[partner] = a;
-          }
-        }
-        __syncthreads();
-      }
+  uint32_t key[1];
+  key[0] = t < nf ? ((uint32_t)list_col(f_rows[(u64)t * D + k]) << 10) | t : 0xffffffffu;
+  if (t < nf) atomicAdd(&cnt[(key[0] >> 10) + 1], 1u);
+  Sort(tmp).Sort(key, 0, 20);
+  if (t < nf) f_lists[(u64)k * f_max + t] = (uint16_t)(key[0] & 1023);  // blocked arrangement: thread t holds rank t
+  __syncthreads();
+  if (t == 0) {
+    unsigned run = 0;
+    for (int c = 0; c <= kListCols; ++c) {
+      run += cnt[c];
+      f_offs[k * (kListCols + 1) + c] = (uint16_t)run;  // points with column < c
     }
-    if (t < nf) {
-      f_lists[(u64)k * f_max + t] = (uint16_t)(keys[t] & 1023);
-      atomicAdd(&cnt[(keys[t] >> 10) + 1], 1u);
-    }
-    __syncthreads();
-    if (t == 0) {
-      unsigned run = 0;
-      for (int c = 0; c <= kListCols; ++c) {
-        run += cnt[c];
-        f_offs[k * (kListCols + 1) + c] = (uint16_t)run;  // points with column < c
-      }
-    }
-    __syncthreads();
   }
 }
 
@@ -1142,68 +1130,92 @@ __global__ void k_list_hist(const T* __restrict__ rows, const uint32_t* __restri
   }
 }
 
-// One CTA per (dimension, array): inclusive scan of a shifted histogram =
-// starts.  The array is processed in smem tiles of 1024 x kScanPer entries:
-// coalesced load, a serial sum over each thread's kScanPer consecutive
-// entries, one block scan of the 1024 run totals, coalesced write-back.
-// blockIdx.x < D: bin arrays (also copied to the scatter cursor);
-// blockIdx.x >= D: column arrays.
+// Inclusive scan of the shifted histograms = starts, in two multi-CTA
+// passes: blockIdx.y < D are the bin arrays (also copied to the scatter
+// cursor), blockIdx.y >= D the column arrays; blockIdx.x is a chunk of
+// kScanChunk entries.  Pass 1 writes each chunk's total; pass 2 adds the
+// totals of the preceding chunks (at most a handful) to its block scan.
 constexpr int kScanPer = 8;
-__global__ void __launch_bounds__(1024) k_list_scan(unsigned* __restrict__ hist, unsigned* __restrict__ cursor, int D) {
-  __shared__ unsigned tile[1024 * kScanPer + 1024 * kScanPer / 32];  // one pad word per 32 entries
+constexpr int kScanChunk = 1024 * kScanPer;
+constexpr int kScanChunks = (kListBins + 1 + kScanChunk - 1) / kScanChunk;
+
+__device__ __forceinline__ unsigned* scan_array(unsigned* hist, int y, int D, int* len) {
+  const bool bins = y < D;
+  *len = bins ? kListBins + 1 : kListCols + 1;
+  return hist + (u64)(bins ? y : y - D) * kListStride + (bins ? 0 : kColBase);
+}
+
+__global__ void __launch_bounds__(1024) k_list_scan_sums(unsigned* __restrict__ hist, int D,
+                                                          unsigned* __restrict__ totals) {
   __shared__ unsigned warp_tot[32];
-  __shared__ unsigned carry_s;
-  const bool bins = (int)blockIdx.x < D;
-  const int k = bins ? blockIdx.x : blockIdx.x - D;
-  unsigned* h = hist + (u64)k * kListStride + (bins ? 0 : kColBase);
-  unsigned* cur = bins ? cursor + (u64)k * kListStride : nullptr;
-  const int len = bins ? kListBins + 1 : kListCols + 1;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int T = 1024 * kScanPer;
-  auto pad = [](int i) { return i + (i >> 5); };  // one pad word per 32: conflict-free strided runs
-  if (threadIdx.x == 0) carry_s = 0;
-  for (int t0 = 0; t0 < len; t0 += T) {
-    for (int i = threadIdx.x; i < T; i += 1024) tile[pad(i)] = (t0 + i < len) ? h[t0 + i] : 0u;
-    __syncthreads();
-    const int r0 = threadIdx.x * kScanPer;
-    unsigned run = 0;
+  int len;
+  const unsigned* h = scan_array(hist, blockIdx.y, D, &len);
+  const int c0 = blockIdx.x * kScanChunk;
+  unsigned v = 0;
+  for (int i = c0 + threadIdx.x; i < min(c0 + kScanChunk, len); i += 1024) v += h[i];
 #pragma unroll
-    for (int e = 0; e < kScanPer; ++e) run += tile[pad(r0 + e)];
-    unsigned incl = run;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  if ((threadIdx.x & 31) == 0) warp_tot[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    unsigned t = warp_tot[threadIdx.x];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(kFull, t, o);
+    if (threadIdx.x == 0) totals[blockIdx.y * kScanChunks + blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_list_scan(unsigned* __restrict__ hist, unsigned* __restrict__ cursor, int D,
+                                                     const unsigned* __restrict__ totals) {
+  __shared__ unsigned tile[kScanChunk + kScanChunk / 32];  // one pad word per 32 entries
+  __shared__ unsigned warp_tot[32];
+  int len;
+  unsigned* h = scan_array(hist, blockIdx.y, D, &len);
+  unsigned* cur = (int)blockIdx.y < D ? cursor + (u64)blockIdx.y * kListStride : nullptr;
+  const int c0 = blockIdx.x * kScanChunk;
+  if (c0 >= len) return;
+  unsigned carry = 0;
+  for (int b = 0; b < (int)blockIdx.x; ++b) carry += totals[blockIdx.y * kScanChunks + b];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  auto pad = [](int i) { return i + (i >> 5); };  // conflict-free strided runs
+  for (int i = threadIdx.x; i < kScanChunk; i += 1024) tile[pad(i)] = (c0 + i < len) ? h[c0 + i] : 0u;
+  __syncthreads();
+  const int r0 = threadIdx.x * kScanPer;
+  unsigned run = 0;
+#pragma unroll
+  for (int e = 0; e < kScanPer; ++e) run += tile[pad(r0 + e)];
+  unsigned incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const unsigned t = warp_tot[lane];
+    unsigned ti = t;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const unsigned y = __shfl_up_sync(kFull, incl, o);
-      if (lane >= o) incl += y;
+      const unsigned y = __shfl_up_sync(kFull, ti, o);
+      if (lane >= o) ti += y;
     }
-    if (lane == 31) warp_tot[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      const unsigned t = warp_tot[lane];
-      unsigned ti = t;
+    warp_tot[lane] = ti - t;
+  }
+  __syncthreads();
+  unsigned acc = carry + warp_tot[warp] + incl - run;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned y = __shfl_up_sync(kFull, ti, o);
-        if (lane >= o) ti += y;
-      }
-      warp_tot[lane] = ti - t;
+  for (int e = 0; e < kScanPer; ++e) {
+    acc += tile[pad(r0 + e)];
+    tile[pad(r0 + e)] = acc;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kScanChunk; i += 1024) {
+    if (c0 + i < len) {
+      const unsigned v = tile[pad(i)];
+      h[c0 + i] = v;
+      if (cur) cur[c0 + i] = v;
     }
-    __syncthreads();
-    unsigned acc = carry_s + warp_tot[warp] + incl - run;
-#pragma unroll
-    for (int e = 0; e < kScanPer; ++e) {
-      acc += tile[pad(r0 + e)];
-      tile[pad(r0 + e)] = acc;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < T; i += 1024) {
-      if (t0 + i < len) {
-        const unsigned v = tile[pad(i)];
-        h[t0 + i] = v;
-        if (cur) cur[t0 + i] = v;
-      }
-    }
-    if (threadIdx.x == 1023) carry_s = acc;
-    __syncthreads();
   }
 }
 
@@ -1234,76 +1246,158 @@ __device__ __forceinline__ bool same_cell(const T* q, const T* p, int L, int top
   return eq;
 }
 
+// Query setup shared by both K5 list phases: the dimension with the
+// shortest candidate prefix, p's column there and its sum bucket.
+template <typename T, int D>
+struct ListQuery {
+  T v[D];
+  u64 ps;
+  uint32_t pid;
+  int bk, pc, sb;
+  __device__ __forceinline__ void init(const T* __restrict__ rows, const u64* __restrict__ fsum,
+                                       const uint32_t* __restrict__ ids, const unsigned* __restrict__ offs, u64 i) {
+    pid = ids[i];
+    ps = fsum[i];
+    load_row_cached<T, D>(rows, i, v);
+    bk = 0;
+    pc = 0;
+    unsigned best = 0xffffffffu;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const int c = list_col(v[k]);
+      const unsigned e = __ldg(offs + k * kListStride + kColBase + c + 1);  // entries with col <= c
+      if (e < best) {
+        best = e;
+        bk = k;
+        pc = c;
+      }
+    }
+    sb = sum_bucket<D>(ps);
+  }
+  // lane's test of candidate list entry e (< end): q precedes and dominates p
+  __device__ __forceinline__ bool test(const T* __restrict__ rows, const uint32_t* __restrict__ ids,
+                                       const u64* __restrict__ fsum, const uint32_t* __restrict__ lst, unsigned e,
+                                       int cell_level, int ctop) const {
+    // independent gathers: sum, id and row are all in flight at once
+    const uint32_t q = __ldg(lst + e);
+    const u64 qs = __ldg(fsum + q);
+    const uint32_t qi = __ldg(ids + q);
+    T w[D];
+    load_row_cached<T, D>(rows, q, w);
+    bool d = precedes(qs, qi, ps, pid) && dominates<T, D>(w, v);
+    // merge_cross_cell = false (refine.cpp:98): phase-1 semantics only, a
+    // dominator must share p's layer-rho cell
+    if (cell_level && d) d = same_cell<T, D>(w, v, cell_level, ctop);
+    return d;
+  }
+};
+
 // flag[i] = 1 iff no point q of the set precedes i (sort-first order,
 // refine.cpp:38-41) and dominates it, for query slots [q_begin, *q_end).
-// One warp per point: per column of its shortest prefix, the 32 lanes test
-// 32 candidates per step (independent gathers in flight) and stop at the
-// first step with a dominator.  A point with sum 0 lies at the
-// origin and has no dominator (normalised coordinates are >= 0); skipping it
-// keeps correlated data's ~8.7e-4 n exact origin duplicates
-// from scanning each other.
+// Phase A, one warp per point: per column of its shortest prefix, the 32
+// lanes test 32 candidates per step (independent gathers in flight) and stop
+// at the first step with a dominator.  A point still undecided after
+// max_steps steps -- in practice a skyline point with a long prefix, which
+// has no early exit -- is queued for phase B (k_allpairs_long) instead of
+// holding its warp for the whole scan: the static warp schedule otherwise
+// ends with a tail of a few long scans (ncu: 15% of warps active).
+// A point with sum 0 lies at the origin and has no dominator (normalised
+// coordinates are >= 0); skipping it keeps correlated data's ~8.7e-4 n exact
+// origin duplicates from scanning each other.
 template <typename T, int D>
 __global__ void __launch_bounds__(256) k_allpairs_lists(const T* __restrict__ rows, const uint32_t* __restrict__ ids,
                                                         const u64* __restrict__ fsum, const u64* __restrict__ count,
                                                         const uint32_t* __restrict__ lists, const unsigned* __restrict__ offs,
                                                         u64 cap, uint8_t* __restrict__ flag, u64 q_begin,
-                                                        const u64* __restrict__ q_end, int cell_level) {
+                                                        const u64* __restrict__ q_end, int cell_level,
+                                                        unsigned max_steps, uint32_t* __restrict__ long_q,
+                                                        u64* __restrict__ long_n) {
   const u64 n = q_end ? *q_end : *count;
   const int lane = threadIdx.x & 31;
   const u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
   const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
   const int ctop = (1 << cell_level) - 1;
   for (u64 i = q_begin + warp; i < n; i += nwarps) {
-    const uint32_t pid = ids[i];
-    if (pid == kNoId) {
+    if (ids[i] == kNoId) {
       if (lane == 0) flag[i] = 0;
       continue;
     }
-    const u64 ps = fsum[i];
-    if (ps == 0) {  // the origin: nothing dominates it
+    if (fsum[i] == 0) {  // the origin: nothing dominates it
       if (lane == 0) flag[i] = 1;
       continue;
     }
-    T v[D];
-    load_row_cached<T, D>(rows, i, v);
-    int bk = 0, pc = 0;
-    unsigned best = 0xffffffffu;
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      const int c = list_col(v[k]);
-      const unsigned e = __ldg(offs + k * kListStride + kColBase + c + 1);  // entries with col <= c
-      if (e < best) { best = e; bk = k; pc = c; }
-    }
-    const uint32_t* lst = lists + (u64)bk * cap;
-    const unsigned* ob = offs + bk * kListStride;
-    const int sb = sum_bucket<D>(ps);
-    bool dom = false;
+    ListQuery<T, D> Q;
+    Q.init(rows, fsum, ids, offs, i);
+    const uint32_t* lst = lists + (u64)Q.bk * cap;
+    const unsigned* ob = offs + Q.bk * kListStride;
+    bool dom = false, deferred = false;
+    unsigned steps = 0;
     // columns 0..pc of dimension bk in ascending order; column c contributes
     // its sum buckets 0..sb, one contiguous range (column-major bins)
-    for (int c = 0; c <= pc && !dom; ++c) {
-      const unsigned s0 = __ldg(ob + list_bin(0, c)), s1 = __ldg(ob + list_bin(sb + 1, c));
+    for (int c = 0; c <= Q.pc && !dom && !deferred; ++c) {
+      const unsigned s0 = __ldg(ob + list_bin(0, c)), s1 = __ldg(ob + list_bin(Q.sb + 1, c));
       for (unsigned base = s0; base < s1; base += 32) {
-        const unsigned e = base + lane;
-        bool d_l = false;
-        if (e < s1) {
-          // independent gathers: sum, id and row are all in flight at once
-          const uint32_t q = __ldg(lst + e);
-          const u64 qs = __ldg(fsum + q);
-          const uint32_t qi = __ldg(ids + q);
-          T w[D];
-          load_row_cached<T, D>(rows, q, w);
-          d_l = precedes(qs, qi, ps, pid) && dominates<T, D>(w, v);
-          // merge_cross_cell = false (refine.cpp:98): phase-1 semantics
-          // only, a dominator must share p's layer-rho cell
-          if (cell_level && d_l) d_l = same_cell<T, D>(w, v, cell_level, ctop);
+        if (++steps > max_steps) {
+          deferred = true;
+          break;
         }
+        const unsigned e = base + lane;
+        const bool d_l = e < s1 && Q.test(rows, ids, fsum, lst, e, cell_level, ctop);
         if (__any_sync(kFull, d_l)) {
           dom = true;
           break;
         }
       }
     }
-    if (lane == 0) flag[i] = dom ? 0 : 1;
+    if (lane == 0) {
+      if (deferred) long_q[atomicAdd(long_n, 1ull)] = (uint32_t)i;
+      else flag[i] = dom ? 0 : 1;
+    }
+  }
+}
+
+// Phase B: one CTA per deferred point, its candidate steps dealt round-robin
+// to the 8 warps, a shared flag for the early exit.
+template <typename T, int D>
+__global__ void __launch_bounds__(256) k_allpairs_long(const T* __restrict__ rows, const uint32_t* __restrict__ ids,
+                                                       const u64* __restrict__ fsum, const uint32_t* __restrict__ lists,
+                                                       const unsigned* __restrict__ offs, u64 cap,
+                                                       uint8_t* __restrict__ flag, int cell_level,
+                                                       const uint32_t* __restrict__ long_q,
+                                                       const u64* __restrict__ long_n) {
+  __shared__ int found;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int ctop = (1 << cell_level) - 1;
+  const u64 nq = *long_n;
+  for (u64 t = blockIdx.x; t < nq; t += gridDim.x) {
+    const uint32_t i = long_q[t];
+    if (threadIdx.x == 0) found = 0;
+    __syncthreads();
+    ListQuery<T, D> Q;
+    Q.init(rows, fsum, ids, offs, i);
+    const uint32_t* lst = lists + (u64)Q.bk * cap;
+    const unsigned* ob = offs + Q.bk * kListStride;
+    unsigned g = 0;  // global step counter (identical in every warp)
+    for (int c = 0; c <= Q.pc; ++c) {
+      const unsigned s0 = __ldg(ob + list_bin(0, c)), s1 = __ldg(ob + list_bin(Q.sb + 1, c));
+      const unsigned nsteps = (s1 - s0 + 31) / 32;
+      // this warp's steps of the column: g + k with (g + k) % nw == warp
+      unsigned k = (unsigned)((warp - (int)(g % nw) + nw) % nw);
+      for (; k < nsteps; k += nw) {
+        if (*(volatile int*)&found) break;
+        const unsigned e = s0 + k * 32 + lane;
+        const bool d_l = e < s1 && Q.test(rows, ids, fsum, lst, e, cell_level, ctop);
+        if (__any_sync(kFull, d_l)) {
+          if (lane == 0) found = 1;
+          break;
+        }
+      }
+      g += nsteps;
+      if (*(volatile int*)&found) break;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) flag[i] = found ? 0 : 1;
+    __syncthreads();
   }
 }
 

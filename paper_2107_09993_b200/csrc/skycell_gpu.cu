@@ -115,6 +115,8 @@ struct skycell_gpu_ctx {
   DevBuf q_bits, q_orig, q_sub, q_ids, q_mm;  // quadrant_skyline
   DevBuf t_keys, t_keys2, t_vals, t_vals2, t_cub, t_rows, t_ids, t_fsum, t_lo, t_hi, t_cs, t_ci;  // K5 tree
   int k5_mode = -1;  // 0 lists, 1 tree, 2 auto (SKYCELL_K5)
+  DevBuf long_q, long_n;  // K5 phase-B queue
+  DevBuf scan_tot;        // K5 list-scan chunk totals
   DevCounters* host_ctr = nullptr;  // pinned
   u64* host_param = nullptr;        // pinned H2D staging
   cudaEvent_t ev[8] = {};
@@ -250,12 +252,23 @@ void run_exact(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uin
   const TOut* trows = static_cast<const TOut*>(rows);
   uint32_t* lists = static_cast<uint32_t*>(ctx->lists.p);
   sk::k_list_hist<TOut, D><<<g, 256, 0, s>>>(trows, ids, fsum, count, hist);
-  sk::k_list_scan<<<2 * D, 1024, 0, s>>>(hist, cursor, D);
+  unsigned* totals = static_cast<unsigned*>(ctx->scan_tot.p);
+  sk::k_list_scan_sums<<<dim3(sk::kScanChunks, 2 * D), 1024, 0, s>>>(hist, D, totals);
+  sk::k_list_scan<<<dim3(sk::kScanChunks, 2 * D), 1024, 0, s>>>(hist, cursor, D, totals);
+  ++ctx->launches;
   sk::k_list_scatter<TOut, D><<<g, 256, 0, s>>>(trows, ids, fsum, count, cursor, lists, cap);
   const unsigned gw = (unsigned)std::max<u64>(1, std::min<u64>((cap * 32 + 255) / 256, (u64)nsm * 8));
+  ensure(ctx->long_q, cap * 4);
+  u64* long_n = static_cast<u64*>(ctx->long_n.p);
+  ck(cudaMemsetAsync(long_n, 0, 8, s), "memset");
+  constexpr unsigned kMaxSteps = 16;
   sk::k_allpairs_lists<TOut, D><<<gw, 256, 0, s>>>(trows, ids, fsum, count, lists, hist, cap,
-                                                   static_cast<uint8_t*>(ctx->flags.p), q_begin, q_end, cell_level);
-  ctx->launches += 4;
+                                                   static_cast<uint8_t*>(ctx->flags.p), q_begin, q_end, cell_level,
+                                                   kMaxSteps, static_cast<uint32_t*>(ctx->long_q.p), long_n);
+  sk::k_allpairs_long<TOut, D><<<nsm * 4, 256, 0, s>>>(trows, ids, fsum, lists, hist, cap,
+                                                       static_cast<uint8_t*>(ctx->flags.p), cell_level,
+                                                       static_cast<const uint32_t*>(ctx->long_q.p), long_n);
+  ctx->launches += 5;
 }
 
 // Exact sort-first pass through the dominance tree (tree.cuh).  Needs the
@@ -444,7 +457,7 @@ struct Pipe final : PipeBase {
     table_entries = 1ull << (u64)(rho * (D - 1));
 
     // K1 geometry: persistent warps over round-robin warp tiles
-    smem1 = (((size_t)lo_words * 4 + 15) & ~(size_t)15) + ((h_entries + 15) & ~15u) + (size_t)kStreamThreads * PPT1 + sk::kOccCache * 8 + 16;
+    smem1 = (((size_t)lo_words * 4 + 15) & ~(size_t)15) + ((h_entries + 15) & ~15u) + (size_t)kStreamThreads * PPT1 + 16;
     kstream = pick_stream(rho);
     ck(cudaFuncSetAttribute(kstream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1), "smem attr");
     int occ_blocks = 0;
@@ -572,8 +585,11 @@ struct Pipe final : PipeBase {
             static_cast<TOut*>(ctx->smp_rows.p), static_cast<u64*>(ctx->smp_fsum.p), &c->fs);
         sk::k_strength_order<TOut, D><<<1, 1024, 0, s>>>(
             static_cast<const TOut*>(ctx->smp_rows.p), static_cast<const u64*>(ctx->smp_fsum.p), &c->fs,
-            (uint32_t)pf_max, static_cast<TOut*>(ctx->f_rows.p), static_cast<u64*>(ctx->f_fsum.p), &c->nf,
-            static_cast<uint16_t*>(ctx->f_lists.p), static_cast<uint16_t*>(ctx->f_offs.p));
+            (uint32_t)pf_max, static_cast<TOut*>(ctx->f_rows.p), static_cast<u64*>(ctx->f_fsum.p), &c->nf);
+        sk::k_filter_lists<TOut, D><<<D, 1024, 0, s>>>(static_cast<const TOut*>(ctx->f_rows.p), &c->nf,
+                                                        (uint32_t)pf_max, static_cast<uint16_t*>(ctx->f_lists.p),
+                                                        static_cast<uint16_t*>(ctx->f_offs.p));
+        ++ctx->launches;
         ctx->launches += 2;
       }
     }
@@ -1061,6 +1077,8 @@ int skycell_gpu_create(int device, skycell_gpu_ctx** out, char* err, size_t err_
     ck(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming), "event");
     ck(cudaMallocHost(reinterpret_cast<void**>(&ctx->host_ctr), sizeof(DevCounters)), "pinned");
     ck(cudaMallocHost(reinterpret_cast<void**>(&ctx->host_param), 64), "pinned");
+    ensure(ctx->long_n, 64);
+    ensure(ctx->scan_tot, (size_t)2 * sk::kMaxD * sk::kScanChunks * 4);
     for (auto& e : ctx->ev) ck(cudaEventCreate(&e), "event");
     *out = ctx;
   });
@@ -1076,7 +1094,7 @@ void skycell_gpu_destroy(skycell_gpu_ctx* ctx) {
                     &ctx->s2_ids, &ctx->s2_fsum, &ctx->flags, &ctx->sky_rows, &ctx->sky_ids, &ctx->sky_fsum,
                     &ctx->q_bits, &ctx->q_orig, &ctx->q_sub, &ctx->q_ids, &ctx->q_mm, &ctx->t_keys,
                     &ctx->t_keys2, &ctx->t_vals, &ctx->t_vals2, &ctx->t_cub, &ctx->t_rows, &ctx->t_ids,
-                    &ctx->t_fsum, &ctx->t_lo, &ctx->t_hi, &ctx->t_cs, &ctx->t_ci};
+                    &ctx->t_fsum, &ctx->t_lo, &ctx->t_hi, &ctx->t_cs, &ctx->t_ci, &ctx->long_q, &ctx->long_n, &ctx->scan_tot};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (auto& e : ctx->ev)
