@@ -342,8 +342,8 @@ __device__ __forceinline__ uint32_t mag_col(float u, float scale) {
 // per tile); their layer-rho cells are marked with fire-and-forget red.or.
 // RHO > 0 (f32 identity path) fixes rho and la at compile time so every index
 // is a constant-weight IMAD chain; RHO == 0 is the general runtime path.
-template <typename TIn, typename TOut, int D, bool IDENT, int THREADS, int PPT, int RHO>
-__global__ void __launch_bounds__(THREADS, 4) k_stream(StreamParams p) {
+template <typename TIn, typename TOut, int D, bool IDENT, int THREADS, int PPT, int RHO, int MINB = 4>
+__global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
   static_assert(PPT <= 8, "survivor codes are (j * 32 + lane) in one byte");
   extern __shared__ __align__(16) uint8_t sm[];
   uint32_t* occ_s = reinterpret_cast<uint32_t*>(sm);

@@ -311,18 +311,19 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
   sk::TreeShape sh{};
   sh.m = m;
   sh.nleaf = (m + sk::kLeaf - 1) / sk::kLeaf;
+  if (sh.nleaf >= (1ull << 27)) throw ApiFail{SKYCELL_UNSUPPORTED, "skycell_gpu: dominance tree too large"};
+  constexpr u64 F = sk::tree_fanout<D>();
   u64 off = 0, cnt = sh.nleaf;
   int L = 0;
   while (true) {
-    sh.off[L] = off;
-    sh.cnt[L] = cnt;
+    sh.off[L] = (uint32_t)off;
+    sh.cnt[L] = (uint32_t)cnt;
     off += cnt;
     ++L;
     if (cnt == 1) break;
-    cnt = (cnt + 1) / 2;
+    cnt = (cnt + F - 1) / F;
   }
   sh.levels = L;
-  if (sh.nleaf >= (1ull << 27) || L > 31) throw ApiFail{SKYCELL_UNSUPPORTED, "skycell_gpu: dominance tree too large"};
   const u64 nodes = off;
   ensure(ctx->t_rows, m * D * sizeof(TOut));
   ensure(ctx->t_ids, m * 4);
@@ -430,6 +431,15 @@ struct Pipe final : PipeBase {
   int cell_level() const { return q.merge ? 0 : rho; }
 
   static auto pick_stream(int rho) {
+    if constexpr (IDENT && D == 4) {
+      // tuning experiment (SKYCELL_K1=ab): occupancy / tile-size variants at the headline shape
+      const char* e = std::getenv("SKYCELL_K1");
+      if (e && rho == 6) {
+        if (!std::strcmp(e, "m3")) return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 6, 3>;
+        if (!std::strcmp(e, "p2")) return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, 2, 6, 4>;
+        if (!std::strcmp(e, "p2m3")) return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, 2, 6, 3>;
+      }
+    }
     if constexpr (IDENT && D <= 8) {
       switch (rho) {
         case 1: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 1>;

@@ -144,31 +144,40 @@ __global__ void k_tree_leaves(const T* __restrict__ srows, const uint32_t* __res
   }
 }
 
-// Level h from level h-1: node j merges children 2j and 2j+1 (the second
-// may be missing at the right edge).
+// Fan-out of the internal nodes: one lane per (child, dimension) pair, so a
+// node visit tests all of its children's boxes with one load per lane.
+template <int D>
+__host__ __device__ constexpr int tree_fanout() {
+  return (32 / D) < 2 ? 2 : (32 / D) > 16 ? 16 : (32 / D);
+}
+
+// Level h from level h-1: node j merges children F j .. F j + F - 1 (fewer at
+// the right edge).
 template <typename T, int D>
 __global__ void k_tree_level(TreeView<T, D> tv, u64 child_off, u64 nchild, u64 node_off, u64 nnode) {
+  constexpr int F = tree_fanout<D>();
   for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < nnode; j += (u64)gridDim.x * blockDim.x) {
-    const u64 a = child_off + 2 * j, b = child_off + 2 * j + 1;
-    const bool hb = 2 * j + 1 < nchild;
+    const u64 a0 = child_off + F * j;
+    const int nc = (int)min((u64)F, nchild - F * j);
     const u64 o = node_off + j;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-      T l = tv.lo[a * D + k], h = tv.hi[a * D + k];
-      if (hb) {
-        const T l2 = tv.lo[b * D + k], h2 = tv.hi[b * D + k];
+      T l = tv.lo[a0 * D + k], h = tv.hi[a0 * D + k];
+      for (int c = 1; c < nc; ++c) {
+        const T l2 = tv.lo[(a0 + c) * D + k], h2 = tv.hi[(a0 + c) * D + k];
         l = l2 < l ? l2 : l;
         h = h2 > h ? h2 : h;
       }
       tv.lo[o * D + k] = l;
       tv.hi[o * D + k] = h;
     }
-    u64 s = tv.cs[a];
-    uint32_t id = tv.ci[a];
-    if (hb && key_less(tv.cs[b], tv.ci[b], s, id)) {
-      s = tv.cs[b];
-      id = tv.ci[b];
-    }
+    u64 s = tv.cs[a0];
+    uint32_t id = tv.ci[a0];
+    for (int c = 1; c < nc; ++c)
+      if (key_less(tv.cs[a0 + c], tv.ci[a0 + c], s, id)) {
+        s = tv.cs[a0 + c];
+        id = tv.ci[a0 + c];
+      }
     tv.cs[o] = s;
     tv.ci[o] = id;
   }
@@ -176,29 +185,34 @@ __global__ void k_tree_level(TreeView<T, D> tv, u64 child_off, u64 nchild, u64 n
 
 struct TreeShape {
   u64 m, nleaf;
-  int levels;            // level 0 .. levels-1; the root is the single node of the last level
-  u64 off[48], cnt[48];  // node offset / count per level
+  int levels;                 // level 0 .. levels-1; the root is the single node of the last level
+  uint32_t off[32], cnt[32];  // node offset / count per level (nodes < 2^31)
 };
 
 // flag[slot] = 1 iff the point at sorted position j (slot = order[j]) is not
 // dominated by a preceding point of the set; only positions whose slot lies
 // in [q_begin, q_end) are decided.  cell_level > 0: merge_cross_cell = false
 // (dominators must share p's layer-rho cell; no champion short-cut).
+// Internal node visit: lane l tests dimension l % D of child l / D; lanes
+// c < F then hold child c's verdict.  Wanted children are pushed with the
+// one lying below p in the most dimensions on top (visited next).
 template <typename T, int D>
 __global__ void __launch_bounds__(256) k_tree_query(const T* __restrict__ srows, const uint32_t* __restrict__ sids,
                                                     const u64* __restrict__ sfsum, const uint32_t* __restrict__ order,
                                                     TreeView<T, D> tv, TreeShape sh, u64 q_begin,
                                                     const u64* __restrict__ q_end, int cell_level,
                                                     uint8_t* __restrict__ flag) {
-  constexpr int kStack = 64;
+  constexpr int F = tree_fanout<D>();
+  constexpr int kStack = 128;
   // stack entries: level << 27 | index within the level (nleaf < 2^27)
   __shared__ uint32_t stack_s[8][kStack];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint32_t* stk = stack_s[wib];
   const u64 qend = q_end ? *q_end : ~0ull;
   const int ctop = (1 << cell_level) - 1;
-  const int ch = lane / D, kd = lane % D;  // lanes [0, D): child 0 dims; [D, 2D): child 1 dims
+  const int ch = lane / D, kd = lane % D;  // (child, dimension) of this lane's box test
   const unsigned m0 = (1u << D) - 1;
+  const unsigned lt = (1u << lane) - 1;
   for (u64 j = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; j < sh.m; j += ((u64)gridDim.x * blockDim.x) >> 5) {
     const uint32_t slot = order[j];
     if (slot < q_begin || slot >= qend) continue;
@@ -218,64 +232,69 @@ __global__ void __launch_bounds__(256) k_tree_query(const T* __restrict__ srows,
     if (lane == 0) stk[0] = (uint32_t)(sh.levels - 1) << 27;
     int top = 1;
     __syncwarp();
-    while (top > 0 && !dom) {
+    while (top > 0) {
       const uint32_t e = stk[--top];
       __syncwarp();
       const int lvl = (int)(e >> 27);
-      const u64 idx = e & ((1u << 27) - 1);
+      const uint32_t idx = e & ((1u << 27) - 1);
       if (lvl == 0) {
-        const u64 q = idx * kLeaf + lane;
+        const u64 q = (u64)idx * kLeaf + lane;
         bool d_l = false;
         if (q < sh.m) {
           const u64 qs = __ldg(sfsum + q);
-          if (qs <= ps) {
-            T w[D];
-            load_row_cached<T, D>(srows, q, w);
-            d_l = precedes(qs, __ldg(sids + q), ps, pid) && dominates<T, D>(w, v);
-            if (cell_level && d_l) d_l = same_cell<T, D>(w, v, cell_level, ctop);
-          }
+          const uint32_t qi = __ldg(sids + q);
+          T w[D];
+          load_row_cached<T, D>(srows, q, w);
+          d_l = precedes(qs, qi, ps, pid) && dominates<T, D>(w, v);
+          if (cell_level && d_l) d_l = same_cell<T, D>(w, v, cell_level, ctop);
         }
-        dom = __any_sync(kFull, d_l);
+        if (__any_sync(kFull, d_l)) {
+          dom = true;
+          break;
+        }
         continue;
       }
-      // internal node: children 2 idx, 2 idx + 1 of level lvl - 1
-      const u64 ci0 = 2 * idx;
-      const bool has1 = ci0 + 1 < sh.cnt[lvl - 1];
-      const u64 c0 = sh.off[lvl - 1] + ci0;
-      bool lo_ok = true, hi_lt = true;
-      if (ch < 2 && (ch == 0 || has1)) {
-        const u64 c = c0 + ch;
-        lo_ok = __ldg(tv.lo + c * D + kd) <= pk;
-        hi_lt = __ldg(tv.hi + c * D + kd) < pk;
+      // internal node: children F idx .. F idx + F - 1 of level lvl - 1
+      const uint32_t cidx0 = F * idx;
+      const int nc = (int)min((uint32_t)F, sh.cnt[lvl - 1] - cidx0);
+      const uint32_t c0 = sh.off[lvl - 1] + cidx0;
+      bool lo_ok = true, hi_lt = false;
+      if (ch < nc) {
+        const uint32_t c = c0 + ch;
+        lo_ok = __ldg(tv.lo + (u64)c * D + kd) <= pk;
+        hi_lt = __ldg(tv.hi + (u64)c * D + kd) < pk;
       }
-      const unsigned lo_bad = __ballot_sync(kFull, !lo_ok), hi_in = __ballot_sync(kFull, hi_lt && ch < 2);
-      const u64 s0 = __ldg(tv.cs + c0), s1 = has1 ? __ldg(tv.cs + c0 + 1) : ~0ull;
-      const uint32_t i0 = __ldg(tv.ci + c0), i1 = has1 ? __ldg(tv.ci + c0 + 1) : kNoId;
-      const unsigned in0 = hi_in & m0, in1 = (hi_in >> D) & m0;
-      const bool want0 = !(lo_bad & m0) && s0 <= ps;
-      const bool want1 = has1 && !((lo_bad >> D) & m0) && s1 <= ps;
-      // a child strictly below p in every dimension: its champion decides
-      if (!cell_level && ((want0 && in0 == m0 && precedes(s0, i0, ps, pid)) ||
-                          (want1 && in1 == m0 && precedes(s1, i1, ps, pid)))) {
+      const unsigned lo_bad = __ballot_sync(kFull, !lo_ok), hi_in = __ballot_sync(kFull, hi_lt);
+      // lanes c < nc: verdict for child c
+      bool want = false, kill = false;
+      int score = -1;
+      if (lane < nc) {
+        const u64 cs = __ldg(tv.cs + c0 + lane);
+        const uint32_t ci = __ldg(tv.ci + c0 + lane);
+        const unsigned in_c = (hi_in >> (lane * D)) & m0;
+        want = !((lo_bad >> (lane * D)) & m0) && cs <= ps;
+        kill = want && !cell_level && in_c == m0 && precedes(cs, ci, ps, pid);
+        score = want ? __popc(in_c) : -1;
+      }
+      if (__any_sync(kFull, kill)) {
+        // a child strictly below p in every dimension whose champion
+        // precedes p: every point of it dominates p
         dom = true;
         break;
       }
-      // visit first the child lying below p in more dimensions (more likely
-      // to hold a dominator), ties: the stronger champion
-      const int n0 = __popc(in0), n1 = __popc(in1);
-      const bool first1 = want0 && want1 && (n1 > n0 || (n1 == n0 && key_less(s1, i1, s0, i0)));
-      const uint32_t e0 = ((uint32_t)(lvl - 1) << 27) | (uint32_t)ci0, e1 = e0 + 1;
-      if (lane == 0) {
-        int t = top;
-        if (first1) {
-          stk[t++] = e0;
-          stk[t++] = e1;
-        } else {
-          if (want1) stk[t++] = e1;
-          if (want0) stk[t++] = e0;
-        }
+      const unsigned wm = __ballot_sync(kFull, want);
+      if (!wm) continue;
+      // best child: highest score, ties to the lowest lane
+      int best = (score << 5) | (31 - lane);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(kFull, best, o));
+      const int bl = 31 - (best & 31);
+      const unsigned rest = wm & ~(1u << bl);
+      if (want) {
+        const uint32_t ent = ((uint32_t)(lvl - 1) << 27) | (cidx0 + lane);
+        stk[top + (lane == bl ? __popc(rest) : __popc(rest & lt))] = ent;
       }
-      top += (int)want0 + (int)want1;
+      top += __popc(wm);
       __syncwarp();
     }
     if (lane == 0) flag[slot] = dom ? 0 : 1;
