@@ -342,7 +342,7 @@ __device__ __forceinline__ uint32_t mag_col(float u, float scale) {
 // per tile); their layer-rho cells are marked with fire-and-forget red.or.
 // RHO > 0 (f32 identity path) fixes rho and la at compile time so every index
 // is a constant-weight IMAD chain; RHO == 0 is the general runtime path.
-template <typename TIn, typename TOut, int D, bool IDENT, int THREADS, int PPT, int RHO, int MINB = 4>
+template <typename TIn, typename TOut, int D, bool IDENT, int THREADS, int PPT, int RHO, int MINB = 3>
 __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
   static_assert(PPT <= 8, "survivor codes are (j * 32 + lane) in one byte");
   extern __shared__ __align__(16) uint8_t sm[];
@@ -370,14 +370,12 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
   const int top = (1 << rho) - 1, top_a = (1 << la) - 1;
   const float fs_r = ldexpf(1.0f, rho), fs_a = ldexpf(1.0f, la);
   const double ds_r = ldexp(1.0, rho), ds_a = ldexp(1.0, la);
-  const uint32_t mul_a = 1u << la, mul_lo = 1u << (la > 1 ? la - 1 : 0), mul_r = 1u << rho;
+  const uint32_t mul_a = 1u << la, mul_lo = 1u << (la > 1 ? la - 1 : 0);
   const float fs_lo = ldexpf(1.0f, la > 1 ? la - 1 : 0);
-  uint32_t hcorr = 0, locorr = 0, rcorr = 0;
+  uint32_t hcorr = 0, locorr = 0;
   for (int k = D - 1; k >= 1; --k) hcorr = hcorr * mul_a + 0x4B000000u;
   for (int k = D - 1; k >= 0; --k) locorr = locorr * mul_lo + 0x4B000000u;
-  for (int k = D - 1; k >= 0; --k) rcorr = rcorr * mul_r + 0x4B000000u;
   const bool rec_lo = la >= 2;
-  const bool lin32 = rho * D <= 32;
   WarpOut wo{0, p.chunk, p.chunk};
   auto stamp = [&](u64 slot) { p.out_ids[slot] = kNoId; };
   unsigned kept = 0;
@@ -452,16 +450,6 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
       tot += __popc(mk[j]);
     }
     if (tot) {
-      // the tile's survivors fill the rest of the current chunk and straddle
-      // into a new one (host guarantees chunk >= 32 * PPT >= tot)
-      const unsigned rem = wo.chunk - wo.fill;
-      u64 nb = 0;
-      if (tot > rem) {
-        if (lane == 0) nb = atomicAdd(p.out_reserved, (u64)wo.chunk);
-        nb = __shfl_sync(kFull, nb, 0);
-      }
-      const u64 o = wo.base + wo.fill;
-      auto out_slot = [&](unsigned sidx) { return sidx < rem ? o + sidx : nb + (sidx - rem); };
       // Survivors (~12% of the tile at the headline config) are compacted
       // onto consecutive lanes before any per-survivor work: their (j, lane)
       // codes are staged in tile order, each lane pulls one survivor's
@@ -490,45 +478,56 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
             const TIn tv = __shfl_sync(kFull, cur[jj][k], src);
             if (sj == jj) x[k] = tv;
           }
-        if (act) {
-          TOut u[D];
+        TOut u[D];
+        int c[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
           if constexpr (IDENT) {
-            uint32_t l = 0;
-#pragma unroll
-            for (int k = D - 1; k >= 0; --k) {
-              u[k] = __saturatef(x[k]);  // the stored proxy (dataset.cpp:45 clamp, 1.0f = 1 - 2^-32)
-              l = l * mul_r + mag_col(fminf(u[k], 0x1.fffffep-1f), fs_r);
-            }
-            if (lin32) set_bit_cached(p.occ_rho, (u64)(l - rcorr));
-            else {
-              u64 lin = 0;
-#pragma unroll
-              for (int k = D - 1; k >= 0; --k)
-                lin = (lin << rho) | (u64)(mag_col(fminf(u[k], 0x1.fffffep-1f), fs_r) - 0x4B000000u);
-              set_bit_cached(p.occ_rho, lin);
-            }
+            u[k] = __saturatef(x[k]);  // the stored proxy (dataset.cpp:45 clamp, 1.0f = 1 - 2^-32)
+            c[k] = (int)(mag_col(fminf(u[k], 0x1.fffffep-1f), fs_r) - 0x4B000000u);
           } else {
-            u64 lin = 0;
-#pragma unroll
-            for (int k = D - 1; k >= 0; --k) {
-              u[k] = Coord<TIn, TOut, IDENT>::value(x[k], p.nm, k);
-              lin = (lin << rho) | (u64)col_at<TIn, TOut, IDENT>(x[k], p.nm, k, fs_r, ds_r, top);
-            }
-            set_bit_cached(p.occ_rho, lin);
+            u[k] = Coord<TIn, TOut, IDENT>::value(x[k], p.nm, k);
+            c[k] = col_at<TIn, TOut, IDENT>(x[k], p.nm, k, fs_r, ds_r, top);
           }
-          const u64 slot = out_slot(sidx);
+        }
+        // Test B: a layer-rho cell strictly dominated by an occupied SAMPLE
+        // cell is no candidate; such a point only needs its
+        // layer rho-1 cell recorded for the coarser layers' counts.
+        bool keep_b = act;
+        if (act && p.PMs) {
+          bool ok = c[0] >= 1;
+          u64 idx = 0;
+#pragma unroll
+          for (int k = D - 1; k >= 1; --k) {
+            ok &= c[k] >= 1;
+            idx = (idx << rho) | (u64)(c[k] - 1);
+          }
+          if (ok) {
+            const int64_t pm = p.pms_wide ? (int64_t)__ldg(static_cast<const uint32_t*>(p.PMs) + idx)
+                                          : (int64_t)__ldg(static_cast<const uint8_t*>(p.PMs) + idx);
+            if (pm <= (int64_t)c[0] - 1) {
+              keep_b = false;
+              u64 lo = 0;
+#pragma unroll
+              for (int k = D - 1; k >= 0; --k) lo = (lo << (rho - 1)) | (u64)(c[k] >> 1);
+              set_bit_cached(p.occ_rm1, lo);
+            }
+          }
+        }
+        if (keep_b) {
+          u64 lin = 0;
+#pragma unroll
+          for (int k = D - 1; k >= 0; --k) lin = (lin << rho) | (u64)c[k];
+          set_bit_cached(p.occ_rho, lin);
+        }
+        const u64 slot = warp_reserve(wo, keep_b, p.out_reserved, stamp);
+        if (keep_b) {
           store_row<TOut, D>(out_rows, slot, u);
           p.out_ids[slot] = p.id_base + t * WT + sj * 32 + src;
         }
+        kept += __popc(__ballot_sync(kFull, keep_b));
       }
       __syncwarp();
-      if (tot > rem) {
-        wo.base = nb;
-        wo.fill = tot - rem;
-      } else {
-        wo.fill += tot;
-      }
-      kept += tot;
     }
     if (__any_sync(kFull, bad)) {  // rare: NaN/Inf (or overflow of the probe sum)
 #pragma unroll

@@ -431,15 +431,6 @@ struct Pipe final : PipeBase {
   int cell_level() const { return q.merge ? 0 : rho; }
 
   static auto pick_stream(int rho) {
-    if constexpr (IDENT && D == 4) {
-      // tuning experiment (SKYCELL_K1=ab): occupancy / tile-size variants at the headline shape
-      const char* e = std::getenv("SKYCELL_K1");
-      if (e && rho == 6) {
-        if (!std::strcmp(e, "m3")) return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 6, 3>;
-        if (!std::strcmp(e, "p2")) return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, 2, 6, 4>;
-        if (!std::strcmp(e, "p2m3")) return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, 2, 6, 3>;
-      }
-    }
     if constexpr (IDENT && D <= 8) {
       switch (rho) {
         case 1: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 1>;
@@ -557,13 +548,14 @@ struct Pipe final : PipeBase {
       sk::k_build_filter<<<1, 1024, h_entries, s>>>(U(o_sla), la, D, static_cast<uint8_t*>(ctx->H.p));
       tracer().mark(s, "K0: build_filter");
       ctx->launches += 2;
+      // layer-rho prefix-min table of the sample: K1's test B
+      if (test_b) {
+        if (wide) launch_tables<uint32_t>(ctx, s, U(o_srho), rho, D, static_cast<uint32_t*>(ctx->table_s.p));
+        else launch_tables<uint8_t>(ctx, s, U(o_srho), rho, D, static_cast<uint8_t*>(ctx->table_s.p));
+      }
       if (q.merge) {
         // The sample skyline only serves as K4's point filter, which phase-1
         // only semantics (merge_cross_cell = false) cannot use.
-        if (test_b) {
-          if (wide) launch_tables<uint32_t>(ctx, s, U(o_srho), rho, D, static_cast<uint32_t*>(ctx->table_s.p));
-          else launch_tables<uint8_t>(ctx, s, U(o_srho), rho, D, static_cast<uint8_t*>(ctx->table_s.p));
-        }
         tracer().mark(s, "K0: sample tables");
         // sample points not strictly dominated at layer rho -> X (s2 buffers)
         sk::CandParams pc{};
