@@ -562,7 +562,11 @@ struct Pipe final : PipeBase {
         pc.rows = ctx->smp_rows.p;
         pc.ids = static_cast<const uint32_t*>(ctx->smp_ids.p);
         pc.count = nullptr;
-        pc.count_const = m;
+        // the filter points come from the skyline of the first mf sample
+        // points (SKYCELL_FSAMPLE overrides; H uses all m)
+        u64 mf = m;
+        if (const char* e = std::getenv("SKYCELL_FSAMPLE")) mf = std::min<u64>(m, std::strtoull(e, nullptr, 10));
+        pc.count_const = mf;
         pc.rho = rho;
         pc.PM = test_b ? ctx->table_s.p : nullptr;
         pc.f_max = 0;
@@ -606,7 +610,12 @@ struct Pipe final : PipeBase {
     p1.h_entries = h_entries;
     p1.nm = q.nm;
     p1.H = static_cast<const uint8_t*>(ctx->H.p);
-    p1.PMs = test_b ? ctx->table_s.p : nullptr;
+    // Test B costs two dependent L2 round trips per K1 survivor; it pays off
+    // when the shared-memory filter level la is at least two layers coarser
+    // than rho (SKYCELL_TESTB=0/1 overrides).
+    bool use_b = test_b && rho - la >= 2;
+    if (const char* e = std::getenv("SKYCELL_TESTB")) use_b = test_b && e[0] == '1';
+    p1.PMs = use_b ? ctx->table_s.p : nullptr;
     p1.pms_wide = wide;
     p1.occ_rho = occ(rho);
     p1.occ_rm1 = rho >= 2 ? occ(rho - 1) : nullptr;
