@@ -296,7 +296,17 @@ struct StreamParams {
   u64* kept;               // exact number of survivors
   u64* nonfinite;          // max of (~record) over non-finite records: 0 = none
   uint32_t id_base;        // global id of local record 0 (shard offset)
+  // filter-point head (K0's strongest filter points): survivors they dominate
+  // with a strictly smaller sum leave only their layer-rho cell index in the
+  // D stream (points_examined still counts them if the cell is a candidate)
+  const void* f_rows;      // nullptr: no head test
+  const u64* f_fsum;
+  const u64* f_count;
+  void* d_cells;           // u32 (rho*d <= 32) or u64 cell indices
+  u64* d_reserved;
 };
+
+constexpr int kK1Head = 8;  // filter points tested per K1 survivor
 
 // Column of a coordinate at an arbitrary level L <= rho: floor(u * 2^L) is
 // the layer-rho column shifted right by rho - L (power-of-two scalings are
@@ -349,6 +359,15 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
   uint32_t* occ_s = reinterpret_cast<uint32_t*>(sm);
   uint8_t* H_s = sm + ((p.lo_words * 4 + 15) & ~15u);
   uint8_t* code_w = H_s + ((p.h_entries + 15) & ~15u) + (threadIdx.x >> 5) * (32 * PPT);  // survivor codes
+  TOut* fh_rows = reinterpret_cast<TOut*>(H_s + ((p.h_entries + 15) & ~15u) + THREADS * PPT);
+  u64* fh_sum = reinterpret_cast<u64*>(fh_rows + kK1Head * D);
+  uint32_t nfh = 0;
+  if (p.f_rows) {
+    const u64 fc = *p.f_count;
+    nfh = (uint32_t)(fc < (u64)kK1Head ? fc : (u64)kK1Head);
+    for (uint32_t e = threadIdx.x; e < nfh * D; e += THREADS) fh_rows[e] = static_cast<const TOut*>(p.f_rows)[e];
+    for (uint32_t e = threadIdx.x; e < nfh; e += THREADS) fh_sum[e] = p.f_fsum[e];
+  }
   for (uint32_t w = threadIdx.x; w < p.lo_words; w += THREADS) occ_s[w] = 0;
   for (uint32_t e = threadIdx.x; e < p.h_entries; e += THREADS) H_s[e] = p.H[e];
   __syncthreads();
@@ -379,6 +398,13 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
   WarpOut wo{0, p.chunk, p.chunk};
   auto stamp = [&](u64 slot) { p.out_ids[slot] = kNoId; };
   unsigned kept = 0;
+  // D stream: empty slots hold the all-ones cell index, which no layer uses
+  const bool d_wide = rho * D >= 32;  // u32 only while the all-ones marker is no cell
+  WarpOut wd{0, p.chunk, p.chunk};
+  auto dstamp = [&](u64 slot) {
+    if (d_wide) static_cast<u64*>(p.d_cells)[slot] = ~0ull;
+    else static_cast<uint32_t*>(p.d_cells)[slot] = ~0u;
+  };
 
   TIn raw[PPT][D];
   auto load_tile = [&](uint32_t t) {
@@ -514,18 +540,34 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
             }
           }
         }
+        u64 lin = 0;
         if (keep_b) {
-          u64 lin = 0;
 #pragma unroll
           for (int k = D - 1; k >= 0; --k) lin = (lin << rho) | (u64)c[k];
           set_bit_cached(p.occ_rho, lin);
         }
-        const u64 slot = warp_reserve(wo, keep_b, p.out_reserved, stamp);
-        if (keep_b) {
+        // filter-point head: branch-free over the 8 strongest filter points
+        bool to_s1 = keep_b;
+        if (nfh) {
+          const u64 ps = fsum_bits<TOut, D>(u);
+          bool dom = false;
+#pragma unroll
+          for (int f = 0; f < kK1Head; ++f)
+            if (f < (int)nfh) dom |= dominates<TOut, D>(fh_rows + f * D, u) && fh_sum[f] < ps;
+          to_s1 = keep_b && !dom;
+          const bool to_d = keep_b && dom;
+          const u64 dslot = warp_reserve(wd, to_d, p.d_reserved, dstamp);
+          if (to_d) {
+            if (d_wide) static_cast<u64*>(p.d_cells)[dslot] = lin;
+            else static_cast<uint32_t*>(p.d_cells)[dslot] = (uint32_t)lin;
+          }
+        }
+        const u64 slot = warp_reserve(wo, to_s1, p.out_reserved, stamp);
+        if (to_s1) {
           store_row<TOut, D>(out_rows, slot, u);
           p.out_ids[slot] = p.id_base + t * WT + sj * 32 + src;
         }
-        kept += __popc(__ballot_sync(kFull, keep_b));
+        kept += __popc(__ballot_sync(kFull, to_s1));
       }
       __syncwarp();
     }
@@ -542,6 +584,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
     t = tn;
   }
   warp_close(wo, stamp);
+  if (p.f_rows) warp_close(wd, dstamp);
   if (lane == 0 && kept) atomicAdd(p.kept, (u64)kept);
   if (p.lo_words) {
     __syncthreads();
@@ -852,6 +895,9 @@ struct CandParams {
   unsigned chunk;        // output chunk per warp reservation
   u64* kept;             // exact number of points written
   u64* examined;         // points_examined (refine.cpp:90-96), may be null
+  const void* d_cells;   // K1's D stream (cells of survivors a filter point removed), may be null
+  const u64* d_count;
+  int d_wide;
 };
 
 template <typename T, int D, typename TT, int THREADS>
@@ -976,6 +1022,21 @@ __global__ void __launch_bounds__(THREADS) k_candidates(CandParams p) {
     }
   }
   warp_close(wo, stamp);
+  // points K1 already removed (filter-point head) still count in
+  // points_examined when their cell is a candidate
+  if (p.d_cells && PM) {
+    const u64 nd = *p.d_count;
+    const u64 cmask = (1ull << rho) - 1;
+    for (u64 e = blockIdx.x * (u64)THREADS + threadIdx.x; e < nd; e += (u64)gridDim.x * THREADS) {
+      const u64 lin = p.d_wide ? static_cast<const u64*>(p.d_cells)[e]
+                               : (u64) static_cast<const uint32_t*>(p.d_cells)[e];
+      if (p.d_wide ? lin == ~0ull : lin == 0xffffffffull) continue;
+      int col[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) col[k] = (int)((lin >> (rho * k)) & cmask);
+      examined += !strictly_dominated_cols<TT, D>(PM, col, rho);
+    }
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     examined += __shfl_xor_sync(kFull, examined, o);
@@ -998,7 +1059,7 @@ __global__ void k_compact_members(const T* __restrict__ rows, const uint32_t* __
   for (u64 wb = ((blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5) * 32; wb < n;
        wb += ((u64)gridDim.x * blockDim.x >> 5) * 32) {
     const u64 i = wb + lane;
-    const bool live = i < n && ids[i] != kNoId && flag[i];
+    const bool live = i < n && ids[i] != kNoId && (!flag || flag[i]);  // flag == nullptr: every member
     const unsigned m = __ballot_sync(kFull, live);
     if (!m) continue;
     u64 b = 0;
@@ -1020,15 +1081,18 @@ __global__ void k_compact_members(const T* __restrict__ rows, const uint32_t* __
 // happen after ~1 test for most points.
 template <typename T, int D>
 __global__ void __launch_bounds__(1024) k_strength_order(const T* __restrict__ rows, const u64* __restrict__ fsum,
-                                                          const u64* __restrict__ count, uint32_t f_max,
-                                                          T* __restrict__ out_rows, u64* __restrict__ out_fsum,
+                                                          const uint32_t* __restrict__ ids, const u64* __restrict__ count,
+                                                          uint32_t f_max, T* __restrict__ out_rows,
+                                                          u64* __restrict__ out_fsum, uint32_t* __restrict__ out_ids,
                                                           u64* __restrict__ out_count) {
+  // ids (optional): empty slots (kNoId) are skipped; out_ids (optional)
   __shared__ unsigned hist[65];
   __shared__ unsigned offs[65];
   const u64 n = *count;
   if (threadIdx.x < 65) hist[threadIdx.x] = 0;
   __syncthreads();
   auto bucket = [&](u64 i) {
+    if (ids && ids[i] == kNoId) return 64;
     double vol = 1.0;
 #pragma unroll
     for (int k = 0; k < D; ++k) vol *= 1.0 - true_value(rows[i * D + k]);
@@ -1043,15 +1107,18 @@ __global__ void __launch_bounds__(1024) k_strength_order(const T* __restrict__ r
       offs[b] = run;
       run += hist[b];
     }
-    *out_count = n < f_max ? n : f_max;
+    *out_count = run < f_max ? run : f_max;
   }
   __syncthreads();
   for (u64 i = threadIdx.x; i < n; i += blockDim.x) {
-    const unsigned o = atomicAdd(&offs[bucket(i)], 1u);
+    const int bk = bucket(i);
+    if (bk == 64) continue;
+    const unsigned o = atomicAdd(&offs[bk], 1u);
     if (o < f_max) {
 #pragma unroll
       for (int k = 0; k < D; ++k) out_rows[(u64)o * D + k] = rows[i * D + k];
       out_fsum[o] = fsum[i];
+      if (out_ids) out_ids[o] = ids ? ids[i] : (uint32_t)i;
     }
   }
 }

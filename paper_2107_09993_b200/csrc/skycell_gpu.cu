@@ -47,6 +47,8 @@ struct DevCounters {
   u64 m, xs, xs_kept, nf, fs, fin, s1_kept, s2_kept;
   u64 lsky;       // local skyline size (sharded)
   u64 tvalid;     // valid slots of the set a dominance tree is built over
+  u64 dres;       // D-stream slots handed out (K1 filter-point head)
+  u64 ys;         // strongest sample candidates entering the sample skyline
   u64 un, qend;   // union slots and own-slice end (sharded finish)
   u64 cand[kMaxLayers];
   u64 key[kMaxLayers];
@@ -112,6 +114,7 @@ struct skycell_gpu_ctx {
   DevBuf smp_rows, smp_ids, smp_fsum, f_rows, f_fsum, f_lists, f_offs, lists, ids_dev;
   DevBuf s1_rows, s1_ids, s2_rows, s2_ids, s2_fsum, flags;
   DevBuf sky_rows, sky_ids, sky_fsum;  // local skyline (sharded)
+  DevBuf d_cells;                      // K1's D stream
   DevBuf q_bits, q_orig, q_sub, q_ids, q_mm;  // quadrant_skyline
   DevBuf t_keys, t_keys2, t_vals, t_vals2, t_cub, t_rows, t_ids, t_fsum, t_lo, t_hi, t_cs, t_ci;  // K5 tree
   int k5_mode = -1;  // 0 lists, 1 tree, 2 auto (SKYCELL_K5)
@@ -418,6 +421,7 @@ struct Pipe final : PipeBase {
   size_t smem_pf;
   u64 id_words;
   unsigned bit_blocks;
+  bool k1_head = false;  // K1 ran the filter-point head (its D stream feeds K4's points_examined)
 
   // ---- zeroed region
   size_t o_ctr, o_sla, o_srho, o_shist, o_scur, o_hist, o_cur, o_fhist, o_fcur, o_idbits, o_bcount, o_end, o_total;
@@ -458,7 +462,8 @@ struct Pipe final : PipeBase {
     table_entries = 1ull << (u64)(rho * (D - 1));
 
     // K1 geometry: persistent warps over round-robin warp tiles
-    smem1 = (((size_t)lo_words * 4 + 15) & ~(size_t)15) + ((h_entries + 15) & ~15u) + (size_t)kStreamThreads * PPT1 + 16;
+    smem1 = (((size_t)lo_words * 4 + 15) & ~(size_t)15) + ((h_entries + 15) & ~15u) + (size_t)kStreamThreads * PPT1 +
+            (size_t)sk::kK1Head * (D * sizeof(TOut) + 8) + 16;
     kstream = pick_stream(rho);
     ck(cudaFuncSetAttribute(kstream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1), "smem attr");
     int occ_blocks = 0;
@@ -513,6 +518,7 @@ struct Pipe final : PipeBase {
     ensure(ctx->f_offs, (size_t)D * (sk::kListCols + 1) * 2);
     ensure(ctx->s1_rows, cap1 * D * sizeof(TOut));
     ensure(ctx->s1_ids, cap1 * 4);
+    ensure(ctx->d_cells, cap1 * (rho * D >= 32 ? 8 : 4));
     ensure(ctx->s2_rows, cap4 * D * sizeof(TOut));
     ensure(ctx->s2_ids, cap4 * 4);
     ensure(ctx->s2_fsum, cap4 * 8);
@@ -581,6 +587,8 @@ struct Pipe final : PipeBase {
         else sk::k_candidates<TOut, D, uint8_t, kThreads><<<grid4, kThreads, 16, s>>>(pc);
         ++ctx->launches;
         tracer().mark(s, "K0: sample X");
+        // Filter points = the strongest points of the sample's skyline (the
+        // whole skyline: its extremes filter the extremes of the data)
         run_dominance<TOut, D>(ctx, s, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
                                static_cast<const u64*>(ctx->s2_fsum.p), &c->xs, cap4, U(o_shist), U(o_scur),
                                &c->tvalid);
@@ -590,8 +598,8 @@ struct Pipe final : PipeBase {
             static_cast<const uint8_t*>(ctx->flags.p), static_cast<const u64*>(ctx->s2_fsum.p), &c->xs,
             static_cast<TOut*>(ctx->smp_rows.p), static_cast<u64*>(ctx->smp_fsum.p), &c->fs);
         sk::k_strength_order<TOut, D><<<1, 1024, 0, s>>>(
-            static_cast<const TOut*>(ctx->smp_rows.p), static_cast<const u64*>(ctx->smp_fsum.p), &c->fs,
-            (uint32_t)pf_max, static_cast<TOut*>(ctx->f_rows.p), static_cast<u64*>(ctx->f_fsum.p), &c->nf);
+            static_cast<const TOut*>(ctx->smp_rows.p), static_cast<const u64*>(ctx->smp_fsum.p), nullptr, &c->fs,
+            (uint32_t)pf_max, static_cast<TOut*>(ctx->f_rows.p), static_cast<u64*>(ctx->f_fsum.p), nullptr, &c->nf);
         sk::k_filter_lists<TOut, D><<<D, 1024, 0, s>>>(static_cast<const TOut*>(ctx->f_rows.p), &c->nf,
                                                         (uint32_t)pf_max, static_cast<uint16_t*>(ctx->f_lists.p),
                                                         static_cast<uint16_t*>(ctx->f_offs.p));
@@ -627,6 +635,17 @@ struct Pipe final : PipeBase {
     p1.kept = &c->s1_kept;
     p1.nonfinite = &c->nonfinite;
     p1.id_base = q.id_base;
+    // K1's filter-point head (SKYCELL_K1HEAD=1): cuts S1 ~8x but costs K1
+    // more than it saves K4 at the headline config
+    const char* he = std::getenv("SKYCELL_K1HEAD");
+    k1_head = q.merge && he && he[0] == '1';
+    if (k1_head) {  // the filter points exist (K0) only with the phase-2 merge
+      p1.f_rows = ctx->f_rows.p;
+      p1.f_fsum = static_cast<const u64*>(ctx->f_fsum.p);
+      p1.f_count = &c->nf;
+      p1.d_cells = ctx->d_cells.p;
+      p1.d_reserved = &c->dres;
+    }
     if (q.timed) ck(cudaEventRecord(ctx->ev[4], s), "event");
     kstream<<<grid1, kStreamThreads, smem1, s>>>(p1);
     ++ctx->launches;
@@ -708,6 +727,11 @@ struct Pipe final : PipeBase {
     pc.chunk = kChunk4;
     pc.kept = &c->s2_kept;
     pc.examined = &c->examined;
+    if (k1_head) {
+      pc.d_cells = ctx->d_cells.p;
+      pc.d_count = &c->dres;
+      pc.d_wide = rho * D >= 32;
+    }
     if (wide) {
       auto kc = sk::k_candidates<TOut, D, uint32_t, kThreads>;
       ck(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pf), "smem attr");
@@ -1105,7 +1129,7 @@ void skycell_gpu_destroy(skycell_gpu_ctx* ctx) {
                     &ctx->s2_ids, &ctx->s2_fsum, &ctx->flags, &ctx->sky_rows, &ctx->sky_ids, &ctx->sky_fsum,
                     &ctx->q_bits, &ctx->q_orig, &ctx->q_sub, &ctx->q_ids, &ctx->q_mm, &ctx->t_keys,
                     &ctx->t_keys2, &ctx->t_vals, &ctx->t_vals2, &ctx->t_cub, &ctx->t_rows, &ctx->t_ids,
-                    &ctx->t_fsum, &ctx->t_lo, &ctx->t_hi, &ctx->t_cs, &ctx->t_ci, &ctx->long_q, &ctx->long_n, &ctx->scan_tot};
+                    &ctx->t_fsum, &ctx->t_lo, &ctx->t_hi, &ctx->t_cs, &ctx->t_ci, &ctx->long_q, &ctx->long_n, &ctx->scan_tot, &ctx->d_cells};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (auto& e : ctx->ev)

@@ -1,5 +1,5 @@
-TAG=r1o
+TAG=${1:-r1q}
 mkdir -p gpurun_out
-for b in 0 1; do for c in c2 c4c c5d3 c5d4 c5d5; do SKYCELL_TESTB=$b timeout 300 python bench.py --config $c --steps 5 --no-cpu > gpurun_out/bench_${c}_b${b}_${TAG}.json 2>&1; echo "b$b $c rc=$?"; done; done
-for fs in 262144 65536; do for c in c2 c4i; do SKYCELL_TESTB=0 SKYCELL_FSAMPLE=$fs timeout 300 python bench.py --config $c --steps 5 --no-cpu > gpurun_out/bench_${c}_fs${fs}_${TAG}.json 2>&1; echo "fs$fs $c rc=$?"; done; done
-SKYCELL_TESTB=0 SKYCELL_K5=tree timeout 300 python bench.py --config c2 --steps 5 --no-cpu > gpurun_out/bench_c2_tree_${TAG}.json 2>&1; echo "tree c2 rc=$?"
+timeout 1500 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu_${TAG}.log 2>&1; echo "pytest rc=$?"; tail -4 gpurun_out/pytest_gpu_${TAG}.log
+for c in c2 c1 c4c c4i c5d2 c5d3 c5d4; do timeout 300 python bench.py --config $c --steps 10 --no-cpu > gpurun_out/bench_${c}_${TAG}.json 2>&1; echo "$c rc=$?"; done
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2_${TAG}.csv python bench.py --config c2 --steps 1 --warmup 3 --no-cpu > /dev/null 2>&1; echo "launch c2 rc=$?"
