@@ -229,6 +229,7 @@ __global__ void __launch_bounds__(256) k_tree_query(const T* __restrict__ srows,
     for (int k = 1; k < D; ++k)
       if (kd == k) pk = v[k];
     bool dom = false;
+    const uint32_t lp = (uint32_t)(j / kLeaf);  // p's own leaf
     if (lane == 0) stk[0] = (uint32_t)(sh.levels - 1) << 27;
     int top = 1;
     __syncwarp();
@@ -284,6 +285,12 @@ __global__ void __launch_bounds__(256) k_tree_query(const T* __restrict__ srows,
       }
       const unsigned wm = __ballot_sync(kFull, want);
       if (!wm) continue;
+      // the child on p's own root-to-leaf path first: dominators of p are
+      // near p, hence near it along the Z-order (anti-correlated data); then
+      // the child lying below p in the most dimensions
+      uint32_t anc = lp;
+      for (int l = 1; l < lvl; ++l) anc /= F;
+      if (lane < nc && cidx0 + lane == anc && want) score = 64;
       // best child: highest score, ties to the lowest lane
       int best = (score << 5) | (31 - lane);
 #pragma unroll

@@ -213,3 +213,16 @@ def test_gpu_k5_variants_large_golden(forced_engine, oracle, rec):
     x, mn, mx = inputs_for(oracle, rec)
     r = forced_engine.compute_skyline(sky.Dataset(x, mn, mx), rec["rho"])
     check(r, load_ids("large_ids.npz")[rec["key"]], rec["points_examined"], rec["keys"], rec["candidates"])
+
+
+@pytest.mark.parametrize("d,rho", [(2, 8), (2, 11), (2, 14), (3, 8), (3, 10), (4, 8), (5, 7), (6, 5)])
+def test_gpu_fine_grids_vs_oracle(engine, oracle, d, rho):
+    """Layers above 7 (u32 prefix-min tables) and the largest grids of the
+    reference's budget that the dense bitmaps cover (grid.cpp:38-43)."""
+    from oracle.oracle import quantize_f32
+    for dist in range(3):
+        v = oracle.generate(dist, 3000, d, 70 + rho)
+        for x, mn, mx in ((quantize_f32(v), np.zeros(d), np.ones(d)), (v * 3 - 1, (v * 3 - 1).min(0), (v * 3 - 1).max(0))):
+            want = oracle.compute_skyline(x.astype(np.float64), mn, mx, rho)
+            got = engine.compute_skyline(sky.Dataset(np.ascontiguousarray(x), mn, mx), rho)
+            check(got, want.ids, want.points_examined, want.keys, want.candidates)
