@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(256) k_tree_query(const T* __restrict__ srows,
                                                     const u64* __restrict__ q_end, int cell_level,
                                                     uint8_t* __restrict__ flag) {
   constexpr int F = tree_fanout<D>();
-  constexpr int kStack = 128;
+  constexpr int kStack = 192;  // >= levels * (F - 1) + levels for every fan-out
   // stack entries: level << 27 | index within the level (nleaf < 2^27)
   __shared__ uint32_t stack_s[8][kStack];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -230,8 +230,22 @@ __global__ void __launch_bounds__(256) k_tree_query(const T* __restrict__ srows,
       if (kd == k) pk = v[k];
     bool dom = false;
     const uint32_t lp = (uint32_t)(j / kLeaf);  // p's own leaf
-    if (lane == 0) stk[0] = (uint32_t)(sh.levels - 1) << 27;
-    int top = 1;
+    // Jump start: dominators of p are usually near p along the Z-order, so
+    // the search begins at p's own leaf and widens level by level -- the
+    // stack holds p's ancestors (each to be expanded without the child on
+    // p's path), root at the bottom, with p's own leaf on top.
+    int top = 0;
+    if (lane == 0) {
+      uint32_t a = lp;
+      uint32_t path[32];
+      for (int l = 0; l < sh.levels; ++l) {
+        path[l] = a;
+        a /= F;
+      }
+      for (int l = sh.levels - 1; l >= 1; --l) stk[top++] = ((uint32_t)l << 27) | path[l];
+      stk[top++] = lp;  // level 0
+    }
+    top = __shfl_sync(kFull, top, 0);
     __syncwarp();
     while (top > 0) {
       const uint32_t e = stk[--top];
@@ -269,7 +283,12 @@ __global__ void __launch_bounds__(256) k_tree_query(const T* __restrict__ srows,
       // lanes c < nc: verdict for child c
       bool want = false, kill = false;
       int score = -1;
-      if (lane < nc) {
+      // an ancestor of p's leaf (jump start) skips the child on p's path:
+      // that subtree has been searched already
+      uint32_t own = lp;
+      for (int l = 1; l < lvl; ++l) own /= F;  // p's ancestor at level lvl - 1
+      const bool ancestor = own / F == idx;
+      if (lane < nc && !(ancestor && cidx0 + lane == own)) {
         const u64 cs = __ldg(tv.cs + c0 + lane);
         const uint32_t ci = __ldg(tv.ci + c0 + lane);
         const unsigned in_c = (hi_in >> (lane * D)) & m0;
@@ -285,12 +304,6 @@ __global__ void __launch_bounds__(256) k_tree_query(const T* __restrict__ srows,
       }
       const unsigned wm = __ballot_sync(kFull, want);
       if (!wm) continue;
-      // the child on p's own root-to-leaf path first: dominators of p are
-      // near p, hence near it along the Z-order (anti-correlated data); then
-      // the child lying below p in the most dimensions
-      uint32_t anc = lp;
-      for (int l = 1; l < lvl; ++l) anc /= F;
-      if (lane < nc && cidx0 + lane == anc && want) score = 64;
       // best child: highest score, ties to the lowest lane
       int best = (score << 5) | (31 - lane);
 #pragma unroll
