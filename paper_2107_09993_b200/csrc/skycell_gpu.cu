@@ -47,6 +47,7 @@ struct DevCounters {
   u64 m, xs, xs_kept, nf, fs, fin, s1_kept, s2_kept;
   u64 lsky;       // local skyline size (sharded)
   u64 tvalid;     // valid slots of the set a dominance tree is built over
+  u64 tkilled;    // ... removed by the champion prefilter (must follow tvalid)
   u64 dres;       // D-stream slots handed out (K1 filter-point head)
   u64 ys;         // strongest sample candidates entering the sample skyline
   u64 un, qend;   // union slots and own-slice end (sharded finish)
@@ -117,6 +118,7 @@ struct skycell_gpu_ctx {
   DevBuf d_cells;                      // K1's D stream
   DevBuf q_bits, q_orig, q_sub, q_ids, q_mm;  // quadrant_skyline
   DevBuf t_keys, t_keys2, t_vals, t_vals2, t_cub, t_rows, t_ids, t_fsum, t_lo, t_hi, t_cs, t_ci;  // K5 tree
+  DevBuf t_cm, t_kill;  // K5 tree champion prefilter
   int k5_mode = -1;  // 0 lists, 1 tree, 2 auto (SKYCELL_K5)
   DevBuf long_q, long_n;  // K5 phase-B queue
   DevBuf scan_tot;        // K5 list-scan chunk totals
@@ -292,7 +294,27 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
   ck(cudaMemsetAsync(valid_ctr, 0, 8, s), "memset");
   const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((nslots + 255) / 256, (u64)nsm * 8));
   tracer().mark(s, "tree: count read");
-  sk::k_tree_keys<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, count,
+  // champion prefilter over a dense level-Lc grid (<= 2^24 cells)
+  const int Lc = std::min(12, 24 / D);
+  const uint8_t* kill = nullptr;
+  if (Lc >= 1 && nslots >= (1ull << 16)) {
+    const u64 cells = 1ull << (u64)(Lc * D);
+    ensure(ctx->t_cm, cells * 8);
+    ensure(ctx->t_kill, nslots);
+    u64* cm = static_cast<u64*>(ctx->t_cm.p);
+    ck(cudaMemsetAsync(cm, 0xff, cells * 8, s), "memset");
+    sk::k_cellmin<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, count, Lc, cm);
+    const u64 lines = cells >> Lc;
+    const unsigned gp = (unsigned)std::max<u64>(1, std::min<u64>((lines + 127) / 128, (u64)nsm * 16));
+    for (int k = 1; k <= D; ++k) sk::k_prefix_min<u64><<<gp, 128, 0, s>>>(cm, Lc, k, lines);
+    sk::k_champ_kill<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, count, Lc, cm, q_begin,
+                                               q_end, static_cast<uint8_t*>(ctx->t_kill.p),
+                                               static_cast<uint8_t*>(ctx->flags.p), valid_ctr + 1);
+    ctx->launches += 2 + D;
+    kill = static_cast<const uint8_t*>(ctx->t_kill.p);
+    tracer().mark(s, "tree: champion prefilter");
+  }
+  sk::k_tree_keys<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, count, kill,
                                             static_cast<u64*>(ctx->t_keys.p), static_cast<uint32_t*>(ctx->t_vals.p),
                                             valid_ctr);
   size_t temp = 0;
@@ -1129,7 +1151,7 @@ void skycell_gpu_destroy(skycell_gpu_ctx* ctx) {
                     &ctx->s2_ids, &ctx->s2_fsum, &ctx->flags, &ctx->sky_rows, &ctx->sky_ids, &ctx->sky_fsum,
                     &ctx->q_bits, &ctx->q_orig, &ctx->q_sub, &ctx->q_ids, &ctx->q_mm, &ctx->t_keys,
                     &ctx->t_keys2, &ctx->t_vals, &ctx->t_vals2, &ctx->t_cub, &ctx->t_rows, &ctx->t_ids,
-                    &ctx->t_fsum, &ctx->t_lo, &ctx->t_hi, &ctx->t_cs, &ctx->t_ci, &ctx->long_q, &ctx->long_n, &ctx->scan_tot, &ctx->d_cells};
+                    &ctx->t_fsum, &ctx->t_lo, &ctx->t_hi, &ctx->t_cs, &ctx->t_ci, &ctx->long_q, &ctx->long_n, &ctx->scan_tot, &ctx->d_cells, &ctx->t_cm, &ctx->t_kill};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (auto& e : ctx->ev)

@@ -45,14 +45,82 @@ __device__ __forceinline__ u64 morton_of(const T (&v)[D]) {
   return key;
 }
 
+// ---- champion prefilter (large sets).  cm[c] = min FP64-sum bits over the
+// set's points in cell c of a dense level-Lc grid; after a d-dimensional
+// inclusive prefix-min, cm[c - 1] is the smallest sum among the points of
+// all cells strictly below c.  Such a point q is < p in every coordinate,
+// so it dominates p, and if its sum is smaller it also precedes p: p is
+// removed (and may be dropped as a dominator too -- q, or whatever removed
+// q, dominates everything p does).  Equal sums are left to the exact pass.
+template <typename T, int D>
+__device__ __forceinline__ void grid_cols(const T (&v)[D], int L, int (&c)[D]) {
+  const T sc = (T)(1u << L);
+#pragma unroll
+  for (int k = 0; k < D; ++k) c[k] = cell_col(v[k], sc, (1 << L) - 1);
+}
+
+template <typename T, int D>
+__global__ void k_cellmin(const T* __restrict__ rows, const uint32_t* __restrict__ ids, const u64* __restrict__ fsum,
+                          const u64* __restrict__ count, int L, u64* __restrict__ cm) {
+  const u64 n = *count;
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    if (ids[i] == kNoId) continue;
+    T v[D];
+    load_row_cached<T, D>(rows, i, v);
+    int c[D];
+    grid_cols<T, D>(v, L, c);
+    u64 lin = 0;
+#pragma unroll
+    for (int k = D - 1; k >= 0; --k) lin = (lin << L) | (u64)c[k];
+    const u64 s = fsum[i];
+    if (s < __ldcg(cm + lin)) atomicMin(cm + lin, s);
+  }
+}
+
+template <typename T, int D>
+__global__ void k_champ_kill(const T* __restrict__ rows, const uint32_t* __restrict__ ids, const u64* __restrict__ fsum,
+                             const u64* __restrict__ count, int L, const u64* __restrict__ cm, u64 q_begin,
+                             const u64* __restrict__ q_end, uint8_t* __restrict__ kill, uint8_t* __restrict__ flag,
+                             u64* __restrict__ killed) {
+  const u64 n = *count;
+  const u64 qe = q_end ? *q_end : ~0ull;
+  u64 mine = 0;
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    uint8_t k_i = 0;
+    if (ids[i] != kNoId) {
+      T v[D];
+      load_row_cached<T, D>(rows, i, v);
+      int c[D];
+      grid_cols<T, D>(v, L, c);
+      bool ok = true;
+      u64 lin = 0;
+#pragma unroll
+      for (int k = D - 1; k >= 0; --k) {
+        ok &= c[k] >= 1;
+        lin = (lin << L) | (u64)(c[k] - 1);
+      }
+      if (ok && __ldg(cm + lin) < fsum[i]) {
+        k_i = 1;
+        ++mine;
+        if (i >= q_begin && i < qe) flag[i] = 0;
+      }
+    }
+    kill[i] = k_i;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(kFull, mine, o);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(killed, mine);
+}
+
 template <typename T, int D>
 __global__ void k_tree_keys(const T* __restrict__ rows, const uint32_t* __restrict__ ids, const u64* __restrict__ count,
-                            u64* __restrict__ keys, uint32_t* __restrict__ vals, u64* __restrict__ valid) {
+                            const uint8_t* __restrict__ kill, u64* __restrict__ keys, uint32_t* __restrict__ vals,
+                            u64* __restrict__ valid) {
   const u64 n = *count;
   u64 mine = 0;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
     u64 key = ~0ull;
-    if (ids[i] != kNoId) {
+    if (ids[i] != kNoId && !(kill && kill[i])) {
       T v[D];
       load_row_cached<T, D>(rows, i, v);
       key = morton_of<T, D>(v) >> 1;  // < ~0: valid slots sort before empty ones
