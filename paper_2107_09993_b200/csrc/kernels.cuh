@@ -1000,6 +1000,10 @@ __global__ void __launch_bounds__(THREADS) k_candidates(CandParams p) {
         if (e < end) { end = e; bk = k; }
       }
       const uint16_t* lst = f_list + (u64)bk * fm;
+      // at most kFSteps steps: a point the filter cannot settle quickly is
+      // left to K5 (anti-correlated data: long prefixes, few kills)
+      constexpr unsigned kFSteps = 8;
+      if (end > kFSteps * 32) end = kFSteps * 32;
       for (unsigned base = 0; base < end && !found; base += 32) {
         const unsigned e = base + lane;
         bool d_l = false;
@@ -1614,7 +1618,7 @@ __global__ void k_pack_members(const T* __restrict__ rows, const uint32_t* __res
   for (u64 wb = ((blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5) * 32; wb < n;
        wb += ((u64)gridDim.x * blockDim.x >> 5) * 32) {
     const u64 i = wb + lane;
-    const bool live = i < n && ids[i] != kNoId && flag[i];
+    const bool live = i < n && ids[i] != kNoId && (!flag || flag[i]);  // flag == nullptr: every member
     const unsigned m = __ballot_sync(kFull, live);
     if (!m) continue;
     u64 b = 0;
@@ -1629,6 +1633,10 @@ __global__ void k_pack_members(const T* __restrict__ rows, const uint32_t* __res
       out_ids[o] = ids[i];
     }
   }
+}
+
+__global__ void k_clamp_count(const u64* __restrict__ src, u64 cap, u64* __restrict__ dst) {
+  if (threadIdx.x == 0) *dst = *src < cap ? *src : cap;
 }
 
 __global__ void k_fill_u32(uint32_t* __restrict__ p, u64 count, uint32_t v) {

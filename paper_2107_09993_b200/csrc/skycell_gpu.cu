@@ -49,7 +49,7 @@ struct DevCounters {
   u64 tvalid;     // valid slots of the set a dominance tree is built over
   u64 tkilled;    // ... removed by the champion prefilter (must follow tvalid)
   u64 dres;       // D-stream slots handed out (K1 filter-point head)
-  u64 ys;         // strongest sample candidates entering the sample skyline
+  u64 xd, xs_cap; // sample candidates (dense) / those entering the sample skyline (capped)
   u64 un, qend;   // union slots and own-slice end (sharded finish)
   u64 cand[kMaxLayers];
   u64 key[kMaxLayers];
@@ -399,16 +399,16 @@ constexpr u64 kTreeMinSlots = 1ull << 20;
 template <typename TOut, int D>
 void run_dominance(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint32_t* ids, const u64* fsum,
                    const u64* count, u64 cap, unsigned* hist, unsigned* cursor, u64* valid_ctr, u64 q_begin = 0,
-                   const u64* q_end = nullptr, int cell_level = 0) {
+                   const u64* q_end = nullptr, int cell_level = 0, u64 tree_min = kTreeMinSlots) {
   int mode = k5_mode(ctx);
   if (mode == 2) {
-    if (cap <= kTreeMinSlots) {
+    if (cap <= tree_min) {
       mode = 0;
     } else {
       u64 nslots = 0;
       ck(cudaMemcpyAsync(&nslots, count, 8, cudaMemcpyDeviceToHost, s), "D2H");
       ck(cudaStreamSynchronize(s), "sync");
-      mode = nslots > kTreeMinSlots ? 1 : 0;
+      mode = nslots > tree_min ? 1 : 0;
     }
   }
   if (mode == 0)
@@ -610,17 +610,27 @@ struct Pipe final : PipeBase {
         ++ctx->launches;
         tracer().mark(s, "K0: sample X");
         // Filter points = the strongest points of the sample's skyline (the
-        // whole skyline: its extremes filter the extremes of the data)
-        run_dominance<TOut, D>(ctx, s, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
-                               static_cast<const u64*>(ctx->s2_fsum.p), &c->xs, cap4, U(o_shist), U(o_scur),
-                               &c->tvalid);
+        // whole skyline: its extremes filter the extremes of the data).  X
+        // is capped at kXMax slots (a random subset: slots follow the sample
+        // order): anti-correlated samples keep ~all points in X, and their
+        // filter points remove little anyway.
+        constexpr u64 kXMax = 1ull << 17;
+        sk::k_pack_members<TOut, D><<<nsm * 4, 256, 0, s>>>(
+            static_cast<const TOut*>(ctx->s2_rows.p), static_cast<const uint32_t*>(ctx->s2_ids.p), nullptr,
+            static_cast<const u64*>(ctx->s2_fsum.p), &c->xs, static_cast<TOut*>(ctx->smp_rows.p),
+            static_cast<u64*>(ctx->smp_fsum.p), static_cast<uint32_t*>(ctx->smp_ids.p), &c->xd);
+        sk::k_clamp_count<<<1, 32, 0, s>>>(&c->xd, kXMax, &c->xs_cap);
+        ctx->launches += 2;
+        run_dominance<TOut, D>(ctx, s, ctx->smp_rows.p, static_cast<const uint32_t*>(ctx->smp_ids.p),
+                               static_cast<const u64*>(ctx->smp_fsum.p), &c->xs_cap, std::min<u64>(m, kXMax),
+                               U(o_shist), U(o_scur), &c->tvalid, 0, nullptr, 0, 96 * 1024);
         tracer().mark(s, "K0: sample skyline");
         sk::k_compact_members<TOut, D><<<nsm * 4, 256, 0, s>>>(
-            static_cast<const TOut*>(ctx->s2_rows.p), static_cast<const uint32_t*>(ctx->s2_ids.p),
-            static_cast<const uint8_t*>(ctx->flags.p), static_cast<const u64*>(ctx->s2_fsum.p), &c->xs,
-            static_cast<TOut*>(ctx->smp_rows.p), static_cast<u64*>(ctx->smp_fsum.p), &c->fs);
+            static_cast<const TOut*>(ctx->smp_rows.p), static_cast<const uint32_t*>(ctx->smp_ids.p),
+            static_cast<const uint8_t*>(ctx->flags.p), static_cast<const u64*>(ctx->smp_fsum.p), &c->xs_cap,
+            static_cast<TOut*>(ctx->s2_rows.p), static_cast<u64*>(ctx->s2_fsum.p), &c->fs);
         sk::k_strength_order<TOut, D><<<1, 1024, 0, s>>>(
-            static_cast<const TOut*>(ctx->smp_rows.p), static_cast<const u64*>(ctx->smp_fsum.p), nullptr, &c->fs,
+            static_cast<const TOut*>(ctx->s2_rows.p), static_cast<const u64*>(ctx->s2_fsum.p), nullptr, &c->fs,
             (uint32_t)pf_max, static_cast<TOut*>(ctx->f_rows.p), static_cast<u64*>(ctx->f_fsum.p), nullptr, &c->nf);
         sk::k_filter_lists<TOut, D><<<D, 1024, 0, s>>>(static_cast<const TOut*>(ctx->f_rows.p), &c->nf,
                                                         (uint32_t)pf_max, static_cast<uint16_t*>(ctx->f_lists.p),

@@ -1,5 +1,4 @@
-TAG=${1:-r1t}
+TAG=${1:-r1y}
 mkdir -p gpurun_out
 timeout 1500 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu_${TAG}.log 2>&1; echo "pytest rc=$?"; tail -4 gpurun_out/pytest_gpu_${TAG}.log
-for c in c2 c5d4 c5d5 c3; do timeout 300 python bench.py --config $c --steps 5 --no-cpu > gpurun_out/bench_${c}_${TAG}.json 2>&1; echo "$c rc=$?"; done
-tail -1 gpurun_out/bench_c2_${TAG}.json | python -c "import json,sys; print(json.loads(sys.stdin.read())['clocks'])"
+for c in c2 c1 c4c c5d2 c5d3 c5d4 c5d5 c3 c5d7; do timeout 300 python bench.py --config $c --steps 5 --no-cpu > gpurun_out/bench_${c}_${TAG}.json 2>&1; echo "$c rc=$?"; done
