@@ -295,22 +295,29 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
   const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((nslots + 255) / 256, (u64)nsm * 8));
   tracer().mark(s, "tree: count read");
   // champion prefilter over a dense level-Lc grid (<= 2^24 cells)
-  const int Lc = std::min(12, 24 / D);
+  // at most 2^24 cells and about 4 cells per set slot (the table's memset and
+  // d prefix passes are a fixed cost; small sets would not amortise them)
+  int lg = 0;
+  while ((1ull << (lg + 1)) <= 4 * nslots) ++lg;
+  const int Lc = std::min(std::min(12, 24 / D), lg / D);
   const uint8_t* kill = nullptr;
   if (Lc >= 1 && nslots >= (1ull << 16)) {
     const u64 cells = 1ull << (u64)(Lc * D);
     ensure(ctx->t_cm, cells * 8);
     ensure(ctx->t_kill, nslots);
     u64* cm = static_cast<u64*>(ctx->t_cm.p);
-    ck(cudaMemsetAsync(cm, 0xff, cells * 8, s), "memset");
-    sk::k_cellmin<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, count, Lc, cm);
     const u64 lines = cells >> Lc;
     const unsigned gp = (unsigned)std::max<u64>(1, std::min<u64>((lines + 127) / 128, (u64)nsm * 16));
-    for (int k = 1; k <= D; ++k) sk::k_prefix_min<u64><<<gp, 128, 0, s>>>(cm, Lc, k, lines);
-    sk::k_champ_kill<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, count, Lc, cm, q_begin,
-                                               q_end, static_cast<uint8_t*>(ctx->t_kill.p),
-                                               static_cast<uint8_t*>(ctx->flags.p), valid_ctr + 1);
-    ctx->launches += 2 + D;
+    uint8_t* killb = static_cast<uint8_t*>(ctx->t_kill.p);
+    for (int pass = 0; pass < 2; ++pass) {  // the plain grid, then the half-cell-shifted one
+      ck(cudaMemsetAsync(cm, 0xff, cells * 8, s), "memset");
+      sk::k_cellmin<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, count, Lc, pass, killb, cm);
+      for (int k = 1; k <= D; ++k) sk::k_prefix_min<u64><<<gp, 128, 0, s>>>(cm, Lc, k, lines);
+      sk::k_champ_kill<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, count, Lc, pass, cm,
+                                                 q_begin, q_end, killb, static_cast<uint8_t*>(ctx->flags.p),
+                                                 valid_ctr + 1);
+      ctx->launches += 2 + D;
+    }
     kill = static_cast<const uint8_t*>(ctx->t_kill.p);
     tracer().mark(s, "tree: champion prefilter");
   }

@@ -52,23 +52,35 @@ __device__ __forceinline__ u64 morton_of(const T (&v)[D]) {
 // so it dominates p, and if its sum is smaller it also precedes p: p is
 // removed (and may be dropped as a dominator too -- q, or whatever removed
 // q, dominates everything p does).  Equal sums are left to the exact pass.
+// Pass 0 uses the grid floor(v 2^L); pass 1 the grid shifted by half a cell,
+// floor(v 2^L + 1/2) (clamped), which catches dominators across the first
+// grid's cell boundaries.  In both, a strictly smaller column in every
+// dimension implies a strictly smaller coordinate.
 template <typename T, int D>
-__device__ __forceinline__ void grid_cols(const T (&v)[D], int L, int (&c)[D]) {
+__device__ __forceinline__ void grid_cols(const T (&v)[D], int L, int pass, int (&c)[D]) {
   const T sc = (T)(1u << L);
+  const T off = pass ? (T)0.5 : (T)0;
+  const int top = (1 << L) - 1;
 #pragma unroll
-  for (int k = 0; k < D; ++k) c[k] = cell_col(v[k], sc, (1 << L) - 1);
+  for (int k = 0; k < D; ++k) {
+    const T x = v[k] * sc + off;  // exact: power-of-two scale, +1/2 on values < 2^24
+    int ci = (int)x;
+    c[k] = ci < 0 ? 0 : (ci > top ? top : ci);
+  }
 }
 
 template <typename T, int D>
 __global__ void k_cellmin(const T* __restrict__ rows, const uint32_t* __restrict__ ids, const u64* __restrict__ fsum,
-                          const u64* __restrict__ count, int L, u64* __restrict__ cm) {
+                          const u64* __restrict__ count, int L, int pass, const uint8_t* __restrict__ kill,
+                          u64* __restrict__ cm) {
   const u64 n = *count;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    // removed points stay valid dominators (they are real records)
     if (ids[i] == kNoId) continue;
     T v[D];
     load_row_cached<T, D>(rows, i, v);
     int c[D];
-    grid_cols<T, D>(v, L, c);
+    grid_cols<T, D>(v, L, pass, c);
     u64 lin = 0;
 #pragma unroll
     for (int k = D - 1; k >= 0; --k) lin = (lin << L) | (u64)c[k];
@@ -79,19 +91,20 @@ __global__ void k_cellmin(const T* __restrict__ rows, const uint32_t* __restrict
 
 template <typename T, int D>
 __global__ void k_champ_kill(const T* __restrict__ rows, const uint32_t* __restrict__ ids, const u64* __restrict__ fsum,
-                             const u64* __restrict__ count, int L, const u64* __restrict__ cm, u64 q_begin,
+                             const u64* __restrict__ count, int L, int pass, const u64* __restrict__ cm, u64 q_begin,
                              const u64* __restrict__ q_end, uint8_t* __restrict__ kill, uint8_t* __restrict__ flag,
                              u64* __restrict__ killed) {
   const u64 n = *count;
   const u64 qe = q_end ? *q_end : ~0ull;
   u64 mine = 0;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    if (pass && kill[i]) continue;  // already removed by pass 0
     uint8_t k_i = 0;
     if (ids[i] != kNoId) {
       T v[D];
       load_row_cached<T, D>(rows, i, v);
       int c[D];
-      grid_cols<T, D>(v, L, c);
+      grid_cols<T, D>(v, L, pass, c);
       bool ok = true;
       u64 lin = 0;
 #pragma unroll
@@ -105,7 +118,7 @@ __global__ void k_champ_kill(const T* __restrict__ rows, const uint32_t* __restr
         if (i >= q_begin && i < qe) flag[i] = 0;
       }
     }
-    kill[i] = k_i;
+    if (!pass || k_i) kill[i] = k_i;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(kFull, mine, o);
@@ -274,6 +287,7 @@ __global__ void __launch_bounds__(256) k_tree_query(const T* __restrict__ srows,
   constexpr int kStack = 192;  // >= levels * (F - 1) + levels for every fan-out
   // stack entries: level << 27 | index within the level (nleaf < 2^27)
   __shared__ uint32_t stack_s[8][kStack];
+  __shared__ uint32_t path_s[8][32];  // p's ancestor index per level
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint32_t* stk = stack_s[wib];
   const u64 qend = q_end ? *q_end : ~0ull;
@@ -302,10 +316,10 @@ __global__ void __launch_bounds__(256) k_tree_query(const T* __restrict__ srows,
     // the search begins at p's own leaf and widens level by level -- the
     // stack holds p's ancestors (each to be expanded without the child on
     // p's path), root at the bottom, with p's own leaf on top.
+    uint32_t* path = path_s[wib];
     int top = 0;
     if (lane == 0) {
       uint32_t a = lp;
-      uint32_t path[32];
       for (int l = 0; l < sh.levels; ++l) {
         path[l] = a;
         a /= F;
@@ -353,9 +367,8 @@ __global__ void __launch_bounds__(256) k_tree_query(const T* __restrict__ srows,
       int score = -1;
       // an ancestor of p's leaf (jump start) skips the child on p's path:
       // that subtree has been searched already
-      uint32_t own = lp;
-      for (int l = 1; l < lvl; ++l) own /= F;  // p's ancestor at level lvl - 1
-      const bool ancestor = own / F == idx;
+      const uint32_t own = path[lvl - 1];  // p's ancestor at level lvl - 1
+      const bool ancestor = path[lvl] == idx;
       if (lane < nc && !(ancestor && cidx0 + lane == own)) {
         const u64 cs = __ldg(tv.cs + c0 + lane);
         const uint32_t ci = __ldg(tv.ci + c0 + lane);

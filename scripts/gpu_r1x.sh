@@ -1,3 +1,5 @@
-python bench.py --config c5d4 --steps 5 --no-cpu 2>&1 | tail -1 | python -c "
-import json,sys; l=json.loads(sys.stdin.read()); print(l['ms_per_step'], l['stages_ms'], l['roofline']['kernel_ms'])"
-SKYCELL_TRACE=1 python bench.py --config c5d4 --steps 2 --warmup 3 --no-cpu 2>&1 | grep skycell | tail -24
+SKYCELL_TRACE=1 python bench.py --config c3 --steps 1 --warmup 1 --no-cpu 2>&1 | grep skycell | tail -14
+bash scripts/ncu_capture.sh prof_tree_c3_r2a k_tree_query 1 -- python bench.py --config c3 --steps 1 --warmup 1 --no-cpu
+python -c "
+import json; j=json.load(open('gpurun_out/prof_tree_c3_r2a.json')); m=j['metrics']
+print({k.split('.')[0]:m[k]['value'] for k in m})"
