@@ -898,6 +898,8 @@ struct CandParams {
   const void* d_cells;   // K1's D stream (cells of survivors a filter point removed), may be null
   const u64* d_count;
   int d_wide;
+  uint32_t head_start;   // first filter point of the branch-free head
+  int coop;              // run the warp-cooperative phase for points the head leaves
 };
 
 template <typename T, int D, typename TT, int THREADS>
@@ -961,12 +963,13 @@ __global__ void __launch_bounds__(THREADS) k_candidates(CandParams p) {
     // ~87% of the candidates at the headline config, tested branch-free by
     // every lane.
     constexpr uint32_t kHead0 = 8;
-    if (nf) {
-      const uint32_t h0 = nf < kHead0 ? nf : kHead0;
+    const uint32_t hs = p.head_start;
+    if (nf > hs) {
+      const uint32_t h0 = nf - hs < kHead0 ? nf - hs : kHead0;
       bool dom = false;
 #pragma unroll
       for (uint32_t f = 0; f < kHead0; ++f)
-        if (f < h0) dom |= dominates<T, D>(f_rows + (u64)f * D, v) && f_sum[f] < ps;
+        if (f < h0) dom |= dominates<T, D>(f_rows + (u64)(hs + f) * D, v) && f_sum[hs + f] < ps;
       keep = keep && !dom;
     }
     // The rest, one pending point at a time with the whole warp: first the
@@ -974,7 +977,7 @@ __global__ void __launch_bounds__(THREADS) k_candidates(CandParams p) {
     // shortest column prefix of F, 32 entries per step (a dominator f has
     // col_k(f) <= col_k(p) in every dimension).  A per-lane loop here ran
     // with ~5 of 32 lanes active (ncu: 68% of K4's instructions).
-    unsigned pend = __ballot_sync(kFull, keep && nf > kHead0);
+    unsigned pend = __ballot_sync(kFull, p.coop && keep && nf > hs + kHead0);
     while (pend) {
       const int src = __ffs(pend) - 1;
       pend &= pend - 1;
@@ -984,14 +987,14 @@ __global__ void __launch_bounds__(THREADS) k_candidates(CandParams p) {
       const u64 pps = __shfl_sync(kFull, ps, src);
       bool found;
       {
-        const uint32_t f = kHead0 + lane;
+        const uint32_t f = hs + kHead0 + lane;
         found = __any_sync(kFull, f < nf && f_sum[f] < pps && dominates<T, D>(f_rows + (u64)f * D, pv));
       }
       if (found) {
         if (lane == src) keep = false;
         continue;
       }
-      if (nf <= kHead0 + 32) continue;
+      if (nf <= hs + kHead0 + 32) continue;
       int bk = 0;
       unsigned end = 0xffffffffu;
 #pragma unroll
@@ -1195,7 +1198,6 @@ __global__ void k_list_hist(const T* __restrict__ rows, const uint32_t* __restri
     for (int k = 0; k < D; ++k) {
       const int c = list_col(v[k]);
       atomicAdd(&hist[k * kListStride + list_bin(sb, c) + 1], 1u);
-      atomicAdd(&hist[k * kListStride + kColBase + c + 1], 1u);
     }
   }
 }
@@ -1335,7 +1337,7 @@ struct ListQuery {
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       const int c = list_col(v[k]);
-      const unsigned e = __ldg(offs + k * kListStride + kColBase + c + 1);  // entries with col <= c
+      const unsigned e = __ldg(offs + k * kListStride + list_bin(0, c + 1));  // entries with col <= c (column-major bins)
       if (e < best) {
         best = e;
         bk = k;

@@ -50,6 +50,7 @@ struct DevCounters {
   u64 tkilled;    // ... removed by the champion prefilter (must follow tvalid)
   u64 dres;       // D-stream slots handed out (K1 filter-point head)
   u64 xd, xs_cap; // sample candidates (dense) / those entering the sample skyline (capped)
+  u64 pres, pkept;  // K4a -> K4b pending stream: slots handed out / points written
   u64 un, qend;   // union slots and own-slice end (sharded finish)
   u64 cand[kMaxLayers];
   u64 key[kMaxLayers];
@@ -79,12 +80,21 @@ inline void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw CudaFail{e, what};
 }
 
+// Grow-only scratch buffers.  Growth takes 25% headroom: data-dependent sizes
+// (survivor slot counts) vary slightly from query to query, and a cudaFree /
+// cudaMalloc pair inside a query would synchronise the device.
 void ensure(DevBuf& b, size_t bytes) {
   if (bytes == 0) bytes = 16;
   if (b.cap >= bytes) return;
   if (b.p) cudaFree(b.p);
   b.p = nullptr;
   b.cap = 0;
+  const size_t want = bytes + bytes / 4;
+  if (cudaMalloc(&b.p, want) == cudaSuccess) {
+    b.cap = want;
+    return;
+  }
+  cudaGetLastError();
   ck(cudaMalloc(&b.p, bytes), "cudaMalloc");
   b.cap = bytes;
 }
@@ -116,6 +126,7 @@ struct skycell_gpu_ctx {
   DevBuf s1_rows, s1_ids, s2_rows, s2_ids, s2_fsum, flags;
   DevBuf sky_rows, sky_ids, sky_fsum;  // local skyline (sharded)
   DevBuf d_cells;                      // K1's D stream
+  DevBuf p_rows, p_ids, p_fsum;        // K4a -> K4b pending points
   DevBuf q_bits, q_orig, q_sub, q_ids, q_mm;  // quadrant_skyline
   DevBuf t_keys, t_keys2, t_vals, t_vals2, t_cub, t_rows, t_ids, t_fsum, t_lo, t_hi, t_cs, t_ci;  // K5 tree
   DevBuf t_cm, t_kill;  // K5 tree champion prefilter
@@ -258,8 +269,8 @@ void run_exact(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uin
   uint32_t* lists = static_cast<uint32_t*>(ctx->lists.p);
   sk::k_list_hist<TOut, D><<<g, 256, 0, s>>>(trows, ids, fsum, count, hist);
   unsigned* totals = static_cast<unsigned*>(ctx->scan_tot.p);
-  sk::k_list_scan_sums<<<dim3(sk::kScanChunks, 2 * D), 1024, 0, s>>>(hist, D, totals);
-  sk::k_list_scan<<<dim3(sk::kScanChunks, 2 * D), 1024, 0, s>>>(hist, cursor, D, totals);
+  sk::k_list_scan_sums<<<dim3(sk::kScanChunks, D), 1024, 0, s>>>(hist, D, totals);
+  sk::k_list_scan<<<dim3(sk::kScanChunks, D), 1024, 0, s>>>(hist, cursor, D, totals);
   ++ctx->launches;
   sk::k_list_scatter<TOut, D><<<g, 256, 0, s>>>(trows, ids, fsum, count, cursor, lists, cap);
   const unsigned gw = (unsigned)std::max<u64>(1, std::min<u64>((cap * 32 + 255) / 256, (u64)nsm * 8));
@@ -771,16 +782,38 @@ struct Pipe final : PipeBase {
       pc.d_count = &c->dres;
       pc.d_wide = rho * D >= 32;
     }
-    if (wide) {
-      auto kc = sk::k_candidates<TOut, D, uint32_t, kThreads>;
-      ck(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pf), "smem attr");
-      kc<<<grid4, kThreads, smem_pf, s>>>(pc);
+    auto kc = wide ? sk::k_candidates<TOut, D, uint32_t, kThreads> : sk::k_candidates<TOut, D, uint8_t, kThreads>;
+    ck(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pf), "smem attr");
+    if (q.merge) {
+      // K4a: cell test + the 8 strongest filter points over S1 -> P (dense
+      // pending points, in the S1 buffers' twin); K4b: the rest of the filter
+      // over P, whose lanes are all pending (no idle lanes in the head test)
+      ensure(ctx->p_rows, cap1 * D * sizeof(TOut));
+      ensure(ctx->p_ids, cap1 * 4);
+      ensure(ctx->p_fsum, cap1 * 8);
+      sk::CandParams pa = pc;
+      pa.out_rows = ctx->p_rows.p;
+      pa.out_ids = static_cast<uint32_t*>(ctx->p_ids.p);
+      pa.out_fsum = static_cast<u64*>(ctx->p_fsum.p);
+      pa.out_reserved = &c->pres;
+      pa.kept = &c->pkept;
+      pa.coop = 0;
+      kc<<<grid4, kThreads, smem_pf, s>>>(pa);
+      sk::CandParams pb = pc;
+      pb.rows = ctx->p_rows.p;
+      pb.ids = static_cast<const uint32_t*>(ctx->p_ids.p);
+      pb.count = &c->pres;
+      pb.PM = nullptr;
+      pb.examined = nullptr;
+      pb.d_cells = nullptr;
+      pb.head_start = 8;
+      pb.coop = 1;
+      kc<<<grid4, kThreads, smem_pf, s>>>(pb);
+      ctx->launches += 2;
     } else {
-      auto kc = sk::k_candidates<TOut, D, uint8_t, kThreads>;
-      ck(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pf), "smem attr");
       kc<<<grid4, kThreads, smem_pf, s>>>(pc);
+      ++ctx->launches;
     }
-    ++ctx->launches;
   }
 
   // ---- K5 over S2 (the local point set)
@@ -1168,7 +1201,7 @@ void skycell_gpu_destroy(skycell_gpu_ctx* ctx) {
                     &ctx->s2_ids, &ctx->s2_fsum, &ctx->flags, &ctx->sky_rows, &ctx->sky_ids, &ctx->sky_fsum,
                     &ctx->q_bits, &ctx->q_orig, &ctx->q_sub, &ctx->q_ids, &ctx->q_mm, &ctx->t_keys,
                     &ctx->t_keys2, &ctx->t_vals, &ctx->t_vals2, &ctx->t_cub, &ctx->t_rows, &ctx->t_ids,
-                    &ctx->t_fsum, &ctx->t_lo, &ctx->t_hi, &ctx->t_cs, &ctx->t_ci, &ctx->long_q, &ctx->long_n, &ctx->scan_tot, &ctx->d_cells, &ctx->t_cm, &ctx->t_kill};
+                    &ctx->t_fsum, &ctx->t_lo, &ctx->t_hi, &ctx->t_cs, &ctx->t_ci, &ctx->long_q, &ctx->long_n, &ctx->scan_tot, &ctx->d_cells, &ctx->t_cm, &ctx->t_kill, &ctx->p_rows, &ctx->p_ids, &ctx->p_fsum};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (auto& e : ctx->ev)

@@ -1,5 +1,4 @@
-SKYCELL_TRACE=1 python bench.py --config c3 --steps 1 --warmup 1 --no-cpu 2>&1 | grep skycell | tail -14
-bash scripts/ncu_capture.sh prof_tree_c3_r2a k_tree_query 1 -- python bench.py --config c3 --steps 1 --warmup 1 --no-cpu
-python -c "
-import json; j=json.load(open('gpurun_out/prof_tree_c3_r2a.json')); m=j['metrics']
-print({k.split('.')[0]:m[k]['value'] for k in m})"
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2_r2e.csv python bench.py --config c2 --steps 1 --warmup 3 --no-cpu > /dev/null 2>&1; echo "launch c2 rc=$?"
+python scripts/ncu_summary.py list gpurun_out/launches_c2_r2e.csv gpurun_out/launches_c2_r2e.txt
+for c in c1 c2 c3; do python bench.py --config $c --steps 10 --no-cpu 2>&1 | tail -1 | python -c "
+import json,sys; l=json.loads(sys.stdin.read()); print('$c', l['ms_per_step'], l['stages_ms'])"; done
