@@ -42,7 +42,10 @@ def shard_range(n_total: int, rank: int, world: int) -> tuple[int, int]:
 class ShardedSkyline:
     """Runs the phase API of one engine against the other ranks of `group`."""
 
-    def __init__(self, engine, group=None, device=None):
+    def __init__(self, engine, group=None, device=None, coll_device=None):
+        """`device` holds the engine's exchange buffers; `coll_device` (default:
+        the same) is where the collectives run.  They differ only in tests that
+        drive real engines over gloo (CPU collectives, buffers staged)."""
         self.eng = engine
         self.group = group
         self.rank = dist.get_rank(group)
@@ -50,7 +53,16 @@ class ShardedSkyline:
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu")
         self.device = torch.device(device)
+        self.coll_device = torch.device(coll_device) if coll_device is not None else self.device
         self._bufs: dict[str, torch.Tensor] = {}
+
+    def _all_gather(self, out: torch.Tensor, inp: torch.Tensor) -> None:
+        if self.coll_device == out.device:
+            dist.all_gather_into_tensor(out, inp, group=self.group)
+            return
+        o = torch.empty(out.shape, dtype=out.dtype, device=self.coll_device)
+        dist.all_gather_into_tensor(o, inp.to(self.coll_device), group=self.group)
+        out.copy_(o)
 
     def _buf(self, name: str, nbytes: int) -> torch.Tensor:
         b = self._bufs.get(name)
@@ -60,8 +72,8 @@ class ShardedSkyline:
         return b[:nbytes]
 
     def _gather_counts(self, value: int) -> list[int]:
-        t = torch.tensor([value], dtype=torch.int64, device=self.device)
-        out = torch.empty(self.world, dtype=torch.int64, device=self.device)
+        t = torch.tensor([value], dtype=torch.int64, device=self.coll_device)
+        out = torch.empty(self.world, dtype=torch.int64, device=self.coll_device)
         dist.all_gather_into_tensor(out, t, group=self.group)
         return [int(v) for v in out.cpu().tolist()]
 
@@ -87,7 +99,7 @@ class ShardedSkyline:
         occ = self._buf("occ", occ_bytes)
         self.eng.shard_export_occ(occ)
         gathered = self._buf("occ_all", world * occ_bytes)
-        dist.all_gather_into_tensor(gathered, occ, group=self.group)
+        self._all_gather(gathered, occ)
 
         # phase 2: prune against the global occupancy, local skyline
         try:
@@ -101,7 +113,7 @@ class ShardedSkyline:
         send = self._buf("send", bb)
         self.eng.shard_pack(send, maxc)
         recv = self._buf("recv", world * bb)
-        dist.all_gather_into_tensor(recv, send, group=self.group)
+        self._all_gather(recv, send)
 
         # phase 3: own local skyline against the union
         if ids_out is None:
@@ -133,7 +145,7 @@ class ShardedSkyline:
         pad = torch.full((max(maxk, 1),), -1, dtype=torch.int32, device=self.device)
         pad[: local.numel()] = local
         allp = torch.empty(self.world * pad.numel(), dtype=torch.int32, device=self.device)
-        dist.all_gather_into_tensor(allp, pad, group=self.group)
+        self._all_gather(allp, pad)
         if self.rank != root:
             return ids
         allp = allp.view(self.world, -1)

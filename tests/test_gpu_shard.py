@@ -112,3 +112,44 @@ def test_nccl_world1(oracle):
         eng.close()
     finally:
         dist.destroy_process_group()
+
+
+def _real_worker(rank, world, port, cases, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.oracle import Oracle, quantize_f32
+        torch.cuda.set_device(0)
+        orc = Oracle()
+        eng = sky.Engine(0)
+        runner = ShardedSkyline(eng, device="cuda:0", coll_device="cpu")
+        for dist_id, n, d in cases:
+            x = quantize_f32(orc.generate(dist_id, n, d, 11 + n))
+            rho = sky.default_rho(n, d)
+            b, e = shard_range(n, rank, world)
+            res = runner.skyline(x[b:e].copy(), e - b, d, np.zeros(d), np.ones(d), rho, b)
+            if rank == 0:
+                want = orc.compute_skyline(x.astype(np.float64), np.zeros(d), np.ones(d), rho)
+                q.put((bool(np.array_equal(res.ids, want.ids)), res.points_examined == want.points_examined,
+                       res.layers.keys == want.keys and res.layers.candidates == want.candidates))
+        eng.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_real_engines_multi_process(world):
+    """The whole multi-rank protocol with real engines (one process per rank,
+    all on cuda:0) -- dist.py's collectives over gloo with staged buffers."""
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cases = [(0, 300_000, 4), (1, 200_000, 4), (2, 50_000, 5)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.start_processes(_real_worker, args=(world, port, cases, q), nprocs=world, start_method="spawn")
+    for case in cases:
+        ok_ids, ok_ex, ok_layers = q.get(timeout=120)
+        assert ok_ids and ok_ex and ok_layers, case
