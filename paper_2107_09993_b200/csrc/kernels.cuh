@@ -352,13 +352,21 @@ __device__ __forceinline__ uint32_t mag_col(float u, float scale) {
 // per tile); their layer-rho cells are marked with fire-and-forget red.or.
 // RHO > 0 (f32 identity path) fixes rho and la at compile time so every index
 // is a constant-weight IMAD chain; RHO == 0 is the general runtime path.
-template <typename TIn, typename TOut, int D, bool IDENT, int THREADS, int PPT, int RHO, int MINB = 3>
+// REC_LA (identity path with fixed RHO): dropped points record their level-la
+// cell -- its index is the H lookup's index plus c_0, no second set of
+// digits -- in a per-CTA 2^(la d)-bit shared bitmap (128 KB at d = 4, la = 5,
+// so one 768-thread CTA per SM).  Otherwise they record their level la-1 cell.
+template <typename TIn, typename TOut, int D, bool IDENT, int THREADS, int PPT, int RHO, int MINB = 3, bool REC_LA = false>
 __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
   static_assert(PPT <= 8, "survivor codes are (j * 32 + lane) in one byte");
   extern __shared__ __align__(16) uint8_t sm[];
   uint32_t* occ_s = reinterpret_cast<uint32_t*>(sm);
   uint8_t* H_s = sm + ((p.lo_words * 4 + 15) & ~15u);
   uint8_t* code_w = H_s + ((p.h_entries + 15) & ~15u) + (threadIdx.x >> 5) * (32 * PPT);  // survivor codes
+  // survivor rows staged per warp (32 * PPT rows), after the codes and the filter head
+  TIn* rows_w = reinterpret_cast<TIn*>(H_s + ((p.h_entries + 15) & ~15u) + THREADS * PPT +
+                                       ((kK1Head * (D * sizeof(TOut) + 8) + 15) & ~(size_t)15)) +
+                (size_t)(threadIdx.x >> 5) * (32 * PPT) * D;
   TOut* fh_rows = reinterpret_cast<TOut*>(H_s + ((p.h_entries + 15) & ~15u) + THREADS * PPT);
   u64* fh_sum = reinterpret_cast<u64*>(fh_rows + kK1Head * D);
   uint32_t nfh = 0;
@@ -394,7 +402,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
   uint32_t hcorr = 0, locorr = 0;
   for (int k = D - 1; k >= 1; --k) hcorr = hcorr * mul_a + 0x4B000000u;
   for (int k = D - 1; k >= 0; --k) locorr = locorr * mul_lo + 0x4B000000u;
-  const bool rec_lo = la >= 2;
+  const bool rec_lo = !REC_LA && la >= 2;
   WarpOut wo{0, p.chunk, p.chunk};
   auto stamp = [&](u64 slot) { p.out_ids[slot] = kNoId; };
   unsigned kept = 0;
@@ -406,24 +414,18 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
     else static_cast<uint32_t*>(p.d_cells)[slot] = ~0u;
   };
 
-  TIn raw[PPT][D];
-  auto load_tile = [&](uint32_t t) {
+  // Two register buffers in ping-pong: the next tile's loads are in flight
+  // while the current one is processed, with no register copies between them
+  // (a copying double buffer cost ~7% of K1's instructions, ncu).
+  TIn buf_a[PPT][D], buf_b[PPT][D];
+  auto load_tile = [&](TIn (&raw)[PPT][D], uint32_t t) {
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
       const uint32_t i = t * WT + j * 32 + lane;
       if (t < nfull || i < n) load_row<TIn, D>(coords, i, raw[j]);
     }
   };
-  uint32_t t = gw;
-  if (t < ntiles) load_tile(t);
-  while (t < ntiles) {
-    TIn cur[PPT][D];
-#pragma unroll
-    for (int j = 0; j < PPT; ++j)
-#pragma unroll
-      for (int k = 0; k < D; ++k) cur[j][k] = raw[j][k];
-    const uint32_t tn = t + nw;
-    if (tn < ntiles) load_tile(tn);  // prefetch: in flight while this tile is processed
+  auto process = [&](TIn (&cur)[PPT][D], uint32_t t) {
     const bool full = t < nfull;
     const uint32_t base = t * WT + lane;
     bool keep[PPT];
@@ -435,11 +437,11 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
       if constexpr (IDENT) {
         // u = min(max(v, 0), 1 - 2^-24): every column stays below 2^L (the
         // reference clamps to 1 - 2^-32, whose column is also 2^L - 1); NaN -> 0
-        float probe = 0.0f;
+        float probe = cur[j][D - 1];
         uint32_t hidx = 0, lo = 0;
 #pragma unroll
         for (int k = D - 1; k >= 1; --k) {
-          probe += cur[j][k];
+          if (k != D - 1) probe += cur[j][k];
           const float u = fminf(fmaxf(cur[j][k], 0.0f), 0x1.fffffep-1f);
           hidx = hidx * mul_a + mag_col(u, fs_a);
           if (rec_lo) lo = lo * mul_lo + mag_col(u, fs_lo);
@@ -449,7 +451,11 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
         const int c0 = (int)(mag_col(u0, fs_a) - 0x4B000000u);
         bad |= !isfinite(probe);
         fail_a = c0 > (int)H_s[hidx - hcorr];
-        if (valid && fail_a && rec_lo) set_bit_shared(occ_s, lo * mul_lo + mag_col(u0, fs_lo) - locorr);
+        if constexpr (REC_LA) {
+          if (valid && fail_a) set_bit_shared(occ_s, (hidx - hcorr) * mul_a + (uint32_t)c0);
+        } else {
+          if (valid && fail_a && rec_lo) set_bit_shared(occ_s, lo * mul_lo + mag_col(u0, fs_lo) - locorr);
+        }
       } else {
         TIn sum = cur[j][0];
 #pragma unroll
@@ -484,7 +490,11 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
         unsigned cum = 0;
 #pragma unroll
         for (int j = 0; j < PPT; ++j) {
-          if (keep[j]) code_w[cum + __popc(mk[j] & lt)] = (uint8_t)(j * 32 + lane);
+          if (keep[j]) {
+            const unsigned sl = cum + __popc(mk[j] & lt);
+            code_w[sl] = (uint8_t)(j * 32 + lane);
+            store_row<TIn, D>(rows_w, sl, cur[j]);
+          }
           cum += __popc(mk[j]);
         }
       }
@@ -495,15 +505,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
         const unsigned cd = act ? code_w[sidx] : 0u;
         const int sj = (int)(cd >> 5), src = (int)(cd & 31);
         TIn x[D];
-#pragma unroll
-        for (int k = 0; k < D; ++k) x[k] = cur[0][k];
-#pragma unroll
-        for (int jj = 0; jj < PPT; ++jj)
-#pragma unroll
-          for (int k = 0; k < D; ++k) {
-            const TIn tv = __shfl_sync(kFull, cur[jj][k], src);
-            if (sj == jj) x[k] = tv;
-          }
+        load_row_cached<TIn, D>(rows_w, act ? sidx : 0u, x);  // staged in shared memory
         TOut u[D];
         int c[D];
 #pragma unroll
@@ -581,6 +583,18 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
         if (i < n && !fin) atomicMax(p.nonfinite, ~(u64)i);
       }
     }
+  };
+  uint32_t t = gw;
+  if (t < ntiles) load_tile(buf_a, t);
+  while (t < ntiles) {
+    uint32_t tn = t + nw;
+    if (tn < ntiles) load_tile(buf_b, tn);
+    process(buf_a, t);
+    t = tn;
+    if (t >= ntiles) break;
+    tn = t + nw;
+    if (tn < ntiles) load_tile(buf_a, tn);
+    process(buf_b, t);
     t = tn;
   }
   warp_close(wo, stamp);
@@ -635,6 +649,83 @@ __global__ void k_rowmin_prefix1(const uint32_t* __restrict__ bits, int L, int d
       run = best < run ? best : run;
       R[r] = run;
     }
+  }
+}
+
+// Row minima only, one thread per row (for grids with few dimension-1 lines,
+// e.g. d = 2, where k_rowmin_prefix1 would run on a handful of threads).
+template <typename TT>
+__global__ void k_rowmin(const uint32_t* __restrict__ bits, int L, u64 rows, TT* __restrict__ R) {
+  const int rowbits = 1 << L;
+  for (u64 r = blockIdx.x * (u64)blockDim.x + threadIdx.x; r < rows; r += (u64)gridDim.x * blockDim.x) {
+    TT best = (TT)~(TT)0;
+    if (L >= 5) {
+      const u64 wpr = (u64)rowbits >> 5;
+      for (u64 w = 0; w < wpr; ++w) {
+        const uint32_t x = __ldg(bits + r * wpr + w);
+        if (x) {
+          best = (TT)(w * 32 + __ffs(x) - 1);
+          break;
+        }
+      }
+    } else {
+      const int rpw = 32 >> L;
+      const uint32_t x = (__ldg(bits + r / rpw) >> ((r % rpw) * rowbits)) & ((1u << rowbits) - 1);
+      if (x) best = (TT)(__ffs(x) - 1);
+    }
+    R[r] = best;
+  }
+}
+
+// Inclusive prefix-min along dimension k of the (d-1)-dim table with one CTA
+// per line (few, long lines): each thread scans a contiguous run, one block
+// scan of the run minima, then the runs are rewritten.
+template <typename TT>
+__global__ void __launch_bounds__(1024) k_prefix_min_cta(TT* __restrict__ R, int L, int k, u64 lines) {
+  __shared__ TT wmin[32];
+  const u64 stride = 1ull << (L * (k - 1));
+  const int n = 1 << L;
+  const int per = (n + 1023) / 1024;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (u64 line = blockIdx.x; line < lines; line += gridDim.x) {
+    const u64 low = line & (stride - 1);
+    const u64 high = line >> (L * (k - 1));
+    const u64 base = (high << (L * k)) + low;
+    const int c0 = threadIdx.x * per, c1 = min(c0 + per, n);
+    TT run = (TT)~(TT)0;
+    for (int c = c0; c < c1; ++c) {
+      const TT v = R[base + (u64)c * stride];
+      run = v < run ? v : run;
+    }
+    // exclusive prefix-min of the run minima
+    TT incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const TT y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl = y < incl ? y : incl;
+    }
+    if (lane == 31) wmin[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      TT t = wmin[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const TT y = __shfl_up_sync(kFull, t, o);
+        if (lane >= o) t = y < t ? y : t;
+      }
+      wmin[lane] = t;
+    }
+    __syncthreads();
+    TT carry = (TT)~(TT)0;
+    if (warp > 0) carry = wmin[warp - 1];
+    const TT prev = __shfl_up_sync(kFull, incl, 1);
+    if (lane > 0) carry = prev < carry ? prev : carry;
+    for (int c = c0; c < c1; ++c) {
+      const TT v = R[base + (u64)c * stride];
+      carry = v < carry ? v : carry;
+      R[base + (u64)c * stride] = carry;
+    }
+    __syncthreads();
   }
 }
 
@@ -1455,17 +1546,24 @@ __global__ void __launch_bounds__(256) k_allpairs_long(const T* __restrict__ row
       const unsigned nsteps = (s1 - s0 + 31) / 32;
       // this warp's steps of the column: g + k with (g + k) % nw == warp
       unsigned k = (unsigned)((warp - (int)(g % nw) + nw) % nw);
+      // the early-exit flag goes through shared atomics (a race by design,
+      // kept visible to compute-sanitizer racecheck as synchronised access)
+      auto seen = [&]() {
+        int f = 0;
+        if (lane == 0) f = atomicAdd(&found, 0);
+        return __shfl_sync(kFull, f, 0) != 0;
+      };
       for (; k < nsteps; k += nw) {
-        if (*(volatile int*)&found) break;
+        if (seen()) break;
         const unsigned e = s0 + k * 32 + lane;
         const bool d_l = e < s1 && Q.test(rows, ids, fsum, lst, e, cell_level, ctop);
         if (__any_sync(kFull, d_l)) {
-          if (lane == 0) found = 1;
+          if (lane == 0) atomicExch(&found, 1);
           break;
         }
       }
       g += nsteps;
-      if (*(volatile int*)&found) break;
+      if (seen()) break;
     }
     __syncthreads();
     if (threadIdx.x == 0) flag[i] = found ? 0 : 1;

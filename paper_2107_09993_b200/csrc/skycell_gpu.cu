@@ -236,10 +236,23 @@ void launch_tables(skycell_gpu_ctx* ctx, cudaStream_t s, const uint32_t* bits, i
   auto grid_for = [&](u64 items) {
     return (unsigned)std::max<u64>(1, std::min<u64>((items + 127) / 128, (u64)nsm * 16));
   };
-  sk::k_rowmin_prefix1<TT><<<grid_for(lines1), 128, 0, s>>>(bits, L, d, lines1, table);
+  // enough dimension-1 lines to fill the GPU: one thread per line; else
+  // (d = 2, or d = 3 at fine layers) row minima per thread + a CTA per line
+  if (lines1 >= (u64)nsm * 128 || L <= 6) {
+    sk::k_rowmin_prefix1<TT><<<grid_for(lines1), 128, 0, s>>>(bits, L, d, lines1, table);
+    ++ctx->launches;
+    for (int k = 2; k < d; ++k) {
+      sk::k_prefix_min<TT><<<grid_for(lines1), 128, 0, s>>>(table, L, k, lines1);
+      ++ctx->launches;
+    }
+    return;
+  }
+  sk::k_rowmin<TT><<<grid_for(rows), 128, 0, s>>>(bits, L, rows, table);
   ++ctx->launches;
-  for (int k = 2; k < d; ++k) {
-    sk::k_prefix_min<TT><<<grid_for(lines1), 128, 0, s>>>(table, L, k, lines1);
+  for (int k = 1; k < d; ++k) {
+    const unsigned g = (unsigned)std::min<u64>(lines1, (u64)nsm * 2);
+    if (lines1 >= (u64)nsm * 128) sk::k_prefix_min<TT><<<grid_for(lines1), 128, 0, s>>>(table, L, k, lines1);
+    else sk::k_prefix_min_cta<TT><<<g, 1024, 0, s>>>(table, L, k, lines1);
     ++ctx->launches;
   }
 }
@@ -451,6 +464,16 @@ struct Pipe final : PipeBase {
   size_t tt;
   u64 table_entries;
   static constexpr int kStreamThreads = 256;
+  static constexpr int kRecLaThreads = 768;
+  // the shape with a record-at-la K1 instance (the headline: d = 4, rho = 6, la = 5)
+  static bool rec_la_shape(int r) {
+    // measured slower than the 3 x 256-thread instance (516 vs 445 us at C2):
+    // kept as an opt-in experiment (SKYCELL_RECLA=1)
+    if constexpr (IDENT && D == 4) return r == 6 && std::getenv("SKYCELL_RECLA") != nullptr;
+    return false;
+  }
+  int k1_threads = kStreamThreads;
+  bool rec_la = false;
   static constexpr int PPT1 = std::max(1, ppt_for<TIn, D>() / 2);
   static constexpr unsigned kChunk1 = 256, kChunk4 = 64;
   static_assert(kChunk1 >= 32 * PPT1, "a stream tile's survivors must fit one output chunk");
@@ -476,6 +499,8 @@ struct Pipe final : PipeBase {
 
   static auto pick_stream(int rho) {
     if constexpr (IDENT && D <= 8) {
+      if constexpr (D == 4)
+        if (rec_la_shape(rho)) return sk::k_stream<TIn, TOut, D, IDENT, kRecLaThreads, PPT1, 6, 1, true>;
       switch (rho) {
         case 1: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 1>;
         case 2: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 2>;
@@ -496,22 +521,26 @@ struct Pipe final : PipeBase {
     test_b = rho > la;
     m = std::min<u64>(n, 1ull << 20);
     h_entries = (uint32_t)(1ull << (u64)(la * (D - 1)));
-    lo_words = la >= 2 ? (uint32_t)words_at(la - 1) : 0;
+    rec_la = rec_la_shape(rho);
+    k1_threads = rec_la ? kRecLaThreads : kStreamThreads;
+    lo_words = rec_la ? (uint32_t)words_at(la) : (la >= 2 ? (uint32_t)words_at(la - 1) : 0);
     wide = rho > 7;
     tt = wide ? 4 : 1;
     table_entries = 1ull << (u64)(rho * (D - 1));
 
     // K1 geometry: persistent warps over round-robin warp tiles
-    smem1 = (((size_t)lo_words * 4 + 15) & ~(size_t)15) + ((h_entries + 15) & ~15u) + (size_t)kStreamThreads * PPT1 +
-            (size_t)sk::kK1Head * (D * sizeof(TOut) + 8) + 16;
+    smem1 = (((size_t)lo_words * 4 + 15) & ~(size_t)15) + ((h_entries + 15) & ~15u) + (size_t)k1_threads * PPT1 +
+            (((size_t)sk::kK1Head * (D * sizeof(TOut) + 8) + 15) & ~(size_t)15) +
+            (size_t)k1_threads * PPT1 * D * sizeof(TIn) + 16;
     kstream = pick_stream(rho);
     ck(cudaFuncSetAttribute(kstream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1), "smem attr");
     int occ_blocks = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_blocks, kstream, kStreamThreads, smem1), "occupancy");
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_blocks, kstream, k1_threads, smem1), "occupancy");
     occ_blocks = std::max(1, occ_blocks);
     const u64 wtiles = (n + 32 * PPT1 - 1) / (32 * PPT1);
-    grid1 = (int)std::max<u64>(1, std::min<u64>((wtiles + 7) / 8, (u64)nsm * occ_blocks));
-    cap1 = n + (u64)grid1 * (kStreamThreads / 32) * kChunk1;
+    const u64 wpc = (u64)k1_threads / 32;
+    grid1 = (int)std::max<u64>(1, std::min<u64>((wtiles + wpc - 1) / wpc, (u64)nsm * occ_blocks));
+    cap1 = n + (u64)grid1 * (k1_threads / 32) * kChunk1;
 
     // K4 geometry
     grid4 = nsm * 4;
@@ -697,13 +726,14 @@ struct Pipe final : PipeBase {
       p1.d_reserved = &c->dres;
     }
     if (q.timed) ck(cudaEventRecord(ctx->ev[4], s), "event");
-    kstream<<<grid1, kStreamThreads, smem1, s>>>(p1);
+    kstream<<<grid1, k1_threads, smem1, s>>>(p1);
     ++ctx->launches;
     if (q.timed) ck(cudaEventRecord(ctx->ev[5], s), "event");
     if (lo_words) {
       const unsigned gx = (unsigned)std::max<u64>(1, std::min<u64>((lo_words + 255) / 256, (u64)nsm * 8));
       const unsigned gy = (unsigned)std::max<u64>(1, std::min<u64>(32, (u64)nsm * 4 / gx));
-      sk::k_reduce_slabs<<<dim3(gx, gy), 256, 0, s>>>(static_cast<uint32_t*>(ctx->slabs.p), grid1, lo_words, occ(la - 1));
+      sk::k_reduce_slabs<<<dim3(gx, gy), 256, 0, s>>>(static_cast<uint32_t*>(ctx->slabs.p), grid1, lo_words,
+                                                       occ(rec_la ? la : la - 1));
       ++ctx->launches;
     }
     if (q.timed) ck(cudaEventRecord(ctx->ev[1], s), "event");

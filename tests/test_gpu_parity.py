@@ -226,3 +226,15 @@ def test_gpu_fine_grids_vs_oracle(engine, oracle, d, rho):
             want = oracle.compute_skyline(x.astype(np.float64), mn, mx, rho)
             got = engine.compute_skyline(sky.Dataset(np.ascontiguousarray(x), mn, mx), rho)
             check(got, want.ids, want.points_examined, want.keys, want.candidates)
+
+
+@pytest.mark.parametrize("dist", [0, 1])
+def test_gpu_f64_general_path_large(engine, oracle, dist):
+    """The general FP64 path (device-side normalisation with the host's
+    scale, dataset.cpp:32-45) at a size where every kernel runs at scale."""
+    v = oracle.generate(dist, 3_000_000, 4, 21)
+    x = v * 10.0 - 3.0
+    mn, mx = x.min(0), x.max(0)
+    want = oracle.compute_skyline(x, mn, mx, 5)
+    got = engine.compute_skyline(sky.Dataset(x, mn, mx), 5)
+    check(got, want.ids, want.points_examined, want.keys, want.candidates)
