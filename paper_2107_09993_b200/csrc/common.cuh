@@ -1,12 +1,12 @@
 // Device-side building blocks shared by the SkyCell kernels (sm_100a).
 //
-//  * ordered tile claiming + decoupled look-back prefix (stable, single-pass
-//    stream compaction: survivors keep input order, so record ids leave every
-//    stage ascending and the final result needs no sort -- refine.cpp:101-103
-//    sorts on the CPU);
+//  * per-warp output chunks (unordered survivor streams; the final ids are
+//    put back in ascending order once, through an id bitmap -- refine.cpp:
+//    101-103 sorts on the CPU instead);
 //  * the point dominance predicate (dataset.hpp:55-62) and the sort-first
 //    precedence order (refine.cpp:38-41) used by every dominance kernel;
-//  * grid-cell arithmetic (grid.cpp:10-16, cell.hpp:102-107).
+//  * grid-cell arithmetic (grid.cpp:10-16, cell.hpp:102-107) and
+//    check-before-set occupancy bits.
 #pragma once
 
 #include <cstdint>
@@ -19,93 +19,6 @@ constexpr double kUnitUpperBound = 1.0 - 0x1p-32;  // dataset.hpp:15
 constexpr unsigned kFull = 0xffffffffu;
 
 typedef unsigned long long u64;
-
-// ---------------------------------------------------------------- memory order
-// Look-back status words are self-contained (flag and value in one 64-bit
-// word) and publish nothing else, so relaxed gpu-scope accesses suffice.  An
-// acquire load would compile to CCTL.IVALL (a full L1 invalidate) per spin
-// iteration -- measured at 45% of K1's stall samples before this change.
-__device__ __forceinline__ void st_status(u64* p, u64 v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ u64 ld_status(const u64* p) {
-  u64 v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// --------------------------------------------------------- mbarrier / TMA
-// Thin wrappers over the Hopper+/Blackwell async-copy primitives used by the
-// streaming kernel: a 1-D bulk copy global -> shared (cp.async.bulk, SASS
-// UBLKCP) that completes a transaction count on an mbarrier.
-__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void fence_barrier_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar))
-      : "memory");
-}
-
-// ------------------------------------------------------- decoupled look-back
-// Status word per tile: bits 62-63 flag (0 empty, 1 aggregate, 2 inclusive
-// prefix), bits 0-61 value.  Status arrays are zeroed once per query.
-constexpr u64 kFlagAgg = 1ull << 62;
-constexpr u64 kFlagInc = 2ull << 62;
-constexpr u64 kValMask = (1ull << 62) - 1;
-
-// Called by all 32 lanes of one warp.  Publishes `agg` for `tile` and returns
-// the exclusive prefix over tiles [0, tile).
-__device__ __forceinline__ u64 warp_lookback(u64* status, u64 tile, u64 agg) {
-  const int lane = threadIdx.x & 31;
-  if (tile == 0) {
-    if (lane == 0) st_status(&status[0], kFlagInc | agg);
-    return 0;
-  }
-  if (lane == 0) st_status(&status[tile], kFlagAgg | agg);
-  u64 excl = 0;
-  long long base = (long long)tile - 1;
-  while (true) {
-    const long long t = base - lane;
-    u64 s;
-    if (t >= 0) {
-      do { s = ld_status(&status[t]); } while ((s >> 62) == 0);
-    } else {
-      s = kFlagInc;  // virtual predecessor with inclusive prefix 0
-    }
-    const unsigned inc = __ballot_sync(kFull, (s >> 62) == 2);
-    const int stop = inc ? __ffs(inc) - 1 : 31;
-    u64 v = (lane <= stop) ? (s & kValMask) : 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-    excl += v;
-    if (inc) break;
-    base -= 32;
-  }
-  if (lane == 0) st_status(&status[tile], kFlagInc | (excl + agg));
-  return excl;
-}
 
 // ------------------------------------------------ unordered warp output
 // Survivor streams that need no order are written through per-warp output
@@ -152,55 +65,6 @@ template <typename Stamp>
 __device__ __forceinline__ void warp_close(WarpOut& wo, Stamp stamp) {
   const int lane = threadIdx.x & 31;
   for (unsigned s = wo.fill + lane; s < wo.chunk; s += 32) stamp(wo.base + s);
-}
-
-// Block-wide stable ranks for PPT flags per thread laid out point-major:
-// point (j, t) precedes (j', t') iff j < j' or (j == j' and t < t').
-// scratch: PPT*NW + 1 u32 in shared memory.  Returns the block total; rank[j]
-// is the exclusive position of flag j (valid only where flag[j]).
-template <int THREADS, int PPT>
-__device__ __forceinline__ unsigned block_ranks(const bool (&flag)[PPT], unsigned (&rank)[PPT],
-                                                unsigned* scratch) {
-  constexpr int NW = THREADS / 32;
-  constexpr int M = PPT * NW;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned lt = (1u << lane) - 1;
-#pragma unroll
-  for (int j = 0; j < PPT; ++j) {
-    const unsigned m = __ballot_sync(kFull, flag[j]);
-    rank[j] = __popc(m & lt);
-    if (lane == 0) scratch[j * NW + warp] = __popc(m);
-  }
-  __syncthreads();
-  if (warp == 0) {
-    constexpr int PER = (M + 31) / 32;
-    unsigned loc[PER];
-    unsigned sum = 0;
-#pragma unroll
-    for (int e = 0; e < PER; ++e) {
-      const int idx = lane * PER + e;
-      loc[e] = idx < M ? scratch[idx] : 0;
-      sum += loc[e];
-    }
-    unsigned incl = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned y = __shfl_up_sync(kFull, incl, o);
-      if (lane >= o) incl += y;
-    }
-    unsigned run = incl - sum;
-#pragma unroll
-    for (int e = 0; e < PER; ++e) {
-      const int idx = lane * PER + e;
-      if (idx < M) scratch[idx] = run;
-      run += loc[e];
-    }
-    if (lane == 31) scratch[M] = incl;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < PPT; ++j) rank[j] += scratch[j * NW + warp];
-  return scratch[M];
 }
 
 // ------------------------------------------------------------- dominance
@@ -253,10 +117,6 @@ __device__ __forceinline__ int cell_col(double u, double scale, int top) {
   return min(max(c, 0), top);
 }
 
-__device__ __forceinline__ bool test_bit(const uint32_t* bits, u64 idx) {
-  return (bits[idx >> 5] >> (idx & 31)) & 1u;
-}
-
 // Check-before-set: dense data re-hits the same words millions of times
 // (SURVEY §7 hard part 5); a plain L2 load turns those into hits.
 __device__ __forceinline__ void set_bit_global(uint32_t* bits, u64 idx) {
@@ -273,10 +133,6 @@ __device__ __forceinline__ void set_bit_cached(uint32_t* bits, u64 idx) {
   uint32_t v;
   asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(v) : "l"(w));
   if (!(v & m)) asm volatile("red.global.or.b32 [%0], %1;" ::"l"(w), "r"(m) : "memory");
-}
-// Fire-and-forget (red.global.or): no result to wait for.
-__device__ __forceinline__ void red_or_global(uint32_t* bits, u64 idx) {
-  asm volatile("red.global.or.b32 [%0], %1;" ::"l"(bits + (idx >> 5)), "r"(1u << (idx & 31)) : "memory");
 }
 __device__ __forceinline__ void set_bit_shared(uint32_t* bits, uint32_t idx) {
   const uint32_t m = 1u << (idx & 31);

@@ -1,30 +1,27 @@
 // SkyCell skyline kernels for B200 (sm_100a).
 //
-// Stage map (DESIGN.md §3 has the roofline of each):
-//   K0  k_sample_occ / k_build_filter  occupancy of a point sample at a coarse
-//                                       level Lf, turned into a per-row height
-//                                       table H: a point whose level-Lf cell is
-//                                       strictly dominated by an occupied
-//                                       sample cell cannot be in a candidate
-//                                       cell, so it is dropped
-//                                       in the single streaming pass.
+// Stage map (DESIGN.md §3 has the bound and the algorithmic bytes of each):
+//   K0  k_sample / k_build_filter /     a sample's occupancy at a coarse level la
+//       sample tables, sample skyline   -> height table H (a point whose level-la
+//       -> k_strength_order,            cell is strictly dominated by an occupied
+//          k_filter_lists               sample cell cannot be in a candidate
+//                                       cell); the sample's skyline
+//                                       -> the filter points F of K4.
 //   K1  k_stream                        THE HBM-bound pass: normalize (dataset.cpp:
 //                                       22-50), point_to_cell (grid.cpp:10-16),
-//                                       occupancy at layers rho and rho-1
-//                                       (grid.cpp:78-102), sample filter, stable
-//                                       compaction of survivors.  Reads every
+//                                       occupancy (grid.cpp:78-102), the H test,
+//                                       survivors compacted to S1.  Reads every
 //                                       coordinate exactly once.
-//   K3  k_rowmin / k_prefix_min /       cell pruning as a d-dimensional prefix-OR,
-//       k_count_cells / k_downsample    expressed as a row-min + (d-1)-dim prefix-
-//                                       min table; per-layer |KS_i|, |CS_i|
-//                                       (replaces shrink_seq.cpp:87-231 and
-//                                       shrink_par.cpp:179-278).
-//   K4  k_candidates                    survivors in candidate cells (refine.cpp:
-//                                       78-96), points_examined.
-//   K5  k_filter_append / k_allpairs /  exact sort-first dominance (refine.cpp:31-
-//       k_compact                       59, 98-99) by a block-recursive filter:
-//                                       skyline of a prefix filters the rest.
-//   K6  ids leave K5 ascending (stable compaction everywhere).
+//   K3  k_rowmin_prefix1 / k_rowmin /   cell pruning as a d-dimensional prefix-OR,
+//       k_prefix_min / k_count_rows /   stored as a (d-1)-dim prefix-min table;
+//       k_downsample*                   per-layer |KS_i|, |CS_i| (replaces
+//                                       shrink_seq.cpp:87-231, shrink_par.cpp:179-278).
+//   K4  k_candidates (K4a, K4b)         survivors in candidate cells (points_examined,
+//                                       refine.cpp:90-96) not dominated by F.
+//   K5  k_list_* / k_allpairs_lists /   exact sort-first dominance (refine.cpp:31-59,
+//       k_allpairs_long, or tree.cuh    98-99): column lists for small sets, the
+//                                       dominance tree for large ones.
+//   K6  k_mark_ids / k_bits_*           ascending ids through an id bitmap.
 #pragma once
 
 #include <cub/block/block_radix_sort.cuh>
@@ -763,64 +760,7 @@ __global__ void k_prefix_min(TT* __restrict__ R, int L, int k, u64 lines) {
 //   key (grid) = occupied && no top column && !OR_k (c_k >= 1 && P[c - e_k])  (Def. 4)
 // Key counts add the d auxiliary cells (cell.hpp:35-40).  Checked against
 // baseline.cpp:76-157 (via the oracle) by tests/test_gpu_parity.py.
-template <typename TT>
-__device__ __forceinline__ bool cell_strictly_dominated(const TT* __restrict__ PM, const int* col, int d, int L) {
-  u64 idx = 0;
-  bool ok = col[0] >= 1;
-  for (int k = d - 1; k >= 1; --k) {
-    ok &= col[k] >= 1;
-    idx = (idx << L) | (u64)(col[k] - 1);
-  }
-  return ok && (int64_t)PM[idx] <= (int64_t)col[0] - 1;
-}
-
-template <typename TT>
-__global__ void k_count_cells(const uint32_t* __restrict__ bits, int L, int d, u64 words,
-                              const TT* __restrict__ PM, u64* cand_out, u64* key_out) {
-  const int top = (1 << L) - 1;
-  const u64 mask = (1ull << L) - 1;
-  u64 nc = 0, nk = 0;
-  for (u64 w = blockIdx.x * (u64)blockDim.x + threadIdx.x; w < words; w += (u64)gridDim.x * blockDim.x) {
-    uint32_t x = bits[w];
-    while (x) {
-      const int b = __ffs(x) - 1;
-      x &= x - 1;
-      u64 lin = w * 32 + b;
-      int col[kMaxD];
-      bool has_top = false;
-      for (int k = 0; k < d; ++k) {
-        col[k] = (int)(lin & mask);
-        lin >>= L;
-        has_top |= col[k] == top;
-      }
-      if (!cell_strictly_dominated(PM, col, d, L)) ++nc;
-      if (!has_top) {
-        // P[c - e_0]
-        u64 idx = 0;
-        for (int k = d - 1; k >= 1; --k) idx = (idx << L) | (u64)col[k];
-        bool sdom = col[0] >= 1 && (int64_t)PM[idx] <= (int64_t)col[0] - 1;
-        for (int j = 1; j < d && !sdom; ++j) {
-          if (col[j] < 1) continue;
-          u64 ij = 0;
-          for (int k = d - 1; k >= 1; --k) ij = (ij << L) | (u64)(col[k] - (k == j ? 1 : 0));
-          sdom = (int64_t)PM[ij] <= (int64_t)col[0];
-        }
-        if (!sdom) ++nk;
-      }
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    nc += __shfl_xor_sync(kFull, nc, o);
-    nk += __shfl_xor_sync(kFull, nk, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    if (nc) atomicAdd(cand_out, nc);
-    if (nk) atomicAdd(key_out, nk);
-  }
-}
-
-// Row-parallel layer counts (same definitions as k_count_cells): one thread
+// Row-parallel layer counts: one thread
 // per row x = (c_1..c_{d-1}) of layer L.  With PM the prefix-min table,
 //   candidate cells of the row:  c_0 <= PM[x - 1]       (all x_k >= 1; else every cell)
 //   key cells (no top in x):      c_0 < min(PM[x] + 1, top, min_{x_k>=1} PM[x - e_k])
