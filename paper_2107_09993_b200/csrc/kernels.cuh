@@ -1,7 +1,7 @@
 // SkyCell skyline kernels for B200 (sm_100a).
 //
 // Stage map (DESIGN.md §3 has the bound and the algorithmic bytes of each):
-//   K0  k_sample / k_build_filter /     a sample's occupancy at a coarse level la
+//   K0  k_sample / k_filter_from_table  a sample's occupancy at a coarse level la
 //       sample tables, sample skyline   -> height table H (a point whose level-la
 //       -> k_strength_order,            cell is strictly dominated by an occupied
 //          k_filter_lists               sample cell cannot be in a candidate
@@ -193,51 +193,12 @@ __global__ void __launch_bounds__(256) k_sample(SampleParams p) {
   }
 }
 
-// Single CTA.  From the sample occupancy at level la build
-//   R[x]  = min{c0 : occupied(c0, x)}       x = (c1..c_{d-1})
-//   PM[x] = min_{y <= x} R[y]                (inclusive prefix-min)
-//   H[x]  = all x_k >= 1 ? PM[x - 1] : 255
-// so that a level-la cell c is strictly dominated by an occupied sample cell
-// iff c0 > H[c1..c_{d-1}].  la <= 7, so u8 entries (255 = none) suffice.
-__global__ void __launch_bounds__(1024) k_build_filter(const uint32_t* __restrict__ occ, int lf, int d,
-                                                        uint8_t* __restrict__ H) {
-  extern __shared__ uint8_t sm_pm[];
-  const uint32_t rows = 1u << (lf * (d - 1));
-  const int rowbits = 1 << lf;
-  for (uint32_t r = threadIdx.x; r < rows; r += blockDim.x) {
-    uint8_t best = 255;
-    if (lf >= 5) {
-      const int wpr = rowbits >> 5;
-      for (int w = 0; w < wpr; ++w) {
-        const uint32_t x = occ[(u64)r * wpr + w];
-        if (x) { best = (uint8_t)(w * 32 + __ffs(x) - 1); break; }
-      }
-    } else {
-      const int rpw = 32 >> lf;
-      const uint32_t x = (occ[r / rpw] >> ((r % rpw) * rowbits)) & ((1u << rowbits) - 1);
-      if (x) best = (uint8_t)(__ffs(x) - 1);
-    }
-    sm_pm[r] = best;
-  }
-  __syncthreads();
-  for (int k = 1; k < d; ++k) {
-    const uint32_t stride = 1u << (lf * (k - 1));
-    const uint32_t lines = rows >> lf;
-    for (uint32_t line = threadIdx.x; line < lines; line += blockDim.x) {
-      const uint32_t low = line & (stride - 1);
-      const uint32_t high = line >> (lf * (k - 1));
-      const uint32_t base = (high << (lf * k)) + low;
-      uint8_t run = 255;
-      for (int c = 0; c < rowbits; ++c) {
-        const uint32_t idx = base + c * stride;
-        run = min(run, sm_pm[idx]);
-        sm_pm[idx] = run;
-      }
-    }
-    __syncthreads();
-  }
+// H from a prefix-min table PM of the sample occupancy at level lf (built by
+// the multi-CTA table kernels): H[x] = all x_k >= 1 ? PM[x - 1] : none.
+__global__ void k_filter_from_table(const uint8_t* __restrict__ PM, int lf, int d, uint32_t rows,
+                                    uint8_t* __restrict__ H) {
   const uint32_t mask = (1u << lf) - 1;
-  for (uint32_t r = threadIdx.x; r < rows; r += blockDim.x) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
     bool ok = true;
     uint32_t prev = 0;
     for (int k = 1; k < d; ++k) {
@@ -245,7 +206,7 @@ __global__ void __launch_bounds__(1024) k_build_filter(const uint32_t* __restric
       ok &= c >= 1;
       prev |= (c - 1) << (lf * (k - 1));
     }
-    H[r] = ok ? sm_pm[prev] : (uint8_t)255;
+    H[r] = ok ? PM[prev] : (uint8_t)255;
   }
 }
 

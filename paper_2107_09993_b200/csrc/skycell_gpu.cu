@@ -623,7 +623,12 @@ struct Pipe final : PipeBase {
       tracer().mark(s, "K0: memset");
       sk::k_sample<TIn, TOut, D, IDENT><<<g, 256, 0, s>>>(sp);
       tracer().mark(s, "K0: sample");
-      sk::k_build_filter<<<1, 1024, h_entries, s>>>(U(o_sla), la, D, static_cast<uint8_t*>(ctx->H.p));
+      // H = the strict-dominance height of the sample's level-la occupancy:
+      // a level-la prefix-min table (multi-CTA) shifted by one cell per dim
+      launch_tables<uint8_t>(ctx, s, U(o_sla), la, D, static_cast<uint8_t*>(ctx->table2.p));
+      sk::k_filter_from_table<<<(unsigned)std::max<u64>(1, std::min<u64>((h_entries + 255) / 256, (u64)nsm * 4)), 256, 0,
+                                s>>>(static_cast<const uint8_t*>(ctx->table2.p), la, D, h_entries,
+                                     static_cast<uint8_t*>(ctx->H.p));
       tracer().mark(s, "K0: build_filter");
       ctx->launches += 2;
       // layer-rho prefix-min table of the sample: K1's test B

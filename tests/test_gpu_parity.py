@@ -238,3 +238,18 @@ def test_gpu_f64_general_path_large(engine, oracle, dist):
     want = oracle.compute_skyline(x, mn, mx, 5)
     got = engine.compute_skyline(sky.Dataset(x, mn, mx), 5)
     check(got, want.ids, want.points_examined, want.keys, want.candidates)
+
+
+@pytest.mark.parametrize("d", [9, 11, 13, 16])
+def test_gpu_high_dimensions(engine, oracle, d):
+    """d up to the reference's kMaxDims = 16 (cell.hpp:15), both K5 variants'
+    dispatch sizes, identity and general paths."""
+    from oracle.oracle import quantize_f32
+    for dist, n in ((0, 3000), (2, 1500)):
+        v = oracle.generate(dist, n, d, 13 + d)
+        rho_max = max(r for r in range(1, 8) if r * d <= 36 and (r - 1) * d <= 32 and r * (d - 1) <= 30)
+        for rho in sorted({1, rho_max}):
+            for x, mn, mx in ((quantize_f32(v), np.zeros(d), np.ones(d)), (v * 2 - 1, (v * 2 - 1).min(0), (v * 2 - 1).max(0))):
+                want = oracle.compute_skyline(x.astype(np.float64), mn, mx, rho)
+                got = engine.compute_skyline(sky.Dataset(np.ascontiguousarray(x), mn, mx), rho)
+                check(got, want.ids, want.points_examined, want.keys, want.candidates)
