@@ -1047,6 +1047,117 @@ __global__ void __launch_bounds__(THREADS) k_candidates(CandParams p) {
   }
 }
 
+// K4a: the candidate-cell test over S1, then the branch-free head of the 8
+// strongest filter points on FULL batches: candidates (about half of S1 at
+// the headline config) are queued per warp in a 64-entry shared ring and
+// tested 32 at a time, so no lane of the head test idles on a non-candidate.
+// Points still pending go to the dense stream P (K4b finishes them).
+template <typename T, int D, typename TT, int THREADS>
+__global__ void __launch_bounds__(THREADS) k_cand_head(CandParams p) {
+  extern __shared__ __align__(16) uint8_t smc[];
+  constexpr int kRing = 64;
+  constexpr uint32_t kHead0 = 8;
+  const u64 n = *p.count;
+  const uint32_t nh = (uint32_t)(*p.f_count < kHead0 ? *p.f_count : kHead0);
+  T* f_rows = reinterpret_cast<T*>(smc);                                  // kHead0 x D
+  u64* f_sum = reinterpret_cast<u64*>(smc + ((kHead0 * D * sizeof(T) + 15) & ~(size_t)15));
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ring_base = smc + ((kHead0 * D * sizeof(T) + 15) & ~(size_t)15) + kHead0 * 8;
+  T* r_rows = reinterpret_cast<T*>(ring_base) + (size_t)wib * kRing * D;
+  u64* r_sum = reinterpret_cast<u64*>(ring_base + (size_t)(THREADS / 32) * kRing * D * sizeof(T)) + (size_t)wib * kRing;
+  uint32_t* r_ids = reinterpret_cast<uint32_t*>(ring_base + (size_t)(THREADS / 32) * kRing * (D * sizeof(T) + 8)) +
+                    (size_t)wib * kRing;
+  {
+    const T* fr = static_cast<const T*>(p.f_rows);
+    for (uint32_t e = threadIdx.x; e < nh * D; e += THREADS) f_rows[e] = fr[e];
+    for (uint32_t e = threadIdx.x; e < nh; e += THREADS) f_sum[e] = p.f_fsum[e];
+  }
+  __syncthreads();
+  const T* rows = static_cast<const T*>(p.rows);
+  T* out_rows = static_cast<T*>(p.out_rows);
+  const TT* PM = static_cast<const TT*>(p.PM);
+  const int rho = p.rho, top = (1 << rho) - 1;
+  const float fscale = ldexpf(1.0f, rho);
+  const double dscale = ldexp(1.0, rho);
+  const u64 gw = (blockIdx.x * (u64)THREADS + threadIdx.x) >> 5;
+  const u64 nw = ((u64)gridDim.x * THREADS) >> 5;
+  const unsigned lt = (1u << lane) - 1;
+  WarpOut wo{0, p.chunk, p.chunk};
+  auto stamp = [&](u64 slot) { p.out_ids[slot] = kNoId; };
+  u64 examined = 0, kept = 0;
+  unsigned head = 0, tail = 0;  // ring positions (warp-uniform)
+  // head-8 test of up to 32 queued candidates; survivors -> P
+  auto drain = [&](unsigned cnt) {
+    const bool act = (unsigned)lane < cnt;
+    const unsigned e = (head + lane) % kRing;
+    T v[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) v[k] = (T)2;
+    u64 ps = 0;
+    uint32_t pid = kNoId;
+    if (act) {
+      load_row_cached<T, D>(r_rows, e, v);
+      ps = r_sum[e];
+      pid = r_ids[e];
+    }
+    bool dom = false;
+#pragma unroll
+    for (uint32_t f = 0; f < kHead0; ++f)
+      if (f < nh) dom |= dominates<T, D>(f_rows + (u64)f * D, v) && f_sum[f] < ps;
+    const bool keep = act && !dom;
+    kept += keep;
+    if (__any_sync(kFull, keep)) {
+      const u64 o = warp_reserve(wo, keep, p.out_reserved, stamp);
+      if (keep) {
+        store_row<T, D>(out_rows, o, v);
+        p.out_ids[o] = pid;
+        p.out_fsum[o] = ps;
+      }
+    }
+    head += cnt;
+    __syncwarp();
+  };
+  for (u64 wbase = gw * 32; wbase < n; wbase += nw * 32) {
+    const u64 i = wbase + lane;
+    uint32_t pid = kNoId;
+    if (i < n) pid = p.ids[i];
+    bool cand = false;
+    T v[D];
+    if (pid != kNoId) {
+      load_row_cached<T, D>(rows, i, v);
+      int col[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        if constexpr (sizeof(T) == 4) col[k] = cell_col(v[k], fscale, top);
+        else col[k] = cell_col(v[k], dscale, top);
+      }
+      cand = !strictly_dominated_cols<TT, D>(PM, col, rho);
+      examined += cand;
+    }
+    const unsigned m = __ballot_sync(kFull, cand);
+    if (cand) {
+      const unsigned e = (tail + __popc(m & lt)) % kRing;
+      store_row<T, D>(r_rows, e, v);
+      r_sum[e] = fsum_bits<T, D>(v);
+      r_ids[e] = pid;
+    }
+    tail += __popc(m);
+    __syncwarp();
+    if (tail - head >= 32) drain(32);
+  }
+  if (tail != head) drain(tail - head);
+  warp_close(wo, stamp);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    examined += __shfl_xor_sync(kFull, examined, o);
+    kept += __shfl_xor_sync(kFull, kept, o);
+  }
+  if (lane == 0) {
+    if (p.examined && examined) atomicAdd(p.examined, examined);
+    if (kept) atomicAdd(p.kept, kept);
+  }
+}
+
 // Compact the members (flag set, id != kNoId) of a slot array: rows and sums.
 template <typename T, int D>
 __global__ void k_compact_members(const T* __restrict__ rows, const uint32_t* __restrict__ ids,

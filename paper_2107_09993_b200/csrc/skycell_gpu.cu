@@ -836,7 +836,15 @@ struct Pipe final : PipeBase {
       pa.out_reserved = &c->pres;
       pa.kept = &c->pkept;
       pa.coop = 0;
-      kc<<<grid4, kThreads, smem_pf, s>>>(pa);
+      if (!k1_head && !std::getenv("SKYCELL_K4A_OLD")) {
+        auto ka = wide ? sk::k_cand_head<TOut, D, uint32_t, kThreads> : sk::k_cand_head<TOut, D, uint8_t, kThreads>;
+        const size_t sa = ((8 * D * sizeof(TOut) + 15) & ~(size_t)15) + 8 * 8 +
+                          (size_t)(kThreads / 32) * 64 * (D * sizeof(TOut) + 8 + 4) + 16;
+        ck(cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sa), "smem attr");
+        ka<<<grid4, kThreads, sa, s>>>(pa);
+      } else {
+        kc<<<grid4, kThreads, smem_pf, s>>>(pa);
+      }
       sk::CandParams pb = pc;
       pb.rows = ctx->p_rows.p;
       pb.ids = static_cast<const uint32_t*>(ctx->p_ids.p);
