@@ -969,7 +969,17 @@ __global__ void __launch_bounds__(THREADS) k_candidates(CandParams p) {
     // shortest column prefix of F, 32 entries per step (a dominator f has
     // col_k(f) <= col_k(p) in every dimension).  A per-lane loop here ran
     // with ~5 of 32 lanes active (ncu: 68% of K4's instructions).
-    unsigned pend = __ballot_sync(kFull, p.coop && keep && nf > hs + kHead0);
+    // K4b (coop): its lanes are dense pending points, so the next 32 filter
+    // points are tested branch-free by every lane (one step per filter point
+    // for the whole warp, instead of one warp step per pending point)
+    if (p.coop && nf > hs + kHead0 && __any_sync(kFull, keep)) {
+      bool dom = false;
+#pragma unroll 8
+      for (uint32_t f = hs + kHead0; f < hs + kHead0 + 32; ++f)
+        if (f < nf) dom |= dominates<T, D>(f_rows + (u64)f * D, v) && f_sum[f] < ps;
+      keep = keep && !dom;
+    }
+    unsigned pend = __ballot_sync(kFull, p.coop && keep && nf > hs + kHead0 + 32);
     while (pend) {
       const int src = __ffs(pend) - 1;
       pend &= pend - 1;
@@ -977,16 +987,7 @@ __global__ void __launch_bounds__(THREADS) k_candidates(CandParams p) {
 #pragma unroll
       for (int k = 0; k < D; ++k) pv[k] = __shfl_sync(kFull, v[k], src);
       const u64 pps = __shfl_sync(kFull, ps, src);
-      bool found;
-      {
-        const uint32_t f = hs + kHead0 + lane;
-        found = __any_sync(kFull, f < nf && f_sum[f] < pps && dominates<T, D>(f_rows + (u64)f * D, pv));
-      }
-      if (found) {
-        if (lane == src) keep = false;
-        continue;
-      }
-      if (nf <= hs + kHead0 + 32) continue;
+      bool found = false;
       int bk = 0;
       unsigned end = 0xffffffffu;
 #pragma unroll
