@@ -185,8 +185,10 @@ __global__ void __launch_bounds__(256) k_sample(SampleParams p) {
       la_lin = (la_lin << p.la) | (u64)(c >> sh);
       lin = (lin << p.rho) | (u64)c;
     }
-    set_bit_global(p.occ_la, la_lin);
-    if (p.occ_rho) set_bit_global(p.occ_rho, lin);
+    // check-before-set through L1 (no dependent L2 round trip on a miss-free
+    // hot word; a stale line only costs a redundant red.or)
+    set_bit_cached(p.occ_la, la_lin);
+    if (p.occ_rho) set_bit_cached(p.occ_rho, lin);
     store_row<TOut, D>(static_cast<TOut*>(p.rows), i, u);
     p.ids[i] = p.id_base + (uint32_t)i;
     p.fsum[i] = fsum_bits<TOut, D>(u);
