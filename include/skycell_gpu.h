@@ -62,6 +62,8 @@ typedef struct skycell_gpu_stats {
   uint64_t survivors_filter;   /* points entering the exact dominance pass (K5)   */
   uint64_t kernel_launches;    /* kernels this call launched                      */
   double stream_kernel_ms;     /* CUDA-event time of the streaming kernel K1 alone */
+  double filter_kernel_ms;     /* ... of the candidate filter K4 (K4a + K4b)      */
+  double dominance_ms;         /* ... of the exact dominance pass K5 (build + query) */
 } skycell_gpu_stats;
 
 typedef struct skycell_gpu_ctx skycell_gpu_ctx;

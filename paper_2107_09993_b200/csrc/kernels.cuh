@@ -346,7 +346,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
   const unsigned lt = (1u << lane) - 1;
   const uint32_t n = (uint32_t)p.n;
   constexpr uint32_t WT = 32u * PPT;
-  const uint32_t ntiles = (n + WT - 1) / WT;
+  // 64-bit here: n + WT - 1 wraps for n within WT of 2^32 (n < 2^32 holds)
+  const uint32_t ntiles = (uint32_t)(((u64)n + WT - 1) / WT);
   const uint32_t nfull = n / WT;
   const uint32_t gw = (blockIdx.x * THREADS + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * THREADS) >> 5;
@@ -381,8 +382,9 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
   auto load_tile = [&](TIn (&raw)[PPT][D], uint32_t t) {
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
-      const uint32_t i = t * WT + j * 32 + lane;
-      if (t < nfull || i < n) load_row<TIn, D>(coords, i, raw[j]);
+      // t * WT < n, so n - t * WT cannot wrap; t * WT + j * 32 + lane can
+      // (for n near 2^32) and is formed only for valid rows
+      if (t < nfull || (uint32_t)(j * 32 + lane) < n - t * WT) load_row<TIn, D>(coords, t * WT + j * 32 + lane, raw[j]);
     }
   };
   auto process = [&](TIn (&cur)[PPT][D], uint32_t t) {
@@ -392,7 +394,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
     bool bad = false;
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
-      const bool valid = full || base + j * 32 < n;
+      const bool valid = full || (uint32_t)(j * 32 + lane) < n - t * WT;
       bool fail_a;
       if constexpr (IDENT) {
         // u = min(max(v, 0), 1 - 2^-24): every column stays below 2^L (the
@@ -536,11 +538,11 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
     if (__any_sync(kFull, bad)) {  // rare: NaN/Inf (or overflow of the probe sum)
 #pragma unroll
       for (int j = 0; j < PPT; ++j) {
-        const uint32_t i = base + j * 32;
+        const bool in = full || (uint32_t)(j * 32 + lane) < n - t * WT;
         bool fin = true;
 #pragma unroll
         for (int k = 0; k < D; ++k) fin &= finite_v(cur[j][k]);
-        if (i < n && !fin) atomicMax(p.nonfinite, ~(u64)i);
+        if (in && !fin) atomicMax(p.nonfinite, ~(u64)(base + j * 32));
       }
     }
   };

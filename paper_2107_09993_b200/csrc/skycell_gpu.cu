@@ -135,7 +135,7 @@ struct skycell_gpu_ctx {
   DevBuf scan_tot;        // K5 list-scan chunk totals
   DevCounters* host_ctr = nullptr;  // pinned
   u64* host_param = nullptr;        // pinned H2D staging
-  cudaEvent_t ev[8] = {};
+  cudaEvent_t ev[10] = {};
   u64 launches = 0;
   std::unique_ptr<PipeBase> shard;  // sharded query in flight
 };
@@ -355,12 +355,12 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
   size_t temp = 0;
   ck(cub::DeviceRadixSort::SortPairs(nullptr, temp, static_cast<const u64*>(ctx->t_keys.p),
                                      static_cast<u64*>(ctx->t_keys2.p), static_cast<const uint32_t*>(ctx->t_vals.p),
-                                     static_cast<uint32_t*>(ctx->t_vals2.p), (int)nslots, 0, 64, s),
+                                     static_cast<uint32_t*>(ctx->t_vals2.p), nslots, 0, 64, s),
      "cub temp");
   ensure(ctx->t_cub, temp);
   ck(cub::DeviceRadixSort::SortPairs(ctx->t_cub.p, temp, static_cast<const u64*>(ctx->t_keys.p),
                                      static_cast<u64*>(ctx->t_keys2.p), static_cast<const uint32_t*>(ctx->t_vals.p),
-                                     static_cast<uint32_t*>(ctx->t_vals2.p), (int)nslots, 0, 64, s),
+                                     static_cast<uint32_t*>(ctx->t_vals2.p), nslots, 0, 64, s),
      "cub sort");
   tracer().mark(s, "tree: keys + sort");
   ck(cudaMemcpyAsync(&hv[1], valid_ctr, 8, cudaMemcpyDeviceToHost, s), "D2H");
@@ -864,6 +864,7 @@ struct Pipe final : PipeBase {
       kc<<<grid4, kThreads, smem_pf, s>>>(pc);
       ++ctx->launches;
     }
+    if (q.timed) ck(cudaEventRecord(ctx->ev[6], s), "event");
   }
 
   // ---- K5 over S2 (the local point set)
@@ -874,6 +875,7 @@ struct Pipe final : PipeBase {
     run_dominance<TOut, D>(ctx, s, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
                            static_cast<const u64*>(ctx->s2_fsum.p), &c->s2, cap4, U(o_hist), U(o_cur), &c->tvalid, 0,
                            nullptr, cell_level(), kTreeMainMin, &c->s2_kept);
+    if (q.timed) ck(cudaEventRecord(ctx->ev[7], s), "event");
   }
 
   // ---- K6: members' ids in ascending order through the id bitmap
@@ -1182,11 +1184,15 @@ int run_query(skycell_gpu_ctx* ctx, const TIn* coords, u64 n, int d, const doubl
       ck(cudaStreamSynchronize(ctx->stream), "sync");
     }
     if (stats) {
-      float a = 0, b = 0, c = 0, k1 = 0;
+      float a = 0, b = 0, c = 0, k1 = 0, k4 = 0, k5 = 0;
       cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
       cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]);
       cudaEventElapsedTime(&c, ctx->ev[2], ctx->ev[3]);
       cudaEventElapsedTime(&k1, ctx->ev[4], ctx->ev[5]);
+      cudaEventElapsedTime(&k4, ctx->ev[2], ctx->ev[6]);
+      cudaEventElapsedTime(&k5, ctx->ev[6], ctx->ev[7]);
+      stats->filter_kernel_ms = k4;
+      stats->dominance_ms = k5;
       stats->normalize_ms = 0.0;  // fused into the streaming pass (grid_ms)
       stats->grid_ms = a;
       stats->shrink_ms = b;
@@ -1374,7 +1380,7 @@ int skycell_gpu_shard_begin(skycell_gpu_ctx* ctx, const void* coords, int coords
   return guarded(err, err_len, [&] {
     if (!ctx || !occ_bytes) throw ApiFail{SKYCELL_USAGE, "skycell_gpu: null context or output pointer"};
     ctx->shard.reset();
-    if (id_base + n > 0xffffffffull + 1) throw ApiFail{SKYCELL_INPUT, "normalize: more than 2^32 - 1 records"};
+    if (id_base + n > 0xffffffffull) throw ApiFail{SKYCELL_INPUT, "normalize: more than 2^32 - 1 records"};
     if (coords_f32) {
       Query q = make_query<float>(ctx, static_cast<const float*>(coords), n, d, dim_min, dim_max, rho, mode, 1,
                                   nullptr, nullptr, id_base);
@@ -1436,9 +1442,13 @@ int skycell_gpu_shard_finish(skycell_gpu_ctx* ctx, const void* dev_recv, int wor
     }
     if (stats) {
       stats->kernel_launches = ctx->launches;
-      float k1 = 0;
+      float k1 = 0, k4 = 0, k5 = 0;
       cudaEventElapsedTime(&k1, ctx->ev[4], ctx->ev[5]);
+      cudaEventElapsedTime(&k4, ctx->ev[2], ctx->ev[6]);
+      cudaEventElapsedTime(&k5, ctx->ev[6], ctx->ev[7]);
       stats->stream_kernel_ms = k1;
+      stats->filter_kernel_ms = k4;
+      stats->dominance_ms = k5;
     }
     ctx->shard.reset();
   });

@@ -28,7 +28,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from .skycell import InputError, SkycellError, SkylineResult
+from .skycell import InputError, SkylineResult, UsageError
 
 
 def shard_range(n_total: int, rank: int, world: int) -> tuple[int, int]:
@@ -87,46 +87,73 @@ class ShardedSkyline:
         if self.device.type == "cuda" and hasattr(self.eng, "set_stream"):
             # kernels and NCCL collectives share torch's current stream
             self.eng.set_stream(torch.cuda.current_stream(self.device))
-        # phase 1: local streaming pass.  A failing rank still takes part in
-        # the collectives (count -1) so that every rank raises, none hangs.
-        err = None
-        try:
-            occ_bytes = self.eng.shard_begin(coords, n_local, d, dim_min, dim_max, rho, mode, id_base)
-        except SkycellError as e:
-            err, occ_bytes = e, 0
-        sizes = self._gather_counts(occ_bytes if err is None else -1)
-        self._reraise(err, sizes)
-        occ = self._buf("occ", occ_bytes)
-        self.eng.shard_export_occ(occ)
-        gathered = self._buf("occ_all", world * occ_bytes)
-        self._all_gather(gathered, occ)
+        # Every step that can fail on one rank (a rejected shard, a failed
+        # kernel, an allocation) runs through _together: the rank reports -1
+        # in the next count exchange instead of skipping it, so every rank
+        # raises and none blocks in a collective.
+        # phase 1: local streaming pass
+        sizes = self._together(lambda: self.eng.shard_begin(coords, n_local, d, dim_min, dim_max, rho, mode,
+                                                            id_base))
+        if len(set(sizes)) != 1:
+            # ranks built different grids (rho or d differ): the all-gather
+            # below would mis-align, so every rank refuses the query
+            raise UsageError(f"sharded skyline: ranks disagree on the occupancy size {sizes} (rho or d differ)")
+        occ_bytes = sizes[0]
+        self._together(lambda: self._export(occ_bytes))
+        gathered = self._bufs["occ_all"][: world * occ_bytes]
+        self._all_gather(gathered, self._bufs["occ"][:occ_bytes])
 
         # phase 2: prune against the global occupancy, local skyline
-        try:
-            cnt = self.eng.shard_prune(gathered, world)
-        except SkycellError as e:
-            err, cnt = e, 0
-        counts = self._gather_counts(cnt if err is None else -1)
-        self._reraise(err, counts)
+        counts = self._together(lambda: self.eng.shard_prune(gathered, world))
         maxc = max(counts)
         bb = self.eng.shard_block_bytes(maxc)
-        send = self._buf("send", bb)
-        self.eng.shard_pack(send, maxc)
-        recv = self._buf("recv", world * bb)
-        self._all_gather(recv, send)
+        self._together(lambda: self._pack(bb, maxc, world))
+        recv = self._bufs["recv"][: world * bb]
+        self._all_gather(recv, self._bufs["send"][:bb])
 
         # phase 3: own local skyline against the union
         if ids_out is None:
             ids_out = np.empty(max(n_local, 1), dtype=np.uint32)
-        res = self.eng.shard_finish(recv, world, maxc, rank, counts[rank], ids_out)
-        examined = self._gather_counts(res.points_examined)
-        res.points_examined = sum(examined)
-        for f in ("survivors_stream", "survivors_filter"):
-            setattr(res, f, sum(self._gather_counts(getattr(res, f))))
+        box = []
+        self._together(lambda: box.append(self.eng.shard_finish(recv, world, maxc, rank, counts[rank], ids_out)))
+        res = box[0]
+        # one exchange for all three summed statistics
+        stats = self._gather_vec([res.points_examined, res.survivors_stream, res.survivors_filter])
+        res.points_examined, res.survivors_stream, res.survivors_filter = (int(v) for v in stats.sum(axis=0))
         if gather_to is None:
             return res
         res.ids = self._gather_ids(res.ids, gather_to)
         return res
+
+    def _together(self, fn) -> list[int]:
+        """Run fn on every rank and exchange its (non-negative int) result;
+        a rank whose fn raised contributes -1 and re-raises, the others raise
+        InputError.  Returns every rank's value."""
+        err, val = None, 0
+        try:
+            r = fn()
+            val = int(r) if isinstance(r, (int, np.integer)) else 0
+        except Exception as e:  # noqa: BLE001 -- re-raised below, after the exchange
+            err = e
+        values = self._gather_counts(val if err is None else -1)
+        self._reraise(err, values)
+        return values
+
+    def _export(self, occ_bytes: int) -> None:
+        occ = self._buf("occ", occ_bytes)
+        self._buf("occ_all", self.world * occ_bytes)
+        self.eng.shard_export_occ(occ)
+
+    def _pack(self, bb: int, maxc: int, world: int) -> None:
+        send = self._buf("send", bb)
+        self._buf("recv", world * bb)
+        self.eng.shard_pack(send, maxc)
+
+    def _gather_vec(self, values) -> np.ndarray:
+        t = torch.tensor(values, dtype=torch.int64, device=self.coll_device)
+        out = torch.empty(self.world * len(values), dtype=torch.int64, device=self.coll_device)
+        dist.all_gather_into_tensor(out, t, group=self.group)
+        return out.cpu().numpy().reshape(self.world, len(values))
 
     def _reraise(self, err, values) -> None:
         if err is not None:

@@ -132,6 +132,8 @@ class SkylineResult:
     survivors_filter: int = 0
     kernel_launches: int = 0
     stream_kernel_ms: float = 0.0
+    filter_kernel_ms: float = 0.0
+    dominance_ms: float = 0.0
 
 
 class _Stats(C.Structure):
@@ -141,7 +143,7 @@ class _Stats(C.Structure):
         ("points_examined", C.c_uint64), ("n_layers", C.c_int32), ("pad_", C.c_int32),
         ("keys", C.c_uint64 * 64), ("candidates", C.c_int64 * 64),
         ("survivors_stream", C.c_uint64), ("survivors_filter", C.c_uint64), ("kernel_launches", C.c_uint64),
-        ("stream_kernel_ms", C.c_double),
+        ("stream_kernel_ms", C.c_double), ("filter_kernel_ms", C.c_double), ("dominance_ms", C.c_double),
     ]
 
 
@@ -237,7 +239,7 @@ class Engine:
     # (device pointer, used in place); ids_out likewise.
     def skyline_raw(self, coords, n: int, d: int, dim_min, dim_max, rho: int, mode: int = 1,
                     merge_cross_cell: bool = True, ids_out=None, with_stats: bool = True):
-        ptr, is_f32 = _data_ptr(coords)
+        ptr, is_f32 = _data_ptr(coords, n, d, self.device)
         mn = np.ascontiguousarray(dim_min, dtype=np.float64)
         mx = np.ascontiguousarray(dim_max, dtype=np.float64)
         if mn.shape[0] < d or mx.shape[0] < d:
@@ -245,7 +247,7 @@ class Engine:
         own = ids_out is None
         if own:
             ids_out = np.empty(max(n, 1), dtype=np.uint32)
-        out_ptr, _ = _data_ptr(ids_out)
+        out_ptr, _ = _data_ptr(ids_out, n, None, self.device, "ids_out", itemsize=4)
         n_out = C.c_uint64(0)
         st = _Stats()
         err = C.create_string_buffer(512)
@@ -286,7 +288,7 @@ class Engine:
     # ---- sharded query phases (include/skycell_gpu.h); the
     # exchanges between them are issued by paper_2107_09993_b200.dist.
     def shard_begin(self, coords, n: int, d: int, dim_min, dim_max, rho: int, mode: int, id_base: int) -> int:
-        ptr, is_f32 = _data_ptr(coords)
+        ptr, is_f32 = _data_ptr(coords, n, d, self.device)
         mn = np.ascontiguousarray(dim_min, dtype=np.float64)
         mx = np.ascontiguousarray(dim_max, dtype=np.float64)
         occ = C.c_uint64(0)
@@ -316,7 +318,7 @@ class Engine:
         _raise(self.lib.skycell_gpu_shard_pack(self._ctx, C.c_void_p(dst.data_ptr()), max_count, err, 512), err)
 
     def shard_finish(self, recv, world: int, max_count: int, rank: int, own_count: int, ids_out):
-        out_ptr, _ = _data_ptr(ids_out)
+        out_ptr, _ = _data_ptr(ids_out, own_count, None, self.device, "ids_out", itemsize=4)
         n_out = C.c_uint64(0)
         st = _Stats()
         err = C.create_string_buffer(512)
@@ -355,18 +357,43 @@ class Engine:
         return _to_result(ids[: n_out.value].copy(), st)
 
 
-def _data_ptr(a):
-    """(pointer, is_f32) of a numpy array or a torch tensor (host or CUDA)."""
+def _data_ptr(a, n: int | None = None, d: int | None = None, device: int | None = None, what: str = "coords",
+              itemsize: int | None = None):
+    """(pointer, is_f32) of a numpy array or a torch tensor (host or CUDA).
+
+    Coordinates must be float32 or float64 (the two C ABI entry points); an
+    output id buffer must be 4-byte integers.  With n (and d) given, the
+    buffer must hold at least n * d elements; a CUDA tensor must live on the
+    engine's device.  Anything else raises UsageError before the C ABI reads
+    out of bounds."""
     if isinstance(a, np.ndarray):
         if not a.flags["C_CONTIGUOUS"]:
             raise UsageError("arrays must be C-contiguous")
-        return C.c_void_p(a.ctypes.data), a.dtype == np.float32
-    if hasattr(a, "data_ptr"):
+        dt, size = a.dtype, a.size
+        ok = dt.itemsize == itemsize and dt.kind in "iu" if itemsize else dt in (np.float32, np.float64)
+        is_f32 = dt == np.float32
+        ptr = C.c_void_p(a.ctypes.data)
+    elif hasattr(a, "data_ptr"):
         import torch
         if not a.is_contiguous():
             raise UsageError("tensors must be contiguous")
-        return C.c_void_p(a.data_ptr()), a.dtype == torch.float32
-    raise UsageError(f"unsupported array type {type(a)!r}")
+        if a.is_cuda and device is not None and a.device.index != device:
+            raise UsageError(f"{what} tensor is on {a.device}, the engine on cuda:{device}")
+        dt, size = a.dtype, a.numel()
+        if itemsize:
+            ok = dt in (torch.int32, torch.uint32) if hasattr(torch, "uint32") else dt == torch.int32
+        else:
+            ok = dt in (torch.float32, torch.float64)
+        is_f32 = dt == torch.float32
+        ptr = C.c_void_p(a.data_ptr())
+    else:
+        raise UsageError(f"unsupported array type {type(a)!r}")
+    if not ok:
+        raise UsageError(f"{what}: unsupported element type {dt} "
+                         + ("(expected 32-bit integers)" if itemsize else "(expected float32 or float64)"))
+    if n is not None and size < n * (d or 1):
+        raise UsageError(f"{what}: buffer holds {size} elements, needs {n * (d or 1)}")
+    return ptr, is_f32
 
 
 def _to_result(ids, st) -> SkylineResult:
@@ -380,6 +407,8 @@ def _to_result(ids, st) -> SkylineResult:
         r.survivors_filter = int(st.survivors_filter)
         r.kernel_launches = int(st.kernel_launches)
         r.stream_kernel_ms = float(st.stream_kernel_ms)
+        r.filter_kernel_ms = float(st.filter_kernel_ms)
+        r.dominance_ms = float(st.dominance_ms)
     return r
 
 

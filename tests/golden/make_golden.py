@@ -7,6 +7,7 @@ them and tests/test_gpu_parity.py pins the GPU path to them.
 
     python tests/golden/make_golden.py            # small + C1 fixtures
     python tests/golden/make_golden.py --large    # + the large-S anchors (minutes)
+    python tests/golden/make_golden.py --bench    # only the benchmark-size anchors (tens of minutes)
 
 Inputs follow BASELINE.md §2: v = generate(dist, n, d, seed), then
 x = (float)(floor(v * 2^24) * 2^-24), fed to the reference as
@@ -66,6 +67,14 @@ def kats(ref: Reference) -> dict:
     add("single_point_rho4", [[0.37, 0.81]], [0, 0], [1, 1], 4, "test_grid.cpp:93-100")
     add("clamped_max", [[8, 0], [12, 0], [10, 0], [26, 0]], [8, 0], [26, 1], 2, "test_grid.cpp:17-30")
     add("constant_dim", [[5, 1], [5, 2], [5, 3]], *minmax([[5, 1], [5, 2], [5, 3]]), 1, "test_grid.cpp:43-47")
+    # FP64 sum tie between a dominating pair: 2^-60 + 0.5 rounds
+    # to 0.5, so sfs_positions (refine.cpp:31-59, which assumes domination
+    # implies a strictly smaller sum, :43-44) orders the pair by id and keeps
+    # both; brute force keeps only record 1.  The GPU must reproduce the
+    # reference's superset, not the mathematical skyline.
+    add("sum_tie_fp64", [[2.0 ** -60, 0.5], [0.0, 0.5]], [0, 0], [1, 1], 1, "refine.cpp:38-44 (SURVEY §0.4)")
+    add("sum_tie_fp64_rho3", [[0.25 + 2.0 ** -55, 0.5, 0.125], [0.25, 0.5, 0.125], [0.3, 0.1, 0.7]], [0, 0, 0],
+        [1, 1, 1], 3, "refine.cpp:38-44 (SURVEY §0.4)")
     # one point per cell after sub-unit shrink: all points in one layer-1 cell
     v = ref.generate(0, 200, 2, 91)
     add("one_cell", (0.1 + v * 0.3).tolist(), [0, 0], [1, 1], 1, "test_refine.cpp:55-64")
@@ -128,11 +137,57 @@ def random_small(ref) -> dict:
     return dict(records=recs), ids
 
 
+# Benchmark-size anchors (BASELINE.json configs at the sizes bench.py times):
+# C2 (n=1e8, d=4, rho=6) for independent and correlated data, the C4 per-GPU
+# shard (n=1.25e8 = the first shard of the n=1e9 dataset: generate() streams
+# are per 65,536-point block and do not depend on n, datagen.cpp:22-23,
+# :75-83), a 1e7 anti-correlated d=4 anchor and the C5 d=2 point at n=1e8.
+BENCH = (
+    ("c2_independent", 0, 10**8, 4, 6),
+    ("c2_correlated", 1, 10**8, 4, 6),
+    ("c4shard_independent", 0, 125_000_000, 4, 6),
+    ("c4shard_correlated", 1, 125_000_000, 4, 6),
+    ("anti_1e7_d4", 2, 10**7, 4, 5),
+    ("c5_d2", 2, 10**8, 2, 6),
+    ("c5_d3", 2, 10**8, 3, 6),
+    ("c5_d4", 2, 10**8, 4, 6),
+    ("c5_d5", 2, 10**8, 5, 5),
+)
+
+
+def bench(ref, only=None):
+    path = os.path.join(OUT, "bench.json")
+    ids_path = os.path.join(OUT, "bench_ids.npz")
+    recs = {r["key"]: r for r in json.load(open(path))["records"]} if os.path.exists(path) else {}
+    ids = dict(np.load(ids_path)) if os.path.exists(ids_path) else {}
+    for key, dist, n, d, rho in BENCH:
+        if only and key not in only:
+            continue
+        rec, r_ids = run_cfg(ref, dist, n, d, 42, rho, True, workers=0)
+        rec["key"] = key
+        rec["cores"] = os.cpu_count()
+        print(json.dumps(rec), flush=True)
+        recs[key] = rec
+        ids[key] = r_ids
+        with open(path, "w") as f:
+            json.dump(dict(records=[recs[k] for k, *_ in BENCH if k in recs]), f, indent=1)
+        np.savez_compressed(ids_path, **ids)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--large", action="store_true")
+    ap.add_argument("--bench", nargs="*", default=None, help="benchmark-size anchors (optionally: keys)")
+    ap.add_argument("--kat", action="store_true", help="only the known-answer fixture (kat.json)")
     args = ap.parse_args()
     ref = Reference()
+    if args.kat:
+        with open(os.path.join(OUT, "kat.json"), "w") as f:
+            json.dump(kats(ref), f, indent=1)
+        return
+    if args.bench is not None:
+        bench(ref, set(args.bench))
+        return
     with open(os.path.join(OUT, "kat.json"), "w") as f:
         json.dump(kats(ref), f, indent=1)
     small, ids = random_small(ref)

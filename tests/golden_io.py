@@ -30,3 +30,18 @@ def inputs_for(orc, rec):
         return quantize_f32(v), np.zeros(d), np.ones(d)
     x = v * 3.0 - 1.0
     return x, x.min(axis=0), x.max(axis=0)
+
+
+def bench_inputs(rec):
+    """Quantised f32 input of a benchmark-size record, made
+    with the reference generator compiled from its own sources
+    (oracle/_ref, multi-threaded) when it is present, else with the C oracle's
+    restatement -- both produce the same bytes (tests/test_oracle.py)."""
+    from oracle.oracle import Oracle, Reference, quantize_f32, reference_available
+    if reference_available():
+        v = Reference().generate(rec["dist_id"], rec["n"], rec["d"], rec["seed"], workers=0)
+    else:
+        v = Oracle().generate(rec["dist_id"], rec["n"], rec["d"], rec["seed"])
+    x = quantize_f32(v)
+    del v
+    return x
