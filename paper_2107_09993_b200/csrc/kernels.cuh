@@ -30,6 +30,9 @@
 
 namespace sk {
 
+// Non-template kernels are `static`: this header is included by several
+// translation units (skycell_gpu.cu, inst.cu per D).
+
 // ------------------------------------------------------------------ rows
 template <typename T, int D>
 __device__ __forceinline__ void load_row(const T* __restrict__ base, u64 i, T (&v)[D]) {
@@ -197,7 +200,7 @@ __global__ void __launch_bounds__(256) k_sample(SampleParams p) {
 
 // H from a prefix-min table PM of the sample occupancy at level lf (built by
 // the multi-CTA table kernels): H[x] = all x_k >= 1 ? PM[x - 1] : none.
-__global__ void k_filter_from_table(const uint8_t* __restrict__ PM, int lf, int d, uint32_t rows,
+static __global__ void k_filter_from_table(const uint8_t* __restrict__ PM, int lf, int d, uint32_t rows,
                                     uint8_t* __restrict__ H) {
   const uint32_t mask = (1u << lf) - 1;
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
@@ -571,7 +574,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
 
 // OR of the per-CTA slabs: blockIdx.y picks a group of slabs, so the
 // (slabs x words) reduction runs on many CTAs; one red.or per word and group.
-__global__ void k_reduce_slabs(const uint32_t* __restrict__ slabs, int nslabs, uint32_t words,
+static __global__ void k_reduce_slabs(const uint32_t* __restrict__ slabs, int nslabs, uint32_t words,
                                uint32_t* __restrict__ out) {
   const int per = (nslabs + gridDim.y - 1) / gridDim.y;
   const int s0 = blockIdx.y * per, s1 = min(nslabs, s0 + per);
@@ -802,7 +805,7 @@ __global__ void k_count_rows(const uint32_t* __restrict__ bits, int L, int d, u6
 // words): coarse word w covers c_0 in [32q, 32q + 32) of row x; its children
 // are the 64 fine bits [64q, 64q + 64) of the 2^(d-1) fine rows (2x_k + b_k).
 // OR them, fold bit pairs, gather the even bits: one 32-bit word, no atomics.
-__global__ void k_downsample_words(const uint32_t* __restrict__ src, int L, int d, u64 dst_words,
+static __global__ void k_downsample_words(const uint32_t* __restrict__ src, int L, int d, u64 dst_words,
                                    uint32_t* __restrict__ dst) {
   const u64 wpr = (1ull << L) >> 5, wpr_f = wpr * 2;
   const u64 mask = (1ull << L) - 1;
@@ -830,7 +833,7 @@ __global__ void k_downsample_words(const uint32_t* __restrict__ src, int L, int 
 }
 
 // Occupancy of layer L from layer L+1 (grid.cpp:80-102, child-OR), OR-ed into dst.
-__global__ void k_downsample(const uint32_t* __restrict__ src, int L, int d, u64 src_words,
+static __global__ void k_downsample(const uint32_t* __restrict__ src, int L, int d, u64 src_words,
                              uint32_t* __restrict__ dst) {
   const u64 mask = (1ull << (L + 1)) - 1;
   for (u64 w = blockIdx.x * (u64)blockDim.x + threadIdx.x; w < src_words; w += (u64)gridDim.x * blockDim.x) {
@@ -1325,7 +1328,7 @@ __device__ __forceinline__ unsigned* scan_array(unsigned* hist, int y, int D, in
   return hist + (u64)(bins ? y : y - D) * kListStride + (bins ? 0 : kColBase);
 }
 
-__global__ void __launch_bounds__(1024) k_list_scan_sums(unsigned* __restrict__ hist, int D,
+static __global__ void __launch_bounds__(1024) k_list_scan_sums(unsigned* __restrict__ hist, int D,
                                                           unsigned* __restrict__ totals) {
   __shared__ unsigned warp_tot[32];
   int len;
@@ -1345,7 +1348,7 @@ __global__ void __launch_bounds__(1024) k_list_scan_sums(unsigned* __restrict__ 
   }
 }
 
-__global__ void __launch_bounds__(1024) k_list_scan(unsigned* __restrict__ hist, unsigned* __restrict__ cursor, int D,
+static __global__ void __launch_bounds__(1024) k_list_scan(unsigned* __restrict__ hist, unsigned* __restrict__ cursor, int D,
                                                      const unsigned* __restrict__ totals) {
   __shared__ unsigned tile[kScanChunk + kScanChunk / 32];  // one pad word per 32 entries
   __shared__ unsigned warp_tot[32];
@@ -1596,7 +1599,7 @@ constexpr int kBitsThreads = 256;
 constexpr int kBitsPer = 8;
 constexpr u64 kBitsBlock = (u64)kBitsThreads * kBitsPer;
 
-__global__ void k_mark_ids(const uint32_t* __restrict__ ids, const uint8_t* __restrict__ flag,
+static __global__ void k_mark_ids(const uint32_t* __restrict__ ids, const uint8_t* __restrict__ flag,
                            const u64* __restrict__ count, uint32_t* __restrict__ bits, uint32_t base) {
   const u64 n = *count;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
@@ -1608,7 +1611,7 @@ __global__ void k_mark_ids(const uint32_t* __restrict__ ids, const uint8_t* __re
   }
 }
 
-__global__ void __launch_bounds__(kBitsThreads) k_bits_count(const uint32_t* __restrict__ bits, u64 words,
+static __global__ void __launch_bounds__(kBitsThreads) k_bits_count(const uint32_t* __restrict__ bits, u64 words,
                                                              unsigned* __restrict__ block_counts) {
   const u64 b0 = blockIdx.x * kBitsBlock;
   unsigned c = 0;
@@ -1630,7 +1633,7 @@ __global__ void __launch_bounds__(kBitsThreads) k_bits_count(const uint32_t* __r
 }
 
 // Single CTA: exclusive scan of the block counts; total -> *out_count.
-__global__ void __launch_bounds__(1024) k_bits_scan(unsigned* __restrict__ block_counts, unsigned nblocks,
+static __global__ void __launch_bounds__(1024) k_bits_scan(unsigned* __restrict__ block_counts, unsigned nblocks,
                                                     u64* __restrict__ out_count) {
   __shared__ unsigned part[1024];
   const unsigned per = (nblocks + 1023) / 1024;
@@ -1659,7 +1662,7 @@ __global__ void __launch_bounds__(1024) k_bits_scan(unsigned* __restrict__ block
   if (threadIdx.x == 1023) *out_count = part[1023];
 }
 
-__global__ void __launch_bounds__(kBitsThreads) k_bits_write(const uint32_t* __restrict__ bits, u64 words,
+static __global__ void __launch_bounds__(kBitsThreads) k_bits_write(const uint32_t* __restrict__ bits, u64 words,
                                                              const unsigned* __restrict__ block_offs,
                                                              uint32_t* __restrict__ out_ids, uint32_t base) {
   // thread t owns words b0 + t*kBitsPer .. +kBitsPer-1 (contiguous, so the
@@ -1709,7 +1712,7 @@ __global__ void k_check_finite(const TIn* __restrict__ coords, u64 total, int d,
 // dst[w] = OR over g < world of gathered[g * words + w]: the bitwise-OR
 // reduction NCCL lacks (nccl.h:260-275), applied to the all-gathered
 // occupancy region of every rank.  uint4 words: 16 B per load.
-__global__ void k_or_gather(const uint4* __restrict__ gathered, int world, u64 words4, uint4* __restrict__ dst) {
+static __global__ void k_or_gather(const uint4* __restrict__ gathered, int world, u64 words4, uint4* __restrict__ dst) {
   for (u64 w = blockIdx.x * (u64)blockDim.x + threadIdx.x; w < words4; w += (u64)gridDim.x * blockDim.x) {
     uint4 x = gathered[w];
     for (int g = 1; g < world; ++g) {
@@ -1752,11 +1755,11 @@ __global__ void k_pack_members(const T* __restrict__ rows, const uint32_t* __res
   }
 }
 
-__global__ void k_clamp_count(const u64* __restrict__ src, u64 cap, u64* __restrict__ dst) {
+static __global__ void k_clamp_count(const u64* __restrict__ src, u64 cap, u64* __restrict__ dst) {
   if (threadIdx.x == 0) *dst = *src < cap ? *src : cap;
 }
 
-__global__ void k_fill_u32(uint32_t* __restrict__ p, u64 count, uint32_t v) {
+static __global__ void k_fill_u32(uint32_t* __restrict__ p, u64 count, uint32_t v) {
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < count; i += (u64)gridDim.x * blockDim.x) p[i] = v;
 }
 
@@ -1830,7 +1833,7 @@ __global__ void k_quadrant_gather(const double* __restrict__ coords, const uint3
 }
 
 // ids[j] = orig[ids[j]] (refine.cpp:182): ascending stays ascending.
-__global__ void k_map_ids(uint32_t* __restrict__ ids, const uint32_t* __restrict__ orig, u64 n) {
+static __global__ void k_map_ids(uint32_t* __restrict__ ids, const uint32_t* __restrict__ orig, u64 n) {
   for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x) ids[j] = orig[ids[j]];
 }
 

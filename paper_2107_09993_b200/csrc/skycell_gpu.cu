@@ -15,1007 +15,11 @@
 // torch.distributed in paper_2107_09993_b200/dist.py) on the stream the
 // context is bound to (skycell_gpu_set_stream), so no phase needs a host
 // synchronisation except where a count must reach the host.
-#include <cuda_runtime.h>
-
-#include <algorithm>
-#include <chrono>
-#include <cmath>
-#include <cstdio>
-#include <cstdlib>
-#include <cstring>
-#include <memory>
-#include <string>
-#include <vector>
-
-#include "../../include/skycell_gpu.h"
-#include <cub/device/device_radix_sort.cuh>
-
-#include "kernels.cuh"
-#include "tree.cuh"
-#include "datagen.cuh"
+#include "engine.cuh"
 
 using sk::u64;
 
-namespace {
-
-constexpr int kMaxLayers = 64;
-
-struct DevCounters {
-  u64 nonfinite;
-  u64 s1, s2, examined;
-  u64 zero;
-  u64 m, xs, xs_kept, nf, fs, fin, s1_kept, s2_kept;
-  u64 lsky;       // local skyline size (sharded)
-  u64 tvalid;     // valid slots of the set a dominance tree is built over
-  u64 tkilled;    // ... removed by the champion prefilter (must follow tvalid)
-  u64 dres;       // D-stream slots handed out (K1 filter-point head)
-  u64 xd, xs_cap; // sample candidates (dense) / those entering the sample skyline (capped)
-  u64 pres, pkept;  // K4a -> K4b pending stream: slots handed out / points written
-  u64 un, qend;   // union slots and own-slice end (sharded finish)
-  u64 cand[kMaxLayers];
-  u64 key[kMaxLayers];
-};
-
-struct DevBuf {
-  void* p = nullptr;
-  size_t cap = 0;
-};
-
-struct Status {
-  int code = SKYCELL_OK;
-  std::string msg;
-};
-
-struct CudaFail {
-  cudaError_t e;
-  const char* what;
-};
-
-struct ApiFail {
-  int code;
-  std::string msg;
-};
-
-inline void ck(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) throw CudaFail{e, what};
-}
-
-// Grow-only scratch buffers.  Growth takes 25% headroom: data-dependent sizes
-// (survivor slot counts) vary slightly from query to query, and a cudaFree /
-// cudaMalloc pair inside a query would synchronise the device.
-void ensure(DevBuf& b, size_t bytes) {
-  if (bytes == 0) bytes = 16;
-  if (b.cap >= bytes) return;
-  if (b.p) cudaFree(b.p);
-  b.p = nullptr;
-  b.cap = 0;
-  const size_t want = bytes + bytes / 4;
-  if (cudaMalloc(&b.p, want) == cudaSuccess) {
-    b.cap = want;
-    return;
-  }
-  cudaGetLastError();
-  ck(cudaMalloc(&b.p, bytes), "cudaMalloc");
-  b.cap = bytes;
-}
-
-struct PipeBase {
-  virtual ~PipeBase() = default;
-  virtual void local() = 0;
-  virtual u64 occ_bytes() const = 0;
-  virtual void export_occ(void* dst) = 0;
-  virtual void or_gathered(const void* gathered, int world) = 0;
-  virtual u64 prune_local_skyline() = 0;
-  virtual u64 block_bytes(u64 maxc) const = 0;
-  virtual void pack(void* dst, u64 maxc) = 0;
-  virtual void finish(const void* recv, int world, u64 maxc, int rank, u64 own_count, uint32_t* ids_out,
-                      uint64_t* n_out, skycell_gpu_stats* stats) = 0;
-};
-
-}  // namespace
-
-struct skycell_gpu_ctx {
-  int device = 0;
-  int num_sms = 148;
-  cudaStream_t own_stream = nullptr;
-  cudaStream_t stream = nullptr;  // the stream every kernel is enqueued on
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  DevBuf reset, slabs, H, table, table2, table_s, staging;
-  DevBuf smp_rows, smp_ids, smp_fsum, f_rows, f_fsum, f_lists, f_offs, lists, ids_dev;
-  DevBuf s1_rows, s1_ids, s2_rows, s2_ids, s2_fsum, flags;
-  DevBuf sky_rows, sky_ids, sky_fsum;  // local skyline (sharded)
-  DevBuf d_cells;                      // K1's D stream
-  DevBuf p_rows, p_ids, p_fsum;        // K4a -> K4b pending points
-  DevBuf q_bits, q_orig, q_sub, q_ids, q_mm;  // quadrant_skyline
-  DevBuf t_keys, t_keys2, t_vals, t_vals2, t_cub, t_rows, t_ids, t_fsum, t_lo, t_hi, t_cs, t_ci;  // K5 tree
-  DevBuf t_cm, t_kill;  // K5 tree champion prefilter
-  int k5_mode = -1;  // 0 lists, 1 tree, 2 auto (SKYCELL_K5)
-  DevBuf long_q, long_n;  // K5 phase-B queue
-  DevBuf scan_tot;        // K5 list-scan chunk totals
-  DevCounters* host_ctr = nullptr;  // pinned
-  u64* host_param = nullptr;        // pinned H2D staging
-  cudaEvent_t ev[10] = {};
-  u64 launches = 0;
-  std::unique_ptr<PipeBase> shard;  // sharded query in flight
-};
-
-namespace {
-
-void put_err(char* err, size_t len, const std::string& m) {
-  if (!err || !len) return;
-  std::strncpy(err, m.c_str(), len - 1);
-  err[len - 1] = '\0';
-}
-
-// Bump allocator over the per-query zeroed region.
-struct Carver {
-  size_t off = 0;
-  size_t take(size_t bytes) {
-    const size_t o = off;
-    off = (off + bytes + 255) & ~size_t(255);
-    return o;
-  }
-};
-
-// Validation in the reference's order: normalize() first (dataset.cpp:23-24),
-// then the grid budget (grid.cpp:38-43).
-Status validate_shape(u64 n, int d) {
-  if (n < 1) return {SKYCELL_INPUT, "normalize: empty dataset"};
-  if (d < 2) return {SKYCELL_INPUT, "normalize: dimensionality must be at least 2"};
-  if (d > sk::kMaxD) return {SKYCELL_INPUT, "normalize: dimensionality must be at most 16"};
-  if (n > 0xffffffffull) return {SKYCELL_INPUT, "normalize: more than 2^32 - 1 records"};
-  return {};
-}
-
-Status validate_rho(int rho, int d) {
-  if (rho < 1) return {SKYCELL_CONFIG, "grid: rho must be at least 1"};
-  if (rho * d > 60)
-    return {SKYCELL_CONFIG, "grid: rho*d = " + std::to_string(rho * d) + " exceeds the 60-bit cell index budget"};
-  if ((rho - 1) * d > 32)
-    return {SKYCELL_CONFIG, "grid: occupancy bit-sets for rho = " + std::to_string(rho) + ", d = " +
-                                std::to_string(d) + " would exceed memory"};
-  return {};
-}
-
-int default_rho(u64 n, int d) {
-  u64 x = n > 0 ? n : 1;
-  int bw = 0;
-  while (x) {
-    ++bw;
-    x >>= 1;
-  }
-  return std::max(1, std::min(6, (bw - 1) / d));
-}
-
-// SKYCELL_TRACE=1: synchronise and print the host time of each phase to
-// stderr (debugging only; it serialises the pipeline).
-struct Tracer {
-  bool on = std::getenv("SKYCELL_TRACE") != nullptr;
-  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
-  void mark(cudaStream_t s, const char* what) {
-    if (!on) return;
-    cudaStreamSynchronize(s);
-    std::fprintf(stderr, "[skycell] %-24s %9.3f ms\n", what,
-                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
-  }
-};
-Tracer& tracer() {
-  static thread_local Tracer t;
-  return t;
-}
-
-// ------------------------------------------------------------------ config
-constexpr int kThreads = 256;
-
-template <typename T, int D>
-constexpr int ppt_for() {
-  constexpr int words = D * (int)sizeof(T) / 4;
-  constexpr int p = 32 / words;
-  return p < 1 ? 1 : (p > 8 ? 8 : p);
-}
-
-// ----------------------------------------------------------------- query
-struct Query {
-  skycell_gpu_ctx* ctx;
-  u64 n;
-  int d, rho, mode, merge;
-  sk::Norm nm;
-  const void* dev_coords;  // device-resident input (user's or staged)
-  uint32_t* ids_dev;       // caller's device output buffer, or nullptr (use ctx->ids_dev)
-  skycell_gpu_stats* stats;
-  bool timed;
-  uint32_t id_base;        // global id of local record 0 (sharded: the shard offset)
-};
-
-template <typename TT>
-void launch_tables(skycell_gpu_ctx* ctx, cudaStream_t s, const uint32_t* bits, int L, int d, TT* table) {
-  const u64 rows = 1ull << (u64)(L * (d - 1));
-  const u64 lines1 = rows >> L;
-  const int nsm = ctx->num_sms;
-  auto grid_for = [&](u64 items) {
-    return (unsigned)std::max<u64>(1, std::min<u64>((items + 127) / 128, (u64)nsm * 16));
-  };
-  // enough dimension-1 lines to fill the GPU: one thread per line; else
-  // (d = 2, or d = 3 at fine layers) row minima per thread + a CTA per line
-  if (lines1 >= (u64)nsm * 128 || L <= 6) {
-    sk::k_rowmin_prefix1<TT><<<grid_for(lines1), 128, 0, s>>>(bits, L, d, lines1, table);
-    ++ctx->launches;
-    for (int k = 2; k < d; ++k) {
-      sk::k_prefix_min<TT><<<grid_for(lines1), 128, 0, s>>>(table, L, k, lines1);
-      ++ctx->launches;
-    }
-    return;
-  }
-  sk::k_rowmin<TT><<<grid_for(rows), 128, 0, s>>>(bits, L, rows, table);
-  ++ctx->launches;
-  for (int k = 1; k < d; ++k) {
-    const unsigned g = (unsigned)std::min<u64>(lines1, (u64)nsm * 2);
-    if (lines1 >= (u64)nsm * 128) sk::k_prefix_min<TT><<<grid_for(lines1), 128, 0, s>>>(table, L, k, lines1);
-    else sk::k_prefix_min_cta<TT><<<g, 1024, 0, s>>>(table, L, k, lines1);
-    ++ctx->launches;
-  }
-}
-
-template <typename TT>
-void launch_count(skycell_gpu_ctx* ctx, cudaStream_t s, const uint32_t* bits, int L, int d, const TT* table, u64* cand,
-                  u64* key) {
-  const u64 rows = 1ull << (u64)(L * (d - 1));
-  const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((rows + 255) / 256, (u64)ctx->num_sms * 16));
-  sk::k_count_rows<TT><<<g, 256, 0, s>>>(bits, L, d, rows, table, cand, key);
-  ++ctx->launches;
-}
-
-// Exact sort-first pass (refine.cpp:31-59 as applied in phase 2, :98-99) over
-// a point set given as slots (ids == kNoId marks an empty slot): per-dimension
-// column lists, then the list-pruned dominance test; flags[i] = 1 for members
-// of the result, for the query slots [q_begin, *q_end) (all slots when q_end
-// is null).  cell_level > 0 restricts dominators to p's own layer-rho cell
-// (merge_cross_cell = false, refine.cpp:98).
-template <typename TOut, int D>
-void run_exact(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint32_t* ids, const u64* fsum,
-               const u64* count, u64 cap, unsigned* hist, unsigned* cursor, u64 q_begin = 0,
-               const u64* q_end = nullptr, int cell_level = 0) {
-  const int nsm = ctx->num_sms;
-  const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((cap + 255) / 256, (u64)nsm * 8));
-  const TOut* trows = static_cast<const TOut*>(rows);
-  uint32_t* lists = static_cast<uint32_t*>(ctx->lists.p);
-  sk::k_list_hist<TOut, D><<<g, 256, 0, s>>>(trows, ids, fsum, count, hist);
-  unsigned* totals = static_cast<unsigned*>(ctx->scan_tot.p);
-  sk::k_list_scan_sums<<<dim3(sk::kScanChunks, D), 1024, 0, s>>>(hist, D, totals);
-  sk::k_list_scan<<<dim3(sk::kScanChunks, D), 1024, 0, s>>>(hist, cursor, D, totals);
-  ++ctx->launches;
-  sk::k_list_scatter<TOut, D><<<g, 256, 0, s>>>(trows, ids, fsum, count, cursor, lists, cap);
-  const unsigned gw = (unsigned)std::max<u64>(1, std::min<u64>((cap * 32 + 255) / 256, (u64)nsm * 8));
-  ensure(ctx->long_q, cap * 4);
-  u64* long_n = static_cast<u64*>(ctx->long_n.p);
-  ck(cudaMemsetAsync(long_n, 0, 8, s), "memset");
-  constexpr unsigned kMaxSteps = 16;
-  sk::k_allpairs_lists<TOut, D><<<gw, 256, 0, s>>>(trows, ids, fsum, count, lists, hist, cap,
-                                                   static_cast<uint8_t*>(ctx->flags.p), q_begin, q_end, cell_level,
-                                                   kMaxSteps, static_cast<uint32_t*>(ctx->long_q.p), long_n);
-  sk::k_allpairs_long<TOut, D><<<nsm * 4, 256, 0, s>>>(trows, ids, fsum, lists, hist, cap,
-                                                       static_cast<uint8_t*>(ctx->flags.p), cell_level,
-                                                       static_cast<const uint32_t*>(ctx->long_q.p), long_n);
-  ctx->launches += 5;
-}
-
-// Exact sort-first pass through the dominance tree (tree.cuh).  Needs the
-// set's slot count on the host (CUB's item count), so it synchronises once.
-template <typename TOut, int D>
-void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint32_t* ids, const u64* fsum,
-              const u64* count, u64* valid_ctr, u64 q_begin, const u64* q_end, int cell_level) {
-  const int nsm = ctx->num_sms;
-  u64 hv[2];
-  ck(cudaMemcpyAsync(&hv[0], count, 8, cudaMemcpyDeviceToHost, s), "D2H");
-  ck(cudaStreamSynchronize(s), "sync");
-  const u64 nslots = hv[0];
-  if (nslots == 0) return;
-  ensure(ctx->t_keys, nslots * 8);
-  ensure(ctx->t_keys2, nslots * 8);
-  ensure(ctx->t_vals, nslots * 4);
-  ensure(ctx->t_vals2, nslots * 4);
-  ck(cudaMemsetAsync(valid_ctr, 0, 8, s), "memset");
-  const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((nslots + 255) / 256, (u64)nsm * 8));
-  tracer().mark(s, "tree: count read");
-  // champion prefilter over a dense level-Lc grid (<= 2^24 cells)
-  // at most 2^24 cells and about 4 cells per set slot (the table's memset and
-  // d prefix passes are a fixed cost; small sets would not amortise them)
-  int lg = 0;
-  while ((1ull << (lg + 1)) <= 4 * nslots) ++lg;
-  const int Lc = std::min(std::min(12, 24 / D), lg / D);
-  const uint8_t* kill = nullptr;
-  if (Lc >= 1 && nslots >= (1ull << 16)) {
-    const u64 cells = 1ull << (u64)(Lc * D);
-    ensure(ctx->t_cm, cells * 8);
-    ensure(ctx->t_kill, nslots);
-    u64* cm = static_cast<u64*>(ctx->t_cm.p);
-    const u64 lines = cells >> Lc;
-    const unsigned gp = (unsigned)std::max<u64>(1, std::min<u64>((lines + 127) / 128, (u64)nsm * 16));
-    uint8_t* killb = static_cast<uint8_t*>(ctx->t_kill.p);
-    // the plain grid, then grids shifted by 1/2, 1/4, 3/4 of a cell: 4 passes
-    // at d >= 5 (C3: 542 -> 499 ms), 2 below (anti d=4: 11.2 vs 11.8 ms with 4)
-    int passes = D >= 5 ? 4 : 2;
-    if (const char* e = std::getenv("SKYCELL_PREPASSES")) passes = std::max(1, std::min(4, std::atoi(e)));
-    for (int pass = 0; pass < passes; ++pass) {
-      ck(cudaMemsetAsync(cm, 0xff, cells * 8, s), "memset");
-      sk::k_cellmin<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, count, Lc, pass, killb, cm);
-      for (int k = 1; k <= D; ++k) sk::k_prefix_min<u64><<<gp, 128, 0, s>>>(cm, Lc, k, lines);
-      sk::k_champ_kill<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, count, Lc, pass, cm,
-                                                 q_begin, q_end, killb, static_cast<uint8_t*>(ctx->flags.p),
-                                                 valid_ctr + 1);
-      ctx->launches += 2 + D;
-    }
-    kill = static_cast<const uint8_t*>(ctx->t_kill.p);
-    tracer().mark(s, "tree: champion prefilter");
-  }
-  sk::k_tree_keys<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, count, kill,
-                                            static_cast<u64*>(ctx->t_keys.p), static_cast<uint32_t*>(ctx->t_vals.p),
-                                            valid_ctr);
-  size_t temp = 0;
-  ck(cub::DeviceRadixSort::SortPairs(nullptr, temp, static_cast<const u64*>(ctx->t_keys.p),
-                                     static_cast<u64*>(ctx->t_keys2.p), static_cast<const uint32_t*>(ctx->t_vals.p),
-                                     static_cast<uint32_t*>(ctx->t_vals2.p), nslots, 0, 64, s),
-     "cub temp");
-  ensure(ctx->t_cub, temp);
-  ck(cub::DeviceRadixSort::SortPairs(ctx->t_cub.p, temp, static_cast<const u64*>(ctx->t_keys.p),
-                                     static_cast<u64*>(ctx->t_keys2.p), static_cast<const uint32_t*>(ctx->t_vals.p),
-                                     static_cast<uint32_t*>(ctx->t_vals2.p), nslots, 0, 64, s),
-     "cub sort");
-  tracer().mark(s, "tree: keys + sort");
-  ck(cudaMemcpyAsync(&hv[1], valid_ctr, 8, cudaMemcpyDeviceToHost, s), "D2H");
-  ck(cudaStreamSynchronize(s), "sync");
-  const u64 m = hv[1];
-  ctx->launches += 2;
-  if (m == 0) return;
-  sk::TreeShape sh{};
-  sh.m = m;
-  sh.nleaf = (m + sk::kLeaf - 1) / sk::kLeaf;
-  if (sh.nleaf >= (1ull << 27)) throw ApiFail{SKYCELL_UNSUPPORTED, "skycell_gpu: dominance tree too large"};
-  constexpr u64 F = sk::tree_fanout<D>();
-  u64 off = 0, cnt = sh.nleaf;
-  int L = 0;
-  while (true) {
-    sh.off[L] = (uint32_t)off;
-    sh.cnt[L] = (uint32_t)cnt;
-    off += cnt;
-    ++L;
-    if (cnt == 1) break;
-    cnt = (cnt + F - 1) / F;
-  }
-  sh.levels = L;
-  const u64 nodes = off;
-  ensure(ctx->t_rows, m * D * sizeof(TOut));
-  ensure(ctx->t_ids, m * 4);
-  ensure(ctx->t_fsum, m * 8);
-  ensure(ctx->t_lo, nodes * D * sizeof(TOut));
-  ensure(ctx->t_hi, nodes * D * sizeof(TOut));
-  ensure(ctx->t_cs, nodes * 8);
-  ensure(ctx->t_ci, nodes * 4);
-  TOut* srows = static_cast<TOut*>(ctx->t_rows.p);
-  uint32_t* sids = static_cast<uint32_t*>(ctx->t_ids.p);
-  u64* sfsum = static_cast<u64*>(ctx->t_fsum.p);
-  const uint32_t* order = static_cast<const uint32_t*>(ctx->t_vals2.p);
-  const unsigned gm = (unsigned)std::max<u64>(1, std::min<u64>((m + 255) / 256, (u64)nsm * 8));
-  sk::k_tree_gather<TOut, D><<<gm, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, order, m, srows, sids, sfsum);
-  sk::TreeView<TOut, D> tv{static_cast<TOut*>(ctx->t_lo.p), static_cast<TOut*>(ctx->t_hi.p),
-                           static_cast<u64*>(ctx->t_cs.p), static_cast<uint32_t*>(ctx->t_ci.p)};
-  const unsigned gl = (unsigned)std::max<u64>(1, std::min<u64>((sh.nleaf * 32 + 255) / 256, (u64)nsm * 8));
-  sk::k_tree_leaves<TOut, D><<<gl, 256, 0, s>>>(srows, sids, sfsum, m, sh.nleaf, tv);
-  ctx->launches += 2;
-  for (int l = 1; l < sh.levels; ++l) {
-    const unsigned gn = (unsigned)std::max<u64>(1, std::min<u64>((sh.cnt[l] + 255) / 256, (u64)nsm * 8));
-    sk::k_tree_level<TOut, D><<<gn, 256, 0, s>>>(tv, sh.off[l - 1], sh.cnt[l - 1], sh.off[l], sh.cnt[l]);
-    ++ctx->launches;
-  }
-  tracer().mark(s, "tree: build");
-  const unsigned gq = (unsigned)std::max<u64>(1, std::min<u64>((m * 32 + 255) / 256, (u64)nsm * 8));
-  sk::k_tree_query<TOut, D><<<gq, 256, 0, s>>>(srows, sids, sfsum, order, tv, sh, q_begin, q_end, cell_level,
-                                              static_cast<uint8_t*>(ctx->flags.p));
-  ++ctx->launches;
-  tracer().mark(s, "tree: query");
-}
-
-// SKYCELL_K5 = lists | tree | auto (default): which K5 variant runs.
-int k5_mode(skycell_gpu_ctx* ctx) {
-  if (ctx->k5_mode < 0) {
-    const char* e = std::getenv("SKYCELL_K5");
-    ctx->k5_mode = (e && !std::strcmp(e, "lists")) ? 0 : (e && !std::strcmp(e, "tree")) ? 1 : 2;
-  }
-  return ctx->k5_mode;
-}
-
-// Sets up to this many slots go through the column lists; larger ones
-// (anti-correlated data: 8e6 at n=1e8 d=4, 5.4e7 at d=6) through the tree,
-// whose cost grows with the skyline boundary instead of the list prefixes.
-constexpr u64 kTreeMinSlots = 1ull << 20;
-constexpr u64 kTreeMainMin = 1ull << 16;  // main K5: decided on the point count
-
-// K5 dispatcher: flags[slot] for the query slots of the set.
-template <typename TOut, int D>
-void run_dominance(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint32_t* ids, const u64* fsum,
-                   const u64* count, u64 cap, unsigned* hist, unsigned* cursor, u64* valid_ctr, u64 q_begin = 0,
-                   const u64* q_end = nullptr, int cell_level = 0, u64 tree_min = kTreeMinSlots,
-                   const u64* valid_count = nullptr) {
-  int mode = k5_mode(ctx);
-  if (mode == 2) {
-    if (cap <= tree_min) {
-      mode = 0;
-    } else {
-      // decide on the number of points (valid_count) when known, else slots
-      u64 nslots = 0;
-      ck(cudaMemcpyAsync(&nslots, valid_count ? valid_count : count, 8, cudaMemcpyDeviceToHost, s), "D2H");
-      ck(cudaStreamSynchronize(s), "sync");
-      mode = nslots > tree_min ? 1 : 0;
-    }
-  }
-  if (mode == 0)
-    run_exact<TOut, D>(ctx, s, rows, ids, fsum, count, cap, hist, cursor, q_begin, q_end, cell_level);
-  else
-    run_tree<TOut, D>(ctx, s, rows, ids, fsum, count, valid_ctr, q_begin, q_end, cell_level);
-}
-
-template <typename TIn, typename TOut, bool IDENT, int D>
-struct Pipe final : PipeBase {
-  Query q;
-  skycell_gpu_ctx* ctx;
-  cudaStream_t s, s2;
-  u64 n;
-  int rho, nsm;
-
-  // ---- geometry
-  int la;
-  bool test_b, wide;
-  u64 m;
-  uint32_t h_entries, lo_words;
-  size_t tt;
-  u64 table_entries;
-  static constexpr int kStreamThreads = 256;
-  static constexpr int kRecLaThreads = 768;
-  // the shape with a record-at-la K1 instance (the headline: d = 4, rho = 6, la = 5)
-  static bool rec_la_shape(int r) {
-    // measured slower than the 3 x 256-thread instance (516 vs 445 us at C2):
-    // kept as an opt-in experiment (SKYCELL_RECLA=1)
-    if constexpr (IDENT && D == 4) return r == 6 && std::getenv("SKYCELL_RECLA") != nullptr;
-    return false;
-  }
-  int k1_threads = kStreamThreads;
-  bool rec_la = false;
-  static constexpr int PPT1 = std::max(1, ppt_for<TIn, D>() / 2);
-  static constexpr unsigned kChunk1 = 256, kChunk4 = 64;
-  static_assert(kChunk1 >= 32 * PPT1, "a stream tile's survivors must fit one output chunk");
-  size_t smem1;
-  void (*kstream)(sk::StreamParams);
-  int grid1, grid4, pf_max;
-  u64 cap1, cap4;
-  size_t smem_pf;
-  u64 id_words;
-  unsigned bit_blocks;
-  bool k1_head = false;  // K1 ran the filter-point head (its D stream feeds K4's points_examined)
-
-  // ---- zeroed region
-  size_t o_ctr, o_sla, o_srho, o_shist, o_scur, o_hist, o_cur, o_fhist, o_fcur, o_idbits, o_bcount, o_end, o_total;
-  std::vector<size_t> o_occ;
-
-  u64 words_at(int L) const { return std::max<u64>(1, (1ull << (u64)(L * D)) / 32); }
-  void* at(size_t off) const { return static_cast<char*>(ctx->reset.p) + off; }
-  uint32_t* occ(int L) const { return static_cast<uint32_t*>(at(o_occ[L])); }
-  DevCounters* ctr() const { return static_cast<DevCounters*>(at(o_ctr)); }
-  unsigned* U(size_t off) const { return static_cast<unsigned*>(at(off)); }
-  int cell_level() const { return q.merge ? 0 : rho; }
-
-  static auto pick_stream(int rho) {
-    if constexpr (IDENT && D <= 8) {
-      if constexpr (D == 4)
-        if (rec_la_shape(rho)) return sk::k_stream<TIn, TOut, D, IDENT, kRecLaThreads, PPT1, 6, 1, true>;
-      switch (rho) {
-        case 1: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 1>;
-        case 2: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 2>;
-        case 3: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 3>;
-        case 4: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 4>;
-        case 5: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 5>;
-        case 6: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 6>;
-        case 7: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 7>;
-        default: break;
-      }
-    }
-    return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 0>;
-  }
-
-  explicit Pipe(const Query& qq) : q(qq), ctx(qq.ctx), s(qq.ctx->stream), s2(qq.ctx->side), n(qq.n), rho(qq.rho) {
-    nsm = ctx->num_sms;
-    la = sk::filter_level(rho, D);
-    test_b = rho > la;
-    m = std::min<u64>(n, 1ull << 20);
-    h_entries = (uint32_t)(1ull << (u64)(la * (D - 1)));
-    rec_la = rec_la_shape(rho);
-    k1_threads = rec_la ? kRecLaThreads : kStreamThreads;
-    lo_words = rec_la ? (uint32_t)words_at(la) : (la >= 2 ? (uint32_t)words_at(la - 1) : 0);
-    wide = rho > 7;
-    tt = wide ? 4 : 1;
-    table_entries = 1ull << (u64)(rho * (D - 1));
-
-    // K1 geometry: persistent warps over round-robin warp tiles
-    smem1 = (((size_t)lo_words * 4 + 15) & ~(size_t)15) + ((h_entries + 15) & ~15u) + (size_t)k1_threads * PPT1 +
-            (((size_t)sk::kK1Head * (D * sizeof(TOut) + 8) + 15) & ~(size_t)15) +
-            (size_t)k1_threads * PPT1 * D * sizeof(TIn) + 16;
-    kstream = pick_stream(rho);
-    ck(cudaFuncSetAttribute(kstream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1), "smem attr");
-    int occ_blocks = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_blocks, kstream, k1_threads, smem1), "occupancy");
-    occ_blocks = std::max(1, occ_blocks);
-    const u64 wtiles = (n + 32 * PPT1 - 1) / (32 * PPT1);
-    const u64 wpc = (u64)k1_threads / 32;
-    grid1 = (int)std::max<u64>(1, std::min<u64>((wtiles + wpc - 1) / wpc, (u64)nsm * occ_blocks));
-    cap1 = n + (u64)grid1 * (k1_threads / 32) * kChunk1;
-
-    // K4 geometry
-    grid4 = nsm * 4;
-    cap4 = std::max(cap1, m) + (u64)grid4 * (kThreads / 32) * kChunk4;
-    pf_max = (int)std::min<u64>(1024, (32 * 1024) / (D * sizeof(TOut) + 8));
-    smem_pf = (((u64)pf_max * D * sizeof(TOut) + 15) & ~15ull) + (u64)pf_max * 8 + (u64)D * pf_max * 2 +
-              (u64)D * (sk::kListCols + 1) * 2 + 16;
-    const size_t bin_words = (size_t)D * sk::kListStride;
-    id_words = (n + 31) / 32;
-    bit_blocks = (unsigned)((id_words + sk::kBitsBlock - 1) / sk::kBitsBlock);
-
-    // zeroed region: counters, occupancy layers 1..rho (contiguous: the
-    // sharded exchange ships [o_occ[1], o_occ[rho] + words) as one block)
-    Carver cv;
-    o_ctr = cv.take(sizeof(DevCounters));
-    o_occ.assign(rho + 1, 0);
-    for (int L = 1; L <= rho; ++L) o_occ[L] = cv.take(words_at(L) * 4);
-    o_end = cv.off;
-    o_sla = cv.take(words_at(la) * 4);
-    o_srho = test_b ? cv.take(words_at(rho) * 4) : 0;
-    o_shist = cv.take(bin_words * 4);
-    o_scur = cv.take(bin_words * 4);
-    o_hist = cv.take(bin_words * 4);
-    o_cur = cv.take(bin_words * 4);
-    o_fhist = cv.take(bin_words * 4);
-    o_fcur = cv.take(bin_words * 4);
-    o_idbits = cv.take(id_words * 4);
-    o_bcount = cv.take((size_t)bit_blocks * 4);
-    o_total = cv.off;
-    ensure(ctx->reset, o_total);
-
-    // working buffers
-    ensure(ctx->H, std::max<u64>(h_entries, 16));
-    if (lo_words) ensure(ctx->slabs, (size_t)grid1 * lo_words * 4);
-    ensure(ctx->table, table_entries * tt);
-    ensure(ctx->table2, table_entries * tt);
-    if (test_b) ensure(ctx->table_s, table_entries * tt);
-    ensure(ctx->smp_rows, m * D * sizeof(TOut));
-    ensure(ctx->smp_ids, m * 4);
-    ensure(ctx->smp_fsum, m * 8);
-    ensure(ctx->f_rows, (size_t)pf_max * D * sizeof(TOut));
-    ensure(ctx->f_fsum, (size_t)pf_max * 8);
-    ensure(ctx->f_lists, (size_t)D * pf_max * 2);
-    ensure(ctx->f_offs, (size_t)D * (sk::kListCols + 1) * 2);
-    ensure(ctx->s1_rows, cap1 * D * sizeof(TOut));
-    ensure(ctx->s1_ids, cap1 * 4);
-    ensure(ctx->d_cells, cap1 * (rho * D >= 32 ? 8 : 4));
-    ensure(ctx->s2_rows, cap4 * D * sizeof(TOut));
-    ensure(ctx->s2_ids, cap4 * 4);
-    ensure(ctx->s2_fsum, cap4 * 8);
-    ensure(ctx->flags, cap4);
-    ensure(ctx->lists, (size_t)D * cap4 * 4);
-    ensure(ctx->ids_dev, n * 4);
-  }
-
-  // ---- K0 + K1 (+ slab reduction): everything that reads the input
-  void local() override {
-    DevCounters* c = ctr();
-    if (q.timed) ck(cudaEventRecord(ctx->ev[0], s), "event");
-    ck(cudaMemsetAsync(ctx->reset.p, 0, o_total, s), "memset");
-
-    // K0: sample occupancy, filter tables, sample skyline -> filter points F
-    {
-      sk::SampleParams sp{};
-      sp.coords = q.dev_coords;
-      sp.m = m;
-      sp.rho = rho;
-      sp.la = la;
-      sp.nm = q.nm;
-      sp.occ_la = U(o_sla);
-      sp.occ_rho = test_b ? U(o_srho) : nullptr;
-      sp.rows = ctx->smp_rows.p;
-      sp.ids = static_cast<uint32_t*>(ctx->smp_ids.p);
-      sp.fsum = static_cast<u64*>(ctx->smp_fsum.p);
-      sp.id_base = q.id_base;
-      const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((m + 255) / 256, (u64)nsm * 8));
-      tracer().mark(s, "K0: memset");
-      sk::k_sample<TIn, TOut, D, IDENT><<<g, 256, 0, s>>>(sp);
-      tracer().mark(s, "K0: sample");
-      // H = the strict-dominance height of the sample's level-la occupancy:
-      // a level-la prefix-min table (multi-CTA) shifted by one cell per dim
-      launch_tables<uint8_t>(ctx, s, U(o_sla), la, D, static_cast<uint8_t*>(ctx->table2.p));
-      sk::k_filter_from_table<<<(unsigned)std::max<u64>(1, std::min<u64>((h_entries + 255) / 256, (u64)nsm * 4)), 256, 0,
-                                s>>>(static_cast<const uint8_t*>(ctx->table2.p), la, D, h_entries,
-                                     static_cast<uint8_t*>(ctx->H.p));
-      tracer().mark(s, "K0: build_filter");
-      ctx->launches += 2;
-      // layer-rho prefix-min table of the sample: K1's test B
-      if (test_b) {
-        if (wide) launch_tables<uint32_t>(ctx, s, U(o_srho), rho, D, static_cast<uint32_t*>(ctx->table_s.p));
-        else launch_tables<uint8_t>(ctx, s, U(o_srho), rho, D, static_cast<uint8_t*>(ctx->table_s.p));
-      }
-      if (q.merge) {
-        // The sample skyline only serves as K4's point filter, which phase-1
-        // only semantics (merge_cross_cell = false) cannot use.
-        tracer().mark(s, "K0: sample tables");
-        // sample points not strictly dominated at layer rho -> X (s2 buffers)
-        sk::CandParams pc{};
-        pc.rows = ctx->smp_rows.p;
-        pc.ids = static_cast<const uint32_t*>(ctx->smp_ids.p);
-        pc.count = nullptr;
-        // the filter points come from the skyline of the first mf sample
-        // points (SKYCELL_FSAMPLE overrides; H uses all m)
-        u64 mf = m;
-        if (const char* e = std::getenv("SKYCELL_FSAMPLE")) mf = std::min<u64>(m, std::strtoull(e, nullptr, 10));
-        pc.count_const = mf;
-        pc.rho = rho;
-        pc.PM = test_b ? ctx->table_s.p : nullptr;
-        pc.f_max = 0;
-        pc.out_rows = ctx->s2_rows.p;
-        pc.out_ids = static_cast<uint32_t*>(ctx->s2_ids.p);
-        pc.out_fsum = static_cast<u64*>(ctx->s2_fsum.p);
-        pc.out_reserved = &c->xs;
-        pc.chunk = kChunk4;
-        pc.kept = &c->xs_kept;
-        pc.examined = nullptr;
-        if (wide) sk::k_candidates<TOut, D, uint32_t, kThreads><<<grid4, kThreads, 16, s>>>(pc);
-        else sk::k_candidates<TOut, D, uint8_t, kThreads><<<grid4, kThreads, 16, s>>>(pc);
-        ++ctx->launches;
-        tracer().mark(s, "K0: sample X");
-        // Filter points = the strongest points of the sample's skyline (the
-        // whole skyline: its extremes filter the extremes of the data).  X
-        // is capped at kXMax slots (a random subset: slots follow the sample
-        // order): anti-correlated samples keep ~all points in X, and their
-        // filter points remove little anyway.
-        constexpr u64 kXMax = 1ull << 17;
-        sk::k_pack_members<TOut, D><<<nsm * 4, 256, 0, s>>>(
-            static_cast<const TOut*>(ctx->s2_rows.p), static_cast<const uint32_t*>(ctx->s2_ids.p), nullptr,
-            static_cast<const u64*>(ctx->s2_fsum.p), &c->xs, static_cast<TOut*>(ctx->smp_rows.p),
-            static_cast<u64*>(ctx->smp_fsum.p), static_cast<uint32_t*>(ctx->smp_ids.p), &c->xd);
-        sk::k_clamp_count<<<1, 32, 0, s>>>(&c->xd, kXMax, &c->xs_cap);
-        ctx->launches += 2;
-        run_dominance<TOut, D>(ctx, s, ctx->smp_rows.p, static_cast<const uint32_t*>(ctx->smp_ids.p),
-                               static_cast<const u64*>(ctx->smp_fsum.p), &c->xs_cap, std::min<u64>(m, kXMax),
-                               U(o_shist), U(o_scur), &c->tvalid, 0, nullptr, 0, 96 * 1024);
-        tracer().mark(s, "K0: sample skyline");
-        sk::k_compact_members<TOut, D><<<nsm * 4, 256, 0, s>>>(
-            static_cast<const TOut*>(ctx->smp_rows.p), static_cast<const uint32_t*>(ctx->smp_ids.p),
-            static_cast<const uint8_t*>(ctx->flags.p), static_cast<const u64*>(ctx->smp_fsum.p), &c->xs_cap,
-            static_cast<TOut*>(ctx->s2_rows.p), static_cast<u64*>(ctx->s2_fsum.p), &c->fs);
-        sk::k_strength_order<TOut, D><<<1, 1024, 0, s>>>(
-            static_cast<const TOut*>(ctx->s2_rows.p), static_cast<const u64*>(ctx->s2_fsum.p), nullptr, &c->fs,
-            (uint32_t)pf_max, static_cast<TOut*>(ctx->f_rows.p), static_cast<u64*>(ctx->f_fsum.p), nullptr, &c->nf);
-        sk::k_filter_lists<TOut, D><<<D, 1024, 0, s>>>(static_cast<const TOut*>(ctx->f_rows.p), &c->nf,
-                                                        (uint32_t)pf_max, static_cast<uint16_t*>(ctx->f_lists.p),
-                                                        static_cast<uint16_t*>(ctx->f_offs.p));
-        ++ctx->launches;
-        ctx->launches += 2;
-      }
-    }
-
-    // K1: the streaming pass
-    sk::StreamParams p1{};
-    p1.coords = q.dev_coords;
-    p1.n = n;
-    p1.rho = rho;
-    p1.la = la;
-    p1.lo_words = lo_words;
-    p1.h_entries = h_entries;
-    p1.nm = q.nm;
-    p1.H = static_cast<const uint8_t*>(ctx->H.p);
-    // Test B costs two dependent L2 round trips per K1 survivor; it pays off
-    // when the shared-memory filter level la is at least two layers coarser
-    // than rho (SKYCELL_TESTB=0/1 overrides).
-    bool use_b = test_b && rho - la >= 2;
-    if (const char* e = std::getenv("SKYCELL_TESTB")) use_b = test_b && e[0] == '1';
-    p1.PMs = use_b ? ctx->table_s.p : nullptr;
-    p1.pms_wide = wide;
-    p1.occ_rho = occ(rho);
-    p1.occ_rm1 = rho >= 2 ? occ(rho - 1) : nullptr;
-    p1.slabs = static_cast<uint32_t*>(ctx->slabs.p);
-    p1.out_rows = ctx->s1_rows.p;
-    p1.out_ids = static_cast<uint32_t*>(ctx->s1_ids.p);
-    p1.out_reserved = &c->s1;
-    p1.chunk = kChunk1;
-    p1.kept = &c->s1_kept;
-    p1.nonfinite = &c->nonfinite;
-    p1.id_base = q.id_base;
-    // K1's filter-point head (SKYCELL_K1HEAD=1): cuts S1 ~8x but costs K1
-    // more than it saves K4 at the headline config
-    const char* he = std::getenv("SKYCELL_K1HEAD");
-    k1_head = q.merge && he && he[0] == '1';
-    if (k1_head) {  // the filter points exist (K0) only with the phase-2 merge
-      p1.f_rows = ctx->f_rows.p;
-      p1.f_fsum = static_cast<const u64*>(ctx->f_fsum.p);
-      p1.f_count = &c->nf;
-      p1.d_cells = ctx->d_cells.p;
-      p1.d_reserved = &c->dres;
-    }
-    if (q.timed) ck(cudaEventRecord(ctx->ev[4], s), "event");
-    kstream<<<grid1, k1_threads, smem1, s>>>(p1);
-    ++ctx->launches;
-    if (q.timed) ck(cudaEventRecord(ctx->ev[5], s), "event");
-    if (lo_words) {
-      const unsigned gx = (unsigned)std::max<u64>(1, std::min<u64>((lo_words + 255) / 256, (u64)nsm * 8));
-      const unsigned gy = (unsigned)std::max<u64>(1, std::min<u64>(32, (u64)nsm * 4 / gx));
-      sk::k_reduce_slabs<<<dim3(gx, gy), 256, 0, s>>>(static_cast<uint32_t*>(ctx->slabs.p), grid1, lo_words,
-                                                       occ(rec_la ? la : la - 1));
-      ++ctx->launches;
-    }
-    if (q.timed) ck(cudaEventRecord(ctx->ev[1], s), "event");
-  }
-
-  // ---- sharded exchange 1: the occupancy region of every layer
-  u64 occ_bytes() const override { return o_end - o_occ[1]; }
-  void export_occ(void* dst) override {
-    ck(cudaMemcpyAsync(dst, at(o_occ[1]), occ_bytes(), cudaMemcpyDeviceToDevice, s), "occ export");
-  }
-  void or_gathered(const void* gathered, int world) override {
-    const u64 w4 = occ_bytes() / 16;
-    const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((w4 + 255) / 256, (u64)nsm * 8));
-    sk::k_or_gather<<<g, 256, 0, s>>>(static_cast<const uint4*>(gathered), world, w4,
-                                      static_cast<uint4*>(at(o_occ[1])));
-    ++ctx->launches;
-  }
-
-  // ---- K3 (tables + per-layer counts on the side stream) + K4
-  void prune() {
-    DevCounters* c = ctr();
-    if (wide) launch_tables<uint32_t>(ctx, s, occ(rho), rho, D, static_cast<uint32_t*>(ctx->table.p));
-    else launch_tables<uint8_t>(ctx, s, occ(rho), rho, D, static_cast<uint8_t*>(ctx->table.p));
-    if (q.timed) ck(cudaEventRecord(ctx->ev[2], s), "event");
-
-    // Per-layer |KS_i|, |CS_i| (refine.cpp:125-147), overlapped with K4/K5.
-    // Layer rho from O'_rho; below, O'_rho is OR-ed down into the partial
-    // occupancies recorded by the filter.
-    ck(cudaEventRecord(ctx->ev_fork, s), "event");
-    ck(cudaStreamWaitEvent(s2, ctx->ev_fork, 0), "wait");
-    if (wide) launch_count<uint32_t>(ctx, s2, occ(rho), rho, D, static_cast<const uint32_t*>(ctx->table.p), &c->cand[rho - 1], &c->key[rho - 1]);
-    else launch_count<uint8_t>(ctx, s2, occ(rho), rho, D, static_cast<const uint8_t*>(ctx->table.p), &c->cand[rho - 1], &c->key[rho - 1]);
-    for (int L = rho - 1; L >= 1; --L) {
-      const u64 src_words = words_at(L + 1);
-      const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((src_words + 255) / 256, (u64)nsm * 8));
-      if (L >= 5) {
-        const u64 dst_words = words_at(L);
-        const unsigned gw = (unsigned)std::max<u64>(1, std::min<u64>((dst_words + 255) / 256, (u64)nsm * 8));
-        sk::k_downsample_words<<<gw, 256, 0, s2>>>(occ(L + 1), L, D, dst_words, occ(L));
-      } else {
-        sk::k_downsample<<<g, 256, 0, s2>>>(occ(L + 1), L, D, src_words, occ(L));
-      }
-      ++ctx->launches;
-      if (L > 7) {
-        launch_tables<uint32_t>(ctx, s2, occ(L), L, D, static_cast<uint32_t*>(ctx->table2.p));
-        launch_count<uint32_t>(ctx, s2, occ(L), L, D, static_cast<const uint32_t*>(ctx->table2.p), &c->cand[L - 1], &c->key[L - 1]);
-      } else {
-        launch_tables<uint8_t>(ctx, s2, occ(L), L, D, static_cast<uint8_t*>(ctx->table2.p));
-        launch_count<uint8_t>(ctx, s2, occ(L), L, D, static_cast<const uint8_t*>(ctx->table2.p), &c->cand[L - 1], &c->key[L - 1]);
-      }
-    }
-    ck(cudaEventRecord(ctx->ev_join, s2), "event");
-
-    // K4: candidate cells + sample-skyline point filter
-    sk::CandParams pc{};
-    pc.rows = ctx->s1_rows.p;
-    pc.ids = static_cast<const uint32_t*>(ctx->s1_ids.p);
-    pc.count = &c->s1;
-    pc.rho = rho;
-    pc.PM = ctx->table.p;
-    pc.f_rows = ctx->f_rows.p;
-    pc.f_fsum = static_cast<const u64*>(ctx->f_fsum.p);
-    pc.f_count = q.merge ? &c->nf : nullptr;
-    pc.f_max = q.merge ? (uint32_t)pf_max : 0;
-    pc.f_lists = static_cast<const uint16_t*>(ctx->f_lists.p);
-    pc.f_offs = static_cast<const uint16_t*>(ctx->f_offs.p);
-    pc.out_rows = ctx->s2_rows.p;
-    pc.out_ids = static_cast<uint32_t*>(ctx->s2_ids.p);
-    pc.out_fsum = static_cast<u64*>(ctx->s2_fsum.p);
-    pc.out_reserved = &c->s2;
-    pc.chunk = kChunk4;
-    pc.kept = &c->s2_kept;
-    pc.examined = &c->examined;
-    if (k1_head) {
-      pc.d_cells = ctx->d_cells.p;
-      pc.d_count = &c->dres;
-      pc.d_wide = rho * D >= 32;
-    }
-    auto kc = wide ? sk::k_candidates<TOut, D, uint32_t, kThreads> : sk::k_candidates<TOut, D, uint8_t, kThreads>;
-    ck(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pf), "smem attr");
-    if (q.merge) {
-      // K4a: cell test + the 8 strongest filter points over S1 -> P (dense
-      // pending points, in the S1 buffers' twin); K4b: the rest of the filter
-      // over P, whose lanes are all pending (no idle lanes in the head test)
-      ensure(ctx->p_rows, cap1 * D * sizeof(TOut));
-      ensure(ctx->p_ids, cap1 * 4);
-      ensure(ctx->p_fsum, cap1 * 8);
-      sk::CandParams pa = pc;
-      pa.out_rows = ctx->p_rows.p;
-      pa.out_ids = static_cast<uint32_t*>(ctx->p_ids.p);
-      pa.out_fsum = static_cast<u64*>(ctx->p_fsum.p);
-      pa.out_reserved = &c->pres;
-      pa.kept = &c->pkept;
-      pa.coop = 0;
-      if (!k1_head && !std::getenv("SKYCELL_K4A_OLD")) {
-        auto ka = wide ? sk::k_cand_head<TOut, D, uint32_t, kThreads> : sk::k_cand_head<TOut, D, uint8_t, kThreads>;
-        const size_t sa = ((8 * D * sizeof(TOut) + 15) & ~(size_t)15) + 8 * 8 +
-                          (size_t)(kThreads / 32) * 64 * (D * sizeof(TOut) + 8 + 4) + 16;
-        ck(cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sa), "smem attr");
-        ka<<<grid4, kThreads, sa, s>>>(pa);
-      } else {
-        kc<<<grid4, kThreads, smem_pf, s>>>(pa);
-      }
-      sk::CandParams pb = pc;
-      pb.rows = ctx->p_rows.p;
-      pb.ids = static_cast<const uint32_t*>(ctx->p_ids.p);
-      pb.count = &c->pres;
-      pb.PM = nullptr;
-      pb.examined = nullptr;
-      pb.d_cells = nullptr;
-      pb.head_start = 8;
-      pb.coop = 1;
-      kc<<<grid4, kThreads, smem_pf, s>>>(pb);
-      ctx->launches += 2;
-    } else {
-      kc<<<grid4, kThreads, smem_pf, s>>>(pc);
-      ++ctx->launches;
-    }
-    if (q.timed) ck(cudaEventRecord(ctx->ev[6], s), "event");
-  }
-
-  // ---- K5 over S2 (the local point set)
-  void exact_local() {
-    DevCounters* c = ctr();
-    // the tree above 64K points: measured on one B200, lists win at C2's 50K
-    // (1.45 vs 1.9 ms per query), the tree at anti d=3's 84K (K5 1.3 vs 2.6 ms)
-    run_dominance<TOut, D>(ctx, s, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
-                           static_cast<const u64*>(ctx->s2_fsum.p), &c->s2, cap4, U(o_hist), U(o_cur), &c->tvalid, 0,
-                           nullptr, cell_level(), kTreeMainMin, &c->s2_kept);
-    if (q.timed) ck(cudaEventRecord(ctx->ev[7], s), "event");
-  }
-
-  // ---- K6: members' ids in ascending order through the id bitmap
-  void ids_out(const uint32_t* ids, const u64* count, u64 cap, uint32_t* dst) {
-    DevCounters* c = ctr();
-    uint32_t* idbits = U(o_idbits);
-    unsigned* bcount = U(o_bcount);
-    const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((cap + 255) / 256, (u64)nsm * 8));
-    sk::k_mark_ids<<<g, 256, 0, s>>>(ids, static_cast<const uint8_t*>(ctx->flags.p), count, idbits, q.id_base);
-    sk::k_bits_count<<<bit_blocks, sk::kBitsThreads, 0, s>>>(idbits, id_words, bcount);
-    sk::k_bits_scan<<<1, 1024, 0, s>>>(bcount, bit_blocks, &c->fin);
-    sk::k_bits_write<<<bit_blocks, sk::kBitsThreads, 0, s>>>(idbits, id_words, bcount, dst, q.id_base);
-    ctx->launches += 4;
-  }
-
-  uint32_t* id_dst() const { return q.ids_dev ? q.ids_dev : static_cast<uint32_t*>(ctx->ids_dev.p); }
-
-  void read_counters() {
-    ck(cudaStreamWaitEvent(s, ctx->ev_join, 0), "join");
-    ck(cudaMemcpyAsync(ctx->host_ctr, ctr(), sizeof(DevCounters), cudaMemcpyDeviceToHost, s), "counters D2H");
-    ck(cudaStreamSynchronize(s), "query");
-  }
-
-  void fill_stats(skycell_gpu_stats* st) const {
-    if (!st) return;
-    const DevCounters& hc = *ctx->host_ctr;
-    st->n_layers = rho;
-    for (int L = 1; L <= rho; ++L) {
-      st->keys[L - 1] = hc.key[L - 1] + (u64)D;
-      st->candidates[L - 1] = (q.mode == SKYCELL_SEQUENTIAL && L != rho) ? -1 : (int64_t)hc.cand[L - 1];
-    }
-    st->points_examined = hc.examined;
-    st->survivors_stream = hc.s1_kept;
-    st->survivors_filter = hc.s2_kept;
-  }
-
-  void check_finite() const {
-    const DevCounters& hc = *ctx->host_ctr;
-    if (hc.nonfinite)
-      throw ApiFail{SKYCELL_INPUT,
-                    "normalize: non-finite coordinate in record " + std::to_string((u64)q.id_base + ~hc.nonfinite)};
-  }
-
-  // ---- the single-device query
-  void run_single() {
-    DevCounters* c = ctr();
-    tracer().t0 = std::chrono::steady_clock::now();
-    local();
-    tracer().mark(s, "K0+K1");
-    prune();
-    tracer().mark(s, "K3+K4");
-    exact_local();
-    tracer().mark(s, "K5");
-    ids_out(static_cast<const uint32_t*>(ctx->s2_ids.p), &c->s2, cap4, id_dst());
-    tracer().mark(s, "K6");
-    ck(cudaGetLastError(), "kernel launch");
-    if (q.timed) ck(cudaEventRecord(ctx->ev[3], s), "event");
-    read_counters();
-    fill_stats(q.stats);
-  }
-
-  // ---- sharded phase 2: prune against the global occupancy, local skyline
-  u64 prune_local_skyline() override {
-    DevCounters* c = ctr();
-    prune();
-    exact_local();
-    ensure(ctx->sky_rows, cap4 * D * sizeof(TOut));
-    ensure(ctx->sky_fsum, cap4 * 8);
-    ensure(ctx->sky_ids, cap4 * 4);
-    sk::k_pack_members<TOut, D><<<nsm * 4, 256, 0, s>>>(
-        static_cast<const TOut*>(ctx->s2_rows.p), static_cast<const uint32_t*>(ctx->s2_ids.p),
-        static_cast<const uint8_t*>(ctx->flags.p), static_cast<const u64*>(ctx->s2_fsum.p), &c->s2,
-        static_cast<TOut*>(ctx->sky_rows.p), static_cast<u64*>(ctx->sky_fsum.p),
-        static_cast<uint32_t*>(ctx->sky_ids.p), &c->lsky);
-    ++ctx->launches;
-    ck(cudaGetLastError(), "kernel launch");
-    read_counters();
-    check_finite();
-    return ctx->host_ctr->lsky;
-  }
-
-  // Block layout of one rank's local skyline in the exchange buffer:
-  // [rows maxc x D x TOut][fsum maxc x u64][ids maxc x u32], 256-B aligned.
-  static u64 al(u64 b) { return (b + 255) & ~255ull; }
-  u64 rows_bytes(u64 maxc) const { return al(maxc * D * sizeof(TOut)); }
-  u64 block_bytes(u64 maxc) const override { return rows_bytes(maxc) + al(maxc * 8) + al(maxc * 4); }
-
-  void pack(void* dst, u64 maxc) override {
-    const u64 cnt = ctx->host_ctr->lsky;
-    char* b = static_cast<char*>(dst);
-    if (cnt) {
-      ck(cudaMemcpyAsync(b, ctx->sky_rows.p, cnt * D * sizeof(TOut), cudaMemcpyDeviceToDevice, s), "pack");
-      ck(cudaMemcpyAsync(b + rows_bytes(maxc), ctx->sky_fsum.p, cnt * 8, cudaMemcpyDeviceToDevice, s), "pack");
-      ck(cudaMemcpyAsync(b + rows_bytes(maxc) + al(maxc * 8), ctx->sky_ids.p, cnt * 4, cudaMemcpyDeviceToDevice, s),
-         "pack");
-    }
-    if (maxc > cnt) {
-      uint32_t* ids = reinterpret_cast<uint32_t*>(b + rows_bytes(maxc) + al(maxc * 8));
-      sk::k_fill_u32<<<nsm, 256, 0, s>>>(ids + cnt, maxc - cnt, sk::kNoId);
-      ++ctx->launches;
-    }
-  }
-
-  // ---- sharded phase 3: own local skyline against the union -> ids
-  void finish(const void* recv, int world, u64 maxc, int rank, u64 own_count, uint32_t* ids_dst, uint64_t* n_out,
-              skycell_gpu_stats* st) override {
-    DevCounters* c = ctr();
-    const u64 un = (u64)world * maxc;
-    const u64 cap = std::max<u64>(un, 1);
-    // the union, unpacked into flat slot arrays (S2's buffers are free now)
-    ensure(ctx->s2_rows, cap * D * sizeof(TOut));
-    ensure(ctx->s2_fsum, cap * 8);
-    ensure(ctx->s2_ids, cap * 4);
-    ensure(ctx->flags, cap);
-    ensure(ctx->lists, (size_t)D * cap * 4);
-    const char* r = static_cast<const char*>(recv);
-    const u64 bb = block_bytes(maxc);
-    if (maxc) {
-      ck(cudaMemcpy2DAsync(ctx->s2_rows.p, maxc * D * sizeof(TOut), r, bb, maxc * D * sizeof(TOut), world,
-                           cudaMemcpyDeviceToDevice, s), "unpack rows");
-      ck(cudaMemcpy2DAsync(ctx->s2_fsum.p, maxc * 8, r + rows_bytes(maxc), bb, maxc * 8, world,
-                           cudaMemcpyDeviceToDevice, s), "unpack sums");
-      ck(cudaMemcpy2DAsync(ctx->s2_ids.p, maxc * 4, r + rows_bytes(maxc) + al(maxc * 8), bb, maxc * 4, world,
-                           cudaMemcpyDeviceToDevice, s), "unpack ids");
-    }
-    ctx->host_param[0] = un;
-    ctx->host_param[1] = (u64)rank * maxc + own_count;
-    ck(cudaMemcpyAsync(&c->un, ctx->host_param, 16, cudaMemcpyHostToDevice, s), "params");
-    ck(cudaMemsetAsync(ctx->flags.p, 0, cap, s), "flags");
-    run_dominance<TOut, D>(ctx, s, ctx->s2_rows.p, static_cast<const uint32_t*>(ctx->s2_ids.p),
-                           static_cast<const u64*>(ctx->s2_fsum.p), &c->un, cap, U(o_fhist), U(o_fcur), &c->tvalid,
-                           (u64)rank * maxc, &c->qend, cell_level());
-    ids_out(static_cast<const uint32_t*>(ctx->s2_ids.p), &c->un, cap, ids_dst ? ids_dst : id_dst());
-    ck(cudaGetLastError(), "kernel launch");
-    if (q.timed) ck(cudaEventRecord(ctx->ev[3], s), "event");
-    read_counters();
-    *n_out = ctx->host_ctr->fin;
-    fill_stats(st);
-  }
-};
+namespace skyeng {
 
 // --------------------------------------------------------- query plumbing
 template <typename TIn>
@@ -1035,7 +39,7 @@ const void* stage_input(skycell_gpu_ctx* ctx, const TIn* coords, u64 n, int d) {
   return ctx->staging.p;
 }
 
-bool is_device_ptr(const void* p) {
+inline bool is_device_ptr(const void* p) {
   cudaPointerAttributes a{};
   const bool dev = p && cudaPointerGetAttributes(&a, p) == cudaSuccess &&
                    (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged);
@@ -1107,45 +111,34 @@ bool identity_range(const Query& q, const double* dmin, const double* dmax) {
   }
 }
 
-// Dispatch on (input type, identity range, d) to a Pipe instance.
-template <typename TIn, template <typename, typename, bool, int> class F, typename... A>
-void dispatch(const Query& q, bool ident, A&&... a) {
-  constexpr bool kF32 = sizeof(TIn) == 4;
-#define SKYCELL_CASE(DD)                                                \
-  case DD:                                                              \
-    if constexpr (kF32) {                                               \
-      if (ident) F<float, float, true, DD>::run(q, a...);               \
-      else F<float, double, false, DD>::run(q, a...);                   \
-    } else {                                                            \
-      F<double, double, false, DD>::run(q, a...);                       \
-    }                                                                   \
-    break;
-  switch (q.d) {
-    SKYCELL_CASE(2) SKYCELL_CASE(3) SKYCELL_CASE(4) SKYCELL_CASE(5) SKYCELL_CASE(6) SKYCELL_CASE(7)
-    SKYCELL_CASE(8) SKYCELL_CASE(9) SKYCELL_CASE(10) SKYCELL_CASE(11) SKYCELL_CASE(12) SKYCELL_CASE(13)
-    SKYCELL_CASE(14) SKYCELL_CASE(15) SKYCELL_CASE(16)
-    default:
-      throw ApiFail{SKYCELL_INPUT, "normalize: dimensionality must be at most 16"};
+// Dispatch on (input type, identity range, d) to a Pipe instance (inst.cu).
+inline int kind_of(bool f32, bool ident) { return f32 ? (ident ? 0 : 1) : 2; }
+
+#define SKYCELL_DCASES(CALL)                                                                          \
+  switch (q.d) {                                                                                    \
+    case 2: CALL(2); break; case 3: CALL(3); break; case 4: CALL(4); break; case 5: CALL(5); break; \
+    case 6: CALL(6); break; case 7: CALL(7); break; case 8: CALL(8); break; case 9: CALL(9); break; \
+    case 10: CALL(10); break; case 11: CALL(11); break; case 12: CALL(12); break;                   \
+    case 13: CALL(13); break; case 14: CALL(14); break; case 15: CALL(15); break;                  \
+    case 16: CALL(16); break;                                                                       \
+    default: throw ApiFail{SKYCELL_INPUT, "normalize: dimensionality must be at most 16"};         \
   }
-#undef SKYCELL_CASE
+
+template <typename TIn>
+void dispatch_single(const Query& q, bool ident) {
+  const int kind = kind_of(sizeof(TIn) == 4, ident);
+#define SKYCELL_RUN(DD) run_single_d<DD>(q, kind)
+  SKYCELL_DCASES(SKYCELL_RUN)
+#undef SKYCELL_RUN
 }
 
-template <typename TIn, typename TOut, bool IDENT, int D>
-struct RunSingle {
-  static void run(const Query& q) {
-    Pipe<TIn, TOut, IDENT, D> p(q);
-    p.run_single();
-  }
-};
-
-template <typename TIn, typename TOut, bool IDENT, int D>
-struct MakeShard {
-  static void run(const Query& q, std::unique_ptr<PipeBase>* out) {
-    auto p = std::make_unique<Pipe<TIn, TOut, IDENT, D>>(q);
-    p->local();
-    *out = std::move(p);
-  }
-};
+template <typename TIn>
+void dispatch_shard(const Query& q, bool ident, std::unique_ptr<PipeBase>* out) {
+  const int kind = kind_of(sizeof(TIn) == 4, ident);
+#define SKYCELL_MAKE(DD) make_shard_d<DD>(q, kind, out)
+  SKYCELL_DCASES(SKYCELL_MAKE)
+#undef SKYCELL_MAKE
+}
 
 template <typename F>
 int guarded(char* err, size_t err_len, F&& body) {
@@ -1173,7 +166,7 @@ int run_query(skycell_gpu_ctx* ctx, const TIn* coords, u64 n, int d, const doubl
     const auto t_begin = std::chrono::steady_clock::now();
     if (!n_out || !ids_out) throw ApiFail{SKYCELL_USAGE, "skycell_gpu: null output pointer"};
     Query q = make_query<TIn>(ctx, coords, n, d, dmin, dmax, rho, mode, merge, ids_out, stats, 0);
-    dispatch<TIn, RunSingle>(q, identity_range<TIn>(q, dmin, dmax));
+    dispatch_single<TIn>(q, identity_range<TIn>(q, dmin, dmax));
     const DevCounters& hc = *ctx->host_ctr;
     if (hc.nonfinite)
       throw ApiFail{SKYCELL_INPUT, "normalize: non-finite coordinate in record " + std::to_string(~hc.nonfinite)};
@@ -1221,7 +214,9 @@ void quadrant_launch(skycell_gpu_ctx* ctx, const double* dev, u64 n, const sk::N
   ctx->launches += 5;
 }
 
-}  // namespace
+}  // namespace skyeng
+
+using namespace skyeng;
 
 extern "C" {
 
@@ -1259,7 +254,7 @@ void skycell_gpu_destroy(skycell_gpu_ctx* ctx) {
                     &ctx->s2_ids, &ctx->s2_fsum, &ctx->flags, &ctx->sky_rows, &ctx->sky_ids, &ctx->sky_fsum,
                     &ctx->q_bits, &ctx->q_orig, &ctx->q_sub, &ctx->q_ids, &ctx->q_mm, &ctx->t_keys,
                     &ctx->t_keys2, &ctx->t_vals, &ctx->t_vals2, &ctx->t_cub, &ctx->t_rows, &ctx->t_ids,
-                    &ctx->t_fsum, &ctx->t_lo, &ctx->t_hi, &ctx->t_cs, &ctx->t_ci, &ctx->long_q, &ctx->long_n, &ctx->scan_tot, &ctx->d_cells, &ctx->t_cm, &ctx->t_kill, &ctx->p_rows, &ctx->p_ids, &ctx->p_fsum};
+                    &ctx->t_fsum, &ctx->t_lo, &ctx->t_hi, &ctx->t_cs, &ctx->t_ci, &ctx->long_q, &ctx->long_n, &ctx->scan_tot, &ctx->d_cells, &ctx->t_cm, &ctx->t_kill, &ctx->p_rows, &ctx->p_ids, &ctx->p_fsum, &ctx->k5dbg};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (auto& e : ctx->ev)
@@ -1385,12 +380,12 @@ int skycell_gpu_shard_begin(skycell_gpu_ctx* ctx, const void* coords, int coords
       Query q = make_query<float>(ctx, static_cast<const float*>(coords), n, d, dim_min, dim_max, rho, mode, 1,
                                   nullptr, nullptr, id_base);
       q.timed = true;  // K1 events: stream_kernel_ms of the finish stats
-      dispatch<float, MakeShard>(q, identity_range<float>(q, dim_min, dim_max), &ctx->shard);
+      dispatch_shard<float>(q, identity_range<float>(q, dim_min, dim_max), &ctx->shard);
     } else {
       Query q = make_query<double>(ctx, static_cast<const double*>(coords), n, d, dim_min, dim_max, rho, mode, 1,
                                    nullptr, nullptr, id_base);
       q.timed = true;
-      dispatch<double, MakeShard>(q, false, &ctx->shard);
+      dispatch_shard<double>(q, false, &ctx->shard);
     }
     ck(cudaGetLastError(), "kernel launch");
     *occ_bytes = ctx->shard->occ_bytes();

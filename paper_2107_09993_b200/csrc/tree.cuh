@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(256) k_tree_query(const T* __restrict__ srows,
                                                     const u64* __restrict__ sfsum, const uint32_t* __restrict__ order,
                                                     TreeView<T, D> tv, TreeShape sh, u64 q_begin,
                                                     const u64* __restrict__ q_end, int cell_level,
-                                                    uint8_t* __restrict__ flag) {
+                                                    uint8_t* __restrict__ flag, u64* __restrict__ vstats) {
   constexpr int F = tree_fanout<D>();
   constexpr int kStack = 192;  // >= levels * (F - 1) + levels for every fan-out
   // stack entries: level << 27 | index within the level (nleaf < 2^27)
@@ -312,6 +312,7 @@ __global__ void __launch_bounds__(256) k_tree_query(const T* __restrict__ srows,
     for (int k = 1; k < D; ++k)
       if (kd == k) pk = v[k];
     bool dom = false;
+    unsigned n_nodes = 0, n_leaves = 0;  // SKYCELL_K5STATS diagnostics
     const uint32_t lp = (uint32_t)(j / kLeaf);  // p's own leaf
     // Jump start: dominators of p are usually near p along the Z-order, so
     // the search begins at p's own leaf and widens level by level -- the
@@ -336,6 +337,7 @@ __global__ void __launch_bounds__(256) k_tree_query(const T* __restrict__ srows,
       const int lvl = (int)(e >> 27);
       const uint32_t idx = e & ((1u << 27) - 1);
       if (lvl == 0) {
+        ++n_leaves;
         const u64 q = (u64)idx * kLeaf + lane;
         bool d_l = false;
         if (q < sh.m) {
@@ -353,6 +355,7 @@ __global__ void __launch_bounds__(256) k_tree_query(const T* __restrict__ srows,
         continue;
       }
       // internal node: children F idx .. F idx + F - 1 of level lvl - 1
+      ++n_nodes;
       const uint32_t cidx0 = F * idx;
       const int nc = (int)min((uint32_t)F, sh.cnt[lvl - 1] - cidx0);
       const uint32_t c0 = sh.off[lvl - 1] + cidx0;
@@ -400,6 +403,11 @@ __global__ void __launch_bounds__(256) k_tree_query(const T* __restrict__ srows,
       __syncwarp();
     }
     if (lane == 0) flag[slot] = dom ? 0 : 1;
+    if (vstats && lane == 0) {
+      atomicAdd(vstats + (dom ? 0 : 3), 1ull);
+      atomicAdd(vstats + (dom ? 1 : 4), (u64)n_nodes);
+      atomicAdd(vstats + (dom ? 2 : 5), (u64)n_leaves);
+    }
     __syncwarp();
   }
 }

@@ -253,3 +253,16 @@ def test_gpu_high_dimensions(engine, oracle, d):
                 want = oracle.compute_skyline(x.astype(np.float64), mn, mx, rho)
                 got = engine.compute_skyline(sky.Dataset(np.ascontiguousarray(x), mn, mx), rho)
                 check(got, want.ids, want.points_examined, want.keys, want.candidates)
+
+
+@pytest.mark.parametrize("d,rho", [(3, 1), (4, 2)])
+def test_gpu_phase1_only_large_tree(forced_engine, oracle, d, rho):
+    """merge_cross_cell = false with more than 64K points in the K5 set (the
+    size at which the tree's champion prefilter would run): dominators must
+    stay inside p's layer-rho cell, so the prefilter must not run."""
+    from oracle.oracle import quantize_f32
+    v = oracle.generate(2, 150_000, d, 77)
+    x = quantize_f32(v)
+    want = oracle.compute_skyline(x.astype(np.float64), np.zeros(d), np.ones(d), rho, 1, False)
+    got = forced_engine.compute_skyline(sky.Dataset(x, np.zeros(d), np.ones(d)), rho, merge_cross_cell=False)
+    check(got, want.ids, want.points_examined, want.keys, want.candidates)
