@@ -155,6 +155,28 @@ int skycell_gpu_generate(skycell_gpu_ctx* ctx, int dist, uint64_t n, int d, uint
 int skycell_gpu_generate_range(skycell_gpu_ctx* ctx, int dist, uint64_t n, int d, uint64_t seed, int kind,
                                uint64_t begin, uint64_t count, void* dev_out, char* err, size_t err_len);
 
+/* ---- SKYC dataset files (skycell::read_bin / write_bin, datagen.cpp:185-221;
+ * declared at proj/include/skycell/datagen.hpp:86-87).
+ * Format: "SKYC" | u32 version 1 | u32 d | u64 n | n*d f64, little-endian.
+ *
+ *   skycell_bin_header   host only: validates the header exactly as read_bin
+ *                        does (bad magic, unsupported version, bad
+ *                        dimensionality -> SKYCELL_INPUT; cannot open ->
+ *                        SKYCELL_IO) and returns n and d
+ *   skycell_gpu_read_bin streams the coordinates into dev_coords (a device
+ *                        buffer of cap_values doubles) through pinned staging
+ *                        and reduces dim_min / dim_max on the device
+ *                        (Dataset::compute_minmax, dataset.cpp:10-20); a short
+ *                        file is "<path>: truncated file" (SKYCELL_INPUT).
+ *                        n >= 2^32 is rejected (the reference truncates
+ *                        Dataset::n to uint32).
+ *   skycell_gpu_write_bin writes n x d doubles from host or device memory. */
+int skycell_bin_header(const char* path, uint64_t* n, int* d, char* err, size_t err_len);
+int skycell_gpu_read_bin(skycell_gpu_ctx* ctx, const char* path, double* dev_coords, uint64_t cap_values,
+                         uint64_t* n_out, int* d_out, double* dim_min, double* dim_max, char* err, size_t err_len);
+int skycell_gpu_write_bin(skycell_gpu_ctx* ctx, const char* path, const double* coords, uint64_t n, int d,
+                          char* err, size_t err_len);
+
 /* MultiLayerGrid::default_rho (grid.cpp:30-33). */
 int skycell_default_rho(uint64_t n, int d);
 

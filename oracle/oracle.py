@@ -197,10 +197,31 @@ class Reference:
                                       C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t]
         L.ref_normalize.argtypes = [C.POINTER(C.c_double), C.c_uint64, C.c_int, C.POINTER(C.c_double),
                                     C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_char_p, C.c_size_t]
+        L.ref_write_bin.argtypes = [C.c_char_p, C.POINTER(C.c_double), C.c_uint64, C.c_int, C.c_char_p, C.c_size_t]
+        L.ref_read_bin.argtypes = [C.c_char_p, C.POINTER(C.c_uint64), C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                   C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_char_p, C.c_size_t]
 
     def _check(self, rc, err):
         if rc != 0:
             raise CpuError(rc, err.value.decode())
+
+    def write_bin(self, path: str, coords) -> None:
+        """skycell::write_bin (datagen.cpp:185-199)."""
+        x = _f64(coords)
+        err = C.create_string_buffer(512)
+        self._check(self.lib.ref_write_bin(path.encode(), _ptr(x, C.c_double), x.shape[0], x.shape[1], err, 512), err)
+
+    def read_bin(self, path: str):
+        """skycell::read_bin (datagen.cpp:201-221): (coords, dim_min, dim_max)."""
+        n, d = C.c_uint64(0), C.c_int(0)
+        err = C.create_string_buffer(512)
+        null = C.POINTER(C.c_double)()
+        self._check(self.lib.ref_read_bin(path.encode(), C.byref(n), C.byref(d), null, null, null, err, 512), err)
+        x = np.empty((n.value, d.value), dtype=np.float64)
+        mn, mx = np.empty(d.value), np.empty(d.value)
+        self._check(self.lib.ref_read_bin(path.encode(), C.byref(n), C.byref(d), _ptr(x, C.c_double),
+                                          _ptr(mn, C.c_double), _ptr(mx, C.c_double), err, 512), err)
+        return x, mn, mx
 
     def generate(self, dist: int, n: int, d: int, seed: int, workers: int = 0) -> np.ndarray:
         out = np.empty((n, d), dtype=np.float64)

@@ -11,6 +11,7 @@
 //   skycell::quadrant_skyline    proj/src/refine.cpp:160-184
 //   skycell::brute_force_skyline proj/src/baseline.cpp:32-58
 //   MultiLayerGrid::default_rho  proj/src/grid.cpp:30-33
+//   skycell::write_bin/read_bin  proj/src/datagen.cpp:185-221
 //
 // Exceptions are mapped onto the same status codes the product C-ABI uses
 // (include/skycell_gpu.h) so that error parity can be asserted code-for-code
@@ -102,6 +103,29 @@ int ref_generate(int dist, uint64_t n, int d, uint64_t seed, int workers, double
 }
 
 int ref_default_rho(uint64_t n, int d) { return skycell::MultiLayerGrid::default_rho(n, d); }
+
+int ref_write_bin(const char* path, const double* coords, uint64_t n, int d, char* err, size_t err_len) {
+  return guarded(err, err_len, [&] {
+    const std::vector<double> lo(d, 0.0), hi(d, 1.0);
+    skycell::write_bin(make_ds(coords, n, d, lo.data(), hi.data()), path);
+  });
+}
+
+// read_bin in two calls: the header (n, d), then the data and min/max into
+// caller buffers (out may be null on the first call).
+int ref_read_bin(const char* path, uint64_t* n, int* d, double* out, double* dmin, double* dmax, char* err,
+                 size_t err_len) {
+  return guarded(err, err_len, [&] {
+    const skycell::Dataset ds = skycell::read_bin(path);
+    *n = ds.n;
+    *d = ds.d;
+    if (out) {
+      std::memcpy(out, ds.coords.data(), ds.coords.size() * sizeof(double));
+      std::memcpy(dmin, ds.dim_min.data(), ds.d * sizeof(double));
+      std::memcpy(dmax, ds.dim_max.data(), ds.d * sizeof(double));
+    }
+  });
+}
 
 static void fill_stats(const skycell::SkylineResult& r, ref_stats* st) {
   if (st == nullptr) return;

@@ -6,12 +6,12 @@ API.  See DESIGN.md.
 """
 from .skycell import (  # noqa: F401
     ConfigError, CudaError, Dataset, Engine, InputError, IoError, LayerCounts, Mode, SkycellError,
-    SkylineResult, StageTimes, UnsupportedError, UsageError, compute_skyline, default_rho, engine,
+    SkylineResult, StageTimes, UnsupportedError, UsageError, bin_header, compute_skyline, default_rho, engine,
     load_library, quadrant_skyline, validate,
 )
 
 __all__ = [
     "ConfigError", "CudaError", "Dataset", "Engine", "InputError", "IoError", "LayerCounts", "Mode",
-    "SkycellError", "SkylineResult", "StageTimes", "UnsupportedError", "UsageError", "compute_skyline",
+    "SkycellError", "SkylineResult", "StageTimes", "UnsupportedError", "UsageError", "bin_header", "compute_skyline",
     "default_rho", "engine", "load_library", "quadrant_skyline", "validate",
 ]

@@ -17,9 +17,10 @@
 
 #include "../../include/skycell_gpu.h"
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include "kernels.cuh"
-#include "tree.cuh"
+#include "packet.cuh"
 #include "datagen.cuh"
 
 using sk::u64;
@@ -119,7 +120,7 @@ struct skycell_gpu_ctx {
   skyeng::DevBuf t_keys, t_keys2, t_vals, t_vals2, t_cub, t_rows, t_ids, t_fsum, t_lo, t_hi, t_cs, t_ci;  // K5 tree
   skyeng::DevBuf t_cm, t_kill;  // K5 tree champion prefilter
   skyeng::DevBuf k5dbg;         // SKYCELL_K5STATS visit counters
-  int k5_mode = -1;  // 0 lists, 1 tree, 2 auto (SKYCELL_K5)
+  int k5_mode = -1;  // 0 lists, 1 tree (packet query), 2 auto, 3 tree (point query); SKYCELL_K5
   skyeng::DevBuf long_q, long_n;  // K5 phase-B queue
   skyeng::DevBuf scan_tot;        // K5 list-scan chunk totals
   skyeng::DevCounters* host_ctr = nullptr;  // pinned
@@ -135,6 +136,25 @@ inline void put_err(char* err, size_t len, const std::string& m) {
   if (!err || !len) return;
   std::strncpy(err, m.c_str(), len - 1);
   err[len - 1] = '\0';
+}
+
+// Runs an entry point's body, mapping exceptions onto status codes + err.
+template <typename F>
+inline int guarded(char* err, size_t err_len, F&& body) {
+  try {
+    body();
+    return SKYCELL_OK;
+  } catch (const ApiFail& f) {
+    put_err(err, err_len, f.msg);
+    return f.code;
+  } catch (const CudaFail& f) {
+    put_err(err, err_len, std::string("CUDA error in ") + f.what + ": " + cudaGetErrorString(f.e));
+    cudaGetLastError();
+    return SKYCELL_CUDA;
+  } catch (const std::exception& e) {
+    put_err(err, err_len, std::string("skycell_gpu: ") + e.what());
+    return SKYCELL_CUDA;
+  }
 }
 
 // Bump allocator over the per-query zeroed region.
@@ -293,7 +313,8 @@ void run_exact(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uin
 // set's slot count on the host (CUB's item count), so it synchronises once.
 template <typename TOut, int D>
 void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint32_t* ids, const u64* fsum,
-              const u64* count, u64* valid_ctr, u64 q_begin, const u64* q_end, int cell_level) {
+              const u64* count, u64* valid_ctr, u64 q_begin, const u64* q_end, int cell_level,
+              bool point_query = false) {
   const int nsm = ctx->num_sms;
   u64 hv[2];
   ck(cudaMemcpyAsync(&hv[0], count, 8, cudaMemcpyDeviceToHost, s), "D2H");
@@ -377,62 +398,125 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
   }
   sh.levels = L;
   const u64 nodes = off;
-  ensure(ctx->t_rows, m * D * sizeof(TOut));
-  ensure(ctx->t_ids, m * 4);
-  ensure(ctx->t_fsum, m * 8);
-  ensure(ctx->t_lo, nodes * D * sizeof(TOut));
-  ensure(ctx->t_hi, nodes * D * sizeof(TOut));
-  ensure(ctx->t_cs, nodes * 8);
-  ensure(ctx->t_ci, nodes * 4);
-  TOut* srows = static_cast<TOut*>(ctx->t_rows.p);
-  uint32_t* sids = static_cast<uint32_t*>(ctx->t_ids.p);
-  u64* sfsum = static_cast<u64*>(ctx->t_fsum.p);
   const uint32_t* order = static_cast<const uint32_t*>(ctx->t_vals2.p);
   const unsigned gm = (unsigned)std::max<u64>(1, std::min<u64>((m + 255) / 256, (u64)nsm * 8));
-  sk::k_tree_gather<TOut, D><<<gm, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, order, m, srows, sids, sfsum);
-  sk::TreeView<TOut, D> tv{static_cast<TOut*>(ctx->t_lo.p), static_cast<TOut*>(ctx->t_hi.p),
-                           static_cast<u64*>(ctx->t_cs.p), static_cast<uint32_t*>(ctx->t_ci.p)};
   const unsigned gl = (unsigned)std::max<u64>(1, std::min<u64>((sh.nleaf * 32 + 255) / 256, (u64)nsm * 8));
-  sk::k_tree_leaves<TOut, D><<<gl, 256, 0, s>>>(srows, sids, sfsum, m, sh.nleaf, tv);
-  ctx->launches += 2;
-  for (int l = 1; l < sh.levels; ++l) {
-    const unsigned gn = (unsigned)std::max<u64>(1, std::min<u64>((sh.cnt[l] + 255) / 256, (u64)nsm * 8));
-    sk::k_tree_level<TOut, D><<<gn, 256, 0, s>>>(tv, sh.off[l - 1], sh.cnt[l - 1], sh.off[l], sh.cnt[l]);
-    ++ctx->launches;
-  }
-  tracer().mark(s, "tree: build");
-  const unsigned gq = (unsigned)std::max<u64>(1, std::min<u64>((m * 32 + 255) / 256, (u64)nsm * 8));
   const bool dbg = std::getenv("SKYCELL_K5STATS") != nullptr;
   u64* vst = nullptr;
   if (dbg) {
-    ensure(ctx->k5dbg, 64);
+    ensure(ctx->k5dbg, 128);
     vst = static_cast<u64*>(ctx->k5dbg.p);
-    ck(cudaMemsetAsync(vst, 0, 64, s), "memset");
+    ck(cudaMemsetAsync(vst, 0, 128, s), "memset");
   }
-  sk::k_tree_query<TOut, D><<<gq, 256, 0, s>>>(srows, sids, sfsum, order, tv, sh, q_begin, q_end, cell_level,
-                                              static_cast<uint8_t*>(ctx->flags.p), vst);
-  ++ctx->launches;
-  tracer().mark(s, "tree: query");
+  // packet query (one warp per leaf of query points) unless merge_cross_cell
+  // = false, whose same-cell restriction the point query keeps
+  const bool packet = cell_level == 0 && !point_query;
+  if (packet) {
+    typedef sk::PkLayout<TOut, D> PL;
+    ensure(ctx->t_rows, m * PL::PW * 4);
+    ensure(ctx->t_lo, nodes * PL::NW * 4);
+    uint32_t* prec = static_cast<uint32_t*>(ctx->t_rows.p);
+    uint32_t* nrec = static_cast<uint32_t*>(ctx->t_lo.p);
+    sk::k_pk_gather<TOut, D><<<gm, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, order, m, prec);
+    sk::k_pk_leaves<TOut, D><<<gl, 256, 0, s>>>(prec, m, sh.nleaf, nrec);
+    ctx->launches += 2;
+    for (int l = 1; l < sh.levels; ++l) {
+      const unsigned gn = (unsigned)std::max<u64>(1, std::min<u64>((sh.cnt[l] + 255) / 256, (u64)nsm * 8));
+      sk::k_pk_level<TOut, D><<<gn, 256, 0, s>>>(nrec, sh.off[l - 1], sh.cnt[l - 1], sh.off[l], sh.cnt[l]);
+      ++ctx->launches;
+    }
+    tracer().mark(s, "tree: build");
+    const unsigned gq = (unsigned)std::max<u64>(1, std::min<u64>((sh.nleaf * 32 + 255) / 256, (u64)nsm * 8));
+    // phase-1 search radius (levels above the own leaf); phase 2 re-packs the
+    // undecided points (SKYCELL_PK_H1 overrides; >= levels: one phase)
+    int h1 = D <= 6 ? 5 : 6;  // measured best (C3 d=6: 131 ms at 5; d=7/8: 765 / 1903 ms at 6)
+    if (const char* e = std::getenv("SKYCELL_PK_H1")) h1 = std::atoi(e);
+    const bool two = h1 < sh.levels - 1;
+    uint32_t* umask = static_cast<uint32_t*>(ctx->t_keys.p);       // free after the sort
+    uint32_t* pcnt = static_cast<uint32_t*>(ctx->t_keys2.p);
+    uint32_t* poff = pcnt + sh.nleaf;
+    uint32_t* list = static_cast<uint32_t*>(ctx->t_vals.p);
+    u64* list_n = static_cast<u64*>(ctx->long_n.p) + 1;
+    sk::k_pk_query<TOut, D, false><<<gq, 256, 0, s>>>(prec, nrec, order, sh, q_begin, q_end, h1, two ? umask : nullptr,
+                                                     nullptr, nullptr, static_cast<uint8_t*>(ctx->flags.p), vst);
+    ++ctx->launches;
+    if (two) {
+      tracer().mark(s, "tree: packet phase 1");
+      const unsigned gc = (unsigned)std::max<u64>(1, std::min<u64>((sh.nleaf + 255) / 256, (u64)nsm * 8));
+      sk::k_pk_counts<<<gc, 256, 0, s>>>(umask, sh.nleaf, pcnt);
+      size_t temp = 0;
+      ck(cub::DeviceScan::ExclusiveSum(nullptr, temp, pcnt, poff, (int64_t)sh.nleaf, s), "cub scan temp");
+      ensure(ctx->t_cub, temp);
+      ck(cub::DeviceScan::ExclusiveSum(ctx->t_cub.p, temp, pcnt, poff, (int64_t)sh.nleaf, s), "cub scan");
+      sk::k_pk_list<<<gc, 256, 0, s>>>(umask, poff, sh.nleaf, list, list_n);
+      sk::k_pk_query<TOut, D, true><<<gq, 256, 0, s>>>(prec, nrec, order, sh, q_begin, q_end, h1, nullptr, list, list_n,
+                                                      static_cast<uint8_t*>(ctx->flags.p), vst);
+      ctx->launches += 4;
+    }
+    tracer().mark(s, "tree: packet query");
+  } else {
+    ensure(ctx->t_rows, m * D * sizeof(TOut));
+    ensure(ctx->t_ids, m * 4);
+    ensure(ctx->t_fsum, m * 8);
+    ensure(ctx->t_lo, nodes * D * sizeof(TOut));
+    ensure(ctx->t_hi, nodes * D * sizeof(TOut));
+    ensure(ctx->t_cs, nodes * 8);
+    ensure(ctx->t_ci, nodes * 4);
+    TOut* srows = static_cast<TOut*>(ctx->t_rows.p);
+    uint32_t* sids = static_cast<uint32_t*>(ctx->t_ids.p);
+    u64* sfsum = static_cast<u64*>(ctx->t_fsum.p);
+    sk::k_tree_gather<TOut, D><<<gm, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, order, m, srows, sids, sfsum);
+    sk::TreeView<TOut, D> tv{static_cast<TOut*>(ctx->t_lo.p), static_cast<TOut*>(ctx->t_hi.p),
+                             static_cast<u64*>(ctx->t_cs.p), static_cast<uint32_t*>(ctx->t_ci.p)};
+    sk::k_tree_leaves<TOut, D><<<gl, 256, 0, s>>>(srows, sids, sfsum, m, sh.nleaf, tv);
+    ctx->launches += 2;
+    for (int l = 1; l < sh.levels; ++l) {
+      const unsigned gn = (unsigned)std::max<u64>(1, std::min<u64>((sh.cnt[l] + 255) / 256, (u64)nsm * 8));
+      sk::k_tree_level<TOut, D><<<gn, 256, 0, s>>>(tv, sh.off[l - 1], sh.cnt[l - 1], sh.off[l], sh.cnt[l]);
+      ++ctx->launches;
+    }
+    tracer().mark(s, "tree: build");
+    const unsigned gq = (unsigned)std::max<u64>(1, std::min<u64>((m * 32 + 255) / 256, (u64)nsm * 8));
+    sk::k_tree_query<TOut, D><<<gq, 256, 0, s>>>(srows, sids, sfsum, order, tv, sh, q_begin, q_end, cell_level,
+                                                static_cast<uint8_t*>(ctx->flags.p), vst);
+    ++ctx->launches;
+    tracer().mark(s, "tree: query");
+  }
   if (dbg) {
-    u64 hs[6], killed = 0;
-    ck(cudaMemcpyAsync(hs, vst, 48, cudaMemcpyDeviceToHost, s), "D2H");
+    u64 hs[13], killed = 0;
+    ck(cudaMemcpyAsync(hs, vst, 104, cudaMemcpyDeviceToHost, s), "D2H");
     ck(cudaMemcpyAsync(&killed, valid_ctr + 1, 8, cudaMemcpyDeviceToHost, s), "D2H");
     ck(cudaStreamSynchronize(s), "sync");
-    std::fprintf(stderr,
-                 "[k5stats] D=%d slots=%llu prefilter_killed=%llu tree=%llu nodes=%llu | dominated %llu: %.1f nodes "
-                 "%.1f leaves | members %llu: %.1f nodes %.1f leaves\n",
-                 D, (unsigned long long)nslots, (unsigned long long)killed, (unsigned long long)m,
-                 (unsigned long long)nodes, (unsigned long long)hs[0], hs[0] ? (double)hs[1] / hs[0] : 0.0,
-                 hs[0] ? (double)hs[2] / hs[0] : 0.0, (unsigned long long)hs[3], hs[3] ? (double)hs[4] / hs[3] : 0.0,
-                 hs[3] ? (double)hs[5] / hs[3] : 0.0);
+    if (packet) {
+      u64 ln = 0;
+      ck(cudaMemcpy(&ln, static_cast<u64*>(ctx->long_n.p) + 1, 8, cudaMemcpyDeviceToHost), "D2H");
+      const double p2 = std::max<double>(1.0, (double)((ln + 31) / 32));
+      std::fprintf(stderr,
+                   "[k5stats] D=%d slots=%llu prefilter_killed=%llu tree=%llu nodes=%llu | phase 1: %llu packets, %.1f "
+                   "nodes %.1f leaves %.1f staged points per packet | phase 2: %llu points, %.1f nodes %.1f leaves %.1f "
+                   "staged points per packet\n",
+                   D, (unsigned long long)nslots, (unsigned long long)killed, (unsigned long long)m,
+                   (unsigned long long)nodes, (unsigned long long)sh.nleaf, (double)hs[6] / sh.nleaf,
+                   (double)hs[7] / sh.nleaf, (double)hs[8] / sh.nleaf, (unsigned long long)ln, (double)hs[10] / p2,
+                   (double)hs[11] / p2, (double)hs[12] / p2);
+    }
+    else
+      std::fprintf(stderr,
+                   "[k5stats] D=%d slots=%llu prefilter_killed=%llu tree=%llu nodes=%llu | dominated %llu: %.1f nodes "
+                   "%.1f leaves | members %llu: %.1f nodes %.1f leaves\n",
+                   D, (unsigned long long)nslots, (unsigned long long)killed, (unsigned long long)m,
+                   (unsigned long long)nodes, (unsigned long long)hs[0], hs[0] ? (double)hs[1] / hs[0] : 0.0,
+                   hs[0] ? (double)hs[2] / hs[0] : 0.0, (unsigned long long)hs[3], hs[3] ? (double)hs[4] / hs[3] : 0.0,
+                   hs[3] ? (double)hs[5] / hs[3] : 0.0);
   }
 }
 
-// SKYCELL_K5 = lists | tree | auto (default): which K5 variant runs.
+// SKYCELL_K5 = lists | tree | tree-point | auto (default): which K5 variant
+// runs (tree-point: the tree with the one-warp-per-point query).
 inline int k5_mode(skycell_gpu_ctx* ctx) {
   if (ctx->k5_mode < 0) {
     const char* e = std::getenv("SKYCELL_K5");
-    ctx->k5_mode = (e && !std::strcmp(e, "lists")) ? 0 : (e && !std::strcmp(e, "tree")) ? 1 : 2;
+    ctx->k5_mode = !e ? 2 : !std::strcmp(e, "lists") ? 0 : !std::strcmp(e, "tree") ? 1 : !std::strcmp(e, "tree-point") ? 3 : 2;
   }
   return ctx->k5_mode;
 }
@@ -464,7 +548,7 @@ void run_dominance(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const
   if (mode == 0)
     run_exact<TOut, D>(ctx, s, rows, ids, fsum, count, cap, hist, cursor, q_begin, q_end, cell_level);
   else
-    run_tree<TOut, D>(ctx, s, rows, ids, fsum, count, valid_ctr, q_begin, q_end, cell_level);
+    run_tree<TOut, D>(ctx, s, rows, ids, fsum, count, valid_ctr, q_begin, q_end, cell_level, mode == 3);
 }
 
 template <typename TIn, typename TOut, bool IDENT, int D>

@@ -140,24 +140,6 @@ void dispatch_shard(const Query& q, bool ident, std::unique_ptr<PipeBase>* out) 
 #undef SKYCELL_MAKE
 }
 
-template <typename F>
-int guarded(char* err, size_t err_len, F&& body) {
-  try {
-    body();
-    return SKYCELL_OK;
-  } catch (const ApiFail& f) {
-    put_err(err, err_len, f.msg);
-    return f.code;
-  } catch (const CudaFail& f) {
-    put_err(err, err_len, std::string("CUDA error in ") + f.what + ": " + cudaGetErrorString(f.e));
-    cudaGetLastError();
-    return SKYCELL_CUDA;
-  } catch (const std::exception& e) {
-    put_err(err, err_len, std::string("skycell_gpu: ") + e.what());
-    return SKYCELL_CUDA;
-  }
-}
-
 template <typename TIn>
 int run_query(skycell_gpu_ctx* ctx, const TIn* coords, u64 n, int d, const double* dmin, const double* dmax,
               int rho, int mode, int merge, uint32_t* ids_out, uint64_t* n_out, skycell_gpu_stats* stats, char* err,

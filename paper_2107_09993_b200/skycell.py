@@ -156,7 +156,7 @@ EXPORTS = (
     "skycell_gpu_skyline_f32", "skycell_gpu_quadrant_f64", "skycell_gpu_shard_begin", "skycell_gpu_shard_export_occ",
     "skycell_gpu_shard_prune", "skycell_gpu_shard_block_bytes", "skycell_gpu_shard_pack", "skycell_gpu_shard_finish",
     "skycell_gpu_generate", "skycell_gpu_generate_range", "skycell_default_rho", "skycell_validate",
-    "skycell_gpu_version",
+    "skycell_gpu_version", "skycell_bin_header", "skycell_gpu_read_bin", "skycell_gpu_write_bin",
 )
 
 
@@ -192,6 +192,9 @@ def load_library(path: str = LIB_PATH):
         lib.skycell_default_rho.argtypes = [u64, i32]
         lib.skycell_validate.argtypes = [u64, i32, i32, C.c_char_p, C.c_size_t]
         lib.skycell_gpu_version.restype = C.c_char_p
+        lib.skycell_bin_header.argtypes = [cp, u64p, C.POINTER(C.c_int), cp, sz]
+        lib.skycell_gpu_read_bin.argtypes = [vp, cp, vp, u64, u64p, C.POINTER(C.c_int), dp, dp, cp, sz]
+        lib.skycell_gpu_write_bin.argtypes = [vp, cp, vp, u64, i32, cp, sz]
         _lib = lib
         return lib
 
@@ -199,6 +202,15 @@ def load_library(path: str = LIB_PATH):
 def _raise(code: int, err) -> None:
     if code != 0:
         raise _ERRORS.get(code, SkycellError)(err.value.decode(errors="replace"))
+
+
+def bin_header(path: str) -> tuple[int, int]:
+    """(n, d) of a SKYC file, with read_bin's header checks (datagen.cpp:201-212)."""
+    lib = load_library()
+    n, d = C.c_uint64(0), C.c_int(0)
+    err = C.create_string_buffer(512)
+    _raise(lib.skycell_bin_header(os.fsencode(path), C.byref(n), C.byref(d), err, 512), err)
+    return int(n.value), int(d.value)
 
 
 def default_rho(n: int, d: int) -> int:
@@ -275,6 +287,40 @@ class Engine:
         _raise(self.lib.skycell_gpu_generate_range(self._ctx, int(dist), n, d, seed, 1 if quantized else 0, begin,
                                                    count, C.c_void_p(out.data_ptr()), err, 512), err)
         return out
+
+    def read_bin(self, path: str):
+        """skycell::read_bin (datagen.cpp:201-221) straight into device memory:
+        returns (CUDA float64 tensor (n, d), dim_min, dim_max)."""
+        import torch
+        n, d = bin_header(path)
+        out = torch.empty((max(n, 1), d), dtype=torch.float64, device=f"cuda:{self.device}")
+        mn, mx = np.empty(d), np.empty(d)
+        n_out, d_out = C.c_uint64(0), C.c_int(0)
+        err = C.create_string_buffer(512)
+        with self._lock:
+            rc = self.lib.skycell_gpu_read_bin(self._ctx, os.fsencode(path), C.c_void_p(out.data_ptr()), n * d,
+                                               C.byref(n_out), C.byref(d_out),
+                                               mn.ctypes.data_as(C.POINTER(C.c_double)),
+                                               mx.ctypes.data_as(C.POINTER(C.c_double)), err, 512)
+        _raise(rc, err)
+        return out[:n], mn, mx
+
+    def write_bin(self, path: str, coords) -> None:
+        """skycell::write_bin (datagen.cpp:185-199) from a float64 host array or
+        CUDA tensor of shape (n, d)."""
+        if isinstance(coords, np.ndarray):
+            if coords.dtype != np.float64 or coords.ndim != 2 or not coords.flags.c_contiguous:
+                raise UsageError("write_bin: coords must be a C-contiguous float64 (n, d) array")
+            ptr, (n, d) = coords.ctypes.data, coords.shape
+        else:
+            import torch
+            if coords.dtype != torch.float64 or coords.dim() != 2 or not coords.is_contiguous():
+                raise UsageError("write_bin: coords must be a contiguous float64 (n, d) tensor")
+            ptr, (n, d) = coords.data_ptr(), tuple(coords.shape)
+        err = C.create_string_buffer(512)
+        with self._lock:
+            rc = self.lib.skycell_gpu_write_bin(self._ctx, os.fsencode(path), C.c_void_p(ptr), n, d, err, 512)
+        _raise(rc, err)
 
     def set_stream(self, stream) -> None:
         """Enqueue all later work on `stream` (a torch.cuda.Stream, a raw

@@ -174,7 +174,7 @@ def test_gpu_quadrant_edges(engine, oracle):
     check(got, want.ids, want.points_examined)
 
 
-@pytest.fixture(scope="module", params=["tree", "lists"])
+@pytest.fixture(scope="module", params=["tree", "tree-point", "lists"])
 def forced_engine(request):
     """An engine pinned to one K5 variant (SKYCELL_K5 is read once per context)."""
     import os
@@ -192,7 +192,8 @@ def forced_engine(request):
 
 @pytest.mark.parametrize("seed", range(12))
 def test_gpu_k5_variants_vs_oracle(forced_engine, oracle, seed):
-    """Both K5 variants (column lists, dominance tree) on every path:
+    """Every K5 variant (column lists, dominance tree with the packet or the
+    point query) on every path:
     identity f32, general f64, merge_cross_cell = false."""
     from oracle.oracle import quantize_f32
     rng = np.random.default_rng(500 + seed)
