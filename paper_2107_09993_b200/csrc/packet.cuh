@@ -223,12 +223,19 @@ __device__ __forceinline__ S diff_or(const K (&a)[D], const K* b) {
 // members holding 30 decided lanes through it.
 // vstats (SKYCELL_K5STATS): [6 + 4 * phase] warps, node visits, leaf visits,
 // staged leaf points.
-template <typename T, int D, bool PHASE2>
+//
+// MODE 0: phase 1 (leaf packets), 1: phase 2 (list positions), 2: external
+// queries -- records qrec[0 .. *list_n) in the point layout, not in the tree
+// (an id of kNoId marks an inactive query); flag[e] is set for query e (the
+// sparse layer-rho cell tests, sparse.cuh).
+template <typename T, int D, int MODE>
 __global__ void __launch_bounds__(256, 4) k_pk_query(const uint32_t* __restrict__ prec, const uint32_t* __restrict__ nrec,
                                                   const uint32_t* __restrict__ order, TreeShape sh, u64 q_begin,
                                                   const u64* __restrict__ q_end, int h1, uint32_t* __restrict__ umask,
                                                   const uint32_t* __restrict__ list, const u64* __restrict__ list_n,
-                                                  uint8_t* __restrict__ flag, u64* __restrict__ vstats) {
+                                                  const uint32_t* __restrict__ qrec, uint8_t* __restrict__ flag,
+                                                  u64* __restrict__ vstats) {
+  constexpr bool PHASE2 = MODE != 0;
   typedef PkLayout<T, D> L;
   typedef typename L::K K;
   typedef typename PkKey<T>::S S;
@@ -238,11 +245,13 @@ __global__ void __launch_bounds__(256, 4) k_pk_query(const uint32_t* __restrict_
   __shared__ uint32_t path_s[8][32];
   __shared__ __align__(16) uint32_t leaf_s[8][kLeaf * L::PW];
   __shared__ __align__(16) uint32_t node_s[8][F * L::NW];
+  __shared__ K pmax_s[8][D];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint32_t* stk = stack_s[wib];
   uint32_t* path = path_s[wib];
   uint32_t* lf = leaf_s[wib];
   uint32_t* nb = node_s[wib];
+  K* pmax_w = pmax_s[wib];
   const u64 qend = q_end ? *q_end : ~0ull;
   const u64 npk = PHASE2 ? (*list_n + kLeaf - 1) / kLeaf : sh.nleaf;
   const u64 lcount = PHASE2 ? *list_n : 0;
@@ -254,7 +263,7 @@ __global__ void __launch_bounds__(256, 4) k_pk_query(const uint32_t* __restrict_
     u64 j = ~0ull;
     if (PHASE2) {
       const u64 e = pk * kLeaf + lane;
-      if (e < lcount) j = list[e];
+      if (e < lcount) j = MODE == 1 ? list[e] : e;
     } else {
       j = pk * kLeaf + lane;
     }
@@ -263,13 +272,13 @@ __global__ void __launch_bounds__(256, 4) k_pk_query(const uint32_t* __restrict_
     K pkk[D];
     u64 ps = 0;
     uint32_t pid = 0;
-    if (j < sh.m) {
-      slot = order[j];
-      const uint32_t* r = prec + j * L::PW;
+    if (j < (MODE == 2 ? lcount : sh.m)) {
+      slot = MODE == 2 ? (uint32_t)j : order[j];
+      const uint32_t* r = (MODE == 2 ? qrec : prec) + j * L::PW;
       memcpy(pkk, r, sizeof(pkk));
       ps = (u64)r[L::KW] | ((u64)r[L::KW + 1] << 32);
       pid = r[L::KW + 2];
-      act = slot >= q_begin && slot < qend;
+      act = MODE == 2 ? pid != kNoId : slot >= q_begin && slot < qend;
       if (!PHASE2 && act && ps == 0) {  // the origin: nothing dominates it
         flag[slot] = 1;
         act = false;
@@ -302,24 +311,29 @@ __global__ void __launch_bounds__(256, 4) k_pk_query(const uint32_t* __restrict_
     }
     top = __shfl_sync(kFull, top, 0);
     __syncwarp();
-    while (top > 0 && __any_sync(kFull, act && !dom)) {
+    while (top > 0) {
+      // Packet bounds over the undecided lanes, refreshed when a lane is
+      // decided: a point can dominate one of them only if it is <= their
+      // componentwise maximum and its sum is <= their largest sum.
+      const unsigned um = __ballot_sync(kFull, act && !dom);
+      if (!um) break;
+      if (um != um_prev) {
+        um_prev = um;
+        const bool u = (um >> lane) & 1;
+#pragma unroll
+        for (int k = 0; k < D; ++k) pmax[k] = shfl_max<K>(u ? pkk[k] : (K)0);
+        psmax = shfl_max<u64>(u ? ps : 0ull);
+        if (lane < D) pmax_w[lane] = pmax[0];
+#pragma unroll
+        for (int k = 1; k < D; ++k)
+          if (lane == k) pmax_w[k] = pmax[k];
+      }
       const uint32_t e = stk[--top];
       __syncwarp();
       const int lvl = (int)(e >> 27);
       const uint32_t idx = e & ((1u << 27) - 1);
       if (lvl == 0) {
         ++n_leaves;
-        // Packet bounds over the undecided lanes (recomputed when a lane is
-        // decided): a leaf point can dominate one of them only if it is <=
-        // their componentwise maximum and its sum is <= their largest sum.
-        const unsigned um = __ballot_sync(kFull, act && !dom);
-        if (um != um_prev) {
-          um_prev = um;
-          const bool u = (um >> lane) & 1;
-#pragma unroll
-          for (int k = 0; k < D; ++k) pmax[k] = shfl_max<K>(u ? pkk[k] : (K)0);
-          psmax = shfl_max<u64>(u ? ps : 0ull);
-        }
         // stage the leaf points that pass the packet bounds, compacted
         const u64 q0 = (u64)idx * kLeaf;
         const int cnt = (int)min((u64)kLeaf, sh.m - q0);
@@ -365,15 +379,8 @@ __global__ void __launch_bounds__(256, 4) k_pk_query(const uint32_t* __restrict_
       const uint32_t cidx0 = F * idx;
       const int nc = (int)min((uint32_t)F, sh.cnt[lvl - 1] - cidx0);
       const uint32_t c0 = sh.off[lvl - 1] + cidx0;
-      const bool ancestor = path[lvl] == idx;
-      const uint32_t own = path[lvl - 1];
-      const bool und = act && !dom;
-      unsigned wm = 0;
-      u64 best_s = ~0ull;
-      int best_c = -1;
-      bool kill = false;
       // the children's records are contiguous: one coalesced load by the
-      // whole warp (one memory round trip per visit), then broadcast reads
+      // whole warp (one memory round trip per visit), then shared reads
       {
         const uint4* src = reinterpret_cast<const uint4*>(nrec + (u64)c0 * L::NW);
         uint4* dst = reinterpret_cast<uint4*>(nb);
@@ -383,49 +390,64 @@ __global__ void __launch_bounds__(256, 4) k_pk_query(const uint32_t* __restrict_
           if (i < nq) dst[i] = __ldg(src + i);
       }
       __syncwarp();
-#pragma unroll
-      for (int c = 0; c < F; ++c) {
-        if (c < nc && !(ancestor && cidx0 + c == own)) {
-          K lo[D], hi1[D];
-          uint32_t w[L::NW];
-          const uint4* r4 = reinterpret_cast<const uint4*>(nb + c * L::NW);
-#pragma unroll
-          for (int i = 0; i < L::NW / 4; ++i) {
-            const uint4 x = r4[i];
-            w[4 * i] = x.x;
-            w[4 * i + 1] = x.y;
-            w[4 * i + 2] = x.z;
-            w[4 * i + 3] = x.w;
-          }
-          memcpy(lo, w, sizeof(lo));
-          memcpy(hi1, w + L::KW, sizeof(hi1));
-          const u64 cs = (u64)w[2 * L::KW] | ((u64)w[2 * L::KW + 1] << 32);
-          const uint32_t ci = w[2 * L::KW + 2];
-          const bool pre = precedes(cs, ci, ps, pid);
-          // some point of the child is <= p everywhere and precedes p
-          const bool want = und && pre && diff_or<K, S, D>(pkk, lo) >= 0;
-          // the whole child lies strictly below p: its champion dominates p
-          kill |= want && diff_or<K, S, D>(pkk, hi1) >= 0;
-          if (__any_sync(kFull, want)) {
-            wm |= 1u << c;
-            if (cs < best_s) {
-              best_s = cs;
-              best_c = c;
-            }
+      // Packet pre-test, all children at once: lane (c, k) checks lo_k of
+      // child c against the packet maximum, lane c < F the champion against
+      // the packet's largest sum.  Only children passing it get the per-lane
+      // test (typically 1-2 of F).
+      bool rej = false;
+      if (lane < F * D) {
+        const int c = lane / D, k = lane - (lane / D) * D;
+        K lo_k;
+        memcpy(&lo_k, nb + c * L::NW + k * (int)(sizeof(K) / 4), sizeof(K));
+        rej = c >= nc || lo_k > pmax_w[k];
+      }
+      unsigned cand = 0;
+      {
+        const unsigned rb = __ballot_sync(kFull, rej);
+        bool crej = true;
+        if (lane < nc) {
+          const uint32_t* r = nb + lane * L::NW;
+          const u64 cs = (u64)r[2 * L::KW] | ((u64)r[2 * L::KW + 1] << 32);
+          crej = cs > psmax || ((rb >> (lane * D)) & ((1u << D) - 1)) != 0;
+          // an ancestor of the own leaf skips the child on the own path
+          crej |= path[lvl] == idx && cidx0 + lane == path[lvl - 1];
+        }
+        cand = __ballot_sync(kFull, !crej) & ((1u << F) - 1);
+      }
+      const bool und = act && !dom;
+      unsigned wm = 0;
+      u64 best_s = ~0ull;
+      int best_c = 0;
+      bool kill = false;
+      while (cand) {
+        const int c = __ffs(cand) - 1;
+        cand &= cand - 1;
+        const uint32_t* r = nb + c * L::NW;
+        K lo[D], hi1[D];
+        memcpy(lo, r, sizeof(lo));
+        memcpy(hi1, r + L::KW, sizeof(hi1));
+        const u64 cs = (u64)r[2 * L::KW] | ((u64)r[2 * L::KW + 1] << 32);
+        const uint32_t ci = r[2 * L::KW + 2];
+        // some point of the child is <= p everywhere and precedes p
+        const bool want = und && precedes(cs, ci, ps, pid) && diff_or<K, S, D>(pkk, lo) >= 0;
+        // the whole child lies strictly below p: its champion dominates p
+        kill |= want && diff_or<K, S, D>(pkk, hi1) >= 0;
+        if (__ballot_sync(kFull, want)) {
+          wm |= 1u << c;
+          if (cs < best_s) {
+            best_s = cs;
+            best_c = c;
           }
         }
       }
       dom |= kill;
       __syncwarp();  // nb is rewritten by the next visit
       if (!wm) continue;
-      // push the wanted children; the one with the strongest champion on top
-      if (lane == 0) {
-#pragma unroll
-        for (int c = 0; c < F; ++c)
-          if (((wm >> c) & 1) && c != best_c) stk[top++] = ((uint32_t)(lvl - 1) << 27) | (cidx0 + c);
-        stk[top++] = ((uint32_t)(lvl - 1) << 27) | (cidx0 + best_c);
-      }
-      top = __shfl_sync(kFull, top, 0);
+      // push the wanted children, lane-parallel; the strongest champion on top
+      const unsigned rest = wm & ~(1u << best_c);
+      if ((wm >> lane) & 1)
+        stk[top + (lane == best_c ? __popc(rest) : __popc(rest & lt))] = ((uint32_t)(lvl - 1) << 27) | (cidx0 + lane);
+      top += __popc(wm);
       __syncwarp();
     }
     // phase 1 with a partial search: undecided lanes go to phase 2
