@@ -144,6 +144,32 @@ int skycell_gpu_shard_finish(skycell_gpu_ctx* ctx, const void* dev_recv, int wor
                              uint64_t own_count, uint32_t* ids_out, uint64_t* n_out, skycell_gpu_stats* stats,
                              char* err, size_t err_len);
 
+/* ---- Single-process multi-device query ("skycell_gpu_create(
+ * int n_gpus, ...)"; §8(e)).  One handle owns a context per listed device,
+ * shards the records by index and runs the sharded protocol above itself:
+ * the exchanges are device-to-device copies (NVLink / NVSwitch peer access
+ * when available), one host thread per device.  Same contract as
+ * skycell_gpu_skyline_f64 / _f32 (the reference's compute_skyline,
+ * refine.hpp:61-62): ids ascending, per-layer counts, points_examined.
+ * Queries sharding cannot serve (one device, n < devices, merge_cross_cell =
+ * 0, a sparse layer rho) run on the first device.  The same device may be
+ * listed more than once (tests run G contexts on one GPU). */
+typedef struct skycell_gpu_multi skycell_gpu_multi;
+int skycell_gpu_multi_create(const int* devices, int n_devices, skycell_gpu_multi** out, char* err,
+                             size_t err_len);
+void skycell_gpu_multi_destroy(skycell_gpu_multi* m);
+int skycell_gpu_multi_size(const skycell_gpu_multi* m);
+/* The context of device slot g (e.g. for quadrant queries); owned by m. */
+skycell_gpu_ctx* skycell_gpu_multi_context(skycell_gpu_multi* m, int g);
+int skycell_gpu_multi_skyline_f64(skycell_gpu_multi* m, const double* coords, uint64_t n, int d,
+                                  const double* dim_min, const double* dim_max, int rho, int mode,
+                                  int merge_cross_cell, uint32_t* ids_out, uint64_t* n_out,
+                                  skycell_gpu_stats* stats, char* err, size_t err_len);
+int skycell_gpu_multi_skyline_f32(skycell_gpu_multi* m, const float* coords, uint64_t n, int d,
+                                  const double* dim_min, const double* dim_max, int rho, int mode,
+                                  int merge_cross_cell, uint32_t* ids_out, uint64_t* n_out,
+                                  skycell_gpu_stats* stats, char* err, size_t err_len);
+
 /* On-device synthetic data with the reference generator's streams
  * (skycell::generate, datagen.cpp:62-87): dist 0 independent, 1 correlated,
  * 2 anti-correlated.  kind 0 writes n*d raw doubles, kind 1 writes n*d floats

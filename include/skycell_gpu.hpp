@@ -10,6 +10,8 @@
 //                                    proj/src/refine.cpp:108-158)
 //   skycell::gpu::quadrant_skyline  replaces  skycell::quadrant_skyline
 //                                   (refine.hpp:66-68, refine.cpp:160-184)
+//   skycell::gpu::MultiDevice       compute_skyline sharded over several
+//                                   GPUs of one process
 //
 // Status codes are rethrown as the reference's exception types
 // (proj/include/skycell/error.hpp:9-26) with the reference's message text.
@@ -115,6 +117,51 @@ class Device {
     r.layers.candidates.assign(st.candidates, st.candidates + st.n_layers);
   }
   skycell_gpu_ctx* ctx_ = nullptr;
+  std::mutex mu_;
+};
+
+// Several devices in one process (skycell_gpu_multi_*): records are sharded
+// by index over the listed devices and the library runs both exchanges
+// itself (device-to-device copies over NVLink / NVSwitch).  Same results as
+// Device::compute_skyline.
+class MultiDevice {
+ public:
+  explicit MultiDevice(const std::vector<int>& devices) {
+    char err[512] = {0};
+    throw_status(skycell_gpu_multi_create(devices.data(), (int)devices.size(), &m_, err, sizeof err), err);
+  }
+  ~MultiDevice() { skycell_gpu_multi_destroy(m_); }
+  MultiDevice(const MultiDevice&) = delete;
+  MultiDevice& operator=(const MultiDevice&) = delete;
+
+  SkylineResult compute_skyline(const Dataset& ds, int rho, Mode mode, bool merge_cross_cell = true) {
+    SkylineResult r;
+    r.ids.resize(ds.n > 0 ? ds.n : 1);
+    skycell_gpu_stats st{};
+    uint64_t n_out = 0;
+    char err[512] = {0};
+    int rc;
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      rc = skycell_gpu_multi_skyline_f64(m_, ds.coords.data(), ds.n, ds.d, ds.dim_min.data(), ds.dim_max.data(), rho,
+                                         mode == Mode::kSequential ? SKYCELL_SEQUENTIAL : SKYCELL_PARALLEL,
+                                         merge_cross_cell ? 1 : 0, r.ids.data(), &n_out, &st, err, sizeof err);
+    }
+    throw_status(rc, err);
+    r.ids.resize(n_out);
+    r.times.normalize_ms = st.normalize_ms;
+    r.times.grid_ms = st.grid_ms;
+    r.times.shrink_ms = st.shrink_ms;
+    r.times.refine_ms = st.refine_ms;
+    r.times.total_ms = st.total_ms;
+    r.points_examined = st.points_examined;
+    r.layers.keys.assign(st.keys, st.keys + st.n_layers);
+    r.layers.candidates.assign(st.candidates, st.candidates + st.n_layers);
+    return r;
+  }
+
+ private:
+  skycell_gpu_multi* m_ = nullptr;
   std::mutex mu_;
 };
 

@@ -20,7 +20,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include "kernels.cuh"
-#include "packet.cuh"
+#include "sparse.cuh"
 #include "datagen.cuh"
 
 using sk::u64;
@@ -120,6 +120,8 @@ struct skycell_gpu_ctx {
   skyeng::DevBuf t_keys, t_keys2, t_vals, t_vals2, t_cub, t_rows, t_ids, t_fsum, t_lo, t_hi, t_cs, t_ci;  // K5 tree
   skyeng::DevBuf t_cm, t_kill;  // K5 tree champion prefilter
   skyeng::DevBuf k5dbg;         // SKYCELL_K5STATS visit counters
+  skyeng::DevBuf sp_keys, sp_keys2, sp_vals, sp_vals2, sp_head, sp_cpos, sp_crows, sp_cfsum, sp_cids, sp_cstart,
+      sp_kflag, sp_cflag, sp_n, sp_qrec;  // sparse layer rho (sparse.cuh)
   int k5_mode = -1;  // 0 lists, 1 tree (packet query), 2 auto, 3 tree (point query); SKYCELL_K5
   skyeng::DevBuf long_q, long_n;  // K5 phase-B queue
   skyeng::DevBuf scan_tot;        // K5 list-scan chunk totals
@@ -314,7 +316,8 @@ void run_exact(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uin
 template <typename TOut, int D>
 void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint32_t* ids, const u64* fsum,
               const u64* count, u64* valid_ctr, u64 q_begin, const u64* q_end, int cell_level,
-              bool point_query = false) {
+              bool point_query = false, bool no_prefilter = false, sk::TreeShape* shape_out = nullptr) {
+  if (shape_out) shape_out->m = 0;
   const int nsm = ctx->num_sms;
   u64 hv[2];
   ck(cudaMemcpyAsync(&hv[0], count, 8, cudaMemcpyDeviceToHost, s), "D2H");
@@ -338,7 +341,7 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
   // Not with merge_cross_cell = false (cell_level > 0): a dominator strictly
   // below p's prefilter cell may sit in another layer-rho cell, which
   // phase-1-only semantics (refine.cpp:98) must not use.
-  if (Lc >= 1 && nslots >= (1ull << 16) && cell_level == 0) {
+  if (Lc >= 1 && nslots >= (1ull << 16) && cell_level == 0 && !no_prefilter) {
     const u64 cells = 1ull << (u64)(Lc * D);
     ensure(ctx->t_cm, cells * 8);
     ensure(ctx->t_kill, nslots);
@@ -397,6 +400,7 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
     cnt = (cnt + F - 1) / F;
   }
   sh.levels = L;
+  if (shape_out) *shape_out = sh;
   const u64 nodes = off;
   const uint32_t* order = static_cast<const uint32_t*>(ctx->t_vals2.p);
   const unsigned gm = (unsigned)std::max<u64>(1, std::min<u64>((m + 255) / 256, (u64)nsm * 8));
@@ -437,8 +441,8 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
     uint32_t* poff = pcnt + sh.nleaf;
     uint32_t* list = static_cast<uint32_t*>(ctx->t_vals.p);
     u64* list_n = static_cast<u64*>(ctx->long_n.p) + 1;
-    sk::k_pk_query<TOut, D, false><<<gq, 256, 0, s>>>(prec, nrec, order, sh, q_begin, q_end, h1, two ? umask : nullptr,
-                                                     nullptr, nullptr, static_cast<uint8_t*>(ctx->flags.p), vst);
+    sk::k_pk_query<TOut, D, 0><<<gq, 256, 0, s>>>(prec, nrec, order, sh, q_begin, q_end, h1, two ? umask : nullptr,
+                                                  nullptr, nullptr, nullptr, static_cast<uint8_t*>(ctx->flags.p), vst);
     ++ctx->launches;
     if (two) {
       tracer().mark(s, "tree: packet phase 1");
@@ -449,8 +453,8 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
       ensure(ctx->t_cub, temp);
       ck(cub::DeviceScan::ExclusiveSum(ctx->t_cub.p, temp, pcnt, poff, (int64_t)sh.nleaf, s), "cub scan");
       sk::k_pk_list<<<gc, 256, 0, s>>>(umask, poff, sh.nleaf, list, list_n);
-      sk::k_pk_query<TOut, D, true><<<gq, 256, 0, s>>>(prec, nrec, order, sh, q_begin, q_end, h1, nullptr, list, list_n,
-                                                      static_cast<uint8_t*>(ctx->flags.p), vst);
+      sk::k_pk_query<TOut, D, 1><<<gq, 256, 0, s>>>(prec, nrec, order, sh, q_begin, q_end, h1, nullptr, list, list_n,
+                                                  nullptr, static_cast<uint8_t*>(ctx->flags.p), vst);
       ctx->launches += 4;
     }
     tracer().mark(s, "tree: packet query");
@@ -598,7 +602,10 @@ struct Pipe final : PipeBase {
   uint32_t* occ(int L) const { return static_cast<uint32_t*>(at(o_occ[L])); }
   DevCounters* ctr() const { return static_cast<DevCounters*>(at(o_ctr)); }
   unsigned* U(size_t off) const { return static_cast<unsigned*>(at(off)); }
-  int cell_level() const { return q.merge ? 0 : rho; }
+  // merge_cross_cell = false: dominators share p's cell at the QUERY's rho
+  int cell_level() const { return q.merge ? 0 : rho_q; }
+  // sparse layer rho (sparse.cuh): the dense pipeline runs up to rho - 1
+  static bool sparse_top(int r) { return r * D > 36 || r * (D - 1) > 30; }
 
   static auto pick_stream(int rho) {
     if constexpr (IDENT && D <= 8) {
@@ -618,7 +625,12 @@ struct Pipe final : PipeBase {
     return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 0>;
   }
 
-  explicit Pipe(const Query& qq) : q(qq), ctx(qq.ctx), s(qq.ctx->stream), s2(qq.ctx->side), n(qq.n), rho(qq.rho) {
+  int rho_q;    // the query's rho (reported layers 1..rho_q)
+  bool sparse;  // layer rho_q is sparse; `rho` (the dense top layer) = rho_q - 1
+
+  explicit Pipe(const Query& qq)
+      : q(qq), ctx(qq.ctx), s(qq.ctx->stream), s2(qq.ctx->side), n(qq.n),
+        rho(sparse_top(qq.rho) ? qq.rho - 1 : qq.rho), rho_q(qq.rho), sparse(sparse_top(qq.rho)) {
     nsm = ctx->num_sms;
     la = sk::filter_level(rho, D);
     test_b = rho > la;
@@ -904,8 +916,10 @@ struct Pipe final : PipeBase {
     pc.PM = ctx->table.p;
     pc.f_rows = ctx->f_rows.p;
     pc.f_fsum = static_cast<const u64*>(ctx->f_fsum.p);
-    pc.f_count = q.merge ? &c->nf : nullptr;
-    pc.f_max = q.merge ? (uint32_t)pf_max : 0;
+    // sparse: K4 is the layer-(rho-1) cell test only; the filter points run
+    // after the sparse layer-rho stage
+    pc.f_count = q.merge && !sparse ? &c->nf : nullptr;
+    pc.f_max = q.merge && !sparse ? (uint32_t)pf_max : 0;
     pc.f_lists = static_cast<const uint16_t*>(ctx->f_lists.p);
     pc.f_offs = static_cast<const uint16_t*>(ctx->f_offs.p);
     pc.out_rows = ctx->s2_rows.p;
@@ -922,7 +936,7 @@ struct Pipe final : PipeBase {
     }
     auto kc = wide ? sk::k_candidates<TOut, D, uint32_t, kThreads> : sk::k_candidates<TOut, D, uint8_t, kThreads>;
     ck(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pf), "smem attr");
-    if (q.merge) {
+    if (q.merge && !sparse) {
       // K4a: cell test + the 8 strongest filter points over S1 -> P (dense
       // pending points, in the S1 buffers' twin); K4b: the rest of the filter
       // over P, whose lanes are all pending (no idle lanes in the head test)
@@ -963,6 +977,119 @@ struct Pipe final : PipeBase {
     if (q.timed) ck(cudaEventRecord(ctx->ev[6], s), "event");
   }
 
+  // ---- sparse layer rho (sparse.cuh): U = the layer-rho cells of K4's
+  // layer-(rho-1) candidates, classified through the dominance tree; the
+  // points of U's candidate cells then meet the filter points -> S2
+  void sparse_layer() {
+    DevCounters* c = ctr();
+    u64 nslots = 0;
+    ck(cudaMemcpyAsync(&nslots, &c->s2, 8, cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "sync");
+    ck(cudaMemsetAsync(&c->examined, 0, 8, s), "memset");
+    const u64 ns = std::max<u64>(nslots, 1);
+    ensure(ctx->sp_keys, ns * 8);
+    ensure(ctx->sp_keys2, ns * 8);
+    ensure(ctx->sp_vals, ns * 4);
+    ensure(ctx->sp_vals2, ns * 4);
+    ensure(ctx->sp_head, ns * 4);
+    ensure(ctx->sp_cpos, ns * 4);
+    ensure(ctx->sp_crows, ns * D * 4);
+    ensure(ctx->sp_cfsum, ns * 8);
+    ensure(ctx->sp_cids, ns * 4);
+    ensure(ctx->sp_cstart, ns * 4);
+    ensure(ctx->sp_kflag, ns);
+    ensure(ctx->sp_cflag, ns);
+    ensure(ctx->sp_n, 64);
+    u64* keys = static_cast<u64*>(ctx->sp_keys.p);
+    u64* keys2 = static_cast<u64*>(ctx->sp_keys2.p);
+    uint32_t* vals = static_cast<uint32_t*>(ctx->sp_vals.p);
+    uint32_t* vals2 = static_cast<uint32_t*>(ctx->sp_vals2.p);
+    uint32_t* head = static_cast<uint32_t*>(ctx->sp_head.p);
+    uint32_t* cpos = static_cast<uint32_t*>(ctx->sp_cpos.p);
+    float* crows = static_cast<float*>(ctx->sp_crows.p);
+    u64* cfsum = static_cast<u64*>(ctx->sp_cfsum.p);
+    uint32_t* cids = static_cast<uint32_t*>(ctx->sp_cids.p);
+    uint32_t* cstart = static_cast<uint32_t*>(ctx->sp_cstart.p);
+    uint8_t* kflag = static_cast<uint8_t*>(ctx->sp_kflag.p);
+    uint8_t* cflag = static_cast<uint8_t*>(ctx->sp_cflag.p);
+    u64* spn = static_cast<u64*>(ctx->sp_n.p);  // [ncells, nvalid, queries]
+    ck(cudaMemsetAsync(spn, 0, 64, s), "memset");
+    const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((ns + 255) / 256, (u64)nsm * 8));
+    sk::k_sp_keys<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(ctx->s2_rows.p),
+                                             static_cast<const uint32_t*>(ctx->s2_ids.p), &c->s2, rho_q, keys, vals);
+    size_t temp = 0, temp2 = 0;
+    ck(cub::DeviceRadixSort::SortPairs(nullptr, temp, keys, keys2, vals, vals2, (int64_t)ns, 0, rho_q * D, s), "cub");
+    ck(cub::DeviceScan::InclusiveSum(nullptr, temp2, head, cpos, (int64_t)ns, s), "cub");
+    ensure(ctx->t_cub, std::max(temp, temp2));
+    ck(cub::DeviceRadixSort::SortPairs(ctx->t_cub.p, temp, keys, keys2, vals, vals2, (int64_t)ns, 0, rho_q * D, s),
+       "cub sort");
+    sk::k_sp_heads<<<g, 256, 0, s>>>(keys2, ns, head);
+    ck(cub::DeviceScan::InclusiveSum(ctx->t_cub.p, temp2, head, cpos, (int64_t)ns, s), "cub scan");
+    sk::k_sp_cells<D><<<g, 256, 0, s>>>(keys2, head, cpos, ns, rho_q, crows, cfsum, cids, cstart, spn, spn + 1);
+    ctx->launches += 5;
+    // key test: corners dominated by another corner of U (no prefilter, so
+    // the tree holds every cell for the strict test below)
+    sk::TreeShape sh{};
+    run_tree<float, D>(ctx, s, crows, cids, cfsum, spn, &c->tvalid, 0, nullptr, 0, false, true, &sh);
+    ck(cudaMemcpyAsync(kflag, ctx->flags.p, ns, cudaMemcpyDeviceToDevice, s), "flags");
+    ck(cudaMemsetAsync(cflag, 0, ns, s), "memset");
+    if (sh.m) {
+      typedef sk::PkLayout<float, D> PL;
+      ensure(ctx->sp_qrec, sh.m * PL::PW * 4);
+      uint32_t* qrec = static_cast<uint32_t*>(ctx->sp_qrec.p);
+      const uint32_t* prec = static_cast<const uint32_t*>(ctx->t_rows.p);
+      const uint32_t* nrec = static_cast<const uint32_t*>(ctx->t_lo.p);
+      const uint32_t* order = static_cast<const uint32_t*>(ctx->t_vals2.p);
+      ctx->host_param[2] = sh.m;
+      ck(cudaMemcpyAsync(spn + 2, ctx->host_param + 2, 8, cudaMemcpyHostToDevice, s), "param");
+      const unsigned gm = (unsigned)std::max<u64>(1, std::min<u64>((sh.m + 255) / 256, (u64)nsm * 8));
+      sk::k_sp_queries<D><<<gm, 256, 0, s>>>(prec, sh.m, rho_q, qrec);
+      const unsigned gq = (unsigned)std::max<u64>(1, std::min<u64>((sh.nleaf * 32 + 255) / 256, (u64)nsm * 8));
+      sk::k_pk_query<float, D, 2><<<gq, 256, 0, s>>>(prec, nrec, order, sh, 0, nullptr, 0, nullptr, nullptr, spn + 2,
+                                                    qrec, static_cast<uint8_t*>(ctx->flags.p), nullptr);
+      sk::k_sp_cand<<<gm, 256, 0, s>>>(static_cast<const uint8_t*>(ctx->flags.p), qrec + PL::KW + 2, PL::PW, order,
+                                      sh.m, cflag);
+      ctx->launches += 3;
+    }
+    sk::k_sp_classify<D><<<g, 256, 0, s>>>(crows, kflag, cflag, cstart, spn, spn + 1, rho_q, &c->key[rho_q - 1],
+                                          &c->cand[rho_q - 1], &c->examined);
+    // the points of candidate cells -> P, then the filter points -> S2
+    ensure(ctx->p_rows, cap4 * D * sizeof(TOut));
+    ensure(ctx->p_ids, cap4 * 4);
+    ensure(ctx->p_fsum, cap4 * 8);
+    ck(cudaMemsetAsync(&c->pres, 0, 8, s), "memset");
+    sk::k_sp_points<TOut, D><<<grid4, kThreads, 0, s>>>(
+        static_cast<const TOut*>(ctx->s2_rows.p), static_cast<const uint32_t*>(ctx->s2_ids.p),
+        static_cast<const u64*>(ctx->s2_fsum.p), vals2, keys2, cpos, cflag, ns, static_cast<TOut*>(ctx->p_rows.p),
+        static_cast<uint32_t*>(ctx->p_ids.p), static_cast<u64*>(ctx->p_fsum.p), &c->pres, kChunk4);
+    ck(cudaMemsetAsync(&c->s2, 0, 8, s), "memset");
+    ck(cudaMemsetAsync(&c->s2_kept, 0, 8, s), "memset");
+    sk::CandParams pb{};
+    pb.rows = ctx->p_rows.p;
+    pb.ids = static_cast<const uint32_t*>(ctx->p_ids.p);
+    pb.count = &c->pres;
+    pb.rho = rho;
+    pb.PM = nullptr;
+    pb.f_rows = ctx->f_rows.p;
+    pb.f_fsum = static_cast<const u64*>(ctx->f_fsum.p);
+    pb.f_count = q.merge ? &c->nf : nullptr;
+    pb.f_max = q.merge ? (uint32_t)pf_max : 0;
+    pb.f_lists = static_cast<const uint16_t*>(ctx->f_lists.p);
+    pb.f_offs = static_cast<const uint16_t*>(ctx->f_offs.p);
+    pb.out_rows = ctx->s2_rows.p;
+    pb.out_ids = static_cast<uint32_t*>(ctx->s2_ids.p);
+    pb.out_fsum = static_cast<u64*>(ctx->s2_fsum.p);
+    pb.out_reserved = &c->s2;
+    pb.chunk = kChunk4;
+    pb.kept = &c->s2_kept;
+    pb.head_start = 0;
+    pb.coop = 1;
+    auto kc = sk::k_candidates<TOut, D, uint8_t, kThreads>;
+    ck(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pf), "smem attr");
+    kc<<<grid4, kThreads, smem_pf, s>>>(pb);
+    ctx->launches += 3;
+  }
+
   // ---- K5 over S2 (the local point set)
   void exact_local() {
     DevCounters* c = ctr();
@@ -998,10 +1125,10 @@ struct Pipe final : PipeBase {
   void fill_stats(skycell_gpu_stats* st) const {
     if (!st) return;
     const DevCounters& hc = *ctx->host_ctr;
-    st->n_layers = rho;
-    for (int L = 1; L <= rho; ++L) {
+    st->n_layers = rho_q;
+    for (int L = 1; L <= rho_q; ++L) {
       st->keys[L - 1] = hc.key[L - 1] + (u64)D;
-      st->candidates[L - 1] = (q.mode == SKYCELL_SEQUENTIAL && L != rho) ? -1 : (int64_t)hc.cand[L - 1];
+      st->candidates[L - 1] = (q.mode == SKYCELL_SEQUENTIAL && L != rho_q) ? -1 : (int64_t)hc.cand[L - 1];
     }
     st->points_examined = hc.examined;
     st->survivors_stream = hc.s1_kept;
@@ -1023,6 +1150,10 @@ struct Pipe final : PipeBase {
     tracer().mark(s, "K0+K1");
     prune();
     tracer().mark(s, "K3+K4");
+    if (sparse) {
+      sparse_layer();
+      tracer().mark(s, "sparse layer rho");
+    }
     exact_local();
     tracer().mark(s, "K5");
     ids_out(static_cast<const uint32_t*>(ctx->s2_ids.p), &c->s2, cap4, id_dst());

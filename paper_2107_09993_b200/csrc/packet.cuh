@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(256, 4) k_pk_query(const uint32_t* __restrict_
     for (int l = 0; l < 32; ++l) path[l] = ~0u;
   for (u64 pk = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; pk < npk; pk += ((u64)gridDim.x * blockDim.x) >> 5) {
     u64 j = ~0ull;
-    if (PHASE2) {
+    if constexpr (PHASE2) {
       const u64 e = pk * kLeaf + lane;
       if (e < lcount) j = MODE == 1 ? list[e] : e;
     } else {

@@ -75,9 +75,6 @@ Query make_query(skycell_gpu_ctx* ctx, const TIn* coords, u64 n, int d, const do
   const void* dev_coords = stage_input<TIn>(ctx, coords, n, d);
   Status rs = validate_rho(rho, d);
   if (rs.code) reject_rho<TIn>(ctx, dev_coords, n, d, rs, id_base);
-  if ((u64)rho * d > 36 || (u64)rho * (d - 1) > 30)
-    throw ApiFail{SKYCELL_UNSUPPORTED, "skycell_gpu: rho*d = " + std::to_string(rho * d) +
-                                           " needs the sparse cell index (dense bitmaps are limited to 2^36 cells)"};
   Query q{};
   q.ctx = ctx;
   q.n = n;
@@ -236,7 +233,7 @@ void skycell_gpu_destroy(skycell_gpu_ctx* ctx) {
                     &ctx->s2_ids, &ctx->s2_fsum, &ctx->flags, &ctx->sky_rows, &ctx->sky_ids, &ctx->sky_fsum,
                     &ctx->q_bits, &ctx->q_orig, &ctx->q_sub, &ctx->q_ids, &ctx->q_mm, &ctx->t_keys,
                     &ctx->t_keys2, &ctx->t_vals, &ctx->t_vals2, &ctx->t_cub, &ctx->t_rows, &ctx->t_ids,
-                    &ctx->t_fsum, &ctx->t_lo, &ctx->t_hi, &ctx->t_cs, &ctx->t_ci, &ctx->long_q, &ctx->long_n, &ctx->scan_tot, &ctx->d_cells, &ctx->t_cm, &ctx->t_kill, &ctx->p_rows, &ctx->p_ids, &ctx->p_fsum, &ctx->k5dbg};
+                    &ctx->t_fsum, &ctx->t_lo, &ctx->t_hi, &ctx->t_cs, &ctx->t_ci, &ctx->long_q, &ctx->long_n, &ctx->scan_tot, &ctx->d_cells, &ctx->t_cm, &ctx->t_kill, &ctx->p_rows, &ctx->p_ids, &ctx->p_fsum, &ctx->k5dbg, &ctx->sp_keys, &ctx->sp_keys2, &ctx->sp_vals, &ctx->sp_vals2, &ctx->sp_head, &ctx->sp_cpos, &ctx->sp_crows, &ctx->sp_cfsum, &ctx->sp_cids, &ctx->sp_cstart, &ctx->sp_kflag, &ctx->sp_cflag, &ctx->sp_n, &ctx->sp_qrec};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   for (auto& e : ctx->ev)
@@ -358,6 +355,9 @@ int skycell_gpu_shard_begin(skycell_gpu_ctx* ctx, const void* coords, int coords
     if (!ctx || !occ_bytes) throw ApiFail{SKYCELL_USAGE, "skycell_gpu: null context or output pointer"};
     ctx->shard.reset();
     if (id_base + n > 0xffffffffull) throw ApiFail{SKYCELL_INPUT, "normalize: more than 2^32 - 1 records"};
+    if ((u64)rho * d > 36 || (u64)rho * (d - 1) > 30)
+      throw ApiFail{SKYCELL_UNSUPPORTED, "skycell_gpu: sharded query with rho*d = " + std::to_string(rho * d) +
+                                             ": the sparse layer-rho index is single-device only"};
     if (coords_f32) {
       Query q = make_query<float>(ctx, static_cast<const float*>(coords), n, d, dim_min, dim_max, rho, mode, 1,
                                   nullptr, nullptr, id_base);

@@ -157,6 +157,8 @@ EXPORTS = (
     "skycell_gpu_shard_prune", "skycell_gpu_shard_block_bytes", "skycell_gpu_shard_pack", "skycell_gpu_shard_finish",
     "skycell_gpu_generate", "skycell_gpu_generate_range", "skycell_default_rho", "skycell_validate",
     "skycell_gpu_version", "skycell_bin_header", "skycell_gpu_read_bin", "skycell_gpu_write_bin",
+    "skycell_gpu_multi_create", "skycell_gpu_multi_destroy", "skycell_gpu_multi_size", "skycell_gpu_multi_context",
+    "skycell_gpu_multi_skyline_f64", "skycell_gpu_multi_skyline_f32",
 )
 
 
@@ -195,6 +197,14 @@ def load_library(path: str = LIB_PATH):
         lib.skycell_bin_header.argtypes = [cp, u64p, C.POINTER(C.c_int), cp, sz]
         lib.skycell_gpu_read_bin.argtypes = [vp, cp, vp, u64, u64p, C.POINTER(C.c_int), dp, dp, cp, sz]
         lib.skycell_gpu_write_bin.argtypes = [vp, cp, vp, u64, i32, cp, sz]
+        lib.skycell_gpu_multi_create.argtypes = [C.POINTER(C.c_int), i32, C.POINTER(vp), cp, sz]
+        lib.skycell_gpu_multi_destroy.argtypes = [vp]
+        lib.skycell_gpu_multi_destroy.restype = None
+        lib.skycell_gpu_multi_size.argtypes = [vp]
+        lib.skycell_gpu_multi_context.argtypes = [vp, i32]
+        lib.skycell_gpu_multi_context.restype = vp
+        for fn in (lib.skycell_gpu_multi_skyline_f64, lib.skycell_gpu_multi_skyline_f32):
+            fn.argtypes = [vp, fp, u64, i32, dp, dp, i32, i32, i32, u32p, u64p, C.POINTER(_Stats), cp, sz]
         _lib = lib
         return lib
 
@@ -401,6 +411,64 @@ class Engine:
                                                    err, 512)
         _raise(rc, err)
         return _to_result(ids[: n_out.value].copy(), st)
+
+
+class MultiEngine:
+    """One process, several devices (include/skycell_gpu.h: skycell_gpu_multi):
+    the records are sharded by index over the devices and the sharded
+    protocol runs inside the library (device-to-device exchanges).  Same
+    results as Engine.compute_skyline; `devices` may repeat a device."""
+
+    def __init__(self, devices):
+        self.lib = load_library()
+        self.devices = [int(x) for x in devices]
+        arr = (C.c_int * len(self.devices))(*self.devices)
+        self._m = C.c_void_p()
+        err = C.create_string_buffer(512)
+        _raise(self.lib.skycell_gpu_multi_create(arr, len(self.devices), C.byref(self._m), err, 512), err)
+        self._lock = threading.Lock()
+
+    def close(self) -> None:
+        if self._m:
+            self.lib.skycell_gpu_multi_destroy(self._m)
+            self._m = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def skyline_raw(self, coords, n: int, d: int, dim_min, dim_max, rho: int, mode: int = 1,
+                    merge_cross_cell: bool = True):
+        if not isinstance(coords, np.ndarray):
+            raise UsageError("MultiEngine: coords must be a host numpy array (sharded over the devices)")
+        ptr, is_f32 = _data_ptr(coords, n, d)
+        mn = np.ascontiguousarray(dim_min, dtype=np.float64)
+        mx = np.ascontiguousarray(dim_max, dtype=np.float64)
+        if mn.shape[0] < d or mx.shape[0] < d:
+            raise UsageError("dim_min/dim_max must hold d values")
+        ids = np.empty(max(n, 1), dtype=np.uint32)
+        n_out = C.c_uint64(0)
+        st = _Stats()
+        err = C.create_string_buffer(512)
+        fn = self.lib.skycell_gpu_multi_skyline_f32 if is_f32 else self.lib.skycell_gpu_multi_skyline_f64
+        with self._lock:
+            rc = fn(self._m, ptr, n, d, mn.ctypes.data_as(C.POINTER(C.c_double)),
+                    mx.ctypes.data_as(C.POINTER(C.c_double)), rho, int(mode), int(bool(merge_cross_cell)),
+                    C.c_void_p(ids.ctypes.data), C.byref(n_out), C.byref(st), err, 512)
+        _raise(rc, err)
+        return _to_result(ids[: n_out.value].copy(), st)
+
+    def compute_skyline(self, ds: Dataset, rho: int, mode: Mode = Mode.kParallel, pool=None,
+                        merge_cross_cell: bool = True) -> SkylineResult:
+        """compute_skyline (refine.hpp:61-62) over every device of the handle."""
+        x = np.asarray(ds.coords)
+        if x.dtype not in (np.float32, np.float64):
+            x = x.astype(np.float64)
+        x = np.ascontiguousarray(x.reshape(x.shape[0], -1) if x.ndim != 2 and x.size else x)
+        n, d = x.shape if x.ndim == 2 else (0, 0)
+        return self.skyline_raw(x, n, d, ds.dim_min, ds.dim_max, rho, int(mode), merge_cross_cell)
 
 
 def _data_ptr(a, n: int | None = None, d: int | None = None, device: int | None = None, what: str = "coords",

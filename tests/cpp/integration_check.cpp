@@ -67,6 +67,8 @@ std::string what_of(F&& f, int* kind) {
 
 int main() {
   skycell::ThreadPool pool(0);
+  // three contexts on device 0: the multi-device handle's sharded protocol
+  skycell::gpu::MultiDevice multi({0, 0, 0});
   const skycell::Distribution dists[] = {skycell::Distribution::kIndependent, skycell::Distribution::kCorrelated,
                                          skycell::Distribution::kAnticorrelated};
   int di = 0;
@@ -80,6 +82,8 @@ int main() {
         auto got = skycell::gpu::compute_skyline(ds, rho, mode, pool);
         expect(same(want, got), "compute_skyline dist=" + std::to_string(di) + " d=" + std::to_string(d) +
                                     " mode=" + std::to_string((int)mode) + " |S|=" + std::to_string(want.ids.size()));
+        auto gm = multi.compute_skyline(ds, rho, mode);
+        expect(same(want, gm), "MultiDevice compute_skyline dist=" + std::to_string(di) + " d=" + std::to_string(d));
       }
       // general FP64 path: raw generator output, observed min/max
       skycell::GenSpec spec;

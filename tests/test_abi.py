@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def header_symbols():
     with open(os.path.join(ROOT, "include", "skycell_gpu.h")) as f:
         src = f.read()
-    return sorted(set(re.findall(r"^\s*(?:int|void|uint64_t|const char\*)\s+(skycell_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|void|uint64_t|const char\*|skycell_gpu_ctx\*)\s+(skycell_\w+)\s*\(", src, re.M)))
 
 
 def test_library_exports_every_header_symbol():

@@ -248,12 +248,45 @@ def test_gpu_high_dimensions(engine, oracle, d):
     from oracle.oracle import quantize_f32
     for dist, n in ((0, 3000), (2, 1500)):
         v = oracle.generate(dist, n, d, 13 + d)
-        rho_max = max(r for r in range(1, 8) if r * d <= 36 and (r - 1) * d <= 32 and r * (d - 1) <= 30)
+        rho_max = max(r for r in range(1, 8) if r * d <= 60 and (r - 1) * d <= 32)  # grid.cpp:38-43
         for rho in sorted({1, rho_max}):
             for x, mn, mx in ((quantize_f32(v), np.zeros(d), np.ones(d)), (v * 2 - 1, (v * 2 - 1).min(0), (v * 2 - 1).max(0))):
                 want = oracle.compute_skyline(x.astype(np.float64), mn, mx, rho)
                 got = engine.compute_skyline(sky.Dataset(np.ascontiguousarray(x), mn, mx), rho)
                 check(got, want.ids, want.points_examined, want.keys, want.candidates)
+
+
+# every (d, rho) of the reference's budget (rho*d <= 60, (rho-1)*d <= 32,
+# grid.cpp:38-43) whose layer rho exceeds the dense bitmaps (sparse.cuh)
+SPARSE = [(8, 5), (9, 4), (10, 4), (11, 3), (12, 3), (13, 3), (14, 3), (15, 3), (16, 3)]
+
+
+@pytest.mark.parametrize("d,rho", SPARSE)
+def test_gpu_sparse_layer_vs_oracle(engine, oracle, d, rho):
+    """Layer rho as sorted unique cells classified through the dominance tree
+    (sparse.cuh) instead of a 2^(rho d)-bit bitmap: ids, points_examined and
+    |KS_i|, |CS_i| of every layer, both merge modes, identity and general
+    normalisation."""
+    from oracle.oracle import quantize_f32
+    for dist in range(3):
+        v = oracle.generate(dist, 3000, d, 90 + d)
+        for x, mn, mx in ((quantize_f32(v), np.zeros(d), np.ones(d)), (v * 3 - 1, (v * 3 - 1).min(0), (v * 3 - 1).max(0))):
+            for merge in (True, False):
+                want = oracle.compute_skyline(x.astype(np.float64), mn, mx, rho, 1, merge)
+                got = engine.compute_skyline(sky.Dataset(np.ascontiguousarray(x), mn, mx), rho, merge_cross_cell=merge)
+                check(got, want.ids, want.points_examined, want.keys, want.candidates)
+
+
+@pytest.mark.parametrize("dist,n", [(0, 400_000), (1, 400_000), (2, 25_000)])
+def test_gpu_sparse_layer_large(engine, oracle, dist, n):
+    """d = 8, rho = 5 at sizes where the cell tree is large (>64K cells:
+    multi-level tree, two-phase packet query)."""
+    from oracle.oracle import quantize_f32
+    d, rho = 8, 5
+    x = quantize_f32(oracle.generate(dist, n, d, 5))
+    want = oracle.compute_skyline(x.astype(np.float64), np.zeros(d), np.ones(d), rho)
+    got = engine.compute_skyline(sky.Dataset(x, np.zeros(d), np.ones(d)), rho)
+    check(got, want.ids, want.points_examined, want.keys, want.candidates)
 
 
 @pytest.mark.parametrize("d,rho", [(3, 1), (4, 2)])

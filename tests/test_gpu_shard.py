@@ -153,3 +153,47 @@ def test_real_engines_multi_process(world):
     for case in cases:
         ok_ids, ok_ex, ok_layers = q.get(timeout=120)
         assert ok_ids and ok_ex and ok_layers, case
+
+
+# ---- the single-process multi-device handle (skycell_gpu_multi_*): the
+# library runs the sharded protocol itself, exchanges included.
+@pytest.fixture(scope="module", params=[2, 3, 4])
+def multi(request):
+    m = sky.MultiEngine([0] * request.param)
+    yield m
+    m.close()
+
+
+@pytest.mark.parametrize("dist,n,d", [(0, 200_000, 4), (1, 150_000, 4), (2, 60_000, 5), (2, 20_000, 3), (0, 7, 2)])
+def test_multi_device_handle_matches_single(multi, oracle, dist, n, d):
+    from oracle.oracle import quantize_f32
+    v = oracle.generate(dist, n, d, 31 + dist)
+    rho = sky.default_rho(n, d)
+    cases = [(quantize_f32(v), np.zeros(d), np.ones(d)),
+             (v * 6.0 - 2.0, (v * 6.0 - 2.0).min(0), (v * 6.0 - 2.0).max(0))]
+    for x, mn, mx in cases:
+        want = oracle.compute_skyline(x.astype(np.float64), mn, mx, rho)
+        got = multi.compute_skyline(sky.Dataset(np.ascontiguousarray(x), mn, mx), rho)
+        assert np.array_equal(np.asarray(got.ids), want.ids)
+        assert got.points_examined == want.points_examined
+        assert got.layers.keys == want.keys and got.layers.candidates == want.candidates
+
+
+def test_multi_device_handle_routes_and_errors(multi, engine, oracle):
+    """Queries sharding cannot serve run on the first device (merge_cross_cell
+    = false, a sparse layer rho); a non-finite record in a later shard is
+    reported with its global record index, as by the single-device query."""
+    from oracle.oracle import quantize_f32
+    x = quantize_f32(oracle.generate(2, 4000, 8, 3))
+    for rho, merge in ((3, False), (5, True)):
+        want = oracle.compute_skyline(x.astype(np.float64), np.zeros(8), np.ones(8), rho, 1, merge)
+        got = multi.compute_skyline(sky.Dataset(x, np.zeros(8), np.ones(8)), rho, merge_cross_cell=merge)
+        assert np.array_equal(np.asarray(got.ids), want.ids)
+        assert got.points_examined == want.points_examined and got.layers.keys == want.keys
+    y = oracle.generate(0, 9000, 3, 4)
+    y[7777, 1] = np.nan
+    with pytest.raises(sky.InputError) as e1:
+        engine.compute_skyline(sky.Dataset(y, np.zeros(3), np.ones(3)), 3)
+    with pytest.raises(sky.InputError) as e2:
+        multi.compute_skyline(sky.Dataset(y, np.zeros(3), np.ones(3)), 3)
+    assert str(e1.value) == str(e2.value) and "7777" in str(e2.value)

@@ -81,6 +81,24 @@ def test_oracle_equals_reference(oracle, reference, seed):
                 assert (a.points_examined, a.keys, a.candidates) == (b.points_examined, b.keys, b.candidates)
 
 
+@pytest.mark.parametrize("d,rho,n", [(8, 5, 1200), (10, 4, 500)])
+def test_oracle_sparse_layer_equals_reference(oracle, reference, d, rho, n):
+    """rho*d > 36: the reference's layer rho is a hash map (grid.hpp:67); the
+    oracle's linear-index cells (u64) cover the whole budget rho*d <= 60
+    (grid.cpp:38-43).  The GPU's sparse layer-rho path is checked against
+    this oracle at every such (d, rho) (tests/test_gpu_parity.py)."""
+    from oracle.oracle import quantize_f32
+    for dist in range(3):
+        v = reference.generate(dist, n, d, 40 + d)
+        for x, mn, mx, merge in ((quantize_f32(v).astype(np.float64), np.zeros(d), np.ones(d), dist != 1),
+                                 (v * 5 - 2, (v * 5 - 2).min(0), (v * 5 - 2).max(0), dist == 1)):
+            if True:
+                a = oracle.compute_skyline(x, mn, mx, rho, 1, merge)
+                b = reference.compute_skyline(x, mn, mx, rho, 1, merge, workers=4)
+                assert np.array_equal(a.ids, b.ids)
+                assert (a.points_examined, a.keys, a.candidates) == (b.points_examined, b.keys, b.candidates)
+
+
 def test_oracle_quadrant_equals_reference(oracle, reference):
     v = reference.generate(0, 2000, 3, 19)
     mn, mx = v.min(0), v.max(0)
