@@ -41,6 +41,7 @@ struct DevCounters {
   u64 xd, xs_cap; // sample candidates (dense) / those entering the sample skyline (capped)
   u64 pres, pkept;  // K4a -> K4b pending stream: slots handed out / points written
   u64 un, qend;   // union slots and own-slice end (sharded finish)
+  u64 fweak;      // the filter points kill little (k_filter_gate): K4a -> S2 directly
   u64 cand[kMaxLayers];
   u64 key[kMaxLayers];
 };
@@ -799,6 +800,8 @@ struct Pipe final : PipeBase {
         sk::k_strength_order<TOut, D><<<1, 1024, 0, s>>>(
             static_cast<const TOut*>(ctx->s2_rows.p), static_cast<const u64*>(ctx->s2_fsum.p), nullptr, &c->fs,
             (uint32_t)pf_max, static_cast<TOut*>(ctx->f_rows.p), static_cast<u64*>(ctx->f_fsum.p), nullptr, &c->nf);
+        sk::k_filter_gate<<<1, 1, 0, s>>>(&c->fs, &c->xs_cap, &c->fweak);
+        ++ctx->launches;
         sk::k_filter_lists<TOut, D><<<D, 1024, 0, s>>>(static_cast<const TOut*>(ctx->f_rows.p), &c->nf,
                                                         (uint32_t)pf_max, static_cast<uint16_t*>(ctx->f_lists.p),
                                                         static_cast<uint16_t*>(ctx->f_offs.p));
@@ -950,6 +953,13 @@ struct Pipe final : PipeBase {
       pa.out_reserved = &c->pres;
       pa.kept = &c->pkept;
       pa.coop = 0;
+      // weak filter (anti-correlated data): K4a's survivors go straight to S2
+      pa.gate = std::getenv("SKYCELL_NOGATE") ? nullptr : &c->fweak;
+      pa.alt_rows = ctx->s2_rows.p;
+      pa.alt_ids = static_cast<uint32_t*>(ctx->s2_ids.p);
+      pa.alt_fsum = static_cast<u64*>(ctx->s2_fsum.p);
+      pa.alt_reserved = &c->s2;
+      pa.alt_kept = &c->s2_kept;
       if (!k1_head && !std::getenv("SKYCELL_K4A_OLD")) {
         auto ka = wide ? sk::k_cand_head<TOut, D, uint32_t, kThreads> : sk::k_cand_head<TOut, D, uint8_t, kThreads>;
         const size_t sa = ((8 * D * sizeof(TOut) + 15) & ~(size_t)15) + 8 * 8 +

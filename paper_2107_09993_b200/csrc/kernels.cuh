@@ -899,6 +899,14 @@ struct CandParams {
   int d_wide;
   uint32_t head_start;   // first filter point of the branch-free head
   int coop;              // run the warp-cooperative phase for points the head leaves
+  // K4a: when *gate != 0 (k_filter_gate) the survivors go to the alt_*
+  // stream (S2) instead of out_* (the K4b input)
+  const u64* gate;
+  void* alt_rows;
+  uint32_t* alt_ids;
+  u64* alt_fsum;
+  u64* alt_reserved;
+  u64* alt_kept;
 };
 
 template <typename T, int D, typename TT, int THREADS>
@@ -1082,7 +1090,12 @@ __global__ void __launch_bounds__(THREADS) k_cand_head(CandParams p) {
   }
   __syncthreads();
   const T* rows = static_cast<const T*>(p.rows);
-  T* out_rows = static_cast<T*>(p.out_rows);
+  const bool alt = p.gate && *p.gate;
+  T* out_rows = static_cast<T*>(alt ? p.alt_rows : p.out_rows);
+  uint32_t* out_ids = alt ? p.alt_ids : p.out_ids;
+  u64* out_fsum = alt ? p.alt_fsum : p.out_fsum;
+  u64* out_reserved = alt ? p.alt_reserved : p.out_reserved;
+  u64* out_kept = alt ? p.alt_kept : p.kept;
   const TT* PM = static_cast<const TT*>(p.PM);
   const int rho = p.rho, top = (1 << rho) - 1;
   const float fscale = ldexpf(1.0f, rho);
@@ -1091,7 +1104,7 @@ __global__ void __launch_bounds__(THREADS) k_cand_head(CandParams p) {
   const u64 nw = ((u64)gridDim.x * THREADS) >> 5;
   const unsigned lt = (1u << lane) - 1;
   WarpOut wo{0, p.chunk, p.chunk};
-  auto stamp = [&](u64 slot) { p.out_ids[slot] = kNoId; };
+  auto stamp = [&](u64 slot) { out_ids[slot] = kNoId; };
   u64 examined = 0, kept = 0;
   unsigned head = 0, tail = 0;  // ring positions (warp-uniform)
   // head-8 test of up to 32 queued candidates; survivors -> P
@@ -1115,24 +1128,37 @@ __global__ void __launch_bounds__(THREADS) k_cand_head(CandParams p) {
     const bool keep = act && !dom;
     kept += keep;
     if (__any_sync(kFull, keep)) {
-      const u64 o = warp_reserve(wo, keep, p.out_reserved, stamp);
+      const u64 o = warp_reserve(wo, keep, out_reserved, stamp);
       if (keep) {
         store_row<T, D>(out_rows, o, v);
-        p.out_ids[o] = pid;
-        p.out_fsum[o] = ps;
+        out_ids[o] = pid;
+        out_fsum[o] = ps;
       }
     }
     head += cnt;
     __syncwarp();
   };
+  // the next batch's id and row are loaded while this one is processed (the
+  // row load does not wait for the id: slots of kNoId hold don't-care rows)
+  uint32_t pid_n = kNoId;
+  T v_n[D];
+  auto fetch = [&](u64 wb) {
+    const u64 i = wb + lane;
+    pid_n = kNoId;
+    if (i < n) {
+      pid_n = p.ids[i];
+      load_row_cached<T, D>(rows, i, v_n);
+    }
+  };
+  if (gw * 32 < n) fetch(gw * 32);
   for (u64 wbase = gw * 32; wbase < n; wbase += nw * 32) {
-    const u64 i = wbase + lane;
-    uint32_t pid = kNoId;
-    if (i < n) pid = p.ids[i];
-    bool cand = false;
+    const uint32_t pid = pid_n;
     T v[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) v[k] = v_n[k];
+    if (wbase + nw * 32 < n) fetch(wbase + nw * 32);
+    bool cand = false;
     if (pid != kNoId) {
-      load_row_cached<T, D>(rows, i, v);
       int col[D];
 #pragma unroll
       for (int k = 0; k < D; ++k) {
@@ -1162,7 +1188,7 @@ __global__ void __launch_bounds__(THREADS) k_cand_head(CandParams p) {
   }
   if (lane == 0) {
     if (p.examined && examined) atomicAdd(p.examined, examined);
-    if (kept) atomicAdd(p.kept, kept);
+    if (kept) atomicAdd(out_kept, kept);
   }
 }
 
@@ -1753,6 +1779,16 @@ __global__ void k_pack_members(const T* __restrict__ rows, const uint32_t* __res
       out_ids[o] = ids[i];
     }
   }
+}
+
+// Filter-point gate: when a quarter or more of the sample's candidates are
+// its own skyline points (anti-correlated data), the filter points kill
+// little and the long column-prefix scans of K4b cost more than the points
+// they remove (C3: 15 ms for ~1%); K4a then sends its survivors straight to
+// S2 and K4b has nothing to do.
+static __global__ void k_filter_gate(const u64* __restrict__ sky, const u64* __restrict__ cands,
+                                     u64* __restrict__ weak) {
+  *weak = *sky * 4 > *cands;
 }
 
 static __global__ void k_clamp_count(const u64* __restrict__ src, u64 cap, u64* __restrict__ dst) {
