@@ -4,9 +4,11 @@
 //   validate (dataset.cpp:23-24, grid.cpp:38-43) -> K0 sample filter -> K1
 //   streaming pass -> K3 cell tables + per-layer counts -> K4 candidate
 //   filter -> K5 exact sort-first dominance -> K6 ids (ascending) + stats.
-// Every data-dependent size stays on the device (kernels read their input
-// counts from device memory), so the whole query is enqueued without a host
-// round trip; the only synchronisation is the final read of the counters.
+// Data-dependent sizes stay on the device (kernels read their input counts
+// from device memory).  The host synchronises only where a count must reach
+// it: before a K5 whose set may exceed the list threshold (lists or tree,
+// and CUB's item count), in the sparse layer-rho stage, and for the final
+// read of the counters.
 //
 // The same pipeline object runs the sharded (multi-GPU) query in phases
 // (DESIGN.md §4): local (K0+K1) | occupancy exchange (K2) | prune + local
