@@ -170,6 +170,35 @@ int skycell_gpu_multi_skyline_f32(skycell_gpu_multi* m, const float* coords, uin
                                   int merge_cross_cell, uint32_t* ids_out, uint64_t* n_out,
                                   skycell_gpu_stats* stats, char* err, size_t err_len);
 
+/* ---- MultiLayerGrid drop-in (proj/include/skycell/grid.hpp:33-70,
+ * proj/src/grid.cpp:35-140).  Built on the device from a normalised PointSet
+ * (coords n x d doubles in [0, 1 - 2^-32], ids n uint32 or NULL for 0..n-1;
+ * host or device pointers): points sorted by the Z-order key of their
+ * layer-rho cell, ties by input position (grid.cpp:47-54); the contiguous
+ * point range of every non-empty layer-rho cell; occupancy of layers
+ * 0..rho-1 by child-OR.  ConfigError on the reference's rho budget
+ * (grid.cpp:38-43).  Cells are named by their linear index
+ * (CellIndex::linear_index, cell.hpp:102-107).
+ *   grid_points          the sorted PointSet (coords, ids; host or device)
+ *   grid_nonempty_count  MultiLayerGrid::nonempty_count(layer)
+ *   grid_nonempty_cells  nonempty_cells(layer): ascending linear indices
+ *                        (enumeration order, lex_less); count entries
+ *   grid_lookup          batch of `count` cells of one layer: occupied
+ *                        (occupied(), grid.cpp:105-113) and, at layer rho,
+ *                        [begin, end) (range(), grid.cpp:115-119; empty cells
+ *                        0, 0); begin/end at another layer is UsageError
+ *                        "range: only layer-rho cells carry point ranges". */
+typedef struct skycell_gpu_grid skycell_gpu_grid;
+int skycell_gpu_grid_build(skycell_gpu_ctx* ctx, const double* coords, const uint32_t* ids, uint64_t n, int d,
+                           int rho, skycell_gpu_grid** out, char* err, size_t err_len);
+void skycell_gpu_grid_destroy(skycell_gpu_grid* g);
+int skycell_gpu_grid_shape(const skycell_gpu_grid* g, uint64_t* n, int* d, int* rho);
+uint64_t skycell_gpu_grid_nonempty_count(const skycell_gpu_grid* g, int layer);
+int skycell_gpu_grid_points(skycell_gpu_grid* g, double* coords_out, uint32_t* ids_out, char* err, size_t err_len);
+int skycell_gpu_grid_nonempty_cells(skycell_gpu_grid* g, int layer, uint64_t* lin_out, char* err, size_t err_len);
+int skycell_gpu_grid_lookup(skycell_gpu_grid* g, int layer, const uint64_t* lin, uint64_t count, uint8_t* occupied,
+                            uint32_t* begin, uint32_t* end, char* err, size_t err_len);
+
 /* On-device synthetic data with the reference generator's streams
  * (skycell::generate, datagen.cpp:62-87): dist 0 independent, 1 correlated,
  * 2 anti-correlated.  kind 0 writes n*d raw doubles, kind 1 writes n*d floats

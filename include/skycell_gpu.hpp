@@ -12,6 +12,8 @@
 //                                   (refine.hpp:66-68, refine.cpp:160-184)
 //   skycell::gpu::MultiDevice       compute_skyline sharded over several
 //                                   GPUs of one process
+//   skycell::gpu::MultiLayerGrid    replaces  skycell::MultiLayerGrid
+//                                   (grid.hpp:33-70, grid.cpp:35-140)
 //
 // Status codes are rethrown as the reference's exception types
 // (proj/include/skycell/error.hpp:9-26) with the reference's message text.
@@ -29,6 +31,7 @@
 
 #include "skycell/dataset.hpp"
 #include "skycell/error.hpp"
+#include "skycell/grid.hpp"
 #include "skycell/parallel.hpp"
 #include "skycell/refine.hpp"
 #include "skycell_gpu.h"
@@ -66,6 +69,9 @@ class Device {
   ~Device() { skycell_gpu_destroy(ctx_); }
   Device(const Device&) = delete;
   Device& operator=(const Device&) = delete;
+
+  skycell_gpu_ctx* context() { return ctx_; }
+  std::mutex& mutex() { return mu_; }
 
   SkylineResult compute_skyline(const Dataset& ds, int rho, Mode mode, bool merge_cross_cell = true) {
     SkylineResult r;
@@ -181,5 +187,77 @@ inline SkylineResult quadrant_skyline(const Dataset& ds, std::span<const double>
                                       ThreadPool& /*pool*/) {
   return default_device().quadrant_skyline(ds, origin, rho, mode);
 }
+
+// Same interface as skycell::MultiLayerGrid (grid.hpp:33-70), built on the
+// device (skycell_gpu_grid_*): the sorted PointSet, layer-rho ranges,
+// occupancy of every layer.  Needs the reference headers and library for
+// CellIndex / point_to_cell, like the rest of this header.
+class MultiLayerGrid {
+ public:
+  MultiLayerGrid(PointSet points, int rho, Device& dev = default_device()) : rho_(rho) {
+    char err[512] = {0};
+    int rc;
+    {
+      std::lock_guard<std::mutex> lock(dev.mutex());
+      rc = skycell_gpu_grid_build(dev.context(), points.coords.data(), points.ids.data(), points.n, points.d, rho, &g_,
+                                  err, sizeof err);
+    }
+    throw_status(rc, err);
+    points_.n = points.n;
+    points_.d = points.d;
+    points_.coords.resize(points.coords.size());
+    points_.ids.resize(points.n);
+    throw_status(skycell_gpu_grid_points(g_, points_.coords.data(), points_.ids.data(), err, sizeof err), err);
+  }
+  ~MultiLayerGrid() { skycell_gpu_grid_destroy(g_); }
+  MultiLayerGrid(const MultiLayerGrid&) = delete;
+  MultiLayerGrid& operator=(const MultiLayerGrid&) = delete;
+
+  int rho() const { return rho_; }
+  int dims() const { return points_.d; }
+  uint32_t size() const { return points_.n; }
+  const PointSet& points() const { return points_; }
+  CellIndex cell_of(uint32_t position, int layer) const { return point_to_cell(points_.point(position), layer); }
+
+  bool occupied(const CellIndex& c) const {
+    if (c.is_auxiliary()) return true;
+    if (!c.in_grid() || c.layer() > rho_) return false;
+    for (int k = 0; k < c.dims(); ++k)
+      if (c.col(k) > c.top_column()) return false;
+    const uint64_t lin = c.linear_index();
+    uint8_t occ = 0;
+    char err[512] = {0};
+    throw_status(skycell_gpu_grid_lookup(g_, c.layer(), &lin, 1, &occ, nullptr, nullptr, err, sizeof err), err);
+    return occ != 0;
+  }
+
+  CellRange range(const CellIndex& leaf_cell) const {
+    if (leaf_cell.layer() != rho_) throw UsageError("range: only layer-rho cells carry point ranges");
+    const uint64_t lin = leaf_cell.linear_index();
+    uint32_t b = 0, e = 0;
+    char err[512] = {0};
+    throw_status(skycell_gpu_grid_lookup(g_, rho_, &lin, 1, nullptr, &b, &e, err, sizeof err), err);
+    return CellRange{b, e};
+  }
+
+  std::vector<CellIndex> nonempty_cells(int layer) const {
+    std::vector<uint64_t> lin(skycell_gpu_grid_nonempty_count(g_, layer));
+    char err[512] = {0};
+    if (!lin.empty()) throw_status(skycell_gpu_grid_nonempty_cells(g_, layer, lin.data(), err, sizeof err), err);
+    std::vector<CellIndex> out;
+    out.reserve(lin.size());
+    for (uint64_t x : lin) out.push_back(CellIndex::from_linear_index(x, layer, points_.d));
+    return out;
+  }
+
+  uint64_t nonempty_count(int layer) const { return skycell_gpu_grid_nonempty_count(g_, layer); }
+  CellIndex origin_cell() const { return CellIndex(0, points_.d); }
+  static int default_rho(uint64_t n, int d) { return skycell_default_rho(n, d); }
+
+ private:
+  skycell_gpu_grid* g_ = nullptr;
+  PointSet points_;
+  int rho_;
+};
 
 }  // namespace skycell::gpu

@@ -197,6 +197,9 @@ class Reference:
                                       C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t]
         L.ref_normalize.argtypes = [C.POINTER(C.c_double), C.c_uint64, C.c_int, C.POINTER(C.c_double),
                                     C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_char_p, C.c_size_t]
+        L.ref_grid.argtypes = [C.POINTER(C.c_double), C.c_uint64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_uint32),
+                               C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint32),
+                               C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t]
         L.ref_write_bin.argtypes = [C.c_char_p, C.POINTER(C.c_double), C.c_uint64, C.c_int, C.c_char_p, C.c_size_t]
         L.ref_read_bin.argtypes = [C.c_char_p, C.POINTER(C.c_uint64), C.POINTER(C.c_int), C.POINTER(C.c_double),
                                    C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_char_p, C.c_size_t]
@@ -204,6 +207,24 @@ class Reference:
     def _check(self, rc, err):
         if rc != 0:
             raise CpuError(rc, err.value.decode())
+
+    def grid(self, coords, rho: int, layer: int):
+        """skycell::MultiLayerGrid (grid.cpp:35-103) over a normalised PointSet
+        with ids 0..n-1: dict(ids, counts, leaf_lin, leaf_begin, leaf_end,
+        layer_lin) -- layer_lin = nonempty_cells(layer) as linear indices."""
+        x = _f64(coords)
+        n, d = x.shape
+        ids = np.empty(max(n, 1), dtype=np.uint32)
+        counts = np.zeros(rho + 1, dtype=np.uint64)
+        lin, beg, end = np.empty(max(n, 1), dtype=np.uint64), np.empty(max(n, 1), dtype=np.uint32), np.empty(max(n, 1), dtype=np.uint32)
+        cells = np.empty(max(n, 1 << min(24, layer * d)), dtype=np.uint64)
+        err = C.create_string_buffer(512)
+        self._check(self.lib.ref_grid(_ptr(x, C.c_double), n, d, rho, layer, _ptr(ids, C.c_uint32),
+                                      _ptr(counts, C.c_uint64), _ptr(lin, C.c_uint64), _ptr(beg, C.c_uint32),
+                                      _ptr(end, C.c_uint32), _ptr(cells, C.c_uint64), err, 512), err)
+        nl, nc = int(counts[rho]), int(counts[layer])
+        return dict(ids=ids[:n], counts=[int(c) for c in counts], leaf_lin=lin[:nl], leaf_begin=beg[:nl],
+                    leaf_end=end[:nl], layer_lin=cells[:nc])
 
     def write_bin(self, path: str, coords) -> None:
         """skycell::write_bin (datagen.cpp:185-199)."""

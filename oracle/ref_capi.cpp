@@ -104,6 +104,34 @@ int ref_generate(int dist, uint64_t n, int d, uint64_t seed, int workers, double
 
 int ref_default_rho(uint64_t n, int d) { return skycell::MultiLayerGrid::default_rho(n, d); }
 
+// MultiLayerGrid over a normalised PointSet (ids 0..n-1): the sorted ids,
+// the non-empty counts of layers 0..rho, the non-empty leaf cells (linear
+// index, range) in enumeration order, and the non-empty cells of `layer`.
+int ref_grid(const double* coords, uint64_t n, int d, int rho, int layer, uint32_t* sorted_ids, uint64_t* counts,
+             uint64_t* leaf_lin, uint32_t* leaf_begin, uint32_t* leaf_end, uint64_t* layer_lin, char* err,
+             size_t err_len) {
+  return guarded(err, err_len, [&] {
+    skycell::PointSet ps;
+    ps.n = static_cast<uint32_t>(n);
+    ps.d = d;
+    ps.coords.assign(coords, coords + n * static_cast<uint64_t>(d));
+    ps.ids.resize(n);
+    for (uint32_t i = 0; i < n; ++i) ps.ids[i] = i;
+    skycell::MultiLayerGrid g(std::move(ps), rho);
+    std::memcpy(sorted_ids, g.points().ids.data(), n * sizeof(uint32_t));
+    for (int L = 0; L <= rho; ++L) counts[L] = g.nonempty_count(L);
+    const auto leaves = g.nonempty_cells(rho);
+    for (size_t i = 0; i < leaves.size(); ++i) {
+      leaf_lin[i] = leaves[i].linear_index();
+      const skycell::CellRange r = g.range(leaves[i]);
+      leaf_begin[i] = r.begin;
+      leaf_end[i] = r.end;
+    }
+    const auto cells = g.nonempty_cells(layer);
+    for (size_t i = 0; i < cells.size(); ++i) layer_lin[i] = cells[i].linear_index();
+  });
+}
+
 int ref_write_bin(const char* path, const double* coords, uint64_t n, int d, char* err, size_t err_len) {
   return guarded(err, err_len, [&] {
     const std::vector<double> lo(d, 0.0), hi(d, 1.0);

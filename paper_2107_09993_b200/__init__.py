@@ -5,13 +5,13 @@ The product is ``lib/libskycell_gpu.so`` (sm_100a kernels behind the C ABI in
 API.  See DESIGN.md.
 """
 from .skycell import (  # noqa: F401
-    ConfigError, CudaError, Dataset, Engine, InputError, IoError, LayerCounts, Mode, MultiEngine,
+    ConfigError, CudaError, Dataset, Engine, InputError, IoError, LayerCounts, Mode, MultiEngine, MultiLayerGrid,
     SkycellError, SkylineResult, StageTimes, UnsupportedError, UsageError, bin_header, compute_skyline, default_rho, engine,
     load_library, quadrant_skyline, validate,
 )
 
 __all__ = [
     "ConfigError", "CudaError", "Dataset", "Engine", "InputError", "IoError", "LayerCounts", "Mode",
-    "MultiEngine", "SkycellError", "SkylineResult", "StageTimes", "UnsupportedError", "UsageError", "bin_header", "compute_skyline",
+    "MultiEngine", "MultiLayerGrid", "SkycellError", "SkylineResult", "StageTimes", "UnsupportedError", "UsageError", "bin_header", "compute_skyline",
     "default_rho", "engine", "load_library", "quadrant_skyline", "validate",
 ]

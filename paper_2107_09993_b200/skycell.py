@@ -159,6 +159,8 @@ EXPORTS = (
     "skycell_gpu_version", "skycell_bin_header", "skycell_gpu_read_bin", "skycell_gpu_write_bin",
     "skycell_gpu_multi_create", "skycell_gpu_multi_destroy", "skycell_gpu_multi_size", "skycell_gpu_multi_context",
     "skycell_gpu_multi_skyline_f64", "skycell_gpu_multi_skyline_f32",
+    "skycell_gpu_grid_build", "skycell_gpu_grid_destroy", "skycell_gpu_grid_shape", "skycell_gpu_grid_nonempty_count",
+    "skycell_gpu_grid_points", "skycell_gpu_grid_nonempty_cells", "skycell_gpu_grid_lookup",
 )
 
 
@@ -205,6 +207,15 @@ def load_library(path: str = LIB_PATH):
         lib.skycell_gpu_multi_context.restype = vp
         for fn in (lib.skycell_gpu_multi_skyline_f64, lib.skycell_gpu_multi_skyline_f32):
             fn.argtypes = [vp, fp, u64, i32, dp, dp, i32, i32, i32, u32p, u64p, C.POINTER(_Stats), cp, sz]
+        lib.skycell_gpu_grid_build.argtypes = [vp, vp, vp, u64, i32, i32, C.POINTER(vp), cp, sz]
+        lib.skycell_gpu_grid_destroy.argtypes = [vp]
+        lib.skycell_gpu_grid_destroy.restype = None
+        lib.skycell_gpu_grid_shape.argtypes = [vp, u64p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        lib.skycell_gpu_grid_nonempty_count.argtypes = [vp, i32]
+        lib.skycell_gpu_grid_nonempty_count.restype = C.c_uint64
+        lib.skycell_gpu_grid_points.argtypes = [vp, vp, vp, cp, sz]
+        lib.skycell_gpu_grid_nonempty_cells.argtypes = [vp, i32, vp, cp, sz]
+        lib.skycell_gpu_grid_lookup.argtypes = [vp, i32, vp, u64, vp, vp, vp, cp, sz]
         _lib = lib
         return lib
 
@@ -297,6 +308,10 @@ class Engine:
         _raise(self.lib.skycell_gpu_generate_range(self._ctx, int(dist), n, d, seed, 1 if quantized else 0, begin,
                                                    count, C.c_void_p(out.data_ptr()), err, 512), err)
         return out
+
+    def grid(self, coords, rho: int, ids=None) -> "MultiLayerGrid":
+        """MultiLayerGrid(PointSet, rho) on this device (grid.cpp:35-103)."""
+        return MultiLayerGrid(self, coords, rho, ids)
 
     def read_bin(self, path: str):
         """skycell::read_bin (datagen.cpp:201-221) straight into device memory:
@@ -411,6 +426,90 @@ class Engine:
                                                    err, 512)
         _raise(rc, err)
         return _to_result(ids[: n_out.value].copy(), st)
+
+
+class MultiLayerGrid:
+    """skycell::MultiLayerGrid (grid.hpp:33-70) built on the device
+    (skycell_gpu_grid_*).  Cells are named by their linear index
+    (CellIndex::linear_index, dim d-1 most significant)."""
+
+    def __init__(self, engine: "Engine", coords, rho: int, ids=None):
+        self.lib = engine.lib
+        x = np.ascontiguousarray(coords, dtype=np.float64)
+        if x.ndim != 2:
+            raise UsageError("MultiLayerGrid: coords must be (n, d)")
+        n, d = x.shape
+        idp = None
+        if ids is not None:
+            ids = np.ascontiguousarray(ids, dtype=np.uint32)
+            if ids.shape != (n,):
+                raise UsageError("MultiLayerGrid: ids must hold n values")
+            idp = C.c_void_p(ids.ctypes.data)
+        self._g = C.c_void_p()
+        err = C.create_string_buffer(512)
+        with engine._lock:
+            rc = self.lib.skycell_gpu_grid_build(engine._ctx, C.c_void_p(x.ctypes.data), idp, n, d, rho,
+                                                 C.byref(self._g), err, 512)
+        _raise(rc, err)
+        self.n, self.d, self._rho = n, d, rho
+
+    def close(self) -> None:
+        if self._g:
+            self.lib.skycell_gpu_grid_destroy(self._g)
+            self._g = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def rho(self) -> int:
+        return self._rho
+
+    def dims(self) -> int:
+        return self.d
+
+    def size(self) -> int:
+        return self.n
+
+    def points(self):
+        """The sorted PointSet: (coords (n, d) float64, ids uint32)."""
+        x = np.empty((self.n, self.d), dtype=np.float64)
+        ids = np.empty(self.n, dtype=np.uint32)
+        err = C.create_string_buffer(512)
+        _raise(self.lib.skycell_gpu_grid_points(self._g, C.c_void_p(x.ctypes.data), C.c_void_p(ids.ctypes.data),
+                                                err, 512), err)
+        return x, ids
+
+    def nonempty_count(self, layer: int) -> int:
+        return int(self.lib.skycell_gpu_grid_nonempty_count(self._g, layer))
+
+    def nonempty_cells(self, layer: int) -> np.ndarray:
+        out = np.empty(max(self.nonempty_count(layer), 1), dtype=np.uint64)
+        err = C.create_string_buffer(512)
+        _raise(self.lib.skycell_gpu_grid_nonempty_cells(self._g, layer, C.c_void_p(out.ctypes.data), err, 512), err)
+        return out[: self.nonempty_count(layer)]
+
+    def _lookup(self, layer: int, lins, ranges: bool):
+        q = np.ascontiguousarray(lins, dtype=np.uint64)
+        occ = np.empty(max(q.size, 1), dtype=np.uint8)
+        b = np.empty(max(q.size, 1), dtype=np.uint32) if ranges else None
+        e = np.empty(max(q.size, 1), dtype=np.uint32) if ranges else None
+        err = C.create_string_buffer(512)
+        _raise(self.lib.skycell_gpu_grid_lookup(self._g, layer, C.c_void_p(q.ctypes.data), q.size,
+                                                C.c_void_p(occ.ctypes.data), C.c_void_p(b.ctypes.data) if ranges else None,
+                                                C.c_void_p(e.ctypes.data) if ranges else None, err, 512), err)
+        return occ[: q.size].astype(bool), (b[: q.size] if ranges else None), (e[: q.size] if ranges else None)
+
+    def occupied(self, layer: int, lins) -> np.ndarray:
+        """MultiLayerGrid::occupied for in-grid cells of one layer (batch)."""
+        return self._lookup(layer, lins, False)[0]
+
+    def range(self, lins):
+        """MultiLayerGrid::range for layer-rho cells (batch): (begin, end)."""
+        _, b, e = self._lookup(self._rho, lins, True)
+        return b, e
 
 
 class MultiEngine:

@@ -45,6 +45,33 @@ skycell::Dataset quantised(skycell::Distribution dist, uint32_t n, int d, uint64
   return ds;
 }
 
+// skycell::gpu::MultiLayerGrid against skycell::MultiLayerGrid on the same
+// normalised PointSet (grid.cpp:35-140).
+bool same_grid(const skycell::PointSet& ps, int rho) {
+  skycell::MultiLayerGrid want(ps, rho);
+  skycell::gpu::MultiLayerGrid got(ps, rho);
+  if (want.points().ids != got.points().ids || want.points().coords != got.points().coords) return false;
+  if (want.rho() != got.rho() || want.dims() != got.dims() || want.size() != got.size()) return false;
+  for (int L = 0; L <= rho; ++L) {
+    if (want.nonempty_count(L) != got.nonempty_count(L)) return false;
+    const auto a = want.nonempty_cells(L), b = got.nonempty_cells(L);
+    if (a.size() != b.size()) return false;
+    for (size_t i = 0; i < a.size(); ++i) {
+      if (a[i].linear_index() != b[i].linear_index()) return false;
+      if (!got.occupied(a[i])) return false;
+      if (L == rho) {
+        const auto ra = want.range(a[i]), rb = got.range(b[i]);
+        if (ra.begin != rb.begin || ra.end != rb.end) return false;
+      }
+    }
+    // auxiliary cells are always occupied; a cell past the top is not
+    if (!got.occupied(skycell::CellIndex::auxiliary(L, ps.d, 0))) return false;
+  }
+  for (uint32_t pos = 0; pos < ps.n; pos += 97)
+    if (!(want.cell_of(pos, rho) == got.cell_of(pos, rho))) return false;
+  return true;
+}
+
 template <typename F>
 std::string what_of(F&& f, int* kind) {
   try {
@@ -100,6 +127,11 @@ int main() {
       auto w3 = skycell::compute_skyline(raw, 2, skycell::Mode::kParallel, pool, false);
       auto g3 = skycell::gpu::compute_skyline(raw, 2, skycell::Mode::kParallel, pool, false);
       expect(same(w3, g3), "compute_skyline merge_cross_cell=false d=" + std::to_string(d));
+      {
+        const skycell::PointSet ps = skycell::normalize(raw);
+        expect(same_grid(ps, std::min(3, skycell::MultiLayerGrid::default_rho(ps.n, d) + 1)),
+               "MultiLayerGrid d=" + std::to_string(d));
+      }
       std::vector<double> origin(d, 0.2);
       auto wq = skycell::quadrant_skyline(raw, origin, 4, skycell::Mode::kParallel, pool);
       auto gq = skycell::gpu::quadrant_skyline(raw, origin, 4, skycell::Mode::kParallel, pool);
