@@ -353,7 +353,7 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
     // the plain grid, then grids shifted by 1/2, 1/4, 3/4 of a cell: 4 passes
     // at d >= 5 (C3: 542 -> 499 ms), 2 below (anti d=4: 11.2 vs 11.8 ms with 4)
     int passes = D >= 5 ? 4 : 2;
-    if (const char* e = std::getenv("SKYCELL_PREPASSES")) passes = std::max(1, std::min(4, std::atoi(e)));
+    if (const char* e = std::getenv("SKYCELL_PREPASSES")) passes = std::max(1, std::min(8, std::atoi(e)));
     for (int pass = 0; pass < passes; ++pass) {
       ck(cudaMemsetAsync(cm, 0xff, cells * 8, s), "memset");
       sk::k_cellmin<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, count, Lc, pass, killb, cm);
@@ -434,7 +434,7 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
     const unsigned gq = (unsigned)std::max<u64>(1, std::min<u64>((sh.nleaf * 32 + 255) / 256, (u64)nsm * 8));
     // phase-1 search radius (levels above the own leaf); phase 2 re-packs the
     // undecided points (SKYCELL_PK_H1 overrides; >= levels: one phase)
-    int h1 = D <= 6 ? 5 : 6;  // measured best (C3 d=6: 131 ms at 5; d=7/8: 765 / 1903 ms at 6)
+    int h1 = D <= 6 ? 4 : 6;  // measured best (profiles/k5_h1_sweep_*: C3 at 4, d=7/8 at 6)
     if (const char* e = std::getenv("SKYCELL_PK_H1")) h1 = std::atoi(e);
     const bool two = h1 < sh.levels - 1;
     uint32_t* umask = static_cast<uint32_t*>(ctx->t_keys.p);       // free after the sort

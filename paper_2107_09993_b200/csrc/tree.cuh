@@ -59,8 +59,10 @@ __device__ __forceinline__ u64 morton_of(const T (&v)[D]) {
 template <typename T, int D>
 __device__ __forceinline__ void grid_cols(const T (&v)[D], int L, int pass, int (&c)[D]) {
   const T sc = (T)(1u << L);
-  // cell offsets of the passes: 0, 1/2, 1/4, 3/4 (exact in binary)
-  const T off = pass == 0 ? (T)0 : pass == 1 ? (T)0.5 : pass == 2 ? (T)0.25 : (T)0.75;
+  // cell offsets of the passes: 0, 1/2, 1/4, 3/4, 1/8, 5/8, 3/8, 7/8 (exact in binary)
+  const int o8 = pass == 0 ? 0 : pass == 1 ? 4 : pass == 2 ? 2 : pass == 3 ? 6 : pass == 4 ? 1 : pass == 5 ? 5
+               : pass == 6 ? 3 : 7;
+  const T off = (T)o8 * (T)0.125;
   const int top = (1 << L) - 1;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
