@@ -95,6 +95,7 @@ struct PipeBase {
   virtual u64 occ_bytes() const = 0;
   virtual void export_occ(void* dst) = 0;
   virtual void or_gathered(const void* gathered, int world) = 0;
+  virtual void or_peers(const void* const* dev_table, int world) = 0;
   virtual u64 prune_local_skyline() = 0;
   virtual u64 block_bytes(u64 maxc) const = 0;
   virtual void pack(void* dst, u64 maxc) = 0;
@@ -872,6 +873,14 @@ struct Pipe final : PipeBase {
     const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((w4 + 255) / 256, (u64)nsm * 8));
     sk::k_or_gather<<<g, 256, 0, s>>>(static_cast<const uint4*>(gathered), world, w4,
                                       static_cast<uint4*>(at(o_occ[1])));
+    ++ctx->launches;
+  }
+
+  void or_peers(const void* const* dev_table, int world) override {
+    const u64 w4 = occ_bytes() / 16;
+    const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((w4 + 255) / 256, (u64)nsm * 8));
+    sk::k_or_peers<<<g, 256, 0, s>>>(reinterpret_cast<const uint4* const*>(dev_table), world, w4,
+                                     static_cast<uint4*>(at(o_occ[1])));
     ++ctx->launches;
   }
 

@@ -1752,6 +1752,23 @@ static __global__ void k_or_gather(const uint4* __restrict__ gathered, int world
   }
 }
 
+// Exchange 1 fused with the OR, single-process multi-GPU (csrc/multi.cu):
+// srcs[g] is device g's exported occupancy region, read in place over NVLink
+// / NVSwitch (peer access); no gather buffer, one pass.
+static __global__ void k_or_peers(const uint4* const* __restrict__ srcs, int world, u64 words4, uint4* __restrict__ dst) {
+  for (u64 w = blockIdx.x * (u64)blockDim.x + threadIdx.x; w < words4; w += (u64)gridDim.x * blockDim.x) {
+    uint4 x = srcs[0][w];
+    for (int g = 1; g < world; ++g) {
+      const uint4 y = srcs[g][w];
+      x.x |= y.x;
+      x.y |= y.y;
+      x.z |= y.z;
+      x.w |= y.w;
+    }
+    dst[w] = x;
+  }
+}
+
 // Members (flag set, id != kNoId) of a slot array -> dense rows / sums / ids
 // (order irrelevant: the final ids are ordered through the id bitmap).
 template <typename T, int D>

@@ -4,13 +4,14 @@
 // skycell::gpu::compute_skyline (the drop-in for refine.hpp:61-62) uses every
 // GPU of the box from plain C++ -- no MPI, no NCCL communicator to set up.
 //
-// The two exchanges are device-to-device copies between the contexts'
-// buffers (over NVLink / NVSwitch on a multi-GPU B200 box: cudaMemcpyPeerAsync
-// with peer access enabled), ordered by cross-device events, with no host
-// round trip except the two counts the protocol needs on the host anyway:
-//   exchange 1: every device gathers all occupancy regions, then ORs them
-//               (k_or_gather inside skycell_gpu_shard_prune);
-//   exchange 2: every device gathers all padded local skylines.
+// The two exchanges run device to device, ordered by cross-device events,
+// with no host round trip except the two counts the protocol needs anyway:
+//   exchange 1: every device ORs all occupancy regions in one kernel that
+//               reads the peers' regions in place over NVLink / NVSwitch
+//               (k_or_peers; peer access) -- or, without peer access, gathers
+//               them with cudaMemcpyPeerAsync and ORs the gather buffer;
+//   exchange 2: every device gathers all padded local skylines
+//               (cudaMemcpyPeerAsync).
 // Each phase runs on one host thread per device, so the devices' H2D
 // staging, K0-K5 and finish passes overlap.
 #include <thread>
@@ -21,8 +22,9 @@ using sk::u64;
 
 struct skycell_gpu_multi {
   std::vector<skycell_gpu_ctx*> ctx;
-  std::vector<skyeng::DevBuf> occ, gath, send, recv;  // per device
-  std::vector<cudaEvent_t> ev;                        // per device: "my exchange buffer is ready"
+  std::vector<skyeng::DevBuf> occ, gath, send, recv, tbl;  // per device
+  std::vector<cudaEvent_t> ev;                             // per device: "my exchange buffer is ready"
+  bool peer = true;  // every device reads every other's memory (peer access or the same device)
 };
 
 namespace skyeng {
@@ -102,19 +104,33 @@ int multi_query(skycell_gpu_multi* m, const TIn* coords, u64 n, int d, const dou
                                              rho, mode, b[g], &occ_bytes[g], e, sizeof e);
       if (rc) throw ApiFail{rc, e};
       ensure(m->occ[g], occ_bytes[g]);
-      ensure(m->gath[g], occ_bytes[g] * G);
+      if (!m->peer) ensure(m->gath[g], occ_bytes[g] * G);
       m->ctx[g]->shard->export_occ(m->occ[g].p);
       ck(cudaEventRecord(m->ev[g], m->ctx[g]->stream), "event");
     });
     const u64 ob = occ_bytes[0];
-    // exchange 1 + phase 2: gather every region, OR, prune, local skyline
+    // exchange 1 + phase 2: OR every region, prune, local skyline.  With
+    // peer access the OR kernel reads the peers' regions in place (one pass
+    // over NVLink / NVSwitch, k_or_peers); otherwise the regions are copied
+    // into a gather buffer first.
     std::vector<uint64_t> local(G);
+    std::vector<const void*> srcs(G);
+    for (int h = 0; h < G; ++h) srcs[h] = m->occ[h].p;
     per_device(m, [&](int g) {
-      for (int h = 0; h < G; ++h)
-        peer_copy(m->ctx[g], static_cast<char*>(m->gath[g].p) + h * ob, m->ctx[h], m->occ[h].p, ob, m->ev[h]);
-      char e[512] = {0};
-      const int rc = skycell_gpu_shard_prune(m->ctx[g], m->gath[g].p, G, &local[g], e, sizeof e);
-      if (rc) throw ApiFail{rc, e};
+      if (m->peer) {
+        ensure(m->tbl[g], sizeof(void*) * G);
+        ck(cudaMemcpyAsync(m->tbl[g].p, srcs.data(), sizeof(void*) * G, cudaMemcpyHostToDevice, m->ctx[g]->stream),
+           "peer table");
+        for (int h = 0; h < G; ++h) ck(cudaStreamWaitEvent(m->ctx[g]->stream, m->ev[h], 0), "wait");
+        m->ctx[g]->shard->or_peers(static_cast<const void* const*>(m->tbl[g].p), G);
+        local[g] = m->ctx[g]->shard->prune_local_skyline();
+      } else {
+        for (int h = 0; h < G; ++h)
+          peer_copy(m->ctx[g], static_cast<char*>(m->gath[g].p) + h * ob, m->ctx[h], m->occ[h].p, ob, m->ev[h]);
+        char e[512] = {0};
+        const int rc = skycell_gpu_shard_prune(m->ctx[g], m->gath[g].p, G, &local[g], e, sizeof e);
+        if (rc) throw ApiFail{rc, e};
+      }
     });
     u64 maxc = 0;
     for (int g = 0; g < G; ++g) maxc = std::max<u64>(maxc, local[g]);
@@ -202,13 +218,18 @@ int skycell_gpu_multi_create(const int* devices, int n_devices, skycell_gpu_mult
         if (devices[a] == devices[b]) continue;
         int can = 0;
         cudaDeviceCanAccessPeer(&can, devices[a], devices[b]);
-        if (!can) continue;
+        if (!can) {
+          m->peer = false;
+          continue;
+        }
         ck(cudaSetDevice(devices[a]), "cudaSetDevice");
         const cudaError_t e = cudaDeviceEnablePeerAccess(devices[b], 0);
         if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ck(e, "peer access");
         cudaGetLastError();
       }
+    if (std::getenv("SKYCELL_MULTI_COPY")) m->peer = false;  // force the gather-copy exchange (tests)
     m->occ.resize(n_devices);
+    m->tbl.resize(n_devices);
     m->gath.resize(n_devices);
     m->send.resize(n_devices);
     m->recv.resize(n_devices);
@@ -220,7 +241,7 @@ void skycell_gpu_multi_destroy(skycell_gpu_multi* m) {
   if (!m) return;
   for (size_t g = 0; g < m->ctx.size(); ++g) {
     cudaSetDevice(m->ctx[g]->device);
-    for (auto* v : {&m->occ, &m->gath, &m->send, &m->recv})
+    for (auto* v : {&m->occ, &m->gath, &m->send, &m->recv, &m->tbl})
       if (g < v->size() && (*v)[g].p) cudaFree((*v)[g].p);
     if (g < m->ev.size()) cudaEventDestroy(m->ev[g]);
     skycell_gpu_destroy(m->ctx[g]);

@@ -157,9 +157,17 @@ def test_real_engines_multi_process(world):
 
 # ---- the single-process multi-device handle (skycell_gpu_multi_*): the
 # library runs the sharded protocol itself, exchanges included.
-@pytest.fixture(scope="module", params=[2, 3, 4])
+@pytest.fixture(scope="module", params=[(2, "peer"), (3, "peer"), (4, "peer"), (3, "copy")], ids=str)
 def multi(request):
-    m = sky.MultiEngine([0] * request.param)
+    """G contexts on device 0; exchange 1 through the in-place peer-read OR
+    (k_or_peers) or the gather-copy path (SKYCELL_MULTI_COPY, read at create)."""
+    G, how = request.param
+    if how == "copy":
+        os.environ["SKYCELL_MULTI_COPY"] = "1"
+    try:
+        m = sky.MultiEngine([0] * G)
+    finally:
+        os.environ.pop("SKYCELL_MULTI_COPY", None)
     yield m
     m.close()
 
