@@ -971,7 +971,7 @@ struct Pipe final : PipeBase {
       pa.alt_kept = &c->s2_kept;
       if (!k1_head && !std::getenv("SKYCELL_K4A_OLD")) {
         auto ka = wide ? sk::k_cand_head<TOut, D, uint32_t, kThreads> : sk::k_cand_head<TOut, D, uint8_t, kThreads>;
-        const size_t sa = ((8 * D * sizeof(TOut) + 15) & ~(size_t)15) + 8 * 8 +
+        const size_t sa = ((sk::kK4aHead * D * sizeof(TOut) + 15) & ~(size_t)15) + sk::kK4aHead * 8 +
                           (size_t)(kThreads / 32) * 64 * (D * sizeof(TOut) + 8 + 4) + 16;
         ck(cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sa), "smem attr");
         ka<<<grid4, kThreads, sa, s>>>(pa);
@@ -985,7 +985,7 @@ struct Pipe final : PipeBase {
       pb.PM = nullptr;
       pb.examined = nullptr;
       pb.d_cells = nullptr;
-      pb.head_start = 8;
+      pb.head_start = sk::kK4aHead;
       pb.coop = 1;
       kc<<<grid4, kThreads, smem_pf, s>>>(pb);
       ctx->launches += 2;
@@ -1139,6 +1139,15 @@ struct Pipe final : PipeBase {
     ck(cudaStreamWaitEvent(s, ctx->ev_join, 0), "join");
     ck(cudaMemcpyAsync(ctx->host_ctr, ctr(), sizeof(DevCounters), cudaMemcpyDeviceToHost, s), "counters D2H");
     ck(cudaStreamSynchronize(s), "query");
+    if (tracer().on) {
+      const DevCounters& h = *ctx->host_ctr;
+      std::fprintf(stderr,
+                   "[skycell] counters: S1 %llu | sample X %llu (capped %llu), sample skyline %llu, filter points %llu, "
+                   "weak filter %llu | K4a pending %llu | S2 %llu | examined %llu\n",
+                   (unsigned long long)h.s1_kept, (unsigned long long)h.xd, (unsigned long long)h.xs_cap,
+                   (unsigned long long)h.fs, (unsigned long long)h.nf, (unsigned long long)h.fweak,
+                   (unsigned long long)h.pkept, (unsigned long long)h.s2_kept, (unsigned long long)h.examined);
+    }
   }
 
   void fill_stats(skycell_gpu_stats* st) const {

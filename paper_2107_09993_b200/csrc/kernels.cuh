@@ -28,6 +28,10 @@
 
 #include "common.cuh"
 
+#ifndef SKY_K4A_HEAD
+#define SKY_K4A_HEAD 8
+#endif
+
 namespace sk {
 
 // Non-template kernels are `static`: this header is included by several
@@ -1068,11 +1072,14 @@ __global__ void __launch_bounds__(THREADS) k_candidates(CandParams p) {
 // the headline config) are queued per warp in a 64-entry shared ring and
 // tested 32 at a time, so no lane of the head test idles on a non-candidate.
 // Points still pending go to the dense stream P (K4b finishes them).
+// filter points in K4a's branch-free head (K4b starts after them)
+constexpr uint32_t kK4aHead = SKY_K4A_HEAD;
+
 template <typename T, int D, typename TT, int THREADS>
 __global__ void __launch_bounds__(THREADS) k_cand_head(CandParams p) {
   extern __shared__ __align__(16) uint8_t smc[];
   constexpr int kRing = 64;
-  constexpr uint32_t kHead0 = 8;
+  constexpr uint32_t kHead0 = kK4aHead;
   const u64 n = *p.count;
   const uint32_t nh = (uint32_t)(*p.f_count < kHead0 ? *p.f_count : kHead0);
   T* f_rows = reinterpret_cast<T*>(smc);                                  // kHead0 x D
