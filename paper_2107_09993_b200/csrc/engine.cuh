@@ -358,7 +358,12 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
     for (int pass = 0; pass < passes; ++pass) {
       ck(cudaMemsetAsync(cm, 0xff, cells * 8, s), "memset");
       sk::k_cellmin<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, count, Lc, pass, killb, cm);
-      for (int k = 1; k <= D; ++k) sk::k_prefix_min<u64><<<gp, 128, 0, s>>>(cm, Lc, k, lines);
+      for (int k = 1; k <= D; ++k) {
+        // few long lines (d = 2: 512 lines of 512 cells): one CTA per line,
+        // else a thread per line
+        if (lines >= (u64)nsm * 4 || Lc < 8) sk::k_prefix_min<u64><<<gp, 128, 0, s>>>(cm, Lc, k, lines);
+        else sk::k_prefix_min_cta<u64><<<(unsigned)std::min<u64>(lines, (u64)nsm * 2), 1024, 0, s>>>(cm, Lc, k, lines);
+      }
       sk::k_champ_kill<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, count, Lc, pass, cm,
                                                  q_begin, q_end, killb, static_cast<uint8_t*>(ctx->flags.p),
                                                  valid_ctr + 1);

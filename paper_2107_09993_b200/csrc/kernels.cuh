@@ -1549,19 +1549,34 @@ __global__ void __launch_bounds__(256) k_allpairs_lists(const T* __restrict__ ro
     bool dom = false, deferred = false;
     unsigned steps = 0;
     // columns 0..pc of dimension bk in ascending order; column c contributes
-    // its sum buckets 0..sb, one contiguous range (column-major bins)
-    for (int c = 0; c <= Q.pc && !dom && !deferred; ++c) {
-      const unsigned s0 = __ldg(ob + list_bin(0, c)), s1 = __ldg(ob + list_bin(Q.sb + 1, c));
-      for (unsigned base = s0; base < s1; base += 32) {
-        if (++steps > max_steps) {
-          deferred = true;
-          break;
-        }
-        const unsigned e = base + lane;
-        const bool d_l = e < s1 && Q.test(rows, ids, fsum, lst, e, cell_level, ctop);
-        if (__any_sync(kFull, d_l)) {
-          dom = true;
-          break;
+    // its sum buckets 0..sb, one contiguous range (column-major bins).  The
+    // bounds of 32 columns are loaded at once (lane l: column c0 + l) and
+    // only the non-empty ones are visited: sparse sets (anti-correlated d=2:
+    // 1.4K points over 1,024 columns) otherwise spend a dependent load pair
+    // per empty column.
+    for (int c0 = 0; c0 <= Q.pc && !dom && !deferred; c0 += 32) {
+      const int cl = c0 + lane;
+      unsigned b0 = 0, b1 = 0;
+      if (cl <= Q.pc) {
+        b0 = __ldg(ob + list_bin(0, cl));
+        b1 = __ldg(ob + list_bin(Q.sb + 1, cl));
+      }
+      unsigned ne = __ballot_sync(kFull, b1 > b0);
+      while (ne && !dom && !deferred) {
+        const int src = __ffs(ne) - 1;
+        ne &= ne - 1;
+        const unsigned s0 = __shfl_sync(kFull, b0, src), s1 = __shfl_sync(kFull, b1, src);
+        for (unsigned base = s0; base < s1; base += 32) {
+          if (++steps > max_steps) {
+            deferred = true;
+            break;
+          }
+          const unsigned e = base + lane;
+          const bool d_l = e < s1 && Q.test(rows, ids, fsum, lst, e, cell_level, ctop);
+          if (__any_sync(kFull, d_l)) {
+            dom = true;
+            break;
+          }
         }
       }
     }
@@ -1594,8 +1609,20 @@ __global__ void __launch_bounds__(256) k_allpairs_long(const T* __restrict__ row
     const uint32_t* lst = lists + (u64)Q.bk * cap;
     const unsigned* ob = offs + Q.bk * kListStride;
     unsigned g = 0;  // global step counter (identical in every warp)
-    for (int c = 0; c <= Q.pc; ++c) {
-      const unsigned s0 = __ldg(ob + list_bin(0, c)), s1 = __ldg(ob + list_bin(Q.sb + 1, c));
+    bool done = false;
+    for (int c0 = 0; c0 <= Q.pc && !done; c0 += 32) {
+      // bounds of 32 columns at once; only the non-empty ones are visited
+      const int cl = c0 + lane;
+      unsigned b0 = 0, b1 = 0;
+      if (cl <= Q.pc) {
+        b0 = __ldg(ob + list_bin(0, cl));
+        b1 = __ldg(ob + list_bin(Q.sb + 1, cl));
+      }
+      unsigned ne = __ballot_sync(kFull, b1 > b0);
+      while (ne && !done) {
+      const int src = __ffs(ne) - 1;
+      ne &= ne - 1;
+      const unsigned s0 = __shfl_sync(kFull, b0, src), s1 = __shfl_sync(kFull, b1, src);
       const unsigned nsteps = (s1 - s0 + 31) / 32;
       // this warp's steps of the column: g + k with (g + k) % nw == warp
       unsigned k = (unsigned)((warp - (int)(g % nw) + nw) % nw);
@@ -1616,7 +1643,8 @@ __global__ void __launch_bounds__(256) k_allpairs_long(const T* __restrict__ row
         }
       }
       g += nsteps;
-      if (seen()) break;
+      if (seen()) done = true;
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) flag[i] = found ? 0 : 1;
