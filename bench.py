@@ -235,7 +235,8 @@ def _default_rho(n, d):
 def newest_profile(kernel_tag: str, config: str):
     """dram bytes per launch from the newest committed ncu --set full summary
     of this kernel at this config (profiles/<run>_<kernel_tag>_<config>.json)."""
-    profs = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_{kernel_tag}_{config}.json")), key=os.path.getmtime)
+    # newest = highest run tag (r1a < r2x < r3b < r4s ...; file times do not survive a checkout)
+    profs = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_{kernel_tag}_{config}.json")))
     for p in reversed(profs):
         try:
             with open(p) as f:
