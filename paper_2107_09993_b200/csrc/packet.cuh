@@ -295,9 +295,38 @@ __global__ void __launch_bounds__(256, 4) k_pk_query(const uint32_t* __restrict_
     for (int k = 0; k < D; ++k) pmax[k] = 0;
     // Jump start (as tree.cuh): the own leaf first, then the ancestors
     // outwards, each expanded without the child on the own path.
+    // Phase 2: if every lane comes from the subtree of one level-h1 node A,
+    // phase 1 has already searched A's subtree for each of them (the packet
+    // tests are exact per lane), so the search starts at A's parent and skips
+    // A -- the phase-1 jump start, one level up.  Otherwise from the root.
+    uint32_t anc_lo = ~0u, anc_hi = 0u;
+    if (MODE == 1 && h1 >= 1 && h1 < sh.levels - 1) {
+      uint32_t a = ~0u;
+      if (act) {
+        a = (uint32_t)(j / kLeaf);
+        for (int l = 0; l < h1; ++l) a /= F;
+      }
+      anc_lo = a;
+      anc_hi = act ? a : 0u;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        anc_lo = min(anc_lo, __shfl_xor_sync(kFull, anc_lo, o));
+        anc_hi = max(anc_hi, __shfl_xor_sync(kFull, anc_hi, o));
+      }
+    }
     int top = 0;
     if (lane == 0) {
-      if (PHASE2) {
+      if (MODE == 1 && anc_lo == anc_hi) {
+        uint32_t a = anc_lo;
+        for (int l = 0; l < h1; ++l) path[l] = ~0u;
+        for (int l = h1; l < sh.levels; ++l) {
+          path[l] = a;
+          a /= F;
+        }
+        for (int l = sh.levels - 1; l > h1; --l) stk[top++] = ((uint32_t)l << 27) | path[l];
+      } else if (PHASE2) {
+        if (MODE == 1)
+          for (int l = 0; l < 32; ++l) path[l] = ~0u;
         stk[top++] = ((uint32_t)(sh.levels - 1) << 27);  // the root
       } else {
         uint32_t a = (uint32_t)pk;
