@@ -376,14 +376,16 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
                                             static_cast<u64*>(ctx->t_keys.p), static_cast<uint32_t*>(ctx->t_vals.p),
                                             valid_ctr);
   size_t temp = 0;
+  // key bits (the Morton key is shifted right by one: empty slots sort last)
+  constexpr int kKeyBits = sk::morton_bits<D>() * D;
   ck(cub::DeviceRadixSort::SortPairs(nullptr, temp, static_cast<const u64*>(ctx->t_keys.p),
                                      static_cast<u64*>(ctx->t_keys2.p), static_cast<const uint32_t*>(ctx->t_vals.p),
-                                     static_cast<uint32_t*>(ctx->t_vals2.p), nslots, 0, 64, s),
+                                     static_cast<uint32_t*>(ctx->t_vals2.p), nslots, 0, kKeyBits, s),
      "cub temp");
   ensure(ctx->t_cub, temp);
   ck(cub::DeviceRadixSort::SortPairs(ctx->t_cub.p, temp, static_cast<const u64*>(ctx->t_keys.p),
                                      static_cast<u64*>(ctx->t_keys2.p), static_cast<const uint32_t*>(ctx->t_vals.p),
-                                     static_cast<uint32_t*>(ctx->t_vals2.p), nslots, 0, 64, s),
+                                     static_cast<uint32_t*>(ctx->t_vals2.p), nslots, 0, kKeyBits, s),
      "cub sort");
   tracer().mark(s, "tree: keys + sort");
   ck(cudaMemcpyAsync(&hv[1], valid_ctr, 8, cudaMemcpyDeviceToHost, s), "D2H");
@@ -440,7 +442,7 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
     const unsigned gq = (unsigned)std::max<u64>(1, std::min<u64>((sh.nleaf * 32 + 255) / 256, (u64)nsm * 8));
     // phase-1 search radius (levels above the own leaf); phase 2 re-packs the
     // undecided points (SKYCELL_PK_H1 overrides; >= levels: one phase)
-    int h1 = D <= 6 ? 4 : 6;  // measured best (profiles/k5_h1_sweep_*: C3 at 4, d=7/8 at 6)
+    int h1 = D <= 6 ? 5 : D == 7 ? 6 : 7;  // measured best (profiles/k5_h1_sweep_*)
     if (const char* e = std::getenv("SKYCELL_PK_H1")) h1 = std::atoi(e);
     const bool two = h1 < sh.levels - 1;
     uint32_t* umask = static_cast<uint32_t*>(ctx->t_keys.p);       // free after the sort

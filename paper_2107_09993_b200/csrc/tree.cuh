@@ -29,11 +29,19 @@ namespace sk {
 
 constexpr int kLeaf = 32;
 
+// Bits per dimension of the Morton key: at most 48 key bits in total (six
+// 8-bit radix passes instead of eight; 2^48 cells are still far finer than
+// the 32-point leaves need).
+template <int D>
+__host__ __device__ constexpr int morton_bits() {
+  return (48 / D) < 16 ? (48 / D) : 16;
+}
+
 // Morton key of a stored row: b bits per dimension, bit j of dim k -> key
 // bit j*D + k (the reference's morton_key layout, grid.cpp:18-28).
 template <typename T, int D>
 __device__ __forceinline__ u64 morton_of(const T (&v)[D]) {
-  constexpr int B = (64 / D) < 16 ? (64 / D) : 16;
+  constexpr int B = morton_bits<D>();
   u64 key = 0;
   int col[D];
 #pragma unroll
