@@ -345,30 +345,34 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
   // phase-1-only semantics (refine.cpp:98) must not use.
   if (Lc >= 1 && nslots >= (1ull << 16) && cell_level == 0 && !no_prefilter) {
     const u64 cells = 1ull << (u64)(Lc * D);
-    ensure(ctx->t_cm, cells * 8);
+    // the plain grid, then grids shifted by 1/2, 1/4, 3/4 (.. 7/8) of a
+    // cell: 4 passes at d >= 5 (C3: 542 -> 499 ms with the round-1 tree), 2
+    // below (anti d=4: 11.2 vs 11.8 ms with 4); all passes' tables are built
+    // in one read of the set and tested in one more
+    int passes = D >= 5 ? 4 : 2;
+    if (const char* e = std::getenv("SKYCELL_PREPASSES")) passes = std::max(1, std::min(8, std::atoi(e)));
+    ensure(ctx->t_cm, cells * 8 * passes);
     ensure(ctx->t_kill, nslots);
     u64* cm = static_cast<u64*>(ctx->t_cm.p);
     const u64 lines = cells >> Lc;
     const unsigned gp = (unsigned)std::max<u64>(1, std::min<u64>((lines + 127) / 128, (u64)nsm * 16));
     uint8_t* killb = static_cast<uint8_t*>(ctx->t_kill.p);
-    // the plain grid, then grids shifted by 1/2, 1/4, 3/4 of a cell: 4 passes
-    // at d >= 5 (C3: 542 -> 499 ms), 2 below (anti d=4: 11.2 vs 11.8 ms with 4)
-    int passes = D >= 5 ? 4 : 2;
-    if (const char* e = std::getenv("SKYCELL_PREPASSES")) passes = std::max(1, std::min(8, std::atoi(e)));
+    ck(cudaMemsetAsync(cm, 0xff, cells * 8 * passes, s), "memset");
+    sk::k_cellmin_multi<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, count, Lc, passes, cells,
+                                                   cm);
     for (int pass = 0; pass < passes; ++pass) {
-      ck(cudaMemsetAsync(cm, 0xff, cells * 8, s), "memset");
-      sk::k_cellmin<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, count, Lc, pass, killb, cm);
+      u64* t = cm + (u64)pass * cells;
       for (int k = 1; k <= D; ++k) {
         // few long lines (d = 2: 512 lines of 512 cells): one CTA per line,
         // else a thread per line
-        if (lines >= (u64)nsm * 4 || Lc < 8) sk::k_prefix_min<u64><<<gp, 128, 0, s>>>(cm, Lc, k, lines);
-        else sk::k_prefix_min_cta<u64><<<(unsigned)std::min<u64>(lines, (u64)nsm * 2), 1024, 0, s>>>(cm, Lc, k, lines);
+        if (lines >= (u64)nsm * 4 || Lc < 8) sk::k_prefix_min<u64><<<gp, 128, 0, s>>>(t, Lc, k, lines);
+        else sk::k_prefix_min_cta<u64><<<(unsigned)std::min<u64>(lines, (u64)nsm * 2), 1024, 0, s>>>(t, Lc, k, lines);
       }
-      sk::k_champ_kill<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, count, Lc, pass, cm,
-                                                 q_begin, q_end, killb, static_cast<uint8_t*>(ctx->flags.p),
-                                                 valid_ctr + 1);
-      ctx->launches += 2 + D;
     }
+    sk::k_champ_kill_multi<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, count, Lc, passes,
+                                                      cells, cm, q_begin, q_end, killb,
+                                                      static_cast<uint8_t*>(ctx->flags.p), valid_ctr + 1);
+    ctx->launches += 2 + passes * D;
     kill = static_cast<const uint8_t*>(ctx->t_kill.p);
     tracer().mark(s, "tree: champion prefilter");
   }

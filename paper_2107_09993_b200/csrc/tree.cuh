@@ -136,6 +136,70 @@ __global__ void k_champ_kill(const T* __restrict__ rows, const uint32_t* __restr
   if ((threadIdx.x & 31) == 0 && mine) atomicAdd(killed, mine);
 }
 
+// All passes in one read of the set: table t (cells entries from cm + t *
+// cells) gets the min-sums of the pass-t grid.
+template <typename T, int D>
+__global__ void k_cellmin_multi(const T* __restrict__ rows, const uint32_t* __restrict__ ids,
+                                const u64* __restrict__ fsum, const u64* __restrict__ count, int L, int passes,
+                                u64 cells, u64* __restrict__ cm) {
+  const u64 n = *count;
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    if (ids[i] == kNoId) continue;
+    T v[D];
+    load_row_cached<T, D>(rows, i, v);
+    const u64 s = fsum[i];
+    for (int pass = 0; pass < passes; ++pass) {
+      int c[D];
+      grid_cols<T, D>(v, L, pass, c);
+      u64 lin = 0;
+#pragma unroll
+      for (int k = D - 1; k >= 0; --k) lin = (lin << L) | (u64)c[k];
+      u64* t = cm + pass * cells + lin;
+      if (s < __ldcg(t)) atomicMin(t, s);
+    }
+  }
+}
+
+// A point is removed if any pass's grid has a strictly smaller sum strictly
+// below its cell (see k_champ_kill).
+template <typename T, int D>
+__global__ void k_champ_kill_multi(const T* __restrict__ rows, const uint32_t* __restrict__ ids,
+                                   const u64* __restrict__ fsum, const u64* __restrict__ count, int L, int passes,
+                                   u64 cells, const u64* __restrict__ cm, u64 q_begin, const u64* __restrict__ q_end,
+                                   uint8_t* __restrict__ kill, uint8_t* __restrict__ flag, u64* __restrict__ killed) {
+  const u64 n = *count;
+  const u64 qe = q_end ? *q_end : ~0ull;
+  u64 mine = 0;
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    uint8_t k_i = 0;
+    if (ids[i] != kNoId) {
+      T v[D];
+      load_row_cached<T, D>(rows, i, v);
+      const u64 s = fsum[i];
+      for (int pass = 0; pass < passes && !k_i; ++pass) {
+        int c[D];
+        grid_cols<T, D>(v, L, pass, c);
+        bool ok = true;
+        u64 lin = 0;
+#pragma unroll
+        for (int k = D - 1; k >= 0; --k) {
+          ok &= c[k] >= 1;
+          lin = (lin << L) | (u64)(c[k] - 1);
+        }
+        if (ok && __ldg(cm + pass * cells + lin) < s) k_i = 1;
+      }
+      if (k_i) {
+        ++mine;
+        if (i >= q_begin && i < qe) flag[i] = 0;
+      }
+    }
+    kill[i] = k_i;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(kFull, mine, o);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(killed, mine);
+}
+
 template <typename T, int D>
 __global__ void k_tree_keys(const T* __restrict__ rows, const uint32_t* __restrict__ ids, const u64* __restrict__ count,
                             const uint8_t* __restrict__ kill, u64* __restrict__ keys, uint32_t* __restrict__ vals,
