@@ -288,15 +288,15 @@ void launch_count(skycell_gpu_ctx* ctx, cudaStream_t s, const uint32_t* bits, in
 template <typename TOut, int D>
 void run_exact(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint32_t* ids, const u64* fsum,
                const u64* count, u64 cap, unsigned* hist, unsigned* cursor, u64 q_begin = 0,
-               const u64* q_end = nullptr, int cell_level = 0) {
+               const u64* q_end = nullptr, int cell_level = 0, const u64* gate = nullptr) {
   const int nsm = ctx->num_sms;
   const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((cap + 255) / 256, (u64)nsm * 8));
   const TOut* trows = static_cast<const TOut*>(rows);
   uint32_t* lists = static_cast<uint32_t*>(ctx->lists.p);
   sk::k_list_hist<TOut, D><<<g, 256, 0, s>>>(trows, ids, fsum, count, hist);
   unsigned* totals = static_cast<unsigned*>(ctx->scan_tot.p);
-  sk::k_list_scan_sums<<<dim3(sk::kScanChunks, D), 1024, 0, s>>>(hist, D, totals);
-  sk::k_list_scan<<<dim3(sk::kScanChunks, D), 1024, 0, s>>>(hist, cursor, D, totals);
+  sk::k_list_scan_sums<<<dim3(sk::kScanChunks, D), 1024, 0, s>>>(hist, D, totals, gate);
+  sk::k_list_scan<<<dim3(sk::kScanChunks, D), 1024, 0, s>>>(hist, cursor, D, totals, gate);
   ++ctx->launches;
   sk::k_list_scatter<TOut, D><<<g, 256, 0, s>>>(trows, ids, fsum, count, cursor, lists, cap);
   const unsigned gw = (unsigned)std::max<u64>(1, std::min<u64>((cap * 32 + 255) / 256, (u64)nsm * 8));
@@ -306,7 +306,7 @@ void run_exact(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uin
   constexpr unsigned kMaxSteps = 16;
   sk::k_allpairs_lists<TOut, D><<<gw, 256, 0, s>>>(trows, ids, fsum, count, lists, hist, cap,
                                                    static_cast<uint8_t*>(ctx->flags.p), q_begin, q_end, cell_level,
-                                                   kMaxSteps, static_cast<uint32_t*>(ctx->long_q.p), long_n);
+                                                   kMaxSteps, static_cast<uint32_t*>(ctx->long_q.p), long_n, gate);
   sk::k_allpairs_long<TOut, D><<<nsm * 4, 256, 0, s>>>(trows, ids, fsum, lists, hist, cap,
                                                        static_cast<uint8_t*>(ctx->flags.p), cell_level,
                                                        static_cast<const uint32_t*>(ctx->long_q.p), long_n);
@@ -551,17 +551,25 @@ void run_dominance(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const
                    const u64* q_end = nullptr, int cell_level = 0, u64 tree_min = kTreeMinSlots,
                    const u64* valid_count = nullptr) {
   int mode = k5_mode(ctx);
-  if (mode == 2) {
-    if (cap <= tree_min) {
-      mode = 0;
-    } else {
-      // decide on the number of points (valid_count) when known, else slots
-      u64 nslots = 0;
-      ck(cudaMemcpyAsync(&nslots, valid_count ? valid_count : count, 8, cudaMemcpyDeviceToHost, s), "D2H");
-      ck(cudaStreamSynchronize(s), "sync");
-      mode = nslots > tree_min ? 1 : 0;
-    }
+  if (mode == 2 && cap > tree_min) {
+    // The column lists are enqueued at once, gated on the device by the
+    // set's point count (valid_count when known, else slots); the host reads
+    // that count meanwhile and adds the tree only for a large set -- no GPU
+    // bubble for the common small set (C2: two host round trips per query
+    // before).
+    const u64* vc = valid_count ? valid_count : count;
+    u64* lc = static_cast<u64*>(ctx->long_n.p) + 2;
+    sk::k_gate_count<<<1, 1, 0, s>>>(vc, count, tree_min, lc);
+    ck(cudaMemcpyAsync(ctx->host_param + 3, vc, 8, cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaEventRecord(ctx->ev[8], s), "event");
+    ++ctx->launches;
+    run_exact<TOut, D>(ctx, s, rows, ids, fsum, lc, cap, hist, cursor, q_begin, q_end, cell_level, lc);
+    ck(cudaEventSynchronize(ctx->ev[8]), "count");
+    if (ctx->host_param[3] > tree_min)
+      run_tree<TOut, D>(ctx, s, rows, ids, fsum, count, valid_ctr, q_begin, q_end, cell_level, false);
+    return;
   }
+  if (mode == 2) mode = 0;  // cap <= tree_min: the lists
   if (mode == 0)
     run_exact<TOut, D>(ctx, s, rows, ids, fsum, count, cap, hist, cursor, q_begin, q_end, cell_level);
   else

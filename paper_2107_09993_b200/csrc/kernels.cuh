@@ -1362,8 +1362,9 @@ __device__ __forceinline__ unsigned* scan_array(unsigned* hist, int y, int D, in
 }
 
 static __global__ void __launch_bounds__(1024) k_list_scan_sums(unsigned* __restrict__ hist, int D,
-                                                          unsigned* __restrict__ totals) {
+                                                          unsigned* __restrict__ totals, const u64* __restrict__ gate) {
   __shared__ unsigned warp_tot[32];
+  if (gate && *gate == 0) return;  // the set goes to the tree (run_dominance)
   int len;
   const unsigned* h = scan_array(hist, blockIdx.y, D, &len);
   const int c0 = blockIdx.x * kScanChunk;
@@ -1382,9 +1383,10 @@ static __global__ void __launch_bounds__(1024) k_list_scan_sums(unsigned* __rest
 }
 
 static __global__ void __launch_bounds__(1024) k_list_scan(unsigned* __restrict__ hist, unsigned* __restrict__ cursor, int D,
-                                                     const unsigned* __restrict__ totals) {
+                                                     const unsigned* __restrict__ totals, const u64* __restrict__ gate) {
   __shared__ unsigned tile[kScanChunk + kScanChunk / 32];  // one pad word per 32 entries
   __shared__ unsigned warp_tot[32];
+  if (gate && *gate == 0) return;
   int len;
   unsigned* h = scan_array(hist, blockIdx.y, D, &len);
   unsigned* cur = (int)blockIdx.y < D ? cursor + (u64)blockIdx.y * kListStride : nullptr;
@@ -1527,7 +1529,8 @@ __global__ void __launch_bounds__(256) k_allpairs_lists(const T* __restrict__ ro
                                                         u64 cap, uint8_t* __restrict__ flag, u64 q_begin,
                                                         const u64* __restrict__ q_end, int cell_level,
                                                         unsigned max_steps, uint32_t* __restrict__ long_q,
-                                                        u64* __restrict__ long_n) {
+                                                        u64* __restrict__ long_n, const u64* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   const u64 n = q_end ? *q_end : *count;
   const int lane = threadIdx.x & 31;
   const u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
@@ -1841,6 +1844,14 @@ __global__ void k_pack_members(const T* __restrict__ rows, const uint32_t* __res
 static __global__ void k_filter_gate(const u64* __restrict__ sky, const u64* __restrict__ cands,
                                      u64* __restrict__ weak) {
   *weak = *sky * 4 > *cands;
+}
+
+// K5 dispatch without a host round trip: the column lists run on
+// *lcount = the set's slot count when its point count is at most tree_min,
+// else on 0 (the tree takes the set, launched once the host has the count).
+static __global__ void k_gate_count(const u64* __restrict__ points, const u64* __restrict__ slots, u64 tree_min,
+                                    u64* __restrict__ lcount) {
+  *lcount = *points <= tree_min ? *slots : 0;
 }
 
 static __global__ void k_clamp_count(const u64* __restrict__ src, u64 cap, u64* __restrict__ dst) {
