@@ -351,22 +351,23 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
     // in one read of the set and tested in one more
     int passes = D >= 5 ? 4 : 2;
     if (const char* e = std::getenv("SKYCELL_PREPASSES")) passes = std::max(1, std::min(8, std::atoi(e)));
-    ensure(ctx->t_cm, cells * 8 * passes);
+    ensure(ctx->t_cm, cells * 4 * passes);
     ensure(ctx->t_kill, nslots);
-    u64* cm = static_cast<u64*>(ctx->t_cm.p);
+    uint32_t* cm = static_cast<uint32_t*>(ctx->t_cm.p);
     const u64 lines = cells >> Lc;
     const unsigned gp = (unsigned)std::max<u64>(1, std::min<u64>((lines + 127) / 128, (u64)nsm * 16));
     uint8_t* killb = static_cast<uint8_t*>(ctx->t_kill.p);
-    ck(cudaMemsetAsync(cm, 0xff, cells * 8 * passes, s), "memset");
+    ck(cudaMemsetAsync(cm, 0xff, cells * 4 * passes, s), "memset");
     sk::k_cellmin_multi<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, count, Lc, passes, cells,
                                                    cm);
     for (int pass = 0; pass < passes; ++pass) {
-      u64* t = cm + (u64)pass * cells;
+      uint32_t* t = cm + (u64)pass * cells;
       for (int k = 1; k <= D; ++k) {
         // few long lines (d = 2: 512 lines of 512 cells): one CTA per line,
         // else a thread per line
-        if (lines >= (u64)nsm * 4 || Lc < 8) sk::k_prefix_min<u64><<<gp, 128, 0, s>>>(t, Lc, k, lines);
-        else sk::k_prefix_min_cta<u64><<<(unsigned)std::min<u64>(lines, (u64)nsm * 2), 1024, 0, s>>>(t, Lc, k, lines);
+        if (lines >= (u64)nsm * 4 || Lc < 8) sk::k_prefix_min<uint32_t><<<gp, 128, 0, s>>>(t, Lc, k, lines);
+        else
+          sk::k_prefix_min_cta<uint32_t><<<(unsigned)std::min<u64>(lines, (u64)nsm * 2), 1024, 0, s>>>(t, Lc, k, lines);
       }
     }
     sk::k_champ_kill_multi<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, count, Lc, passes,

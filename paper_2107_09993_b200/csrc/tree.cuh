@@ -53,16 +53,16 @@ __device__ __forceinline__ u64 morton_of(const T (&v)[D]) {
   return key;
 }
 
-// ---- champion prefilter (large sets).  cm[c] = min FP64-sum bits over the
-// set's points in cell c of a dense level-Lc grid; after a d-dimensional
-// inclusive prefix-min, cm[c - 1] is the smallest sum among the points of
-// all cells strictly below c.  Such a point q is < p in every coordinate,
+// ---- champion prefilter (large sets).  cm[c] = min FP64 sum (its upper 32
+// bits) over the set's points in cell c of a dense level-Lc grid; after a
+// d-dimensional inclusive prefix-min, cm[c - 1] bounds the smallest sum among
+// the points of all cells strictly below c.  Such a point q is < p in every coordinate,
 // so it dominates p, and if its sum is smaller it also precedes p: p is
 // removed (and may be dropped as a dominator too -- q, or whatever removed
 // q, dominates everything p does).  Equal sums are left to the exact pass.
-// Pass 0 uses the grid floor(v 2^L); pass 1 the grid shifted by half a cell,
-// floor(v 2^L + 1/2) (clamped), which catches dominators across the first
-// grid's cell boundaries.  In both, a strictly smaller column in every
+// Pass 0 uses the grid floor(v 2^L); the others grids shifted by a fraction
+// of a cell, floor(v 2^L + off) (clamped), which catch dominators across the
+// first grid's cell boundaries.  In each, a strictly smaller column in every
 // dimension implies a strictly smaller coordinate.
 template <typename T, int D>
 __device__ __forceinline__ void grid_cols(const T (&v)[D], int L, int pass, int (&c)[D]) {
@@ -80,93 +80,41 @@ __device__ __forceinline__ void grid_cols(const T (&v)[D], int L, int pass, int 
   }
 }
 
-template <typename T, int D>
-__global__ void k_cellmin(const T* __restrict__ rows, const uint32_t* __restrict__ ids, const u64* __restrict__ fsum,
-                          const u64* __restrict__ count, int L, int pass, const uint8_t* __restrict__ kill,
-                          u64* __restrict__ cm) {
-  const u64 n = *count;
-  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
-    // removed points stay valid dominators (they are real records)
-    if (ids[i] == kNoId) continue;
-    T v[D];
-    load_row_cached<T, D>(rows, i, v);
-    int c[D];
-    grid_cols<T, D>(v, L, pass, c);
-    u64 lin = 0;
-#pragma unroll
-    for (int k = D - 1; k >= 0; --k) lin = (lin << L) | (u64)c[k];
-    const u64 s = fsum[i];
-    if (s < __ldcg(cm + lin)) atomicMin(cm + lin, s);
-  }
-}
-
-template <typename T, int D>
-__global__ void k_champ_kill(const T* __restrict__ rows, const uint32_t* __restrict__ ids, const u64* __restrict__ fsum,
-                             const u64* __restrict__ count, int L, int pass, const u64* __restrict__ cm, u64 q_begin,
-                             const u64* __restrict__ q_end, uint8_t* __restrict__ kill, uint8_t* __restrict__ flag,
-                             u64* __restrict__ killed) {
-  const u64 n = *count;
-  const u64 qe = q_end ? *q_end : ~0ull;
-  u64 mine = 0;
-  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
-    if (pass && kill[i]) continue;  // already removed by pass 0
-    uint8_t k_i = 0;
-    if (ids[i] != kNoId) {
-      T v[D];
-      load_row_cached<T, D>(rows, i, v);
-      int c[D];
-      grid_cols<T, D>(v, L, pass, c);
-      bool ok = true;
-      u64 lin = 0;
-#pragma unroll
-      for (int k = D - 1; k >= 0; --k) {
-        ok &= c[k] >= 1;
-        lin = (lin << L) | (u64)(c[k] - 1);
-      }
-      if (ok && __ldg(cm + lin) < fsum[i]) {
-        k_i = 1;
-        ++mine;
-        if (i >= q_begin && i < qe) flag[i] = 0;
-      }
-    }
-    if (!pass || k_i) kill[i] = k_i;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(kFull, mine, o);
-  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(killed, mine);
-}
-
 // All passes in one read of the set: table t (cells entries from cm + t *
-// cells) gets the min-sums of the pass-t grid.
+// cells) gets the min over the cell of the upper 32 bits of the points' sums
+// (u32 tables: half the bytes and 32-bit atomics).  The kill test below
+// stays exact: cm < hi32(s) implies the minimum sum is < s; an equal upper
+// half is left to the exact pass.
 template <typename T, int D>
 __global__ void k_cellmin_multi(const T* __restrict__ rows, const uint32_t* __restrict__ ids,
                                 const u64* __restrict__ fsum, const u64* __restrict__ count, int L, int passes,
-                                u64 cells, u64* __restrict__ cm) {
+                                u64 cells, uint32_t* __restrict__ cm) {
   const u64 n = *count;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
     if (ids[i] == kNoId) continue;
     T v[D];
     load_row_cached<T, D>(rows, i, v);
-    const u64 s = fsum[i];
+    const uint32_t s = (uint32_t)(fsum[i] >> 32);
     for (int pass = 0; pass < passes; ++pass) {
       int c[D];
       grid_cols<T, D>(v, L, pass, c);
       u64 lin = 0;
 #pragma unroll
       for (int k = D - 1; k >= 0; --k) lin = (lin << L) | (u64)c[k];
-      u64* t = cm + pass * cells + lin;
+      uint32_t* t = cm + pass * cells + lin;
       if (s < __ldcg(t)) atomicMin(t, s);
     }
   }
 }
 
 // A point is removed if any pass's grid has a strictly smaller sum strictly
-// below its cell (see k_champ_kill).
+// below its cell.
 template <typename T, int D>
 __global__ void k_champ_kill_multi(const T* __restrict__ rows, const uint32_t* __restrict__ ids,
                                    const u64* __restrict__ fsum, const u64* __restrict__ count, int L, int passes,
-                                   u64 cells, const u64* __restrict__ cm, u64 q_begin, const u64* __restrict__ q_end,
-                                   uint8_t* __restrict__ kill, uint8_t* __restrict__ flag, u64* __restrict__ killed) {
+                                   u64 cells, const uint32_t* __restrict__ cm, u64 q_begin,
+                                   const u64* __restrict__ q_end, uint8_t* __restrict__ kill, uint8_t* __restrict__ flag,
+                                   u64* __restrict__ killed) {
   const u64 n = *count;
   const u64 qe = q_end ? *q_end : ~0ull;
   u64 mine = 0;
@@ -175,7 +123,7 @@ __global__ void k_champ_kill_multi(const T* __restrict__ rows, const uint32_t* _
     if (ids[i] != kNoId) {
       T v[D];
       load_row_cached<T, D>(rows, i, v);
-      const u64 s = fsum[i];
+      const uint32_t s = (uint32_t)(fsum[i] >> 32);
       for (int pass = 0; pass < passes && !k_i; ++pass) {
         int c[D];
         grid_cols<T, D>(v, L, pass, c);
