@@ -544,6 +544,14 @@ inline int k5_mode(skycell_gpu_ctx* ctx) {
 // whose cost grows with the skyline boundary instead of the list prefixes.
 constexpr u64 kTreeMinSlots = 1ull << 20;
 constexpr u64 kTreeMainMin = 1ull << 16;  // main K5: decided on the point count
+// sample skyline (K0): lists up to this many candidates (SKYCELL_SAMPLE_TREE_MIN)
+inline u64 sample_tree_min() {
+  static const u64 v = [] {
+    const char* e = std::getenv("SKYCELL_SAMPLE_TREE_MIN");
+    return e ? (u64)std::strtoull(e, nullptr, 10) : (u64)(96 * 1024);
+  }();
+  return v;
+}
 
 // K5 dispatcher: flags[slot] for the query slots of the set.
 template <typename TOut, int D>
@@ -812,7 +820,7 @@ struct Pipe final : PipeBase {
         ctx->launches += 2;
         run_dominance<TOut, D>(ctx, s, ctx->smp_rows.p, static_cast<const uint32_t*>(ctx->smp_ids.p),
                                static_cast<const u64*>(ctx->smp_fsum.p), &c->xs_cap, std::min<u64>(m, kXMax),
-                               U(o_shist), U(o_scur), &c->tvalid, 0, nullptr, 0, 96 * 1024);
+                               U(o_shist), U(o_scur), &c->tvalid, 0, nullptr, 0, sample_tree_min());
         tracer().mark(s, "K0: sample skyline");
         sk::k_compact_members<TOut, D><<<nsm * 4, 256, 0, s>>>(
             static_cast<const TOut*>(ctx->smp_rows.p), static_cast<const uint32_t*>(ctx->smp_ids.p),
