@@ -91,15 +91,19 @@ class ShardedSkyline:
         # kernel, an allocation) runs through _together: the rank reports -1
         # in the next count exchange instead of skipping it, so every rank
         # raises and none blocks in a collective.
-        # phase 1: local streaming pass
-        sizes = self._together(lambda: self.eng.shard_begin(coords, n_local, d, dim_min, dim_max, rho, mode,
-                                                            id_base))
+        # phase 1: local streaming pass, and the export of the occupancy
+        # region (one status exchange for both)
+        def begin():
+            nb = self.eng.shard_begin(coords, n_local, d, dim_min, dim_max, rho, mode, id_base)
+            self._export(nb)
+            return nb
+
+        sizes = self._together(begin)
         if len(set(sizes)) != 1:
             # ranks built different grids (rho or d differ): the all-gather
             # below would mis-align, so every rank refuses the query
             raise UsageError(f"sharded skyline: ranks disagree on the occupancy size {sizes} (rho or d differ)")
         occ_bytes = sizes[0]
-        self._together(lambda: self._export(occ_bytes))
         gathered = self._bufs["occ_all"][: world * occ_bytes]
         self._all_gather(gathered, self._bufs["occ"][:occ_bytes])
 
@@ -114,12 +118,16 @@ class ShardedSkyline:
         # phase 3: own local skyline against the union
         if ids_out is None:
             ids_out = np.empty(max(n_local, 1), dtype=np.uint32)
-        box = []
-        self._together(lambda: box.append(self.eng.shard_finish(recv, world, maxc, rank, counts[rank], ids_out)))
-        res = box[0]
-        # one exchange for all three summed statistics
-        stats = self._gather_vec([res.points_examined, res.survivors_stream, res.survivors_filter])
-        res.points_examined, res.survivors_stream, res.survivors_filter = (int(v) for v in stats.sum(axis=0))
+        # the finish status and the three summed statistics in one exchange
+        res, err = None, None
+        try:
+            res = self.eng.shard_finish(recv, world, maxc, rank, counts[rank], ids_out)
+            vec = [0, res.points_examined, res.survivors_stream, res.survivors_filter]
+        except Exception as e:  # noqa: BLE001 -- re-raised below, after the exchange
+            err, vec = e, [-1, 0, 0, 0]
+        stats = self._gather_vec(vec)
+        self._reraise(err, [int(v) for v in stats[:, 0]])
+        res.points_examined, res.survivors_stream, res.survivors_filter = (int(v) for v in stats[:, 1:].sum(axis=0))
         if gather_to is None:
             return res
         res.ids = self._gather_ids(res.ids, gather_to)
