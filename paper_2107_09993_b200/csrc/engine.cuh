@@ -252,10 +252,14 @@ void launch_tables(skycell_gpu_ctx* ctx, cudaStream_t s, const uint32_t* bits, i
   // enough dimension-1 lines to fill the GPU: one thread per line; else
   // (d = 2, or d = 3 at fine layers) row minima per thread + a CTA per line
   if (lines1 >= (u64)nsm * 128 || L <= 6) {
-    sk::k_rowmin_prefix1<TT><<<grid_for(lines1), 128, 0, s>>>(bits, L, d, lines1, table);
+    // one warp per dimension-1 line
+    const unsigned gw = (unsigned)std::max<u64>(1, std::min<u64>((lines1 * 32 + 255) / 256, (u64)nsm * 16));
+    sk::k_rowmin_prefix1w<TT><<<gw, 256, 0, s>>>(bits, L, lines1, table);
     ++ctx->launches;
     for (int k = 2; k < d; ++k) {
-      sk::k_prefix_min<TT><<<grid_for(lines1), 128, 0, s>>>(table, L, k, lines1);
+      // a thread per line when lines fill the GPU, else a warp per line
+      if (lines1 >= (u64)nsm * 128 || L < 5) sk::k_prefix_min<TT><<<grid_for(lines1), 128, 0, s>>>(table, L, k, lines1);
+      else sk::k_prefix_minw<TT><<<gw, 256, 0, s>>>(table, L, k, lines1);
       ++ctx->launches;
     }
     return;

@@ -12,7 +12,7 @@
 //                                       occupancy (grid.cpp:78-102), the H test,
 //                                       survivors compacted to S1.  Reads every
 //                                       coordinate exactly once.
-//   K3  k_rowmin_prefix1 / k_rowmin /   cell pruning as a d-dimensional prefix-OR,
+//   K3  k_rowmin_prefix1w / k_rowmin /  cell pruning as a d-dimensional prefix-OR,
 //       k_prefix_min / k_count_rows /   stored as a (d-1)-dim prefix-min table;
 //       k_downsample*                   per-layer |KS_i|, |CS_i| (replaces
 //                                       shrink_seq.cpp:87-231, shrink_par.cpp:179-278).
@@ -591,38 +591,56 @@ static __global__ void k_reduce_slabs(const uint32_t* __restrict__ slabs, int ns
 
 // ------------------------------------------------- K3: cell pruning tables
 // Row-min of dimension 0 (the innermost `L` bits of the linear index) fused
-// with the inclusive prefix-min along dimension 1: one thread per dimension-1
-// line computes the 2^L row minima of that line and scans them.
+// with the inclusive prefix-min along dimension 1, one warp per dimension-1
+// line: lane l takes rows l, l+32, .. of the line (coalesced row reads) and
+// the prefix-min along the line is a warp scan per 32 rows with a carry.  A
+// thread per line left the GPU nearly idle at the small tables K0 and K3
+// build (4,096 lines at d=4, L=6: 24 us).
 template <typename TT>
-__global__ void k_rowmin_prefix1(const uint32_t* __restrict__ bits, int L, int d, u64 lines, TT* __restrict__ R) {
+__global__ void k_rowmin_prefix1w(const uint32_t* __restrict__ bits, int L, u64 lines, TT* __restrict__ R) {
   const int n = 1 << L;
   const int rowbits = 1 << L;
-  for (u64 line = blockIdx.x * (u64)blockDim.x + threadIdx.x; line < lines; line += (u64)gridDim.x * blockDim.x) {
-    // rows of this line: r = high * n * n + c1 * n + ... ; with d == 2 there is one line
-    const u64 row0 = line * (u64)n;  // dimension-1 index is the lowest digit of the row index
-    TT run = (TT)~(TT)0;
-    for (int c1 = 0; c1 < n; ++c1) {
-      const u64 r = row0 + c1;
+  const int lane = threadIdx.x & 31;
+  for (u64 line = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; line < lines;
+       line += ((u64)gridDim.x * blockDim.x) >> 5) {
+    // rows of this line: the dimension-1 index is the lowest digit of the row index
+    const u64 row0 = line * (u64)n;
+    TT carry = (TT)~(TT)0;
+    for (int c0 = 0; c0 < n; c0 += 32) {
+      const int c1 = c0 + lane;
       TT best = (TT)~(TT)0;
-      if (L >= 5) {
-        const u64 wpr = (u64)rowbits >> 5;
-        for (u64 w = 0; w < wpr; ++w) {
-          const uint32_t x = __ldg(bits + r * wpr + w);
-          if (x) { best = (TT)(w * 32 + __ffs(x) - 1); break; }
+      if (c1 < n) {
+        const u64 r = row0 + c1;
+        if (L >= 5) {
+          const u64 wpr = (u64)rowbits >> 5;
+          for (u64 w = 0; w < wpr; ++w) {
+            const uint32_t x = __ldg(bits + r * wpr + w);
+            if (x) {
+              best = (TT)(w * 32 + __ffs(x) - 1);
+              break;
+            }
+          }
+        } else {
+          const int rpw = 32 >> L;
+          const uint32_t x = (__ldg(bits + r / rpw) >> ((r % rpw) * rowbits)) & ((1u << rowbits) - 1);
+          if (x) best = (TT)(__ffs(x) - 1);
         }
-      } else {
-        const int rpw = 32 >> L;
-        const uint32_t x = (__ldg(bits + r / rpw) >> ((r % rpw) * rowbits)) & ((1u << rowbits) - 1);
-        if (x) best = (TT)(__ffs(x) - 1);
       }
-      run = best < run ? best : run;
-      R[r] = run;
+      // inclusive prefix-min over the lanes, then the carry of earlier chunks
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const TT y = __shfl_up_sync(kFull, best, o);
+        if (lane >= o) best = y < best ? y : best;
+      }
+      best = carry < best ? carry : best;
+      if (c1 < n) R[row0 + c1] = best;
+      carry = __shfl_sync(kFull, best, 31);
     }
   }
 }
 
 // Row minima only, one thread per row (for grids with few dimension-1 lines,
-// e.g. d = 2, where k_rowmin_prefix1 would run on a handful of threads).
+// e.g. d = 2 at fine layers, which one CTA per line then scans).
 template <typename TT>
 __global__ void k_rowmin(const uint32_t* __restrict__ bits, int L, u64 rows, TT* __restrict__ R) {
   const int rowbits = 1 << L;
@@ -700,6 +718,36 @@ __global__ void __launch_bounds__(1024) k_prefix_min_cta(TT* __restrict__ R, int
 
 // Inclusive prefix-min along dimension k (2..d-1) of the (d-1)-dim table.
 // Loads are issued 16 at a time ahead of the dependent min-scan.
+// One warp per line (grids with a few thousand lines: a thread per line
+// runs 2^L dependent steps on a few threads per SM): lanes take the line's
+// entries lane, lane+32, .. (strided loads, all in flight) and scan them in
+// chunks of 32 with a carry.
+template <typename TT>
+__global__ void k_prefix_minw(TT* __restrict__ R, int L, int k, u64 lines) {
+  const u64 stride = 1ull << (L * (k - 1));
+  const int n = 1 << L;
+  const int lane = threadIdx.x & 31;
+  for (u64 line = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; line < lines;
+       line += ((u64)gridDim.x * blockDim.x) >> 5) {
+    const u64 low = line & (stride - 1);
+    const u64 high = line >> (L * (k - 1));
+    const u64 base = (high << (L * k)) + low;
+    TT carry = (TT)~(TT)0;
+    for (int c0 = 0; c0 < n; c0 += 32) {
+      const int c = c0 + lane;
+      TT v = c < n ? R[base + (u64)c * stride] : (TT)~(TT)0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const TT y = __shfl_up_sync(kFull, v, o);
+        if (lane >= o) v = y < v ? y : v;
+      }
+      v = carry < v ? carry : v;
+      if (c < n) R[base + (u64)c * stride] = v;
+      carry = __shfl_sync(kFull, v, 31);
+    }
+  }
+}
+
 template <typename TT>
 __global__ void k_prefix_min(TT* __restrict__ R, int L, int k, u64 lines) {
   const u64 stride = 1ull << (L * (k - 1));
