@@ -1019,6 +1019,7 @@ struct Pipe final : PipeBase {
       pb.d_cells = nullptr;
       pb.head_start = sk::kK4aHead;
       pb.coop = 1;
+      pb.coop_mid = 16;  // measured: 16 best at C2 / C4 shards (8..64 swept)
       kc<<<grid4, kThreads, smem_pf, s>>>(pb);
       ctx->launches += 2;
     } else {
@@ -1135,6 +1136,7 @@ struct Pipe final : PipeBase {
     pb.kept = &c->s2_kept;
     pb.head_start = 0;
     pb.coop = 1;
+    pb.coop_mid = 16;
     auto kc = sk::k_candidates<TOut, D, uint8_t, kThreads>;
     ck(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pf), "smem attr");
     kc<<<grid4, kThreads, smem_pf, s>>>(pb);

@@ -951,6 +951,7 @@ struct CandParams {
   int d_wide;
   uint32_t head_start;   // first filter point of the branch-free head
   int coop;              // run the warp-cooperative phase for points the head leaves
+  uint32_t coop_mid;     // K4b: filter points after the head tested branch-free before the list scan
   // K4a: when *gate != 0 (k_filter_gate) the survivors go to the alt_*
   // stream (S2) instead of out_* (the K4b input)
   const u64* gate;
@@ -1039,14 +1040,15 @@ __global__ void __launch_bounds__(THREADS) k_candidates(CandParams p) {
     // K4b (coop): its lanes are dense pending points, so the next 32 filter
     // points are tested branch-free by every lane (one step per filter point
     // for the whole warp, instead of one warp step per pending point)
-    if (p.coop && nf > hs + kHead0 && __any_sync(kFull, keep)) {
+    const uint32_t mid = p.coop_mid;
+    if (p.coop && mid && nf > hs + kHead0 && __any_sync(kFull, keep)) {
       bool dom = false;
 #pragma unroll 8
-      for (uint32_t f = hs + kHead0; f < hs + kHead0 + 32; ++f)
+      for (uint32_t f = hs + kHead0; f < hs + kHead0 + mid; ++f)
         if (f < nf) dom |= dominates<T, D>(f_rows + (u64)f * D, v) && f_sum[f] < ps;
       keep = keep && !dom;
     }
-    unsigned pend = __ballot_sync(kFull, p.coop && keep && nf > hs + kHead0 + 32);
+    unsigned pend = __ballot_sync(kFull, p.coop && keep && nf > hs + kHead0 + mid);
     while (pend) {
       const int src = __ffs(pend) - 1;
       pend &= pend - 1;
