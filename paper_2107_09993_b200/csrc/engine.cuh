@@ -307,7 +307,7 @@ void run_exact(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uin
   ensure(ctx->long_q, cap * 4);
   u64* long_n = static_cast<u64*>(ctx->long_n.p);
   ck(cudaMemsetAsync(long_n, 0, 8, s), "memset");
-  constexpr unsigned kMaxSteps = 16;
+  constexpr unsigned kMaxSteps = 8;  // phase A budget (4..64 swept: 4-8 best at C2 / C4 shards)
   sk::k_allpairs_lists<TOut, D><<<gw, 256, 0, s>>>(trows, ids, fsum, count, lists, hist, cap,
                                                    static_cast<uint8_t*>(ctx->flags.p), q_begin, q_end, cell_level,
                                                    kMaxSteps, static_cast<uint32_t*>(ctx->long_q.p), long_n, gate);
