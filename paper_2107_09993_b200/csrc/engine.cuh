@@ -564,21 +564,27 @@ void run_dominance(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const
                    const u64* q_end = nullptr, int cell_level = 0, u64 tree_min = kTreeMinSlots,
                    const u64* valid_count = nullptr) {
   int mode = k5_mode(ctx);
-  if (mode == 2 && cap > tree_min) {
+  if (mode == 2 && cell_level == 0) {
     // The column lists are enqueued at once, gated on the device by the
-    // set's point count (valid_count when known, else slots); the host reads
-    // that count meanwhile and adds the tree only for a large set -- no GPU
-    // bubble for the common small set (C2: two host round trips per query
-    // before).
+    // set's point count (valid_count when known, else slots) and by exact
+    // origins (k_origin_count: a set holding one is decided in O(n)); the
+    // host reads both counts meanwhile and adds the tree only for a large
+    // set without origins -- no GPU bubble for the common small set.
     const u64* vc = valid_count ? valid_count : count;
     u64* lc = static_cast<u64*>(ctx->long_n.p) + 2;
-    sk::k_gate_count<<<1, 1, 0, s>>>(vc, count, tree_min, lc);
+    u64* org = static_cast<u64*>(ctx->long_n.p) + 3;
+    const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((cap + 255) / 256, (u64)ctx->num_sms * 8));
+    ck(cudaMemsetAsync(org, 0, 8, s), "memset");
+    sk::k_origin_count<<<g, 256, 0, s>>>(ids, fsum, count, org);
+    sk::k_origin_flags<<<g, 256, 0, s>>>(ids, fsum, count, q_begin, q_end, org, static_cast<uint8_t*>(ctx->flags.p));
+    sk::k_gate_count<<<1, 1, 0, s>>>(vc, count, tree_min, org, lc);
     ck(cudaMemcpyAsync(ctx->host_param + 3, vc, 8, cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaMemcpyAsync(ctx->host_param + 4, org, 8, cudaMemcpyDeviceToHost, s), "D2H");
     ck(cudaEventRecord(ctx->ev[8], s), "event");
-    ++ctx->launches;
+    ctx->launches += 3;
     run_exact<TOut, D>(ctx, s, rows, ids, fsum, lc, cap, hist, cursor, q_begin, q_end, cell_level, lc);
     ck(cudaEventSynchronize(ctx->ev[8]), "count");
-    if (ctx->host_param[3] > tree_min)
+    if (ctx->host_param[4] == 0 && ctx->host_param[3] > tree_min)
       run_tree<TOut, D>(ctx, s, rows, ids, fsum, count, valid_ctr, q_begin, q_end, cell_level, false);
     return;
   }
