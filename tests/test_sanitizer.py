@@ -1,5 +1,7 @@
 """compute-sanitizer over small queries (race detection).
-memcheck: every kernel of both K5 variants, quadrant and the sharded phases;
+memcheck: every kernel of both K5 variants, quadrant, the sparse layer rho
+(sparse.cuh), the packet tree with point queries, the multi-layer grid, the
+multi-device peer OR and the .bin reader/writer;
 racecheck: shared-memory hazards of the same small queries."""
 import os
 import shutil
@@ -35,7 +37,31 @@ eng = sky.Engine(0)
 x = quantize_f32(o.generate(2, 70000, 4, 8))
 r = eng.compute_skyline(sky.Dataset(x, np.zeros(4), np.ones(4)), 3)
 assert np.array_equal(r.ids, o.compute_skyline(x.astype(np.float64), np.zeros(4), np.ones(4), 3).ids)
+x = quantize_f32(o.generate(1, 5000, 8, 9))
+r = eng.compute_skyline(sky.Dataset(x, np.zeros(8), np.ones(8)), 5)
+assert np.array_equal(r.ids, o.compute_skyline(x.astype(np.float64), np.zeros(8), np.ones(8), 5).ids)
 eng.close()
+os.environ["SKYCELL_K5"] = "tree-point"
+eng = sky.Engine(0)
+x = quantize_f32(o.generate(0, 30000, 6, 3))
+r = eng.compute_skyline(sky.Dataset(x, np.zeros(6), np.ones(6)), 2)
+assert np.array_equal(r.ids, o.compute_skyline(x.astype(np.float64), np.zeros(6), np.ones(6), 2).ids)
+os.environ.pop("SKYCELL_K5")
+pts = o.normalize(x.astype(np.float64), np.zeros(6), np.ones(6))
+g = eng.grid(pts, 3)
+assert g.size() == len(x) and g.nonempty_cells(3).size == g.nonempty_count(3)
+g.close()
+import tempfile
+with tempfile.TemporaryDirectory() as t:
+    eng.write_bin(t + "/a.bin", np.ascontiguousarray(x, dtype=np.float64))
+    back, _, _ = eng.read_bin(t + "/a.bin")
+    assert np.array_equal(back.cpu().numpy(), x.astype(np.float64))
+eng.close()
+m = sky.MultiEngine([0, 0])
+x = quantize_f32(o.generate(2, 20000, 4, 4))
+r = m.compute_skyline(sky.Dataset(x, np.zeros(4), np.ones(4)), 4)
+assert np.array_equal(np.asarray(r.ids), o.compute_skyline(x.astype(np.float64), np.zeros(4), np.ones(4), 4).ids)
+m.close()
 print("SANITIZED OK")
 '''
 
