@@ -10,6 +10,8 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <cuda_runtime.h>
 
 namespace sk {
@@ -19,6 +21,42 @@ constexpr double kUnitUpperBound = 1.0 - 0x1p-32;  // dataset.hpp:15
 constexpr unsigned kFull = 0xffffffffu;
 
 typedef unsigned long long u64;
+
+// ------------------------------------------------ programmatic dependent launch
+// Every kernel opens with pdl_enter(): wait until the grid it depends on has
+// completed and flushed (griddepcontrol.wait -- a no-op for a plain launch),
+// then let the next kernel of the stream be scheduled.  launch() enqueues
+// with programmatic stream serialisation, so a dependent kernel's CTAs are
+// resident and waiting when its predecessor drains: the 2-5 us launch gap
+// between the ~60 dependent kernels of a query overlaps the predecessor's
+// tail instead of idling the GPU.  SKYCELL_PDL=0 launches plainly.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+inline bool pdl_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("SKYCELL_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  (void)cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ------------------------------------------------ unordered warp output
 // Survivor streams that need no order are written through per-warp output

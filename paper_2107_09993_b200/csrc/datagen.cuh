@@ -54,6 +54,7 @@ __device__ __forceinline__ double clamp_unit(double v) {
 // (record rbegin at out[0]): a shard generates only its own index range.
 template <int D>
 __global__ void k_generate(int dist, u64 n, u64 seed, int kind, u64 rbegin, u64 rcount, void* out) {
+  pdl_enter();
   const u64 b0 = rbegin / 65536, b1 = (rbegin + rcount + 65535) / 65536;
   for (u64 b = b0 + blockIdx.x * (u64)blockDim.x + threadIdx.x; b < b1; b += (u64)gridDim.x * blockDim.x) {
     Xo rng;

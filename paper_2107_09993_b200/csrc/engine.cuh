@@ -89,6 +89,10 @@ inline void ensure(DevBuf& b, size_t bytes) {
   b.cap = bytes;
 }
 
+// Small fills as a PDL kernel rather than cudaMemsetAsync: a memset node
+// breaks the programmatic-launch chain (a 2-3 us gap on each side).
+inline void fill_words(skycell_gpu_ctx* ctx, cudaStream_t s, void* p, u64 words, uint32_t v = 0);
+
 struct PipeBase {
   virtual ~PipeBase() = default;
   virtual void local() = 0;
@@ -129,12 +133,21 @@ struct skycell_gpu_ctx {
   skyeng::DevBuf scan_tot;        // K5 list-scan chunk totals
   skyeng::DevCounters* host_ctr = nullptr;  // pinned
   u64* host_param = nullptr;        // pinned H2D staging
+  u64* host_ctr_dev = nullptr;      // device views of the two (mapped pinned)
+  u64* host_param_dev = nullptr;
   cudaEvent_t ev[10] = {};
   u64 launches = 0;
   std::unique_ptr<skyeng::PipeBase> shard;  // sharded query in flight
 };
 
 namespace skyeng {
+
+inline void fill_words(skycell_gpu_ctx* ctx, cudaStream_t s, void* p, u64 words, uint32_t v) {
+  const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((words + 255) / 256, (u64)ctx->num_sms * 8));
+  sk::launch(sk::k_fill_u32, g, 256, 0, s, static_cast<uint32_t*>(p), words, v);
+  ++ctx->launches;
+}
+
 
 inline void put_err(char* err, size_t len, const std::string& m) {
   if (!err || !len) return;
@@ -254,22 +267,22 @@ void launch_tables(skycell_gpu_ctx* ctx, cudaStream_t s, const uint32_t* bits, i
   if (lines1 >= (u64)nsm * 128 || L <= 6) {
     // one warp per dimension-1 line
     const unsigned gw = (unsigned)std::max<u64>(1, std::min<u64>((lines1 * 32 + 255) / 256, (u64)nsm * 16));
-    sk::k_rowmin_prefix1w<TT><<<gw, 256, 0, s>>>(bits, L, lines1, table);
+    sk::launch(sk::k_rowmin_prefix1w<TT>, gw, 256, 0, s, bits, L, lines1, table);
     ++ctx->launches;
     for (int k = 2; k < d; ++k) {
       // a thread per line when lines fill the GPU, else a warp per line
-      if (lines1 >= (u64)nsm * 128 || L < 5) sk::k_prefix_min<TT><<<grid_for(lines1), 128, 0, s>>>(table, L, k, lines1);
-      else sk::k_prefix_minw<TT><<<gw, 256, 0, s>>>(table, L, k, lines1);
+      if (lines1 >= (u64)nsm * 128 || L < 5) sk::launch(sk::k_prefix_min<TT>, grid_for(lines1), 128, 0, s, table, L, k, lines1);
+      else sk::launch(sk::k_prefix_minw<TT>, gw, 256, 0, s, table, L, k, lines1);
       ++ctx->launches;
     }
     return;
   }
-  sk::k_rowmin<TT><<<grid_for(rows), 128, 0, s>>>(bits, L, rows, table);
+  sk::launch(sk::k_rowmin<TT>, grid_for(rows), 128, 0, s, bits, L, rows, table);
   ++ctx->launches;
   for (int k = 1; k < d; ++k) {
     const unsigned g = (unsigned)std::min<u64>(lines1, (u64)nsm * 2);
-    if (lines1 >= (u64)nsm * 128) sk::k_prefix_min<TT><<<grid_for(lines1), 128, 0, s>>>(table, L, k, lines1);
-    else sk::k_prefix_min_cta<TT><<<g, 1024, 0, s>>>(table, L, k, lines1);
+    if (lines1 >= (u64)nsm * 128) sk::launch(sk::k_prefix_min<TT>, grid_for(lines1), 128, 0, s, table, L, k, lines1);
+    else sk::launch(sk::k_prefix_min_cta<TT>, g, 1024, 0, s, table, L, k, lines1);
     ++ctx->launches;
   }
 }
@@ -279,7 +292,7 @@ void launch_count(skycell_gpu_ctx* ctx, cudaStream_t s, const uint32_t* bits, in
                   u64* key) {
   const u64 rows = 1ull << (u64)(L * (d - 1));
   const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((rows + 255) / 256, (u64)ctx->num_sms * 16));
-  sk::k_count_rows<TT><<<g, 256, 0, s>>>(bits, L, d, rows, table, cand, key);
+  sk::launch(sk::k_count_rows<TT>, g, 256, 0, s, bits, L, d, rows, table, cand, key);
   ++ctx->launches;
 }
 
@@ -297,21 +310,21 @@ void run_exact(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uin
   const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((cap + 255) / 256, (u64)nsm * 8));
   const TOut* trows = static_cast<const TOut*>(rows);
   uint32_t* lists = static_cast<uint32_t*>(ctx->lists.p);
-  sk::k_list_hist<TOut, D><<<g, 256, 0, s>>>(trows, ids, fsum, count, hist);
+  sk::launch(sk::k_list_hist<TOut, D>, g, 256, 0, s, trows, ids, fsum, count, hist);
   unsigned* totals = static_cast<unsigned*>(ctx->scan_tot.p);
-  sk::k_list_scan_sums<<<dim3(sk::kScanChunks, D), 1024, 0, s>>>(hist, D, totals, gate);
-  sk::k_list_scan<<<dim3(sk::kScanChunks, D), 1024, 0, s>>>(hist, cursor, D, totals, gate);
+  sk::launch(sk::k_list_scan_sums, dim3(sk::kScanChunks, D), 1024, 0, s, hist, D, totals, gate);
+  sk::launch(sk::k_list_scan, dim3(sk::kScanChunks, D), 1024, 0, s, hist, cursor, D, totals, gate);
   ++ctx->launches;
-  sk::k_list_scatter<TOut, D><<<g, 256, 0, s>>>(trows, ids, fsum, count, cursor, lists, cap);
+  sk::launch(sk::k_list_scatter<TOut, D>, g, 256, 0, s, trows, ids, fsum, count, cursor, lists, cap);
   const unsigned gw = (unsigned)std::max<u64>(1, std::min<u64>((cap * 32 + 255) / 256, (u64)nsm * 8));
   ensure(ctx->long_q, cap * 4);
   u64* long_n = static_cast<u64*>(ctx->long_n.p);
-  ck(cudaMemsetAsync(long_n, 0, 8, s), "memset");
+  fill_words(ctx, s, long_n, 2);
   constexpr unsigned kMaxSteps = 8;  // phase A budget (4..64 swept: 4-8 best at C2 / C4 shards)
-  sk::k_allpairs_lists<TOut, D><<<gw, 256, 0, s>>>(trows, ids, fsum, count, lists, hist, cap,
+  sk::launch(sk::k_allpairs_lists<TOut, D>, gw, 256, 0, s, trows, ids, fsum, count, lists, hist, cap,
                                                    static_cast<uint8_t*>(ctx->flags.p), q_begin, q_end, cell_level,
                                                    kMaxSteps, static_cast<uint32_t*>(ctx->long_q.p), long_n, gate);
-  sk::k_allpairs_long<TOut, D><<<nsm * 4, 256, 0, s>>>(trows, ids, fsum, lists, hist, cap,
+  sk::launch(sk::k_allpairs_long<TOut, D>, nsm * 4, 256, 0, s, trows, ids, fsum, lists, hist, cap,
                                                        static_cast<uint8_t*>(ctx->flags.p), cell_level,
                                                        static_cast<const uint32_t*>(ctx->long_q.p), long_n);
   ctx->launches += 5;
@@ -334,7 +347,7 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
   ensure(ctx->t_keys2, nslots * 8);
   ensure(ctx->t_vals, nslots * 4);
   ensure(ctx->t_vals2, nslots * 4);
-  ck(cudaMemsetAsync(valid_ctr, 0, 8, s), "memset");
+  fill_words(ctx, s, valid_ctr, 2);
   const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((nslots + 255) / 256, (u64)nsm * 8));
   tracer().mark(s, "tree: count read");
   // champion prefilter over a dense level-Lc grid (<= 2^24 cells)
@@ -361,27 +374,27 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
     const u64 lines = cells >> Lc;
     const unsigned gp = (unsigned)std::max<u64>(1, std::min<u64>((lines + 127) / 128, (u64)nsm * 16));
     uint8_t* killb = static_cast<uint8_t*>(ctx->t_kill.p);
-    ck(cudaMemsetAsync(cm, 0xff, cells * 4 * passes, s), "memset");
-    sk::k_cellmin_multi<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, count, Lc, passes, cells,
+    fill_words(ctx, s, cm, (u64)cells * passes, 0xffffffffu);
+    sk::launch(sk::k_cellmin_multi<TOut, D>, g, 256, 0, s, static_cast<const TOut*>(rows), ids, fsum, count, Lc, passes, cells,
                                                    cm);
     for (int pass = 0; pass < passes; ++pass) {
       uint32_t* t = cm + (u64)pass * cells;
       for (int k = 1; k <= D; ++k) {
         // few long lines (d = 2: 512 lines of 512 cells): one CTA per line,
         // else a thread per line
-        if (lines >= (u64)nsm * 4 || Lc < 8) sk::k_prefix_min<uint32_t><<<gp, 128, 0, s>>>(t, Lc, k, lines);
+        if (lines >= (u64)nsm * 4 || Lc < 8) sk::launch(sk::k_prefix_min<uint32_t>, gp, 128, 0, s, t, Lc, k, lines);
         else
-          sk::k_prefix_min_cta<uint32_t><<<(unsigned)std::min<u64>(lines, (u64)nsm * 2), 1024, 0, s>>>(t, Lc, k, lines);
+          sk::launch(sk::k_prefix_min_cta<uint32_t>, (unsigned)std::min<u64>(lines, (u64)nsm * 2), 1024, 0, s, t, Lc, k, lines);
       }
     }
-    sk::k_champ_kill_multi<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, count, Lc, passes,
+    sk::launch(sk::k_champ_kill_multi<TOut, D>, g, 256, 0, s, static_cast<const TOut*>(rows), ids, fsum, count, Lc, passes,
                                                       cells, cm, q_begin, q_end, killb,
                                                       static_cast<uint8_t*>(ctx->flags.p), valid_ctr + 1);
     ctx->launches += 2 + passes * D;
     kill = static_cast<const uint8_t*>(ctx->t_kill.p);
     tracer().mark(s, "tree: champion prefilter");
   }
-  sk::k_tree_keys<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, count, kill,
+  sk::launch(sk::k_tree_keys<TOut, D>, g, 256, 0, s, static_cast<const TOut*>(rows), ids, count, kill,
                                             static_cast<u64*>(ctx->t_keys.p), static_cast<uint32_t*>(ctx->t_vals.p),
                                             valid_ctr);
   size_t temp = 0;
@@ -428,7 +441,7 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
   if (dbg) {
     ensure(ctx->k5dbg, 128);
     vst = static_cast<u64*>(ctx->k5dbg.p);
-    ck(cudaMemsetAsync(vst, 0, 128, s), "memset");
+    fill_words(ctx, s, vst, 32);
   }
   // packet query (one warp per leaf of query points) unless merge_cross_cell
   // = false, whose same-cell restriction the point query keeps
@@ -439,12 +452,12 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
     ensure(ctx->t_lo, nodes * PL::NW * 4);
     uint32_t* prec = static_cast<uint32_t*>(ctx->t_rows.p);
     uint32_t* nrec = static_cast<uint32_t*>(ctx->t_lo.p);
-    sk::k_pk_gather<TOut, D><<<gm, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, order, m, prec);
-    sk::k_pk_leaves<TOut, D><<<gl, 256, 0, s>>>(prec, m, sh.nleaf, nrec);
+    sk::launch(sk::k_pk_gather<TOut, D>, gm, 256, 0, s, static_cast<const TOut*>(rows), ids, fsum, order, m, prec);
+    sk::launch(sk::k_pk_leaves<TOut, D>, gl, 256, 0, s, prec, m, sh.nleaf, nrec);
     ctx->launches += 2;
     for (int l = 1; l < sh.levels; ++l) {
       const unsigned gn = (unsigned)std::max<u64>(1, std::min<u64>((sh.cnt[l] + 255) / 256, (u64)nsm * 8));
-      sk::k_pk_level<TOut, D><<<gn, 256, 0, s>>>(nrec, sh.off[l - 1], sh.cnt[l - 1], sh.off[l], sh.cnt[l]);
+      sk::launch(sk::k_pk_level<TOut, D>, gn, 256, 0, s, nrec, sh.off[l - 1], sh.cnt[l - 1], sh.off[l], sh.cnt[l]);
       ++ctx->launches;
     }
     tracer().mark(s, "tree: build");
@@ -459,19 +472,19 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
     uint32_t* poff = pcnt + sh.nleaf;
     uint32_t* list = static_cast<uint32_t*>(ctx->t_vals.p);
     u64* list_n = static_cast<u64*>(ctx->long_n.p) + 1;
-    sk::k_pk_query<TOut, D, 0><<<gq, 256, 0, s>>>(prec, nrec, order, sh, q_begin, q_end, h1, two ? umask : nullptr,
+    sk::launch(sk::k_pk_query<TOut, D, 0>, gq, 256, 0, s, prec, nrec, order, sh, q_begin, q_end, h1, two ? umask : nullptr,
                                                   nullptr, nullptr, nullptr, static_cast<uint8_t*>(ctx->flags.p), vst);
     ++ctx->launches;
     if (two) {
       tracer().mark(s, "tree: packet phase 1");
       const unsigned gc = (unsigned)std::max<u64>(1, std::min<u64>((sh.nleaf + 255) / 256, (u64)nsm * 8));
-      sk::k_pk_counts<<<gc, 256, 0, s>>>(umask, sh.nleaf, pcnt);
+      sk::launch(sk::k_pk_counts, gc, 256, 0, s, umask, sh.nleaf, pcnt);
       size_t temp = 0;
       ck(cub::DeviceScan::ExclusiveSum(nullptr, temp, pcnt, poff, (int64_t)sh.nleaf, s), "cub scan temp");
       ensure(ctx->t_cub, temp);
       ck(cub::DeviceScan::ExclusiveSum(ctx->t_cub.p, temp, pcnt, poff, (int64_t)sh.nleaf, s), "cub scan");
-      sk::k_pk_list<<<gc, 256, 0, s>>>(umask, poff, sh.nleaf, list, list_n);
-      sk::k_pk_query<TOut, D, 1><<<gq, 256, 0, s>>>(prec, nrec, order, sh, q_begin, q_end, h1, nullptr, list, list_n,
+      sk::launch(sk::k_pk_list, gc, 256, 0, s, umask, poff, sh.nleaf, list, list_n);
+      sk::launch(sk::k_pk_query<TOut, D, 1>, gq, 256, 0, s, prec, nrec, order, sh, q_begin, q_end, h1, nullptr, list, list_n,
                                                   nullptr, static_cast<uint8_t*>(ctx->flags.p), vst);
       ctx->launches += 4;
     }
@@ -487,19 +500,19 @@ void run_tree(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint
     TOut* srows = static_cast<TOut*>(ctx->t_rows.p);
     uint32_t* sids = static_cast<uint32_t*>(ctx->t_ids.p);
     u64* sfsum = static_cast<u64*>(ctx->t_fsum.p);
-    sk::k_tree_gather<TOut, D><<<gm, 256, 0, s>>>(static_cast<const TOut*>(rows), ids, fsum, order, m, srows, sids, sfsum);
+    sk::launch(sk::k_tree_gather<TOut, D>, gm, 256, 0, s, static_cast<const TOut*>(rows), ids, fsum, order, m, srows, sids, sfsum);
     sk::TreeView<TOut, D> tv{static_cast<TOut*>(ctx->t_lo.p), static_cast<TOut*>(ctx->t_hi.p),
                              static_cast<u64*>(ctx->t_cs.p), static_cast<uint32_t*>(ctx->t_ci.p)};
-    sk::k_tree_leaves<TOut, D><<<gl, 256, 0, s>>>(srows, sids, sfsum, m, sh.nleaf, tv);
+    sk::launch(sk::k_tree_leaves<TOut, D>, gl, 256, 0, s, srows, sids, sfsum, m, sh.nleaf, tv);
     ctx->launches += 2;
     for (int l = 1; l < sh.levels; ++l) {
       const unsigned gn = (unsigned)std::max<u64>(1, std::min<u64>((sh.cnt[l] + 255) / 256, (u64)nsm * 8));
-      sk::k_tree_level<TOut, D><<<gn, 256, 0, s>>>(tv, sh.off[l - 1], sh.cnt[l - 1], sh.off[l], sh.cnt[l]);
+      sk::launch(sk::k_tree_level<TOut, D>, gn, 256, 0, s, tv, sh.off[l - 1], sh.cnt[l - 1], sh.off[l], sh.cnt[l]);
       ++ctx->launches;
     }
     tracer().mark(s, "tree: build");
     const unsigned gq = (unsigned)std::max<u64>(1, std::min<u64>((m * 32 + 255) / 256, (u64)nsm * 8));
-    sk::k_tree_query<TOut, D><<<gq, 256, 0, s>>>(srows, sids, sfsum, order, tv, sh, q_begin, q_end, cell_level,
+    sk::launch(sk::k_tree_query<TOut, D>, gq, 256, 0, s, srows, sids, sfsum, order, tv, sh, q_begin, q_end, cell_level,
                                                 static_cast<uint8_t*>(ctx->flags.p), vst);
     ++ctx->launches;
     tracer().mark(s, "tree: query");
@@ -574,12 +587,10 @@ void run_dominance(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const
     u64* lc = static_cast<u64*>(ctx->long_n.p) + 2;
     u64* org = static_cast<u64*>(ctx->long_n.p) + 3;
     const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((cap + 255) / 256, (u64)ctx->num_sms * 8));
-    ck(cudaMemsetAsync(org, 0, 8, s), "memset");
-    sk::k_origin_count<<<g, 256, 0, s>>>(ids, fsum, count, org);
-    sk::k_origin_flags<<<g, 256, 0, s>>>(ids, fsum, count, q_begin, q_end, org, static_cast<uint8_t*>(ctx->flags.p));
-    sk::k_gate_count<<<1, 1, 0, s>>>(vc, count, tree_min, org, lc);
-    ck(cudaMemcpyAsync(ctx->host_param + 3, vc, 8, cudaMemcpyDeviceToHost, s), "D2H");
-    ck(cudaMemcpyAsync(ctx->host_param + 4, org, 8, cudaMemcpyDeviceToHost, s), "D2H");
+    fill_words(ctx, s, org, 2);
+    sk::launch(sk::k_origin_count, g, 256, 0, s, ids, fsum, count, org);
+    sk::launch(sk::k_origin_flags, g, 256, 0, s, ids, fsum, count, q_begin, q_end, org, static_cast<uint8_t*>(ctx->flags.p));
+    sk::launch(sk::k_gate_count, 1, 1, 0, s, vc, count, tree_min, org, lc, ctx->host_param_dev + 3);
     ck(cudaEventRecord(ctx->ev[8], s), "event");
     ctx->launches += 3;
     run_exact<TOut, D>(ctx, s, rows, ids, fsum, lc, cap, hist, cursor, q_begin, q_end, cell_level, lc);
@@ -773,13 +784,12 @@ struct Pipe final : PipeBase {
       sp.id_base = q.id_base;
       const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((m + 255) / 256, (u64)nsm * 8));
       tracer().mark(s, "K0: memset");
-      sk::k_sample<TIn, TOut, D, IDENT><<<g, 256, 0, s>>>(sp);
+      sk::launch(sk::k_sample<TIn, TOut, D, IDENT>, g, 256, 0, s, sp);
       tracer().mark(s, "K0: sample");
       // H = the strict-dominance height of the sample's level-la occupancy:
       // a level-la prefix-min table (multi-CTA) shifted by one cell per dim
       launch_tables<uint8_t>(ctx, s, U(o_sla), la, D, static_cast<uint8_t*>(ctx->table2.p));
-      sk::k_filter_from_table<<<(unsigned)std::max<u64>(1, std::min<u64>((h_entries + 255) / 256, (u64)nsm * 4)), 256, 0,
-                                s>>>(static_cast<const uint8_t*>(ctx->table2.p), la, D, h_entries,
+      sk::launch(sk::k_filter_from_table, (unsigned)std::max<u64>(1, std::min<u64>((h_entries + 255) / 256, (u64)nsm * 4)), 256, 0, s, static_cast<const uint8_t*>(ctx->table2.p), la, D, h_entries,
                                      static_cast<uint8_t*>(ctx->H.p));
       tracer().mark(s, "K0: build_filter");
       ctx->launches += 2;
@@ -812,8 +822,8 @@ struct Pipe final : PipeBase {
         pc.chunk = kChunk4;
         pc.kept = &c->xs_kept;
         pc.examined = nullptr;
-        if (wide) sk::k_candidates<TOut, D, uint32_t, kThreads><<<grid4, kThreads, 16, s>>>(pc);
-        else sk::k_candidates<TOut, D, uint8_t, kThreads><<<grid4, kThreads, 16, s>>>(pc);
+        if (wide) sk::launch(sk::k_candidates<TOut, D, uint32_t, kThreads>, grid4, kThreads, 16, s, pc);
+        else sk::launch(sk::k_candidates<TOut, D, uint8_t, kThreads>, grid4, kThreads, 16, s, pc);
         ++ctx->launches;
         tracer().mark(s, "K0: sample X");
         // Filter points = the strongest points of the sample's skyline (the
@@ -822,26 +832,26 @@ struct Pipe final : PipeBase {
         // order): anti-correlated samples keep ~all points in X, and their
         // filter points remove little anyway.
         constexpr u64 kXMax = 1ull << 17;
-        sk::k_pack_members<TOut, D><<<nsm * 4, 256, 0, s>>>(
+        sk::launch(sk::k_pack_members<TOut, D>, nsm * 4, 256, 0, s, 
             static_cast<const TOut*>(ctx->s2_rows.p), static_cast<const uint32_t*>(ctx->s2_ids.p), nullptr,
             static_cast<const u64*>(ctx->s2_fsum.p), &c->xs, static_cast<TOut*>(ctx->smp_rows.p),
             static_cast<u64*>(ctx->smp_fsum.p), static_cast<uint32_t*>(ctx->smp_ids.p), &c->xd);
-        sk::k_clamp_count<<<1, 32, 0, s>>>(&c->xd, kXMax, &c->xs_cap);
+        sk::launch(sk::k_clamp_count, 1, 32, 0, s, &c->xd, kXMax, &c->xs_cap);
         ctx->launches += 2;
         run_dominance<TOut, D>(ctx, s, ctx->smp_rows.p, static_cast<const uint32_t*>(ctx->smp_ids.p),
                                static_cast<const u64*>(ctx->smp_fsum.p), &c->xs_cap, std::min<u64>(m, kXMax),
                                U(o_shist), U(o_scur), &c->tvalid, 0, nullptr, 0, sample_tree_min());
         tracer().mark(s, "K0: sample skyline");
-        sk::k_compact_members<TOut, D><<<nsm * 4, 256, 0, s>>>(
+        sk::launch(sk::k_compact_members<TOut, D>, nsm * 4, 256, 0, s, 
             static_cast<const TOut*>(ctx->smp_rows.p), static_cast<const uint32_t*>(ctx->smp_ids.p),
             static_cast<const uint8_t*>(ctx->flags.p), static_cast<const u64*>(ctx->smp_fsum.p), &c->xs_cap,
             static_cast<TOut*>(ctx->s2_rows.p), static_cast<u64*>(ctx->s2_fsum.p), &c->fs);
-        sk::k_strength_order<TOut, D><<<1, 1024, 0, s>>>(
+        sk::launch(sk::k_strength_order<TOut, D>, 1, 1024, 0, s, 
             static_cast<const TOut*>(ctx->s2_rows.p), static_cast<const u64*>(ctx->s2_fsum.p), nullptr, &c->fs,
             (uint32_t)pf_max, static_cast<TOut*>(ctx->f_rows.p), static_cast<u64*>(ctx->f_fsum.p), nullptr, &c->nf);
-        sk::k_filter_gate<<<1, 1, 0, s>>>(&c->fs, &c->xs_cap, &c->fweak);
+        sk::launch(sk::k_filter_gate, 1, 1, 0, s, &c->fs, &c->xs_cap, &c->fweak);
         ++ctx->launches;
-        sk::k_filter_lists<TOut, D><<<D, 1024, 0, s>>>(static_cast<const TOut*>(ctx->f_rows.p), &c->nf,
+        sk::launch(sk::k_filter_lists<TOut, D>, D, 1024, 0, s, static_cast<const TOut*>(ctx->f_rows.p), &c->nf,
                                                         (uint32_t)pf_max, static_cast<uint16_t*>(ctx->f_lists.p),
                                                         static_cast<uint16_t*>(ctx->f_offs.p));
         ++ctx->launches;
@@ -888,13 +898,13 @@ struct Pipe final : PipeBase {
       p1.d_reserved = &c->dres;
     }
     if (q.timed) ck(cudaEventRecord(ctx->ev[4], s), "event");
-    kstream<<<grid1, k1_threads, smem1, s>>>(p1);
+    sk::launch(kstream, grid1, k1_threads, smem1, s, p1);
     ++ctx->launches;
     if (q.timed) ck(cudaEventRecord(ctx->ev[5], s), "event");
     if (lo_words) {
       const unsigned gx = (unsigned)std::max<u64>(1, std::min<u64>((lo_words + 255) / 256, (u64)nsm * 8));
       const unsigned gy = (unsigned)std::max<u64>(1, std::min<u64>(32, (u64)nsm * 4 / gx));
-      sk::k_reduce_slabs<<<dim3(gx, gy), 256, 0, s>>>(static_cast<uint32_t*>(ctx->slabs.p), grid1, lo_words,
+      sk::launch(sk::k_reduce_slabs, dim3(gx, gy), 256, 0, s, static_cast<uint32_t*>(ctx->slabs.p), grid1, lo_words,
                                                        occ(rec_la ? la : la - 1));
       ++ctx->launches;
     }
@@ -909,7 +919,7 @@ struct Pipe final : PipeBase {
   void or_gathered(const void* gathered, int world) override {
     const u64 w4 = occ_bytes() / 16;
     const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((w4 + 255) / 256, (u64)nsm * 8));
-    sk::k_or_gather<<<g, 256, 0, s>>>(static_cast<const uint4*>(gathered), world, w4,
+    sk::launch(sk::k_or_gather, g, 256, 0, s, static_cast<const uint4*>(gathered), world, w4,
                                       static_cast<uint4*>(at(o_occ[1])));
     ++ctx->launches;
   }
@@ -917,7 +927,7 @@ struct Pipe final : PipeBase {
   void or_peers(const void* const* dev_table, int world) override {
     const u64 w4 = occ_bytes() / 16;
     const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((w4 + 255) / 256, (u64)nsm * 8));
-    sk::k_or_peers<<<g, 256, 0, s>>>(reinterpret_cast<const uint4* const*>(dev_table), world, w4,
+    sk::launch(sk::k_or_peers, g, 256, 0, s, reinterpret_cast<const uint4* const*>(dev_table), world, w4,
                                      static_cast<uint4*>(at(o_occ[1])));
     ++ctx->launches;
   }
@@ -942,9 +952,9 @@ struct Pipe final : PipeBase {
       if (L >= 5) {
         const u64 dst_words = words_at(L);
         const unsigned gw = (unsigned)std::max<u64>(1, std::min<u64>((dst_words + 255) / 256, (u64)nsm * 8));
-        sk::k_downsample_words<<<gw, 256, 0, s2>>>(occ(L + 1), L, D, dst_words, occ(L));
+        sk::launch(sk::k_downsample_words, gw, 256, 0, s2, occ(L + 1), L, D, dst_words, occ(L));
       } else {
-        sk::k_downsample<<<g, 256, 0, s2>>>(occ(L + 1), L, D, src_words, occ(L));
+        sk::launch(sk::k_downsample, g, 256, 0, s2, occ(L + 1), L, D, src_words, occ(L));
       }
       ++ctx->launches;
       if (L > 7) {
@@ -1012,9 +1022,9 @@ struct Pipe final : PipeBase {
         const size_t sa = ((sk::kK4aHead * D * sizeof(TOut) + 15) & ~(size_t)15) + sk::kK4aHead * 8 +
                           (size_t)(kThreads / 32) * 64 * (D * sizeof(TOut) + 8 + 4) + 16;
         ck(cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sa), "smem attr");
-        ka<<<grid4, kThreads, sa, s>>>(pa);
+        sk::launch(ka, grid4, kThreads, sa, s, pa);
       } else {
-        kc<<<grid4, kThreads, smem_pf, s>>>(pa);
+        sk::launch(kc, grid4, kThreads, smem_pf, s, pa);
       }
       sk::CandParams pb = pc;
       pb.rows = ctx->p_rows.p;
@@ -1026,10 +1036,10 @@ struct Pipe final : PipeBase {
       pb.head_start = sk::kK4aHead;
       pb.coop = 1;
       pb.coop_mid = 16;  // measured: 16 best at C2 / C4 shards (8..64 swept)
-      kc<<<grid4, kThreads, smem_pf, s>>>(pb);
+      sk::launch(kc, grid4, kThreads, smem_pf, s, pb);
       ctx->launches += 2;
     } else {
-      kc<<<grid4, kThreads, smem_pf, s>>>(pc);
+      sk::launch(kc, grid4, kThreads, smem_pf, s, pc);
       ++ctx->launches;
     }
     if (q.timed) ck(cudaEventRecord(ctx->ev[6], s), "event");
@@ -1043,7 +1053,7 @@ struct Pipe final : PipeBase {
     u64 nslots = 0;
     ck(cudaMemcpyAsync(&nslots, &c->s2, 8, cudaMemcpyDeviceToHost, s), "D2H");
     ck(cudaStreamSynchronize(s), "sync");
-    ck(cudaMemsetAsync(&c->examined, 0, 8, s), "memset");
+    fill_words(ctx, s, &c->examined, 2);
     const u64 ns = std::max<u64>(nslots, 1);
     ensure(ctx->sp_keys, ns * 8);
     ensure(ctx->sp_keys2, ns * 8);
@@ -1071,9 +1081,9 @@ struct Pipe final : PipeBase {
     uint8_t* kflag = static_cast<uint8_t*>(ctx->sp_kflag.p);
     uint8_t* cflag = static_cast<uint8_t*>(ctx->sp_cflag.p);
     u64* spn = static_cast<u64*>(ctx->sp_n.p);  // [ncells, nvalid, queries]
-    ck(cudaMemsetAsync(spn, 0, 64, s), "memset");
+    fill_words(ctx, s, spn, 16);
     const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((ns + 255) / 256, (u64)nsm * 8));
-    sk::k_sp_keys<TOut, D><<<g, 256, 0, s>>>(static_cast<const TOut*>(ctx->s2_rows.p),
+    sk::launch(sk::k_sp_keys<TOut, D>, g, 256, 0, s, static_cast<const TOut*>(ctx->s2_rows.p),
                                              static_cast<const uint32_t*>(ctx->s2_ids.p), &c->s2, rho_q, keys, vals);
     size_t temp = 0, temp2 = 0;
     ck(cub::DeviceRadixSort::SortPairs(nullptr, temp, keys, keys2, vals, vals2, (int64_t)ns, 0, rho_q * D, s), "cub");
@@ -1081,9 +1091,9 @@ struct Pipe final : PipeBase {
     ensure(ctx->t_cub, std::max(temp, temp2));
     ck(cub::DeviceRadixSort::SortPairs(ctx->t_cub.p, temp, keys, keys2, vals, vals2, (int64_t)ns, 0, rho_q * D, s),
        "cub sort");
-    sk::k_sp_heads<<<g, 256, 0, s>>>(keys2, ns, head);
+    sk::launch(sk::k_sp_heads, g, 256, 0, s, keys2, ns, head);
     ck(cub::DeviceScan::InclusiveSum(ctx->t_cub.p, temp2, head, cpos, (int64_t)ns, s), "cub scan");
-    sk::k_sp_cells<D><<<g, 256, 0, s>>>(keys2, head, cpos, ns, rho_q, crows, cfsum, cids, cstart, spn, spn + 1);
+    sk::launch(sk::k_sp_cells<D>, g, 256, 0, s, keys2, head, cpos, ns, rho_q, crows, cfsum, cids, cstart, spn, spn + 1);
     ctx->launches += 5;
     // key test: corners dominated by another corner of U (no prefilter, so
     // the tree holds every cell for the strict test below)
@@ -1101,27 +1111,27 @@ struct Pipe final : PipeBase {
       ctx->host_param[2] = sh.m;
       ck(cudaMemcpyAsync(spn + 2, ctx->host_param + 2, 8, cudaMemcpyHostToDevice, s), "param");
       const unsigned gm = (unsigned)std::max<u64>(1, std::min<u64>((sh.m + 255) / 256, (u64)nsm * 8));
-      sk::k_sp_queries<D><<<gm, 256, 0, s>>>(prec, sh.m, rho_q, qrec);
+      sk::launch(sk::k_sp_queries<D>, gm, 256, 0, s, prec, sh.m, rho_q, qrec);
       const unsigned gq = (unsigned)std::max<u64>(1, std::min<u64>((sh.nleaf * 32 + 255) / 256, (u64)nsm * 8));
-      sk::k_pk_query<float, D, 2><<<gq, 256, 0, s>>>(prec, nrec, order, sh, 0, nullptr, 0, nullptr, nullptr, spn + 2,
+      sk::launch(sk::k_pk_query<float, D, 2>, gq, 256, 0, s, prec, nrec, order, sh, 0, nullptr, 0, nullptr, nullptr, spn + 2,
                                                     qrec, static_cast<uint8_t*>(ctx->flags.p), nullptr);
-      sk::k_sp_cand<<<gm, 256, 0, s>>>(static_cast<const uint8_t*>(ctx->flags.p), qrec + PL::KW + 2, PL::PW, order,
+      sk::launch(sk::k_sp_cand, gm, 256, 0, s, static_cast<const uint8_t*>(ctx->flags.p), qrec + PL::KW + 2, PL::PW, order,
                                       sh.m, cflag);
       ctx->launches += 3;
     }
-    sk::k_sp_classify<D><<<g, 256, 0, s>>>(crows, kflag, cflag, cstart, spn, spn + 1, rho_q, &c->key[rho_q - 1],
+    sk::launch(sk::k_sp_classify<D>, g, 256, 0, s, crows, kflag, cflag, cstart, spn, spn + 1, rho_q, &c->key[rho_q - 1],
                                           &c->cand[rho_q - 1], &c->examined);
     // the points of candidate cells -> P, then the filter points -> S2
     ensure(ctx->p_rows, cap4 * D * sizeof(TOut));
     ensure(ctx->p_ids, cap4 * 4);
     ensure(ctx->p_fsum, cap4 * 8);
-    ck(cudaMemsetAsync(&c->pres, 0, 8, s), "memset");
-    sk::k_sp_points<TOut, D><<<grid4, kThreads, 0, s>>>(
+    fill_words(ctx, s, &c->pres, 2);
+    sk::launch(sk::k_sp_points<TOut, D>, grid4, kThreads, 0, s, 
         static_cast<const TOut*>(ctx->s2_rows.p), static_cast<const uint32_t*>(ctx->s2_ids.p),
         static_cast<const u64*>(ctx->s2_fsum.p), vals2, keys2, cpos, cflag, ns, static_cast<TOut*>(ctx->p_rows.p),
         static_cast<uint32_t*>(ctx->p_ids.p), static_cast<u64*>(ctx->p_fsum.p), &c->pres, kChunk4);
-    ck(cudaMemsetAsync(&c->s2, 0, 8, s), "memset");
-    ck(cudaMemsetAsync(&c->s2_kept, 0, 8, s), "memset");
+    fill_words(ctx, s, &c->s2, 2);
+    fill_words(ctx, s, &c->s2_kept, 2);
     sk::CandParams pb{};
     pb.rows = ctx->p_rows.p;
     pb.ids = static_cast<const uint32_t*>(ctx->p_ids.p);
@@ -1145,7 +1155,7 @@ struct Pipe final : PipeBase {
     pb.coop_mid = 16;
     auto kc = sk::k_candidates<TOut, D, uint8_t, kThreads>;
     ck(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pf), "smem attr");
-    kc<<<grid4, kThreads, smem_pf, s>>>(pb);
+    sk::launch(kc, grid4, kThreads, smem_pf, s, pb);
     ctx->launches += 3;
   }
 
@@ -1166,10 +1176,10 @@ struct Pipe final : PipeBase {
     uint32_t* idbits = U(o_idbits);
     unsigned* bcount = U(o_bcount);
     const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((cap + 255) / 256, (u64)nsm * 8));
-    sk::k_mark_ids<<<g, 256, 0, s>>>(ids, static_cast<const uint8_t*>(ctx->flags.p), count, idbits, q.id_base);
-    sk::k_bits_count<<<bit_blocks, sk::kBitsThreads, 0, s>>>(idbits, id_words, bcount);
-    sk::k_bits_scan<<<1, 1024, 0, s>>>(bcount, bit_blocks, &c->fin);
-    sk::k_bits_write<<<bit_blocks, sk::kBitsThreads, 0, s>>>(idbits, id_words, bcount, dst, q.id_base);
+    sk::launch(sk::k_mark_ids, g, 256, 0, s, ids, static_cast<const uint8_t*>(ctx->flags.p), count, idbits, q.id_base);
+    sk::launch(sk::k_bits_count, bit_blocks, sk::kBitsThreads, 0, s, idbits, id_words, bcount);
+    sk::launch(sk::k_bits_scan, 1, 1024, 0, s, bcount, bit_blocks, &c->fin);
+    sk::launch(sk::k_bits_write, bit_blocks, sk::kBitsThreads, 0, s, idbits, id_words, bcount, dst, q.id_base);
     ctx->launches += 4;
   }
 
@@ -1177,7 +1187,10 @@ struct Pipe final : PipeBase {
 
   void read_counters() {
     ck(cudaStreamWaitEvent(s, ctx->ev_join, 0), "join");
-    ck(cudaMemcpyAsync(ctx->host_ctr, ctr(), sizeof(DevCounters), cudaMemcpyDeviceToHost, s), "counters D2H");
+    static_assert(sizeof(DevCounters) % 8 == 0, "counters are whole words");
+    sk::launch(sk::k_copy_words, 1, 64, 0, s, reinterpret_cast<const u64*>(ctr()), ctx->host_ctr_dev,
+               (unsigned)(sizeof(DevCounters) / 8));
+    ++ctx->launches;
     ck(cudaStreamSynchronize(s), "query");
     if (tracer().on) {
       const DevCounters& h = *ctx->host_ctr;
@@ -1240,7 +1253,7 @@ struct Pipe final : PipeBase {
     ensure(ctx->sky_rows, cap4 * D * sizeof(TOut));
     ensure(ctx->sky_fsum, cap4 * 8);
     ensure(ctx->sky_ids, cap4 * 4);
-    sk::k_pack_members<TOut, D><<<nsm * 4, 256, 0, s>>>(
+    sk::launch(sk::k_pack_members<TOut, D>, nsm * 4, 256, 0, s, 
         static_cast<const TOut*>(ctx->s2_rows.p), static_cast<const uint32_t*>(ctx->s2_ids.p),
         static_cast<const uint8_t*>(ctx->flags.p), static_cast<const u64*>(ctx->s2_fsum.p), &c->s2,
         static_cast<TOut*>(ctx->sky_rows.p), static_cast<u64*>(ctx->sky_fsum.p),
@@ -1269,7 +1282,7 @@ struct Pipe final : PipeBase {
     }
     if (maxc > cnt) {
       uint32_t* ids = reinterpret_cast<uint32_t*>(b + rows_bytes(maxc) + al(maxc * 8));
-      sk::k_fill_u32<<<nsm, 256, 0, s>>>(ids + cnt, maxc - cnt, sk::kNoId);
+      sk::launch(sk::k_fill_u32, nsm, 256, 0, s, ids + cnt, maxc - cnt, sk::kNoId);
       ++ctx->launches;
     }
   }

@@ -41,6 +41,7 @@ __device__ __forceinline__ int32_t grid_col(double u, double scale) { return (in
 
 static __global__ void k_grid_keys(const double* __restrict__ coords, u64 n, int d, int rho, u64* __restrict__ keys,
                                    uint32_t* __restrict__ vals) {
+  sk::pdl_enter();
   const double scale = ldexp(1.0, rho);
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
     u64 key = 0;
@@ -57,6 +58,7 @@ static __global__ void k_grid_keys(const double* __restrict__ coords, u64 n, int
 static __global__ void k_grid_gather(const double* __restrict__ coords, const uint32_t* __restrict__ ids,
                                      const uint32_t* __restrict__ order, u64 n, int d, double* __restrict__ scoords,
                                      uint32_t* __restrict__ sids) {
+  sk::pdl_enter();
   for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x) {
     const uint32_t i = order[j];
     for (int k = 0; k < d; ++k) scoords[j * d + k] = coords[(u64)i * d + k];
@@ -65,6 +67,7 @@ static __global__ void k_grid_gather(const double* __restrict__ coords, const ui
 }
 
 static __global__ void k_grid_heads(const u64* __restrict__ keys, u64 n, uint32_t* __restrict__ head) {
+  sk::pdl_enter();
   for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x)
     head[j] = j == 0 || keys[j] != keys[j - 1];
 }
@@ -74,6 +77,7 @@ static __global__ void k_grid_heads(const u64* __restrict__ keys, u64 n, uint32_
 static __global__ void k_grid_runs(const double* __restrict__ scoords, const uint32_t* __restrict__ head,
                                    const uint32_t* __restrict__ cpos, u64 n, int d, int rho, u64* __restrict__ lin,
                                    uint32_t* __restrict__ begin, uint32_t* __restrict__ end) {
+  sk::pdl_enter();
   const double scale = ldexp(1.0, rho);
   for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x) {
     const uint32_t r = cpos[j] - 1;
@@ -87,17 +91,20 @@ static __global__ void k_grid_runs(const double* __restrict__ scoords, const uin
 }
 
 static __global__ void k_grid_iota(uint32_t* __restrict__ v, u64 m) {
+  sk::pdl_enter();
   for (u64 r = blockIdx.x * (u64)blockDim.x + threadIdx.x; r < m; r += (u64)gridDim.x * blockDim.x) v[r] = (uint32_t)r;
 }
 
 static __global__ void k_grid_permute(const uint32_t* __restrict__ src, const uint32_t* __restrict__ order, u64 m,
                                       uint32_t* __restrict__ dst) {
+  sk::pdl_enter();
   for (u64 r = blockIdx.x * (u64)blockDim.x + threadIdx.x; r < m; r += (u64)gridDim.x * blockDim.x)
     dst[r] = src[order[r]];
 }
 
 // Layer rho-1 occupancy: the parent of every non-empty leaf (grid.cpp:84-86).
 static __global__ void k_grid_parents(const u64* __restrict__ lin, u64 m, int d, int rho, uint32_t* __restrict__ occ) {
+  sk::pdl_enter();
   const u64 mask = (1ull << rho) - 1;
   for (u64 r = blockIdx.x * (u64)blockDim.x + threadIdx.x; r < m; r += (u64)gridDim.x * blockDim.x) {
     u64 p = 0;
@@ -107,6 +114,7 @@ static __global__ void k_grid_parents(const u64* __restrict__ lin, u64 m, int d,
 }
 
 static __global__ void k_grid_popc(const uint32_t* __restrict__ bits, u64 words, u64* __restrict__ out) {
+  sk::pdl_enter();
   u64 c = 0;
   for (u64 w = blockIdx.x * (u64)blockDim.x + threadIdx.x; w < words; w += (u64)gridDim.x * blockDim.x)
     c += __popc(bits[w]);
@@ -121,6 +129,7 @@ static __global__ void k_grid_lookup(const u64* __restrict__ q, u64 nq, const u6
                                      const uint32_t* __restrict__ begin, const uint32_t* __restrict__ end,
                                      const uint32_t* __restrict__ bits, uint32_t* __restrict__ out_begin,
                                      uint32_t* __restrict__ out_end, uint8_t* __restrict__ out_occ) {
+  sk::pdl_enter();
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nq; i += (u64)gridDim.x * blockDim.x) {
     const u64 x = q[i];
     if (bits) {
@@ -195,7 +204,7 @@ int skycell_gpu_grid_build(skycell_gpu_ctx* ctx, const double* coords, const uin
     ensure(g->coords, nn * d * 8);
     ensure(g->ids, nn * 4);
     if (n) {
-      k_grid_keys<<<gr, 256, 0, s>>>(static_cast<const double*>(in_c.p), n, d, rho, static_cast<u64*>(keys.p),
+      sk::launch(k_grid_keys, gr, 256, 0, s, static_cast<const double*>(in_c.p), n, d, rho, static_cast<u64*>(keys.p),
                                      static_cast<uint32_t*>(vals.p));
       size_t t1 = 0, t2 = 0;
       ck(cub::DeviceRadixSort::SortPairs(nullptr, t1, static_cast<u64*>(keys.p), static_cast<u64*>(keys2.p),
@@ -212,12 +221,12 @@ int skycell_gpu_grid_build(skycell_gpu_ctx* ctx, const double* coords, const uin
                                          static_cast<uint32_t*>(vals.p), static_cast<uint32_t*>(vals2.p), (int64_t)n, 0,
                                          rho * d, s),
          "cub sort");
-      k_grid_gather<<<gr, 256, 0, s>>>(static_cast<const double*>(in_c.p), dev_ids,
+      sk::launch(k_grid_gather, gr, 256, 0, s, static_cast<const double*>(in_c.p), dev_ids,
                                        static_cast<const uint32_t*>(vals2.p), n, d, static_cast<double*>(g->coords.p),
                                        static_cast<uint32_t*>(g->ids.p));
       ensure(head, nn * 4);
       ensure(cpos, nn * 4);
-      k_grid_heads<<<gr, 256, 0, s>>>(static_cast<const u64*>(keys2.p), n, static_cast<uint32_t*>(head.p));
+      sk::launch(k_grid_heads, gr, 256, 0, s, static_cast<const u64*>(keys2.p), n, static_cast<uint32_t*>(head.p));
       ck(cub::DeviceScan::InclusiveSum(tmp.p, t2, static_cast<uint32_t*>(head.p), static_cast<uint32_t*>(cpos.p),
                                        (int64_t)n, s),
          "cub scan");
@@ -228,7 +237,7 @@ int skycell_gpu_grid_build(skycell_gpu_ctx* ctx, const double* coords, const uin
       ensure(lin_r, (u64)runs * 8);
       ensure(beg_r, (u64)runs * 4);
       ensure(end_r, (u64)runs * 4);
-      k_grid_runs<<<gr, 256, 0, s>>>(static_cast<const double*>(g->coords.p), static_cast<const uint32_t*>(head.p),
+      sk::launch(k_grid_runs, gr, 256, 0, s, static_cast<const double*>(g->coords.p), static_cast<const uint32_t*>(head.p),
                                      static_cast<const uint32_t*>(cpos.p), n, d, rho, static_cast<u64*>(lin_r.p),
                                      static_cast<uint32_t*>(beg_r.p), static_cast<uint32_t*>(end_r.p));
       // leaves by linear index (enumeration order): sort (lin, run)
@@ -238,7 +247,7 @@ int skycell_gpu_grid_build(skycell_gpu_ctx* ctx, const double* coords, const uin
       ensure(g->leaf_lin, (u64)runs * 8);
       ensure(g->leaf_begin, (u64)runs * 4);
       ensure(g->leaf_end, (u64)runs * 4);
-      k_grid_iota<<<gl, 256, 0, s>>>(rid, runs);
+      sk::launch(k_grid_iota, gl, 256, 0, s, rid, runs);
       size_t t3 = 0;
       ck(cub::DeviceRadixSort::SortPairs(nullptr, t3, static_cast<u64*>(lin_r.p), static_cast<u64*>(g->leaf_lin.p), rid,
                                          rid2, (int64_t)runs, 0, rho * d, s),
@@ -247,9 +256,9 @@ int skycell_gpu_grid_build(skycell_gpu_ctx* ctx, const double* coords, const uin
       ck(cub::DeviceRadixSort::SortPairs(tmp.p, t3, static_cast<u64*>(lin_r.p), static_cast<u64*>(g->leaf_lin.p), rid,
                                          rid2, (int64_t)runs, 0, rho * d, s),
          "cub sort");
-      k_grid_permute<<<gl, 256, 0, s>>>(static_cast<const uint32_t*>(beg_r.p), rid2, runs,
+      sk::launch(k_grid_permute, gl, 256, 0, s, static_cast<const uint32_t*>(beg_r.p), rid2, runs,
                                         static_cast<uint32_t*>(g->leaf_begin.p));
-      k_grid_permute<<<gl, 256, 0, s>>>(static_cast<const uint32_t*>(end_r.p), rid2, runs,
+      sk::launch(k_grid_permute, gl, 256, 0, s, static_cast<const uint32_t*>(end_r.p), rid2, runs,
                                         static_cast<uint32_t*>(g->leaf_end.p));
     }
     // occupancy of layers 0 .. rho-1 by child-OR
@@ -266,20 +275,20 @@ int skycell_gpu_grid_build(skycell_gpu_ctx* ctx, const double* coords, const uin
       if (!n) continue;
       if (L == rho - 1) {
         const unsigned gl = (unsigned)std::max<u64>(1, std::min<u64>((g->nleaf + 255) / 256, (u64)nsm * 8));
-        k_grid_parents<<<gl, 256, 0, s>>>(static_cast<const u64*>(g->leaf_lin.p), g->nleaf, d, rho, dst);
+        sk::launch(k_grid_parents, gl, 256, 0, s, static_cast<const u64*>(g->leaf_lin.p), g->nleaf, d, rho, dst);
       } else {
         const uint32_t* src = static_cast<const uint32_t*>(g->occ[L + 1].p);
         const u64 sw = words_of(L + 1, d);
         if (L >= 5) {
           const unsigned gw = (unsigned)std::max<u64>(1, std::min<u64>((words + 255) / 256, (u64)nsm * 8));
-          sk::k_downsample_words<<<gw, 256, 0, s>>>(src, L, d, words, dst);
+          sk::launch(sk::k_downsample_words, gw, 256, 0, s, src, L, d, words, dst);
         } else {
           const unsigned gw = (unsigned)std::max<u64>(1, std::min<u64>((sw + 255) / 256, (u64)nsm * 8));
-          sk::k_downsample<<<gw, 256, 0, s>>>(src, L, d, sw, dst);
+          sk::launch(sk::k_downsample, gw, 256, 0, s, src, L, d, sw, dst);
         }
       }
       const unsigned gp = (unsigned)std::max<u64>(1, std::min<u64>((words + 255) / 256, (u64)nsm * 8));
-      k_grid_popc<<<gp, 256, 0, s>>>(dst, words, cnt + L);
+      sk::launch(k_grid_popc, gp, 256, 0, s, dst, words, cnt + L);
     }
     ck(cudaGetLastError(), "kernel launch");
     ck(cudaMemcpyAsync(g->nonempty.data(), cnt, 8 * rho, cudaMemcpyDeviceToHost, s), "D2H");
@@ -342,10 +351,10 @@ int skycell_gpu_grid_nonempty_cells(skycell_gpu_grid* g, int layer, uint64_t* li
     ensure(bc, (u64)blocks * 4);
     ensure(tot, 8);
     ensure(ids32, m * 4);
-    sk::k_bits_count<<<blocks, sk::kBitsThreads>>>(static_cast<const uint32_t*>(g->occ[layer].p), words,
+    sk::launch(sk::k_bits_count, blocks, sk::kBitsThreads, 0, 0, static_cast<const uint32_t*>(g->occ[layer].p), words,
                                                    static_cast<unsigned*>(bc.p));
-    sk::k_bits_scan<<<1, 1024>>>(static_cast<unsigned*>(bc.p), blocks, static_cast<u64*>(tot.p));
-    sk::k_bits_write<<<blocks, sk::kBitsThreads>>>(static_cast<const uint32_t*>(g->occ[layer].p), words,
+    sk::launch(sk::k_bits_scan, 1, 1024, 0, 0, static_cast<unsigned*>(bc.p), blocks, static_cast<u64*>(tot.p));
+    sk::launch(sk::k_bits_write, blocks, sk::kBitsThreads, 0, 0, static_cast<const uint32_t*>(g->occ[layer].p), words,
                                                    static_cast<const unsigned*>(bc.p),
                                                    static_cast<uint32_t*>(ids32.p), 0);
     ck(cudaGetLastError(), "kernel launch");
@@ -377,7 +386,7 @@ int skycell_gpu_grid_lookup(skycell_gpu_grid* g, int layer, const uint64_t* lin,
       ensure(oe, count * 4);
     }
     const unsigned gq = (unsigned)std::max<u64>(1, std::min<u64>((count + 255) / 256, 1184));
-    k_grid_lookup<<<gq, 256>>>(static_cast<const u64*>(q.p), count, static_cast<const u64*>(g->leaf_lin.p), g->nleaf,
+    sk::launch(k_grid_lookup, gq, 256, 0, 0, static_cast<const u64*>(q.p), count, static_cast<const u64*>(g->leaf_lin.p), g->nleaf,
                                static_cast<const uint32_t*>(g->leaf_begin.p), static_cast<const uint32_t*>(g->leaf_end.p),
                                layer == g->rho ? nullptr : static_cast<const uint32_t*>(g->occ[layer].p),
                                static_cast<uint32_t*>(ob.p), static_cast<uint32_t*>(oe.p), static_cast<uint8_t*>(oo.p));

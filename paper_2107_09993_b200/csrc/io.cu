@@ -33,6 +33,7 @@ constexpr size_t kIoChunk = 64ull << 20;  // bytes per pinned staging chunk
 // v[0 .. count), the first of which belongs to dimension 0.  A thread's
 // values all share one dimension (its stride is a multiple of d).
 static __global__ void k_minmax_rows(const double* __restrict__ v, u64 count, int d, u64* __restrict__ mm) {
+  sk::pdl_enter();
   const u64 tid = blockIdx.x * (u64)blockDim.x + threadIdx.x;
   const u64 total = (u64)gridDim.x * blockDim.x;
   const u64 stride = total / d * d;
@@ -145,7 +146,7 @@ int skycell_gpu_read_bin(skycell_gpu_ctx* ctx, const char* path, double* dev_coo
       if (std::fread(pin[bi], 8, cnt, fc.f) != cnt) throw ApiFail{SKYCELL_INPUT, std::string(path) + ": truncated file"};
       ck(cudaMemcpyAsync(dev_coords + at, pin[bi], cnt * 8, cudaMemcpyHostToDevice, s), "H2D");
       ck(cudaEventRecord(done[bi], s), "event");
-      k_minmax_rows<<<g, 256, 0, s>>>(dev_coords + at, cnt, d, mm);
+      sk::launch(k_minmax_rows, g, 256, 0, s, dev_coords + at, cnt, d, mm);
       at += cnt;
       bi ^= 1;
     }

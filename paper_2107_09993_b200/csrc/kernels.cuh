@@ -175,6 +175,7 @@ struct SampleParams {
 
 template <typename TIn, typename TOut, int D, bool IDENT>
 __global__ void __launch_bounds__(256) k_sample(SampleParams p) {
+  pdl_enter();
   const TIn* coords = static_cast<const TIn*>(p.coords);
   const int top = (1 << p.rho) - 1;
   const float fscale = ldexpf(1.0f, p.rho);
@@ -206,6 +207,7 @@ __global__ void __launch_bounds__(256) k_sample(SampleParams p) {
 // the multi-CTA table kernels): H[x] = all x_k >= 1 ? PM[x - 1] : none.
 static __global__ void k_filter_from_table(const uint8_t* __restrict__ PM, int lf, int d, uint32_t rows,
                                     uint8_t* __restrict__ H) {
+  pdl_enter();
   const uint32_t mask = (1u << lf) - 1;
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
     bool ok = true;
@@ -325,6 +327,7 @@ __device__ __forceinline__ uint32_t mag_col(float u, float scale) {
 // so one 768-thread CTA per SM).  Otherwise they record their level la-1 cell.
 template <typename TIn, typename TOut, int D, bool IDENT, int THREADS, int PPT, int RHO, int MINB = 3, bool REC_LA = false>
 __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
+  pdl_enter();
   static_assert(PPT <= 8, "survivor codes are (j * 32 + lane) in one byte");
   extern __shared__ __align__(16) uint8_t sm[];
   uint32_t* occ_s = reinterpret_cast<uint32_t*>(sm);
@@ -580,6 +583,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
 // (slabs x words) reduction runs on many CTAs; one red.or per word and group.
 static __global__ void k_reduce_slabs(const uint32_t* __restrict__ slabs, int nslabs, uint32_t words,
                                uint32_t* __restrict__ out) {
+  pdl_enter();
   const int per = (nslabs + gridDim.y - 1) / gridDim.y;
   const int s0 = blockIdx.y * per, s1 = min(nslabs, s0 + per);
   for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x) {
@@ -598,6 +602,7 @@ static __global__ void k_reduce_slabs(const uint32_t* __restrict__ slabs, int ns
 // build (4,096 lines at d=4, L=6: 24 us).
 template <typename TT>
 __global__ void k_rowmin_prefix1w(const uint32_t* __restrict__ bits, int L, u64 lines, TT* __restrict__ R) {
+  pdl_enter();
   const int n = 1 << L;
   const int rowbits = 1 << L;
   const int lane = threadIdx.x & 31;
@@ -643,6 +648,7 @@ __global__ void k_rowmin_prefix1w(const uint32_t* __restrict__ bits, int L, u64 
 // e.g. d = 2 at fine layers, which one CTA per line then scans).
 template <typename TT>
 __global__ void k_rowmin(const uint32_t* __restrict__ bits, int L, u64 rows, TT* __restrict__ R) {
+  pdl_enter();
   const int rowbits = 1 << L;
   for (u64 r = blockIdx.x * (u64)blockDim.x + threadIdx.x; r < rows; r += (u64)gridDim.x * blockDim.x) {
     TT best = (TT)~(TT)0;
@@ -669,6 +675,7 @@ __global__ void k_rowmin(const uint32_t* __restrict__ bits, int L, u64 rows, TT*
 // scan of the run minima, then the runs are rewritten.
 template <typename TT>
 __global__ void __launch_bounds__(1024) k_prefix_min_cta(TT* __restrict__ R, int L, int k, u64 lines) {
+  pdl_enter();
   __shared__ TT wmin[32];
   const u64 stride = 1ull << (L * (k - 1));
   const int n = 1 << L;
@@ -724,6 +731,7 @@ __global__ void __launch_bounds__(1024) k_prefix_min_cta(TT* __restrict__ R, int
 // chunks of 32 with a carry.
 template <typename TT>
 __global__ void k_prefix_minw(TT* __restrict__ R, int L, int k, u64 lines) {
+  pdl_enter();
   const u64 stride = 1ull << (L * (k - 1));
   const int n = 1 << L;
   const int lane = threadIdx.x & 31;
@@ -750,6 +758,7 @@ __global__ void k_prefix_minw(TT* __restrict__ R, int L, int k, u64 lines) {
 
 template <typename TT>
 __global__ void k_prefix_min(TT* __restrict__ R, int L, int k, u64 lines) {
+  pdl_enter();
   const u64 stride = 1ull << (L * (k - 1));
   const int n = 1 << L;
   for (u64 line = blockIdx.x * (u64)blockDim.x + threadIdx.x; line < lines; line += (u64)gridDim.x * blockDim.x) {
@@ -789,6 +798,7 @@ __global__ void k_prefix_min(TT* __restrict__ R, int L, int k, u64 lines) {
 template <typename TT>
 __global__ void k_count_rows(const uint32_t* __restrict__ bits, int L, int d, u64 rows, const TT* __restrict__ PM,
                              u64* cand_out, u64* key_out) {
+  pdl_enter();
   const int n0 = 1 << L, top = n0 - 1;
   const u64 mask = (u64)top;
   const TT none = (TT)~(TT)0;
@@ -859,6 +869,7 @@ __global__ void k_count_rows(const uint32_t* __restrict__ bits, int L, int d, u6
 // OR them, fold bit pairs, gather the even bits: one 32-bit word, no atomics.
 static __global__ void k_downsample_words(const uint32_t* __restrict__ src, int L, int d, u64 dst_words,
                                    uint32_t* __restrict__ dst) {
+  pdl_enter();
   const u64 wpr = (1ull << L) >> 5, wpr_f = wpr * 2;
   const u64 mask = (1ull << L) - 1;
   for (u64 w = blockIdx.x * (u64)blockDim.x + threadIdx.x; w < dst_words; w += (u64)gridDim.x * blockDim.x) {
@@ -887,6 +898,7 @@ static __global__ void k_downsample_words(const uint32_t* __restrict__ src, int 
 // Occupancy of layer L from layer L+1 (grid.cpp:80-102, child-OR), OR-ed into dst.
 static __global__ void k_downsample(const uint32_t* __restrict__ src, int L, int d, u64 src_words,
                              uint32_t* __restrict__ dst) {
+  pdl_enter();
   const u64 mask = (1ull << (L + 1)) - 1;
   for (u64 w = blockIdx.x * (u64)blockDim.x + threadIdx.x; w < src_words; w += (u64)gridDim.x * blockDim.x) {
     uint32_t x = src[w];
@@ -964,6 +976,7 @@ struct CandParams {
 
 template <typename T, int D, typename TT, int THREADS>
 __global__ void __launch_bounds__(THREADS) k_candidates(CandParams p) {
+  pdl_enter();
   extern __shared__ __align__(16) uint8_t smc[];
   const u64 n = p.count ? *p.count : p.count_const;
   uint32_t nf = 0;
@@ -1127,6 +1140,7 @@ constexpr uint32_t kK4aHead = SKY_K4A_HEAD;
 
 template <typename T, int D, typename TT, int THREADS>
 __global__ void __launch_bounds__(THREADS) k_cand_head(CandParams p) {
+  pdl_enter();
   extern __shared__ __align__(16) uint8_t smc[];
   constexpr int kRing = 64;
   constexpr uint32_t kHead0 = kK4aHead;
@@ -1255,6 +1269,7 @@ __global__ void k_compact_members(const T* __restrict__ rows, const uint32_t* __
                                   const uint8_t* __restrict__ flag, const u64* __restrict__ fsum,
                                   const u64* __restrict__ count, T* __restrict__ out_rows, u64* __restrict__ out_fsum,
                                   u64* __restrict__ out_count) {
+  pdl_enter();
   const u64 n = *count;
   const int lane = threadIdx.x & 31;
   for (u64 wb = ((blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5) * 32; wb < n;
@@ -1286,6 +1301,7 @@ __global__ void __launch_bounds__(1024) k_strength_order(const T* __restrict__ r
                                                           uint32_t f_max, T* __restrict__ out_rows,
                                                           u64* __restrict__ out_fsum, uint32_t* __restrict__ out_ids,
                                                           u64* __restrict__ out_count) {
+  pdl_enter();
   // ids (optional): empty slots (kNoId) are skipped; out_ids (optional)
   __shared__ unsigned hist[65];
   __shared__ unsigned offs[65];
@@ -1331,6 +1347,7 @@ template <typename T, int D>
 __global__ void __launch_bounds__(1024) k_filter_lists(const T* __restrict__ f_rows, const u64* __restrict__ f_count,
                                                         uint32_t f_max, uint16_t* __restrict__ f_lists,
                                                         uint16_t* __restrict__ f_offs) {
+  pdl_enter();
   using Sort = cub::BlockRadixSort<uint32_t, 1024, 1>;
   __shared__ typename Sort::TempStorage tmp;
   __shared__ unsigned cnt[kListCols + 1];
@@ -1382,6 +1399,7 @@ __device__ __forceinline__ int list_bin(int b, int c) { return c * kSumBuckets +
 template <typename T, int D>
 __global__ void k_list_hist(const T* __restrict__ rows, const uint32_t* __restrict__ ids, const u64* __restrict__ fsum,
                             const u64* __restrict__ count, unsigned* __restrict__ hist) {
+  pdl_enter();
   const u64 n = *count;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
     if (ids[i] == kNoId) continue;
@@ -1413,6 +1431,7 @@ __device__ __forceinline__ unsigned* scan_array(unsigned* hist, int y, int D, in
 
 static __global__ void __launch_bounds__(1024) k_list_scan_sums(unsigned* __restrict__ hist, int D,
                                                           unsigned* __restrict__ totals, const u64* __restrict__ gate) {
+  pdl_enter();
   __shared__ unsigned warp_tot[32];
   if (gate && *gate == 0) return;  // the set goes to the tree (run_dominance)
   int len;
@@ -1434,6 +1453,7 @@ static __global__ void __launch_bounds__(1024) k_list_scan_sums(unsigned* __rest
 
 static __global__ void __launch_bounds__(1024) k_list_scan(unsigned* __restrict__ hist, unsigned* __restrict__ cursor, int D,
                                                      const unsigned* __restrict__ totals, const u64* __restrict__ gate) {
+  pdl_enter();
   __shared__ unsigned tile[kScanChunk + kScanChunk / 32];  // one pad word per 32 entries
   __shared__ unsigned warp_tot[32];
   if (gate && *gate == 0) return;
@@ -1491,6 +1511,7 @@ template <typename T, int D>
 __global__ void k_list_scatter(const T* __restrict__ rows, const uint32_t* __restrict__ ids,
                                const u64* __restrict__ fsum, const u64* __restrict__ count,
                                unsigned* __restrict__ cursor, uint32_t* __restrict__ lists, u64 cap) {
+  pdl_enter();
   const u64 n = *count;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
     if (ids[i] == kNoId) continue;
@@ -1580,6 +1601,7 @@ __global__ void __launch_bounds__(256) k_allpairs_lists(const T* __restrict__ ro
                                                         const u64* __restrict__ q_end, int cell_level,
                                                         unsigned max_steps, uint32_t* __restrict__ long_q,
                                                         u64* __restrict__ long_n, const u64* __restrict__ gate) {
+  pdl_enter();
   if (gate && *gate == 0) return;
   const u64 n = q_end ? *q_end : *count;
   const int lane = threadIdx.x & 31;
@@ -1649,6 +1671,7 @@ __global__ void __launch_bounds__(256) k_allpairs_long(const T* __restrict__ row
                                                        uint8_t* __restrict__ flag, int cell_level,
                                                        const uint32_t* __restrict__ long_q,
                                                        const u64* __restrict__ long_n) {
+  pdl_enter();
   __shared__ int found;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int ctop = (1 << cell_level) - 1;
@@ -1715,6 +1738,7 @@ constexpr u64 kBitsBlock = (u64)kBitsThreads * kBitsPer;
 
 static __global__ void k_mark_ids(const uint32_t* __restrict__ ids, const uint8_t* __restrict__ flag,
                            const u64* __restrict__ count, uint32_t* __restrict__ bits, uint32_t base) {
+  pdl_enter();
   const u64 n = *count;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
     const uint32_t id = ids[i];
@@ -1727,6 +1751,7 @@ static __global__ void k_mark_ids(const uint32_t* __restrict__ ids, const uint8_
 
 static __global__ void __launch_bounds__(kBitsThreads) k_bits_count(const uint32_t* __restrict__ bits, u64 words,
                                                              unsigned* __restrict__ block_counts) {
+  pdl_enter();
   const u64 b0 = blockIdx.x * kBitsBlock;
   unsigned c = 0;
 #pragma unroll
@@ -1749,6 +1774,7 @@ static __global__ void __launch_bounds__(kBitsThreads) k_bits_count(const uint32
 // Single CTA: exclusive scan of the block counts; total -> *out_count.
 static __global__ void __launch_bounds__(1024) k_bits_scan(unsigned* __restrict__ block_counts, unsigned nblocks,
                                                     u64* __restrict__ out_count) {
+  pdl_enter();
   __shared__ unsigned part[1024];
   const unsigned per = (nblocks + 1023) / 1024;
   unsigned sum = 0;
@@ -1779,6 +1805,7 @@ static __global__ void __launch_bounds__(1024) k_bits_scan(unsigned* __restrict_
 static __global__ void __launch_bounds__(kBitsThreads) k_bits_write(const uint32_t* __restrict__ bits, u64 words,
                                                              const unsigned* __restrict__ block_offs,
                                                              uint32_t* __restrict__ out_ids, uint32_t base) {
+  pdl_enter();
   // thread t owns words b0 + t*kBitsPer .. +kBitsPer-1 (contiguous, so the
   // block-local exclusive scan over threads preserves id order)
   const u64 w0 = blockIdx.x * kBitsBlock + (u64)threadIdx.x * kBitsPer;
@@ -1817,6 +1844,7 @@ static __global__ void __launch_bounds__(kBitsThreads) k_bits_write(const uint32
 // (and reports non-finite records) before the grid rejects rho.
 template <typename TIn>
 __global__ void k_check_finite(const TIn* __restrict__ coords, u64 total, int d, u64* nonfinite) {
+  pdl_enter();
   for (u64 e = blockIdx.x * (u64)blockDim.x + threadIdx.x; e < total; e += (u64)gridDim.x * blockDim.x) {
     if (!finite_v(coords[e])) atomicMax(nonfinite, ~(e / d));
   }
@@ -1827,6 +1855,7 @@ __global__ void k_check_finite(const TIn* __restrict__ coords, u64 total, int d,
 // reduction NCCL lacks (nccl.h:260-275), applied to the all-gathered
 // occupancy region of every rank.  uint4 words: 16 B per load.
 static __global__ void k_or_gather(const uint4* __restrict__ gathered, int world, u64 words4, uint4* __restrict__ dst) {
+  pdl_enter();
   for (u64 w = blockIdx.x * (u64)blockDim.x + threadIdx.x; w < words4; w += (u64)gridDim.x * blockDim.x) {
     uint4 x = gathered[w];
     for (int g = 1; g < world; ++g) {
@@ -1844,6 +1873,7 @@ static __global__ void k_or_gather(const uint4* __restrict__ gathered, int world
 // srcs[g] is device g's exported occupancy region, read in place over NVLink
 // / NVSwitch (peer access); no gather buffer, one pass.
 static __global__ void k_or_peers(const uint4* const* __restrict__ srcs, int world, u64 words4, uint4* __restrict__ dst) {
+  pdl_enter();
   for (u64 w = blockIdx.x * (u64)blockDim.x + threadIdx.x; w < words4; w += (u64)gridDim.x * blockDim.x) {
     uint4 x = srcs[0][w];
     for (int g = 1; g < world; ++g) {
@@ -1864,6 +1894,7 @@ __global__ void k_pack_members(const T* __restrict__ rows, const uint32_t* __res
                                const uint8_t* __restrict__ flag, const u64* __restrict__ fsum,
                                const u64* __restrict__ count, T* __restrict__ out_rows, u64* __restrict__ out_fsum,
                                uint32_t* __restrict__ out_ids, u64* __restrict__ out_count) {
+  pdl_enter();
   const u64 n = *count;
   const int lane = threadIdx.x & 31;
   for (u64 wb = ((blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5) * 32; wb < n;
@@ -1893,15 +1924,28 @@ __global__ void k_pack_members(const T* __restrict__ rows, const uint32_t* __res
 // S2 and K4b has nothing to do.
 static __global__ void k_filter_gate(const u64* __restrict__ sky, const u64* __restrict__ cands,
                                      u64* __restrict__ weak) {
+  pdl_enter();
   *weak = *sky * 4 > *cands;
 }
 
 // K5 dispatch without a host round trip: the column lists run on
 // *lcount = the set's slot count when its point count is at most tree_min,
 // else on 0 (the tree takes the set, launched once the host has the count).
+// host: mapped pinned memory the host reads after an event (no copy-engine
+// round trip in the stream: the lists launched next start at once).
 static __global__ void k_gate_count(const u64* __restrict__ points, const u64* __restrict__ slots, u64 tree_min,
-                                    const u64* __restrict__ origins, u64* __restrict__ lcount) {
-  *lcount = (*origins == 0 && *points <= tree_min) ? *slots : 0;
+                                    const u64* __restrict__ origins, u64* __restrict__ lcount, u64* host) {
+  pdl_enter();
+  const u64 p = *points, o = *origins;
+  *lcount = (o == 0 && p <= tree_min) ? *slots : 0;
+  host[0] = p;
+  host[1] = o;
+}
+
+// Device -> mapped pinned host words (the query's counters at the end).
+static __global__ void k_copy_words(const u64* __restrict__ src, u64* dst, unsigned n) {
+  pdl_enter();
+  for (unsigned i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
 
 // Exact origins (FP64 sum 0: every normalised coordinate 0 -- correlated
@@ -1910,6 +1954,7 @@ static __global__ void k_gate_count(const u64* __restrict__ points, const u64* _
 // one is decided in O(n): members are exactly its origins.
 static __global__ void k_origin_count(const uint32_t* __restrict__ ids, const u64* __restrict__ fsum,
                                       const u64* __restrict__ count, u64* __restrict__ origins) {
+  pdl_enter();
   const u64 n = *count;
   unsigned c = 0;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
@@ -1922,6 +1967,7 @@ static __global__ void k_origin_count(const uint32_t* __restrict__ ids, const u6
 static __global__ void k_origin_flags(const uint32_t* __restrict__ ids, const u64* __restrict__ fsum,
                                       const u64* __restrict__ count, u64 q_begin, const u64* __restrict__ q_end,
                                       const u64* __restrict__ origins, uint8_t* __restrict__ flag) {
+  pdl_enter();
   if (*origins == 0) return;
   const u64 n = q_end ? *q_end : *count;
   for (u64 i = q_begin + blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
@@ -1929,10 +1975,12 @@ static __global__ void k_origin_flags(const uint32_t* __restrict__ ids, const u6
 }
 
 static __global__ void k_clamp_count(const u64* __restrict__ src, u64 cap, u64* __restrict__ dst) {
+  pdl_enter();
   if (threadIdx.x == 0) *dst = *src < cap ? *src : cap;
 }
 
 static __global__ void k_fill_u32(uint32_t* __restrict__ p, u64 count, uint32_t v) {
+  pdl_enter();
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < count; i += (u64)gridDim.x * blockDim.x) p[i] = v;
 }
 
@@ -1943,6 +1991,7 @@ static __global__ void k_fill_u32(uint32_t* __restrict__ p, u64 count, uint32_t 
 // which is the reference's original_ids vector.
 template <int D>
 __global__ void k_quadrant_mark(const double* __restrict__ coords, u64 n, Norm origin, uint32_t* __restrict__ bits) {
+  pdl_enter();
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
     double v[D];
     load_row_cached<double, D>(coords, i, v);
@@ -1971,6 +2020,7 @@ __host__ __device__ inline double dkey_inv(u64 k) {
 template <int D>
 __global__ void k_quadrant_gather(const double* __restrict__ coords, const uint32_t* __restrict__ orig,
                                   const u64* __restrict__ count, double* __restrict__ sub, u64* __restrict__ mm) {
+  pdl_enter();
   const u64 n = *count;
   u64 lo[D], hi[D];
 #pragma unroll
@@ -2007,6 +2057,7 @@ __global__ void k_quadrant_gather(const double* __restrict__ coords, const uint3
 
 // ids[j] = orig[ids[j]] (refine.cpp:182): ascending stays ascending.
 static __global__ void k_map_ids(uint32_t* __restrict__ ids, const uint32_t* __restrict__ orig, u64 n) {
+  pdl_enter();
   for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x) ids[j] = orig[ids[j]];
 }
 

@@ -77,6 +77,7 @@ __device__ __forceinline__ void pk_store_point(uint32_t* __restrict__ rec, const
 template <typename T, int D>
 __global__ void k_pk_gather(const T* __restrict__ rows, const uint32_t* __restrict__ ids, const u64* __restrict__ fsum,
                             const uint32_t* __restrict__ order, u64 m, uint32_t* __restrict__ prec) {
+  pdl_enter();
   typedef PkLayout<T, D> L;
   for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < m; j += (u64)gridDim.x * blockDim.x) {
     const uint32_t i = order[j];
@@ -108,6 +109,7 @@ __device__ __forceinline__ K shfl_max(K a) {
 // One warp per leaf: box (lo, hi + 1) and champion of its points.
 template <typename T, int D>
 __global__ void k_pk_leaves(const uint32_t* __restrict__ prec, u64 m, u64 nleaf, uint32_t* __restrict__ nrec) {
+  pdl_enter();
   typedef PkLayout<T, D> L;
   typedef typename L::K K;
   const int lane = threadIdx.x & 31;
@@ -159,6 +161,7 @@ __global__ void k_pk_leaves(const uint32_t* __restrict__ prec, u64 m, u64 nleaf,
 // Level h from level h-1 (fan-out F = tree_fanout<D>()).
 template <typename T, int D>
 __global__ void k_pk_level(uint32_t* __restrict__ nrec, u64 child_off, u64 nchild, u64 node_off, u64 nnode) {
+  pdl_enter();
   typedef PkLayout<T, D> L;
   typedef typename L::K K;
   constexpr int F = tree_fanout<D>();
@@ -235,6 +238,7 @@ __global__ void __launch_bounds__(256, 4) k_pk_query(const uint32_t* __restrict_
                                                   const uint32_t* __restrict__ list, const u64* __restrict__ list_n,
                                                   const uint32_t* __restrict__ qrec, uint8_t* __restrict__ flag,
                                                   u64* __restrict__ vstats) {
+  pdl_enter();
   constexpr bool PHASE2 = MODE != 0;
   typedef PkLayout<T, D> L;
   typedef typename L::K K;
@@ -504,11 +508,13 @@ namespace sk {
 // Phase-1 -> phase-2 compaction: per-packet undecided counts, their exclusive
 // scan (CUB), then the positions of the undecided lanes in Z-order.
 static __global__ void k_pk_counts(const uint32_t* __restrict__ umask, u64 npk, uint32_t* __restrict__ cnt) {
+  pdl_enter();
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < npk; i += (u64)gridDim.x * blockDim.x)
     cnt[i] = __popc(umask[i]);
 }
 static __global__ void k_pk_list(const uint32_t* __restrict__ umask, const uint32_t* __restrict__ off, u64 npk,
                                  uint32_t* __restrict__ list, u64* __restrict__ list_n) {
+  pdl_enter();
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < npk; i += (u64)gridDim.x * blockDim.x) {
     uint32_t m = umask[i];
     uint32_t o = off[i];

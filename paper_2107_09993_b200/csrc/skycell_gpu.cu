@@ -55,7 +55,7 @@ template <typename TIn>
 void reject_rho(skycell_gpu_ctx* ctx, const void* dev_coords, u64 n, int d, const Status& rs, u64 id_base) {
   ensure(ctx->reset, 256);
   ck(cudaMemsetAsync(ctx->reset.p, 0, 8, ctx->stream), "memset");
-  sk::k_check_finite<TIn><<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(static_cast<const TIn*>(dev_coords), n * d, d,
+  sk::launch(sk::k_check_finite<TIn>, ctx->num_sms * 4, 256, 0, ctx->stream, static_cast<const TIn*>(dev_coords), n * d, d,
                                                                       static_cast<u64*>(ctx->reset.p));
   u64 nf = 0;
   ck(cudaMemcpyAsync(&nf, ctx->reset.p, 8, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
@@ -186,11 +186,11 @@ void quadrant_launch(skycell_gpu_ctx* ctx, const double* dev, u64 n, const sk::N
   uint32_t* bits = static_cast<uint32_t*>(ctx->q_bits.p);
   unsigned* bcount = reinterpret_cast<unsigned*>(bits + id_words);
   const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((n + 255) / 256, (u64)nsm * 8));
-  sk::k_quadrant_mark<D><<<g, 256, 0, s>>>(dev, n, org, bits);
-  sk::k_bits_count<<<blocks, sk::kBitsThreads, 0, s>>>(bits, id_words, bcount);
-  sk::k_bits_scan<<<1, 1024, 0, s>>>(bcount, blocks, d_count);
-  sk::k_bits_write<<<blocks, sk::kBitsThreads, 0, s>>>(bits, id_words, bcount, static_cast<uint32_t*>(ctx->q_orig.p), 0);
-  sk::k_quadrant_gather<D><<<g, 256, 0, s>>>(dev, static_cast<const uint32_t*>(ctx->q_orig.p), d_count,
+  sk::launch(sk::k_quadrant_mark<D>, g, 256, 0, s, dev, n, org, bits);
+  sk::launch(sk::k_bits_count, blocks, sk::kBitsThreads, 0, s, bits, id_words, bcount);
+  sk::launch(sk::k_bits_scan, 1, 1024, 0, s, bcount, blocks, d_count);
+  sk::launch(sk::k_bits_write, blocks, sk::kBitsThreads, 0, s, bits, id_words, bcount, static_cast<uint32_t*>(ctx->q_orig.p), 0);
+  sk::launch(sk::k_quadrant_gather<D>, g, 256, 0, s, dev, static_cast<const uint32_t*>(ctx->q_orig.p), d_count,
                                              static_cast<double*>(ctx->q_sub.p), static_cast<u64*>(ctx->q_mm.p) + 2);
   ctx->launches += 5;
 }
@@ -216,8 +216,10 @@ int skycell_gpu_create(int device, skycell_gpu_ctx** out, char* err, size_t err_
     ck(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming), "event");
     ck(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming), "event");
-    ck(cudaMallocHost(reinterpret_cast<void**>(&ctx->host_ctr), sizeof(DevCounters)), "pinned");
-    ck(cudaMallocHost(reinterpret_cast<void**>(&ctx->host_param), 64), "pinned");
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&ctx->host_ctr), sizeof(DevCounters), cudaHostAllocMapped), "pinned");
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&ctx->host_param), 64, cudaHostAllocMapped), "pinned");
+    ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->host_ctr_dev), ctx->host_ctr, 0), "mapped");
+    ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->host_param_dev), ctx->host_param, 0), "mapped");
     ensure(ctx->long_n, 64);
     ensure(ctx->scan_tot, (size_t)2 * sk::kMaxD * sk::kScanChunks * 4);
     for (auto& e : ctx->ev) ck(cudaEventCreate(&e), "event");
@@ -337,7 +339,7 @@ int skycell_gpu_quadrant_f64(skycell_gpu_ctx* ctx, const double* coords, uint64_
     ctx->launches += prior;
     if (k) {
       const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((k + 255) / 256, (u64)ctx->num_sms * 8));
-      sk::k_map_ids<<<g, 256, 0, s>>>(sub_ids, static_cast<const uint32_t*>(ctx->q_orig.p), k);
+      sk::launch(sk::k_map_ids, g, 256, 0, s, sub_ids, static_cast<const uint32_t*>(ctx->q_orig.p), k);
       ++ctx->launches;
       ck(cudaGetLastError(), "kernel launch");
       if (is_device_ptr(ids_out)) ck(cudaMemcpyAsync(ids_out, sub_ids, k * 4, cudaMemcpyDeviceToDevice, s), "ids");
@@ -454,7 +456,7 @@ int skycell_gpu_generate_range(skycell_gpu_ctx* ctx, int dist, uint64_t n, int d
     const u64 b0 = begin / 65536, b1 = (begin + count + 65535) / 65536;
     const unsigned g = (unsigned)std::max<u64>(1, (b1 - b0 + 127) / 128);
 #define SKYCELL_GEN(DD) \
-  case DD: sk::k_generate<DD><<<g, 128, 0, ctx->stream>>>(dist, n, seed, kind, begin, count, dev_out); break;
+  case DD: sk::launch(sk::k_generate<DD>, g, 128, 0, ctx->stream, dist, n, seed, kind, begin, count, dev_out); break;
     switch (d) {
       SKYCELL_GEN(2) SKYCELL_GEN(3) SKYCELL_GEN(4) SKYCELL_GEN(5) SKYCELL_GEN(6) SKYCELL_GEN(7) SKYCELL_GEN(8)
       SKYCELL_GEN(9) SKYCELL_GEN(10) SKYCELL_GEN(11) SKYCELL_GEN(12) SKYCELL_GEN(13) SKYCELL_GEN(14)

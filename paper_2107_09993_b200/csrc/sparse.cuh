@@ -30,6 +30,7 @@ namespace sk {
 template <typename T, int D>
 __global__ void k_sp_keys(const T* __restrict__ rows, const uint32_t* __restrict__ ids, const u64* __restrict__ count,
                           int rho, u64* __restrict__ keys, uint32_t* __restrict__ vals) {
+  pdl_enter();
   const u64 n = *count;
   const int top = (1 << rho) - 1;
   const T scale = (T)(1u << rho);
@@ -48,6 +49,7 @@ __global__ void k_sp_keys(const T* __restrict__ rows, const uint32_t* __restrict
 }
 
 static __global__ void k_sp_heads(const u64* __restrict__ keys, u64 n, uint32_t* __restrict__ head) {
+  pdl_enter();
   for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x)
     head[j] = keys[j] != ~0ull && (j == 0 || keys[j] != keys[j - 1]);
 }
@@ -59,6 +61,7 @@ __global__ void k_sp_cells(const u64* __restrict__ keys, const uint32_t* __restr
                            const uint32_t* __restrict__ cpos, u64 n, int rho, float* __restrict__ crows,
                            u64* __restrict__ cfsum, uint32_t* __restrict__ cids, uint32_t* __restrict__ cstart,
                            u64* __restrict__ ncells, u64* __restrict__ nvalid) {
+  pdl_enter();
   const u64 mask = (1ull << rho) - 1;
   const float inv = ldexpf(1.0f, -rho);
   for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x) {
@@ -88,6 +91,7 @@ __global__ void k_sp_cells(const u64* __restrict__ keys, const uint32_t* __restr
 // cell has nothing strictly below it.
 template <int D>
 __global__ void k_sp_queries(const uint32_t* __restrict__ prec, u64 m, int rho, uint32_t* __restrict__ qrec) {
+  pdl_enter();
   typedef PkLayout<float, D> L;
   const float half = ldexpf(1.0f, -(rho + 1));
   for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < m; j += (u64)gridDim.x * blockDim.x) {
@@ -111,6 +115,7 @@ __global__ void k_sp_queries(const uint32_t* __restrict__ prec, u64 m, int rho, 
 // record -- a zero column -- are candidates: nothing is strictly below).
 static __global__ void k_sp_cand(const uint8_t* __restrict__ qflag, const uint32_t* __restrict__ qrec_ids, int pw,
                                  const uint32_t* __restrict__ order, u64 m, uint8_t* __restrict__ cand) {
+  pdl_enter();
   for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < m; j += (u64)gridDim.x * blockDim.x) {
     const bool inactive = qrec_ids[j * pw] == kNoId;
     cand[order[j]] = inactive ? 1 : qflag[j];
@@ -123,6 +128,7 @@ __global__ void k_sp_classify(const float* __restrict__ crows, const uint8_t* __
                               const uint8_t* __restrict__ cand, const uint32_t* __restrict__ cstart,
                               const u64* __restrict__ ncells, const u64* __restrict__ nvalid, int rho,
                               u64* __restrict__ n_key, u64* __restrict__ n_cand, u64* __restrict__ examined) {
+  pdl_enter();
   const u64 nc = *ncells;
   const float topv = (float)((1 << rho) - 1) * ldexpf(1.0f, -rho);
   u64 a = 0, b = 0, e = 0;
@@ -156,6 +162,7 @@ __global__ void k_sp_points(const T* __restrict__ rows, const uint32_t* __restri
                             const uint32_t* __restrict__ cpos, const uint8_t* __restrict__ cand, u64 n,
                             T* __restrict__ out_rows, uint32_t* __restrict__ out_ids, u64* __restrict__ out_fsum,
                             u64* __restrict__ out_reserved, unsigned chunk) {
+  pdl_enter();
   const u64 gw = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
   const u64 nw = ((u64)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;

@@ -89,6 +89,7 @@ template <typename T, int D>
 __global__ void k_cellmin_multi(const T* __restrict__ rows, const uint32_t* __restrict__ ids,
                                 const u64* __restrict__ fsum, const u64* __restrict__ count, int L, int passes,
                                 u64 cells, uint32_t* __restrict__ cm) {
+  pdl_enter();
   const u64 n = *count;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
     if (ids[i] == kNoId) continue;
@@ -115,6 +116,7 @@ __global__ void k_champ_kill_multi(const T* __restrict__ rows, const uint32_t* _
                                    u64 cells, const uint32_t* __restrict__ cm, u64 q_begin,
                                    const u64* __restrict__ q_end, uint8_t* __restrict__ kill, uint8_t* __restrict__ flag,
                                    u64* __restrict__ killed) {
+  pdl_enter();
   const u64 n = *count;
   const u64 qe = q_end ? *q_end : ~0ull;
   u64 mine = 0;
@@ -152,6 +154,7 @@ template <typename T, int D>
 __global__ void k_tree_keys(const T* __restrict__ rows, const uint32_t* __restrict__ ids, const u64* __restrict__ count,
                             const uint8_t* __restrict__ kill, u64* __restrict__ keys, uint32_t* __restrict__ vals,
                             u64* __restrict__ valid) {
+  pdl_enter();
   const u64 n = *count;
   u64 mine = 0;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
@@ -175,6 +178,7 @@ template <typename T, int D>
 __global__ void k_tree_gather(const T* __restrict__ rows, const uint32_t* __restrict__ ids, const u64* __restrict__ fsum,
                               const uint32_t* __restrict__ order, u64 m, T* __restrict__ srows,
                               uint32_t* __restrict__ sids, u64* __restrict__ sfsum) {
+  pdl_enter();
   for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < m; j += (u64)gridDim.x * blockDim.x) {
     const uint32_t i = order[j];
     T v[D];
@@ -205,6 +209,7 @@ __device__ __forceinline__ bool key_less(u64 as, uint32_t ai, u64 bs, uint32_t b
 template <typename T, int D>
 __global__ void k_tree_leaves(const T* __restrict__ srows, const uint32_t* __restrict__ sids,
                               const u64* __restrict__ sfsum, u64 m, u64 nleaf, TreeView<T, D> tv) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   for (u64 leaf = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; leaf < nleaf;
        leaf += ((u64)gridDim.x * blockDim.x) >> 5) {
@@ -259,6 +264,7 @@ __host__ __device__ constexpr int tree_fanout() {
 // the right edge).
 template <typename T, int D>
 __global__ void k_tree_level(TreeView<T, D> tv, u64 child_off, u64 nchild, u64 node_off, u64 nnode) {
+  pdl_enter();
   constexpr int F = tree_fanout<D>();
   for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < nnode; j += (u64)gridDim.x * blockDim.x) {
     const u64 a0 = child_off + F * j;
@@ -306,6 +312,7 @@ __global__ void __launch_bounds__(256) k_tree_query(const T* __restrict__ srows,
                                                     TreeView<T, D> tv, TreeShape sh, u64 q_begin,
                                                     const u64* __restrict__ q_end, int cell_level,
                                                     uint8_t* __restrict__ flag, u64* __restrict__ vstats) {
+  pdl_enter();
   constexpr int F = tree_fanout<D>();
   constexpr int kStack = 192;  // >= levels * (F - 1) + levels for every fan-out
   // stack entries: level << 27 | index within the level (nleaf < 2^27)
