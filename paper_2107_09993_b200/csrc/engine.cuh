@@ -116,8 +116,9 @@ struct skycell_gpu_ctx {
   cudaStream_t stream = nullptr;  // the stream every kernel is enqueued on
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_k0 = nullptr;  // K0's sample-skyline chain done (side stream, overlapped with K1)
   skyeng::DevBuf reset, slabs, H, table, table2, table_s, staging;
-  skyeng::DevBuf smp_rows, smp_ids, smp_fsum, f_rows, f_fsum, f_lists, f_offs, lists, ids_dev;
+  skyeng::DevBuf smp_rows, smp_ids, smp_fsum, f_rows, f_fsum, f_lists, f_offs, ids_dev;
   skyeng::DevBuf s1_rows, s1_ids, s2_rows, s2_ids, s2_fsum, flags;
   skyeng::DevBuf sky_rows, sky_ids, sky_fsum;  // local skyline (sharded)
   skyeng::DevBuf d_cells;                      // K1's D stream
@@ -130,6 +131,7 @@ struct skycell_gpu_ctx {
       sp_kflag, sp_cflag, sp_n, sp_qrec;  // sparse layer rho (sparse.cuh)
   int k5_mode = -1;  // 0 lists, 1 tree (packet query), 2 auto, 3 tree (point query); SKYCELL_K5
   skyeng::DevBuf long_q, long_n;  // K5 phase-B queue
+  skyeng::DevBuf l_rows, l_sums, l_ids;  // K5 column lists (entries materialised per dimension)
   skyeng::DevBuf scan_tot;        // K5 list-scan chunk totals
   skyeng::DevCounters* host_ctr = nullptr;  // pinned
   u64* host_param = nullptr;        // pinned H2D staging
@@ -305,26 +307,33 @@ void launch_count(skycell_gpu_ctx* ctx, cudaStream_t s, const uint32_t* bits, in
 template <typename TOut, int D>
 void run_exact(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uint32_t* ids, const u64* fsum,
                const u64* count, u64 cap, unsigned* hist, unsigned* cursor, u64 q_begin = 0,
-               const u64* q_end = nullptr, int cell_level = 0, const u64* gate = nullptr) {
+               const u64* q_end = nullptr, int cell_level = 0, const u64* gate = nullptr, u64 lcap = 0) {
   const int nsm = ctx->num_sms;
   const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((cap + 255) / 256, (u64)nsm * 8));
   const TOut* trows = static_cast<const TOut*>(rows);
-  uint32_t* lists = static_cast<uint32_t*>(ctx->lists.p);
+  // list entries: at most the set's points (gated: at most the gate's limit)
+  if (lcap == 0 || lcap > cap) lcap = cap;
+  lcap = std::max<u64>(lcap, 1);
+  ensure(ctx->l_rows, (size_t)D * lcap * D * sizeof(TOut));
+  ensure(ctx->l_sums, (size_t)D * lcap * 8);
+  ensure(ctx->l_ids, (size_t)D * lcap * 4);
+  sk::ListArrays<TOut, D> la{static_cast<TOut*>(ctx->l_rows.p), static_cast<u64*>(ctx->l_sums.p),
+                             static_cast<uint32_t*>(ctx->l_ids.p), lcap};
   sk::launch(sk::k_list_hist<TOut, D>, g, 256, 0, s, trows, ids, fsum, count, hist);
   unsigned* totals = static_cast<unsigned*>(ctx->scan_tot.p);
   sk::launch(sk::k_list_scan_sums, dim3(sk::kScanChunks, D), 1024, 0, s, hist, D, totals, gate);
   sk::launch(sk::k_list_scan, dim3(sk::kScanChunks, D), 1024, 0, s, hist, cursor, D, totals, gate);
   ++ctx->launches;
-  sk::launch(sk::k_list_scatter<TOut, D>, g, 256, 0, s, trows, ids, fsum, count, cursor, lists, cap);
+  sk::launch(sk::k_list_scatter<TOut, D>, g, 256, 0, s, trows, ids, fsum, count, cursor, la);
   const unsigned gw = (unsigned)std::max<u64>(1, std::min<u64>((cap * 32 + 255) / 256, (u64)nsm * 8));
   ensure(ctx->long_q, cap * 4);
   u64* long_n = static_cast<u64*>(ctx->long_n.p);
   fill_words(ctx, s, long_n, 2);
-  constexpr unsigned kMaxSteps = 8;  // phase A budget (4..64 swept: 4-8 best at C2 / C4 shards)
-  sk::launch(sk::k_allpairs_lists<TOut, D>, gw, 256, 0, s, trows, ids, fsum, count, lists, hist, cap,
+  constexpr unsigned kMaxSteps = 8;  // phase A budget in 32-entry steps (4..64 swept: 4-8 best at C2 / C4 shards)
+  sk::launch(sk::k_allpairs_lists<TOut, D>, gw, 256, 0, s, trows, ids, fsum, count, la, hist,
                                                    static_cast<uint8_t*>(ctx->flags.p), q_begin, q_end, cell_level,
                                                    kMaxSteps, static_cast<uint32_t*>(ctx->long_q.p), long_n, gate);
-  sk::launch(sk::k_allpairs_long<TOut, D>, nsm * 4, 256, 0, s, trows, ids, fsum, lists, hist, cap,
+  sk::launch(sk::k_allpairs_long<TOut, D>, nsm * 4, 256, 0, s, trows, ids, fsum, la, hist,
                                                        static_cast<uint8_t*>(ctx->flags.p), cell_level,
                                                        static_cast<const uint32_t*>(ctx->long_q.p), long_n);
   ctx->launches += 5;
@@ -593,7 +602,7 @@ void run_dominance(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const
     sk::launch(sk::k_gate_count, 1, 1, 0, s, vc, count, tree_min, org, lc, ctx->host_param_dev + 3);
     ck(cudaEventRecord(ctx->ev[8], s), "event");
     ctx->launches += 3;
-    run_exact<TOut, D>(ctx, s, rows, ids, fsum, lc, cap, hist, cursor, q_begin, q_end, cell_level, lc);
+    run_exact<TOut, D>(ctx, s, rows, ids, fsum, lc, cap, hist, cursor, q_begin, q_end, cell_level, lc, tree_min);
     ck(cudaEventSynchronize(ctx->ev[8]), "count");
     if (ctx->host_param[4] == 0 && ctx->host_param[3] > tree_min)
       run_tree<TOut, D>(ctx, s, rows, ids, fsum, count, valid_ctr, q_begin, q_end, cell_level, false);
@@ -642,6 +651,7 @@ struct Pipe final : PipeBase {
   size_t smem_pf;
   u64 id_words;
   unsigned bit_blocks;
+  bool k0_side = false;  // K0's sample-skyline chain runs on the side stream (joined before K4)
   bool k1_head = false;  // K1 ran the filter-point head (its D stream feeds K4's points_examined)
 
   // ---- zeroed region
@@ -703,9 +713,14 @@ struct Pipe final : PipeBase {
     int occ_blocks = 0;
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_blocks, kstream, k1_threads, smem1), "occupancy");
     occ_blocks = std::max(1, occ_blocks);
+    if (const char* e = std::getenv("SKYCELL_K1_CTAS")) occ_blocks = std::max(1, std::min(occ_blocks, std::atoi(e)));
     const u64 wtiles = (n + 32 * PPT1 - 1) / (32 * PPT1);
     const u64 wpc = (u64)k1_threads / 32;
     grid1 = (int)std::max<u64>(1, std::min<u64>((wtiles + wpc - 1) / wpc, (u64)nsm * occ_blocks));
+    if (q.merge && k0_overlap() && !k1_head_wanted()) {
+      // leave CTA slots free for K0's sample-skyline chain, which runs beside K1
+      if (const char* e = std::getenv("SKYCELL_K1_FREE")) grid1 = std::max(nsm, grid1 - std::atoi(e));
+    }
     cap1 = n + (u64)grid1 * (k1_threads / 32) * kChunk1;
 
     // K4 geometry
@@ -758,7 +773,6 @@ struct Pipe final : PipeBase {
     ensure(ctx->s2_ids, cap4 * 4);
     ensure(ctx->s2_fsum, cap4 * 8);
     ensure(ctx->flags, cap4);
-    ensure(ctx->lists, (size_t)D * cap4 * 4);
     ensure(ctx->ids_dev, n * 4);
   }
 
@@ -798,9 +812,37 @@ struct Pipe final : PipeBase {
         if (wide) launch_tables<uint32_t>(ctx, s, U(o_srho), rho, D, static_cast<uint32_t*>(ctx->table_s.p));
         else launch_tables<uint8_t>(ctx, s, U(o_srho), rho, D, static_cast<uint8_t*>(ctx->table_s.p));
       }
-      if (q.merge) {
-        // The sample skyline only serves as K4's point filter, which phase-1
-        // only semantics (merge_cross_cell = false) cannot use.
+    }
+    // The sample skyline only serves as K4's point filter, which phase-1
+    // only semantics (merge_cross_cell = false) cannot use.  K1 does not
+    // read it (unless its filter-point head is on), so with
+    // SKYCELL_K0_OVERLAP=1 it runs on the side stream behind K1's launch.
+    k0_side = q.merge && !k1_head_wanted() && k0_overlap();
+    if (q.merge && !k0_side) sample_chain(s);
+    // fork point: K0's sample buffers and tables are complete here
+    if (k0_side) ck(cudaEventRecord(ctx->ev_fork, s), "event");
+    launch_k1(c);
+    if (k0_side) sample_chain(s2);
+    if (q.timed) ck(cudaEventRecord(ctx->ev[1], s), "event");
+  }
+
+  static bool k0_overlap() {
+    static const bool v = [] { const char* e = std::getenv("SKYCELL_K0_OVERLAP"); return e && e[0] == '1'; }();
+    return v;
+  }
+  bool k1_head_wanted() const {
+    const char* he = std::getenv("SKYCELL_K1HEAD");
+    return q.merge && he && he[0] == '1';
+  }
+
+  // K0's sample skyline -> filter points F (+ their column lists), on stream st
+  void sample_chain(cudaStream_t st) {
+    DevCounters* c = ctr();
+    const bool side = st != s;
+    cudaStream_t s = st;  // every launch below goes to st
+    if (side) ck(cudaStreamWaitEvent(s, ctx->ev_fork, 0), "fork");
+    {
+      {
         tracer().mark(s, "K0: sample tables");
         // sample points not strictly dominated at layer rho -> X (s2 buffers)
         sk::CandParams pc{};
@@ -858,7 +900,10 @@ struct Pipe final : PipeBase {
         ctx->launches += 2;
       }
     }
+    if (side) ck(cudaEventRecord(ctx->ev_k0, s), "event");
+  }
 
+  void launch_k1(DevCounters* c) {
     // K1: the streaming pass
     sk::StreamParams p1{};
     p1.coords = q.dev_coords;
@@ -908,7 +953,6 @@ struct Pipe final : PipeBase {
                                                        occ(rec_la ? la : la - 1));
       ++ctx->launches;
     }
-    if (q.timed) ck(cudaEventRecord(ctx->ev[1], s), "event");
   }
 
   // ---- sharded exchange 1: the occupancy region of every layer
@@ -996,6 +1040,7 @@ struct Pipe final : PipeBase {
     }
     auto kc = wide ? sk::k_candidates<TOut, D, uint32_t, kThreads> : sk::k_candidates<TOut, D, uint8_t, kThreads>;
     ck(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pf), "smem attr");
+    if (k0_side) ck(cudaStreamWaitEvent(s, ctx->ev_k0, 0), "join K0");
     if (q.merge && !sparse) {
       // K4a: cell test + the 8 strongest filter points over S1 -> P (dense
       // pending points, in the S1 buffers' twin); K4b: the rest of the filter
@@ -1298,7 +1343,6 @@ struct Pipe final : PipeBase {
     ensure(ctx->s2_fsum, cap * 8);
     ensure(ctx->s2_ids, cap * 4);
     ensure(ctx->flags, cap);
-    ensure(ctx->lists, (size_t)D * cap * 4);
     const char* r = static_cast<const char*>(recv);
     const u64 bb = block_bytes(maxc);
     if (maxc) {

@@ -1507,21 +1507,38 @@ static __global__ void __launch_bounds__(1024) k_list_scan(unsigned* __restrict_
   }
 }
 
+// The lists hold the entries themselves (row, FP64 sum bits, id; one
+// structure-of-arrays copy per dimension), so a list scan step is one
+// coalesced read of consecutive entries instead of an index load followed by
+// a gather of random slots (two dependent L2 round trips per step).
+template <typename T, int D>
+struct ListArrays {
+  T* rows;         // [D][lcap][D]
+  u64* sums;       // [D][lcap]
+  uint32_t* ids;   // [D][lcap]
+  u64 lcap;
+};
+
 template <typename T, int D>
 __global__ void k_list_scatter(const T* __restrict__ rows, const uint32_t* __restrict__ ids,
                                const u64* __restrict__ fsum, const u64* __restrict__ count,
-                               unsigned* __restrict__ cursor, uint32_t* __restrict__ lists, u64 cap) {
+                               unsigned* __restrict__ cursor, ListArrays<T, D> la) {
   pdl_enter();
   const u64 n = *count;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
-    if (ids[i] == kNoId) continue;
+    const uint32_t id = ids[i];
+    if (id == kNoId) continue;
     T v[D];
     load_row_cached<T, D>(rows, i, v);
-    const int sb = sum_bucket<D>(fsum[i]);
+    const u64 fs = fsum[i];
+    const int sb = sum_bucket<D>(fs);
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       const unsigned pos = atomicAdd(&cursor[k * kListStride + list_bin(sb, list_col(v[k]))], 1u);
-      lists[(u64)k * cap + pos] = (uint32_t)i;
+      const u64 e = (u64)k * la.lcap + pos;
+      store_row<T, D>(la.rows, e, v);
+      la.sums[e] = fs;
+      la.ids[e] = id;
     }
   }
 }
@@ -1563,20 +1580,28 @@ struct ListQuery {
     }
     sb = sum_bucket<D>(ps);
   }
-  // lane's test of candidate list entry e (< end): q precedes and dominates p
-  __device__ __forceinline__ bool test(const T* __restrict__ rows, const uint32_t* __restrict__ ids,
-                                       const u64* __restrict__ fsum, const uint32_t* __restrict__ lst, unsigned e,
-                                       int cell_level, int ctop) const {
-    // independent gathers: sum, id and row are all in flight at once
-    const uint32_t q = __ldg(lst + e);
-    const u64 qs = __ldg(fsum + q);
-    const uint32_t qi = __ldg(ids + q);
+  // one list entry, loaded with a single round trip (row, sum, id independent)
+  struct Cand {
     T w[D];
-    load_row_cached<T, D>(rows, q, w);
-    bool d = precedes(qs, qi, ps, pid) && dominates<T, D>(w, v);
+    u64 qs;
+    uint32_t qi;
+  };
+  __device__ __forceinline__ void fetch(const ListArrays<T, D>& la, u64 base, unsigned e, bool ok, Cand& c) const {
+    if (ok) {
+      load_row_cached<T, D>(la.rows, base + e, c.w);
+      c.qs = __ldg(la.sums + base + e);
+      c.qi = __ldg(la.ids + base + e);
+    } else {
+      c.qi = kNoId;
+      c.qs = ~0ull;
+    }
+  }
+  // q precedes and dominates p
+  __device__ __forceinline__ bool check(const Cand& c, int cell_level, int ctop) const {
+    bool d = c.qi != kNoId && precedes(c.qs, c.qi, ps, pid) && dominates<T, D>(c.w, v);
     // merge_cross_cell = false (refine.cpp:98): phase-1 semantics only, a
     // dominator must share p's layer-rho cell
-    if (cell_level && d) d = same_cell<T, D>(w, v, cell_level, ctop);
+    if (cell_level && d) d = same_cell<T, D>(c.w, v, cell_level, ctop);
     return d;
   }
 };
@@ -1596,8 +1621,8 @@ struct ListQuery {
 template <typename T, int D>
 __global__ void __launch_bounds__(256) k_allpairs_lists(const T* __restrict__ rows, const uint32_t* __restrict__ ids,
                                                         const u64* __restrict__ fsum, const u64* __restrict__ count,
-                                                        const uint32_t* __restrict__ lists, const unsigned* __restrict__ offs,
-                                                        u64 cap, uint8_t* __restrict__ flag, u64 q_begin,
+                                                        ListArrays<T, D> la, const unsigned* __restrict__ offs,
+                                                        uint8_t* __restrict__ flag, u64 q_begin,
                                                         const u64* __restrict__ q_end, int cell_level,
                                                         unsigned max_steps, uint32_t* __restrict__ long_q,
                                                         u64* __restrict__ long_n, const u64* __restrict__ gate) {
@@ -1619,7 +1644,7 @@ __global__ void __launch_bounds__(256) k_allpairs_lists(const T* __restrict__ ro
     }
     ListQuery<T, D> Q;
     Q.init(rows, fsum, ids, offs, i);
-    const uint32_t* lst = lists + (u64)Q.bk * cap;
+    const u64 lb = (u64)Q.bk * la.lcap;
     const unsigned* ob = offs + Q.bk * kListStride;
     bool dom = false, deferred = false;
     unsigned steps = 0;
@@ -1628,7 +1653,7 @@ __global__ void __launch_bounds__(256) k_allpairs_lists(const T* __restrict__ ro
     // bounds of 32 columns are loaded at once (lane l: column c0 + l) and
     // only the non-empty ones are visited: sparse sets (anti-correlated d=2:
     // 1.4K points over 1,024 columns) otherwise spend a dependent load pair
-    // per empty column.
+    // per empty column.  Two 32-entry steps are in flight per iteration.
     for (int c0 = 0; c0 <= Q.pc && !dom && !deferred; c0 += 32) {
       const int cl = c0 + lane;
       unsigned b0 = 0, b1 = 0;
@@ -1641,13 +1666,17 @@ __global__ void __launch_bounds__(256) k_allpairs_lists(const T* __restrict__ ro
         const int src = __ffs(ne) - 1;
         ne &= ne - 1;
         const unsigned s0 = __shfl_sync(kFull, b0, src), s1 = __shfl_sync(kFull, b1, src);
-        for (unsigned base = s0; base < s1; base += 32) {
-          if (++steps > max_steps) {
+        for (unsigned base = s0; base < s1; base += 64) {
+          steps += 2;
+          if (steps > max_steps + 1) {
             deferred = true;
             break;
           }
-          const unsigned e = base + lane;
-          const bool d_l = e < s1 && Q.test(rows, ids, fsum, lst, e, cell_level, ctop);
+          const unsigned e0 = base + lane, e1 = e0 + 32;
+          typename ListQuery<T, D>::Cand ca, cb;
+          Q.fetch(la, lb, e0, e0 < s1, ca);
+          Q.fetch(la, lb, e1, e1 < s1, cb);
+          const bool d_l = Q.check(ca, cell_level, ctop) || Q.check(cb, cell_level, ctop);
           if (__any_sync(kFull, d_l)) {
             dom = true;
             break;
@@ -1662,12 +1691,13 @@ __global__ void __launch_bounds__(256) k_allpairs_lists(const T* __restrict__ ro
   }
 }
 
-// Phase B: one CTA per deferred point, its candidate steps dealt round-robin
-// to the 8 warps, a shared flag for the early exit.
+// Phase B: one CTA per deferred point, its candidate steps (64 entries each,
+// two 32-entry loads in flight per warp) dealt round-robin to the 8 warps, a
+// shared flag for the early exit.
 template <typename T, int D>
 __global__ void __launch_bounds__(256) k_allpairs_long(const T* __restrict__ rows, const uint32_t* __restrict__ ids,
-                                                       const u64* __restrict__ fsum, const uint32_t* __restrict__ lists,
-                                                       const unsigned* __restrict__ offs, u64 cap,
+                                                       const u64* __restrict__ fsum, ListArrays<T, D> la,
+                                                       const unsigned* __restrict__ offs,
                                                        uint8_t* __restrict__ flag, int cell_level,
                                                        const uint32_t* __restrict__ long_q,
                                                        const u64* __restrict__ long_n) {
@@ -1682,7 +1712,7 @@ __global__ void __launch_bounds__(256) k_allpairs_long(const T* __restrict__ row
     __syncthreads();
     ListQuery<T, D> Q;
     Q.init(rows, fsum, ids, offs, i);
-    const uint32_t* lst = lists + (u64)Q.bk * cap;
+    const u64 lb = (u64)Q.bk * la.lcap;
     const unsigned* ob = offs + Q.bk * kListStride;
     unsigned g = 0;  // global step counter (identical in every warp)
     bool done = false;
@@ -1696,30 +1726,33 @@ __global__ void __launch_bounds__(256) k_allpairs_long(const T* __restrict__ row
       }
       unsigned ne = __ballot_sync(kFull, b1 > b0);
       while (ne && !done) {
-      const int src = __ffs(ne) - 1;
-      ne &= ne - 1;
-      const unsigned s0 = __shfl_sync(kFull, b0, src), s1 = __shfl_sync(kFull, b1, src);
-      const unsigned nsteps = (s1 - s0 + 31) / 32;
-      // this warp's steps of the column: g + k with (g + k) % nw == warp
-      unsigned k = (unsigned)((warp - (int)(g % nw) + nw) % nw);
-      // the early-exit flag goes through shared atomics (a race by design,
-      // kept visible to compute-sanitizer racecheck as synchronised access)
-      auto seen = [&]() {
-        int f = 0;
-        if (lane == 0) f = atomicAdd(&found, 0);
-        return __shfl_sync(kFull, f, 0) != 0;
-      };
-      for (; k < nsteps; k += nw) {
-        if (seen()) break;
-        const unsigned e = s0 + k * 32 + lane;
-        const bool d_l = e < s1 && Q.test(rows, ids, fsum, lst, e, cell_level, ctop);
-        if (__any_sync(kFull, d_l)) {
-          if (lane == 0) atomicExch(&found, 1);
-          break;
+        const int src = __ffs(ne) - 1;
+        ne &= ne - 1;
+        const unsigned s0 = __shfl_sync(kFull, b0, src), s1 = __shfl_sync(kFull, b1, src);
+        const unsigned nsteps = (s1 - s0 + 63) / 64;
+        // this warp's steps of the column: g + k with (g + k) % nw == warp
+        unsigned k = (unsigned)((warp - (int)(g % nw) + nw) % nw);
+        // the early-exit flag goes through shared atomics (a race by design,
+        // kept visible to compute-sanitizer racecheck as synchronised access)
+        auto seen = [&]() {
+          int f = 0;
+          if (lane == 0) f = atomicAdd(&found, 0);
+          return __shfl_sync(kFull, f, 0) != 0;
+        };
+        for (; k < nsteps; k += nw) {
+          if (seen()) break;
+          const unsigned e0 = s0 + k * 64 + lane, e1 = e0 + 32;
+          typename ListQuery<T, D>::Cand ca, cb;
+          Q.fetch(la, lb, e0, e0 < s1, ca);
+          Q.fetch(la, lb, e1, e1 < s1, cb);
+          const bool d_l = Q.check(ca, cell_level, ctop) || Q.check(cb, cell_level, ctop);
+          if (__any_sync(kFull, d_l)) {
+            if (lane == 0) atomicExch(&found, 1);
+            break;
+          }
         }
-      }
-      g += nsteps;
-      if (seen()) done = true;
+        g += nsteps;
+        if (seen()) done = true;
       }
     }
     __syncthreads();

@@ -216,6 +216,7 @@ int skycell_gpu_create(int device, skycell_gpu_ctx** out, char* err, size_t err_
     ck(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming), "event");
     ck(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&ctx->ev_k0, cudaEventDisableTiming), "event");
     ck(cudaHostAlloc(reinterpret_cast<void**>(&ctx->host_ctr), sizeof(DevCounters), cudaHostAllocMapped), "pinned");
     ck(cudaHostAlloc(reinterpret_cast<void**>(&ctx->host_param), 64, cudaHostAllocMapped), "pinned");
     ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->host_ctr_dev), ctx->host_ctr, 0), "mapped");
@@ -233,7 +234,7 @@ void skycell_gpu_destroy(skycell_gpu_ctx* ctx) {
   ctx->shard.reset();
   DevBuf* bufs[] = {&ctx->reset, &ctx->slabs, &ctx->H, &ctx->table, &ctx->table2, &ctx->table_s, &ctx->staging,
                     &ctx->smp_rows, &ctx->smp_ids, &ctx->smp_fsum, &ctx->f_rows, &ctx->f_fsum, &ctx->f_lists,
-                    &ctx->f_offs, &ctx->lists, &ctx->ids_dev, &ctx->s1_rows, &ctx->s1_ids, &ctx->s2_rows,
+                    &ctx->f_offs, &ctx->l_rows, &ctx->l_sums, &ctx->l_ids, &ctx->ids_dev, &ctx->s1_rows, &ctx->s1_ids, &ctx->s2_rows,
                     &ctx->s2_ids, &ctx->s2_fsum, &ctx->flags, &ctx->sky_rows, &ctx->sky_ids, &ctx->sky_fsum,
                     &ctx->q_bits, &ctx->q_orig, &ctx->q_sub, &ctx->q_ids, &ctx->q_mm, &ctx->t_keys,
                     &ctx->t_keys2, &ctx->t_vals, &ctx->t_vals2, &ctx->t_cub, &ctx->t_rows, &ctx->t_ids,
@@ -246,6 +247,7 @@ void skycell_gpu_destroy(skycell_gpu_ctx* ctx) {
   if (ctx->host_param) cudaFreeHost(ctx->host_param);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->ev_k0) cudaEventDestroy(ctx->ev_k0);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;

@@ -5,7 +5,8 @@
     python scripts/gap_probe.py [n] [d] [dist] [rho]
 
 Prints the query span, the sum of kernel durations, and the largest idle
-gaps between consecutive kernels (with the kernels either side)."""
+gaps between consecutive kernels (with the kernels either side); TIMELINE=1
+also lists every activity of the last repetition (start offset, duration)."""
 import os
 import sys
 
@@ -55,6 +56,10 @@ def main(n=100_000_000, d=4, dist=0, rho=6):
               f"{len(ev)} activities, {len(gaps)} gaps")
         for g, a, b in gaps[:int(os.environ.get("GAPS", "12"))]:
             print(f"   {g:7.1f} us  {a[:60]:60s} -> {b[:60]}")
+        if os.environ.get("TIMELINE") and rep == 2:
+            # every activity of the last rep: start offset, duration, name
+            for e in ev:
+                print(f"   +{e.time_range.start - t0:8.1f} {e.time_range.end - e.time_range.start:7.1f} us  {e.name[:90]}")
     eng.close()
 
 
