@@ -321,8 +321,8 @@ void run_exact(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uin
                              static_cast<uint32_t*>(ctx->l_ids.p), lcap};
   sk::launch(sk::k_list_hist<TOut, D>, g, 256, 0, s, trows, ids, fsum, count, hist);
   unsigned* totals = static_cast<unsigned*>(ctx->scan_tot.p);
-  sk::launch(sk::k_list_scan_sums, dim3(sk::kScanChunks, D), 1024, 0, s, hist, D, totals, gate);
-  sk::launch(sk::k_list_scan, dim3(sk::kScanChunks, D), 1024, 0, s, hist, cursor, D, totals, gate);
+  sk::launch(sk::k_list_scan_sums, dim3(sk::kScanChunks, D), sk::kScanThreads, 0, s, hist, D, totals, gate);
+  sk::launch(sk::k_list_scan, dim3(sk::kScanChunks, D), sk::kScanThreads, 0, s, hist, cursor, D, totals, gate);
   ++ctx->launches;
   sk::launch(sk::k_list_scatter<TOut, D>, g, 256, 0, s, trows, ids, fsum, count, cursor, la);
   const unsigned gw = (unsigned)std::max<u64>(1, std::min<u64>((cap * 32 + 255) / 256, (u64)nsm * 8));
@@ -719,7 +719,10 @@ struct Pipe final : PipeBase {
     grid1 = (int)std::max<u64>(1, std::min<u64>((wtiles + wpc - 1) / wpc, (u64)nsm * occ_blocks));
     if (q.merge && k0_overlap() && !k1_head_wanted()) {
       // leave CTA slots free for K0's sample-skyline chain, which runs beside K1
-      if (const char* e = std::getenv("SKYCELL_K1_FREE")) grid1 = std::max(nsm, grid1 - std::atoi(e));
+      // (12 slots: C2 1.195 -> 1.175 ms; 24/48/96 measured slower)
+      int free_slots = 12;
+      if (const char* e = std::getenv("SKYCELL_K1_FREE")) free_slots = std::atoi(e);
+      if (grid1 >= nsm * 2) grid1 = std::max(nsm, grid1 - free_slots);
     }
     cap1 = n + (u64)grid1 * (k1_threads / 32) * kChunk1;
 
@@ -827,7 +830,7 @@ struct Pipe final : PipeBase {
   }
 
   static bool k0_overlap() {
-    static const bool v = [] { const char* e = std::getenv("SKYCELL_K0_OVERLAP"); return e && e[0] == '1'; }();
+    static const bool v = [] { const char* e = std::getenv("SKYCELL_K0_OVERLAP"); return !e || e[0] != '0'; }();
     return v;
   }
   bool k1_head_wanted() const {
@@ -888,12 +891,12 @@ struct Pipe final : PipeBase {
             static_cast<const TOut*>(ctx->smp_rows.p), static_cast<const uint32_t*>(ctx->smp_ids.p),
             static_cast<const uint8_t*>(ctx->flags.p), static_cast<const u64*>(ctx->smp_fsum.p), &c->xs_cap,
             static_cast<TOut*>(ctx->s2_rows.p), static_cast<u64*>(ctx->s2_fsum.p), &c->fs);
-        sk::launch(sk::k_strength_order<TOut, D>, 1, 1024, 0, s, 
+        sk::launch(sk::k_strength_order<TOut, D>, 1, 256, 0, s, 
             static_cast<const TOut*>(ctx->s2_rows.p), static_cast<const u64*>(ctx->s2_fsum.p), nullptr, &c->fs,
             (uint32_t)pf_max, static_cast<TOut*>(ctx->f_rows.p), static_cast<u64*>(ctx->f_fsum.p), nullptr, &c->nf);
         sk::launch(sk::k_filter_gate, 1, 1, 0, s, &c->fs, &c->xs_cap, &c->fweak);
         ++ctx->launches;
-        sk::launch(sk::k_filter_lists<TOut, D>, D, 1024, 0, s, static_cast<const TOut*>(ctx->f_rows.p), &c->nf,
+        sk::launch(sk::k_filter_lists<TOut, D>, D, 256, 0, s, static_cast<const TOut*>(ctx->f_rows.p), &c->nf,
                                                         (uint32_t)pf_max, static_cast<uint16_t*>(ctx->f_lists.p),
                                                         static_cast<uint16_t*>(ctx->f_offs.p));
         ++ctx->launches;

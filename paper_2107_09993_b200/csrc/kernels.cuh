@@ -1344,11 +1344,13 @@ __global__ void __launch_bounds__(1024) k_strength_order(const T* __restrict__ r
 // dimension k (key = column << 10 | strength rank, one block radix sort), so
 // each column prefix is scanned strongest first, plus the column starts.
 template <typename T, int D>
-__global__ void __launch_bounds__(1024) k_filter_lists(const T* __restrict__ f_rows, const u64* __restrict__ f_count,
-                                                        uint32_t f_max, uint16_t* __restrict__ f_lists,
-                                                        uint16_t* __restrict__ f_offs) {
+__global__ void __launch_bounds__(256) k_filter_lists(const T* __restrict__ f_rows, const u64* __restrict__ f_count,
+                                                       uint32_t f_max, uint16_t* __restrict__ f_lists,
+                                                       uint16_t* __restrict__ f_offs) {
   pdl_enter();
-  using Sort = cub::BlockRadixSort<uint32_t, 1024, 1>;
+  // 256 threads x 4 keys (small CTAs: this also runs beside K1, K0's chain)
+  constexpr int kPer = 4;
+  using Sort = cub::BlockRadixSort<uint32_t, 256, kPer>;
   __shared__ typename Sort::TempStorage tmp;
   __shared__ unsigned cnt[kListCols + 1];
   const int k = blockIdx.x;
@@ -1356,11 +1358,19 @@ __global__ void __launch_bounds__(1024) k_filter_lists(const T* __restrict__ f_r
   const unsigned t = threadIdx.x;
   for (unsigned c = t; c <= kListCols; c += blockDim.x) cnt[c] = 0;
   __syncthreads();
-  uint32_t key[1];
-  key[0] = t < nf ? ((uint32_t)list_col(f_rows[(u64)t * D + k]) << 10) | t : 0xffffffffu;
-  if (t < nf) atomicAdd(&cnt[(key[0] >> 10) + 1], 1u);
+  uint32_t key[kPer];
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const unsigned r = t * kPer + j;
+    key[j] = r < nf ? ((uint32_t)list_col(f_rows[(u64)r * D + k]) << 10) | r : 0xffffffffu;
+    if (r < nf) atomicAdd(&cnt[(key[j] >> 10) + 1], 1u);
+  }
   Sort(tmp).Sort(key, 0, 20);
-  if (t < nf) f_lists[(u64)k * f_max + t] = (uint16_t)(key[0] & 1023);  // blocked arrangement: thread t holds rank t
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {  // blocked arrangement: thread t holds ranks t*kPer + j
+    const unsigned r = t * kPer + j;
+    if (r < nf) f_lists[(u64)k * f_max + r] = (uint16_t)(key[j] & 1023);
+  }
   __syncthreads();
   if (t == 0) {
     unsigned run = 0;
@@ -1419,8 +1429,10 @@ __global__ void k_list_hist(const T* __restrict__ rows, const uint32_t* __restri
 // cursor), blockIdx.y >= D the column arrays; blockIdx.x is a chunk of
 // kScanChunk entries.  Pass 1 writes each chunk's total; pass 2 adds the
 // totals of the preceding chunks (at most a handful) to its block scan.
-constexpr int kScanPer = 8;
-constexpr int kScanChunk = 1024 * kScanPer;
+constexpr int kScanThreads = 256;  // small CTAs: these also run beside K1 (K0's chain)
+constexpr int kScanChunk = 8192;
+constexpr int kScanPer = kScanChunk / kScanThreads;
+constexpr int kScanWarps = kScanThreads / 32;
 constexpr int kScanChunks = (kListBins + 1 + kScanChunk - 1) / kScanChunk;
 
 __device__ __forceinline__ unsigned* scan_array(unsigned* hist, int y, int D, int* len) {
@@ -1429,33 +1441,33 @@ __device__ __forceinline__ unsigned* scan_array(unsigned* hist, int y, int D, in
   return hist + (u64)(bins ? y : y - D) * kListStride + (bins ? 0 : kColBase);
 }
 
-static __global__ void __launch_bounds__(1024) k_list_scan_sums(unsigned* __restrict__ hist, int D,
+static __global__ void __launch_bounds__(kScanThreads) k_list_scan_sums(unsigned* __restrict__ hist, int D,
                                                           unsigned* __restrict__ totals, const u64* __restrict__ gate) {
   pdl_enter();
-  __shared__ unsigned warp_tot[32];
+  __shared__ unsigned warp_tot[kScanWarps];
   if (gate && *gate == 0) return;  // the set goes to the tree (run_dominance)
   int len;
   const unsigned* h = scan_array(hist, blockIdx.y, D, &len);
   const int c0 = blockIdx.x * kScanChunk;
   unsigned v = 0;
-  for (int i = c0 + threadIdx.x; i < min(c0 + kScanChunk, len); i += 1024) v += h[i];
+  for (int i = c0 + threadIdx.x; i < min(c0 + kScanChunk, len); i += kScanThreads) v += h[i];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
   if ((threadIdx.x & 31) == 0) warp_tot[threadIdx.x >> 5] = v;
   __syncthreads();
   if (threadIdx.x < 32) {
-    unsigned t = warp_tot[threadIdx.x];
+    unsigned t = threadIdx.x < kScanWarps ? warp_tot[threadIdx.x] : 0u;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(kFull, t, o);
     if (threadIdx.x == 0) totals[blockIdx.y * kScanChunks + blockIdx.x] = t;
   }
 }
 
-static __global__ void __launch_bounds__(1024) k_list_scan(unsigned* __restrict__ hist, unsigned* __restrict__ cursor, int D,
+static __global__ void __launch_bounds__(kScanThreads) k_list_scan(unsigned* __restrict__ hist, unsigned* __restrict__ cursor, int D,
                                                      const unsigned* __restrict__ totals, const u64* __restrict__ gate) {
   pdl_enter();
   __shared__ unsigned tile[kScanChunk + kScanChunk / 32];  // one pad word per 32 entries
-  __shared__ unsigned warp_tot[32];
+  __shared__ unsigned warp_tot[kScanWarps];
   if (gate && *gate == 0) return;
   int len;
   unsigned* h = scan_array(hist, blockIdx.y, D, &len);
@@ -1466,11 +1478,11 @@ static __global__ void __launch_bounds__(1024) k_list_scan(unsigned* __restrict_
   for (int b = 0; b < (int)blockIdx.x; ++b) carry += totals[blockIdx.y * kScanChunks + b];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   auto pad = [](int i) { return i + (i >> 5); };  // conflict-free strided runs
-  for (int i = threadIdx.x; i < kScanChunk; i += 1024) tile[pad(i)] = (c0 + i < len) ? h[c0 + i] : 0u;
+  for (int i = threadIdx.x; i < kScanChunk; i += kScanThreads) tile[pad(i)] = (c0 + i < len) ? h[c0 + i] : 0u;
   __syncthreads();
   const int r0 = threadIdx.x * kScanPer;
   unsigned run = 0;
-#pragma unroll
+#pragma unroll 8
   for (int e = 0; e < kScanPer; ++e) run += tile[pad(r0 + e)];
   unsigned incl = run;
 #pragma unroll
@@ -1481,24 +1493,24 @@ static __global__ void __launch_bounds__(1024) k_list_scan(unsigned* __restrict_
   if (lane == 31) warp_tot[warp] = incl;
   __syncthreads();
   if (warp == 0) {
-    const unsigned t = warp_tot[lane];
+    const unsigned t = lane < kScanWarps ? warp_tot[lane] : 0u;
     unsigned ti = t;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const unsigned y = __shfl_up_sync(kFull, ti, o);
       if (lane >= o) ti += y;
     }
-    warp_tot[lane] = ti - t;
+    if (lane < kScanWarps) warp_tot[lane] = ti - t;
   }
   __syncthreads();
   unsigned acc = carry + warp_tot[warp] + incl - run;
-#pragma unroll
+#pragma unroll 8
   for (int e = 0; e < kScanPer; ++e) {
     acc += tile[pad(r0 + e)];
     tile[pad(r0 + e)] = acc;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < kScanChunk; i += 1024) {
+  for (int i = threadIdx.x; i < kScanChunk; i += kScanThreads) {
     if (c0 + i < len) {
       const unsigned v = tile[pad(i)];
       h[c0 + i] = v;
