@@ -820,12 +820,15 @@ struct Pipe final : PipeBase {
     // only semantics (merge_cross_cell = false) cannot use.  K1 does not
     // read it (unless its filter-point head is on), so with
     // SKYCELL_K0_OVERLAP=1 it runs on the side stream behind K1's launch.
+    // Part A (X) stays on the main stream: on K1's few free CTA slots it
+    // would hold up part B's host-read gate until K1's end.
     k0_side = q.merge && !k1_head_wanted() && k0_overlap();
-    if (q.merge && !k0_side) sample_chain(s);
+    if (q.merge) sample_candidates();
+    if (q.merge && !k0_side) sample_skyline(s);
     // fork point: K0's sample buffers and tables are complete here
     if (k0_side) ck(cudaEventRecord(ctx->ev_fork, s), "event");
     launch_k1(c);
-    if (k0_side) sample_chain(s2);
+    if (k0_side) sample_skyline(s2);
     if (q.timed) ck(cudaEventRecord(ctx->ev[1], s), "event");
   }
 
@@ -838,12 +841,9 @@ struct Pipe final : PipeBase {
     return q.merge && he && he[0] == '1';
   }
 
-  // K0's sample skyline -> filter points F (+ their column lists), on stream st
-  void sample_chain(cudaStream_t st) {
+  // K0 part A (main stream): the sample's candidates X, packed and capped
+  void sample_candidates() {
     DevCounters* c = ctr();
-    const bool side = st != s;
-    cudaStream_t s = st;  // every launch below goes to st
-    if (side) ck(cudaStreamWaitEvent(s, ctx->ev_fork, 0), "fork");
     {
       {
         tracer().mark(s, "K0: sample tables");
@@ -883,6 +883,19 @@ struct Pipe final : PipeBase {
             static_cast<u64*>(ctx->smp_fsum.p), static_cast<uint32_t*>(ctx->smp_ids.p), &c->xd);
         sk::launch(sk::k_clamp_count, 1, 32, 0, s, &c->xd, kXMax, &c->xs_cap);
         ctx->launches += 2;
+      }
+    }
+  }
+
+  // K0 part B: the sample skyline of X -> filter points F (+ column lists)
+  void sample_skyline(cudaStream_t st) {
+    DevCounters* c = ctr();
+    const bool side = st != s;
+    cudaStream_t s = st;  // every launch below goes to st
+    if (side) ck(cudaStreamWaitEvent(s, ctx->ev_fork, 0), "fork");
+    constexpr u64 kXMax = 1ull << 17;
+    {
+      {
         run_dominance<TOut, D>(ctx, s, ctx->smp_rows.p, static_cast<const uint32_t*>(ctx->smp_ids.p),
                                static_cast<const u64*>(ctx->smp_fsum.p), &c->xs_cap, std::min<u64>(m, kXMax),
                                U(o_shist), U(o_scur), &c->tvalid, 0, nullptr, 0, sample_tree_min());

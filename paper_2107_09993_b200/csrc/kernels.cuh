@@ -1430,7 +1430,7 @@ __global__ void k_list_hist(const T* __restrict__ rows, const uint32_t* __restri
 // kScanChunk entries.  Pass 1 writes each chunk's total; pass 2 adds the
 // totals of the preceding chunks (at most a handful) to its block scan.
 constexpr int kScanThreads = 256;  // small CTAs: these also run beside K1 (K0's chain)
-constexpr int kScanChunk = 8192;
+constexpr int kScanChunk = 2048;  // 8.4 KB of shared memory: fits beside K1
 constexpr int kScanPer = kScanChunk / kScanThreads;
 constexpr int kScanWarps = kScanThreads / 32;
 constexpr int kScanChunks = (kListBins + 1 + kScanChunk - 1) / kScanChunk;
