@@ -180,4 +180,18 @@ __device__ __forceinline__ void set_bit_shared(uint32_t* bits, uint32_t idx) {
   if (!(w & m)) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(m) : "memory");
 }
 
+// Branch-free variant: the word is always read, the red.or is predicated on
+// `cond` and on the bit being clear (no divergent region around it).
+__device__ __forceinline__ void set_bit_shared_if(uint32_t* bits, uint32_t idx, bool cond) {
+  const uint32_t m = 1u << (idx & 31);
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bits) + ((idx >> 5) << 2);
+  uint32_t w;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(a));
+  const uint32_t need = (cond && !(w & m)) ? 1u : 0u;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.shared.or.b32 [%0], %1;\n\t}" ::"r"(a), "r"(m),
+      "r"(need)
+      : "memory");
+}
+
 }  // namespace sk

@@ -402,6 +402,42 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
     const uint32_t base = t * WT + lane;
     bool keep[PPT];
     bool bad = false;
+    // Fast path (identity f32 input, full tile, every coordinate of the tile
+    // in [+0, 1) -- one unsigned max of the bit patterns per point): no
+    // clamps, no NaN/Inf probe and no divergent occupancy update.  Anything
+    // else (negative, >= 1, NaN, Inf, the last partial tile) takes the
+    // general path below.
+    bool fastp = false;
+    if constexpr (IDENT && !REC_LA) {
+      if (full) {
+        bool inr = true;
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          uint32_t mx = __float_as_uint(cur[j][0]);
+#pragma unroll
+          for (int k = 1; k < D; ++k) mx = max(mx, __float_as_uint(cur[j][k]));
+          inr &= mx < 0x3F800000u;
+        }
+        fastp = __all_sync(kFull, inr);
+      }
+    }
+    if (fastp) {
+      if constexpr (IDENT && !REC_LA) {
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          uint32_t hidx = 0, lo = 0;
+#pragma unroll
+          for (int k = D - 1; k >= 1; --k) {
+            hidx = hidx * mul_a + mag_col(cur[j][k], fs_a);
+            if (rec_lo) lo = lo * mul_lo + mag_col(cur[j][k], fs_lo);
+          }
+          const int c0 = (int)(mag_col(cur[j][0], fs_a) - 0x4B000000u);
+          const bool fail_a = c0 > (int)H_s[hidx - hcorr];
+          if (rec_lo) set_bit_shared_if(occ_s, lo * mul_lo + mag_col(cur[j][0], fs_lo) - locorr, fail_a);
+          keep[j] = !fail_a;
+        }
+      }
+    } else
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
       const bool valid = full || (uint32_t)(j * 32 + lane) < n - t * WT;
