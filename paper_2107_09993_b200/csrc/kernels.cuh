@@ -397,6 +397,14 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
       if (t < nfull || (uint32_t)(j * 32 + lane) < n - t * WT) load_row<TIn, D>(coords, t * WT + j * 32 + lane, raw[j]);
     }
   };
+  // deferred check-before-set of a layer-rho occupancy bit (K1 survivors)
+  uint32_t* pend_w = nullptr;
+  uint32_t pend_m = 0, pend_v = 0;
+  bool pend_on = false;
+  auto resolve_pending = [&]() {
+    if (pend_on && !(pend_v & pend_m)) asm volatile("red.global.or.b32 [%0], %1;" ::"l"(pend_w), "r"(pend_m) : "memory");
+    pend_on = false;
+  };
   auto process = [&](TIn (&cur)[PPT][D], uint32_t t) {
     const bool full = t < nfull;
     const uint32_t base = t * WT + lane;
@@ -554,6 +562,20 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
         if (keep_b) {
 #pragma unroll
           for (int k = D - 1; k >= 0; --k) lin = (lin << rho) | (u64)c[k];
+        }
+        if (r == 0) {
+          // The first survivor batch's check-before-set is deferred to the
+          // next tile: its L1/L2 load is issued now and tested after that
+          // tile's main work, so no warp waits on it (a stale word only
+          // costs a redundant red).
+          resolve_pending();
+          if (keep_b) {
+            pend_w = p.occ_rho + (lin >> 5);
+            pend_m = 1u << (lin & 31);
+            asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(pend_v) : "l"(pend_w));
+            pend_on = true;
+          }
+        } else if (keep_b) {
           set_bit_cached(p.occ_rho, lin);
         }
         // filter-point head: branch-free over the 8 strongest filter points
@@ -605,6 +627,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
     process(buf_b, t);
     t = tn;
   }
+  resolve_pending();
   warp_close(wo, stamp);
   if (p.f_rows) warp_close(wd, dstamp);
   if (lane == 0 && kept) atomicAdd(p.kept, (u64)kept);
