@@ -329,11 +329,19 @@ void run_exact(skycell_gpu_ctx* ctx, cudaStream_t s, const void* rows, const uin
   ensure(ctx->long_q, cap * 4);
   u64* long_n = static_cast<u64*>(ctx->long_n.p);
   fill_words(ctx, s, long_n, 2);
-  constexpr unsigned kMaxSteps = 8;  // phase A budget in 32-entry steps (4..64 swept: 4-8 best at C2 / C4 shards)
+  // phase A budget in 32-entry steps (4..64 swept: 4-8 best at C2 / C4 shards; SKYCELL_LIST_STEPS)
+  static const unsigned kMaxSteps = [] {
+    const char* e = std::getenv("SKYCELL_LIST_STEPS");
+    return e ? (unsigned)std::max(2, std::atoi(e)) : 8u;
+  }();
   sk::launch(sk::k_allpairs_lists<TOut, D>, gw, 256, 0, s, trows, ids, fsum, count, la, hist,
                                                    static_cast<uint8_t*>(ctx->flags.p), q_begin, q_end, cell_level,
                                                    kMaxSteps, static_cast<uint32_t*>(ctx->long_q.p), long_n, gate);
-  sk::launch(sk::k_allpairs_long<TOut, D>, nsm * 4, 256, 0, s, trows, ids, fsum, la, hist,
+  static const int kLongPerSm = [] {
+    const char* e = std::getenv("SKYCELL_LONG_CTAS");
+    return e ? std::max(1, std::atoi(e)) : 4;
+  }();
+  sk::launch(sk::k_allpairs_long<TOut, D>, nsm * kLongPerSm, 256, 0, s, trows, ids, fsum, la, hist,
                                                        static_cast<uint8_t*>(ctx->flags.p), cell_level,
                                                        static_cast<const uint32_t*>(ctx->long_q.p), long_n);
   ctx->launches += 5;
@@ -1097,6 +1105,7 @@ struct Pipe final : PipeBase {
       pb.head_start = sk::kK4aHead;
       pb.coop = 1;
       pb.coop_mid = 16;  // measured: 16 best at C2 / C4 shards (8..64 swept)
+      if (const char* e = std::getenv("SKYCELL_K4B_MID")) pb.coop_mid = (uint32_t)std::max(0, std::atoi(e));
       sk::launch(kc, grid4, kThreads, smem_pf, s, pb);
       ctx->launches += 2;
     } else {
