@@ -676,22 +676,41 @@ struct Pipe final : PipeBase {
   // sparse layer rho (sparse.cuh): the dense pipeline runs up to rho - 1
   static bool sparse_top(int r) { return r * D > 36 || r * (D - 1) > 30; }
 
-  static auto pick_stream(int rho) {
+  // K1 tiles by cp.async.bulk into a shared-memory ring (identity f32 input at
+  // d = 4, whose 16-byte rows make every tile a whole number of 16-byte
+  // chunks): C2 K1 0.429 -> 0.404 ms, correlated 0.409 -> 0.375 ms
+  // (profiles/ab_k1bulk_r9e.txt).  SKYCELL_K1_BULK=0: per-lane LDG.128 into
+  // two register buffers.
+  static bool k1_bulk_env() {
+    static const bool v = [] { const char* e = std::getenv("SKYCELL_K1_BULK"); return !e || e[0] != '0'; }();
+    return v;
+  }
+  bool k1_bulk() const {
+    if constexpr (IDENT && D == 4) return k1_bulk_env() && !rec_la_shape(rho);
+    return false;
+  }
+  template <bool B>
+  static auto pick_stream_b(int rho) {
     if constexpr (IDENT && D <= 8) {
-      if constexpr (D == 4)
-        if (rec_la_shape(rho)) return sk::k_stream<TIn, TOut, D, IDENT, kRecLaThreads, PPT1, 6, 1, true>;
       switch (rho) {
-        case 1: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 1>;
-        case 2: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 2>;
-        case 3: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 3>;
-        case 4: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 4>;
-        case 5: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 5>;
-        case 6: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 6>;
-        case 7: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 7>;
+        case 1: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 1, 3, false, B>;
+        case 2: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 2, 3, false, B>;
+        case 3: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 3, 3, false, B>;
+        case 4: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 4, 3, false, B>;
+        case 5: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 5, 3, false, B>;
+        case 6: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 6, 3, false, B>;
+        case 7: return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 7, 3, false, B>;
         default: break;
       }
     }
-    return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 0>;
+    return sk::k_stream<TIn, TOut, D, IDENT, kStreamThreads, PPT1, 0, 3, false, B>;
+  }
+  static auto pick_stream(int rho) {
+    if constexpr (IDENT && D == 4) {
+      if (rec_la_shape(rho)) return sk::k_stream<TIn, TOut, D, IDENT, kRecLaThreads, PPT1, 6, 1, true>;
+      if (k1_bulk_env()) return pick_stream_b<true>(rho);
+    }
+    return pick_stream_b<false>(rho);
   }
 
   int rho_q;    // the query's rho (reported layers 1..rho_q)
@@ -715,7 +734,7 @@ struct Pipe final : PipeBase {
     // K1 geometry: persistent warps over round-robin warp tiles
     smem1 = (((size_t)lo_words * 4 + 15) & ~(size_t)15) + ((h_entries + 15) & ~15u) + (size_t)k1_threads * PPT1 +
             (((size_t)sk::kK1Head * (D * sizeof(TOut) + 8) + 15) & ~(size_t)15) +
-            (size_t)k1_threads * PPT1 * D * sizeof(TIn) + 16;
+            (size_t)k1_threads * PPT1 * D * sizeof(TIn) * (k1_bulk() ? 2 : 1) + (size_t)(k1_threads / 32) * 16 + 16;
     kstream = pick_stream(rho);
     ck(cudaFuncSetAttribute(kstream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1), "smem attr");
     int occ_blocks = 0;

@@ -325,7 +325,12 @@ __device__ __forceinline__ uint32_t mag_col(float u, float scale) {
 // cell -- its index is the H lookup's index plus c_0, no second set of
 // digits -- in a per-CTA 2^(la d)-bit shared bitmap (128 KB at d = 4, la = 5,
 // so one 768-thread CTA per SM).  Otherwise they record their level la-1 cell.
-template <typename TIn, typename TOut, int D, bool IDENT, int THREADS, int PPT, int RHO, int MINB = 3, bool REC_LA = false>
+// BULK (f32 rows of 16-byte multiples): each warp's tiles arrive by
+// cp.async.bulk into a two-stage shared-memory ring (one instruction per tile
+// from one lane, completion on an mbarrier) instead of per-lane LDG.128 into
+// two register buffers; survivors are read back from the ring stage.
+template <typename TIn, typename TOut, int D, bool IDENT, int THREADS, int PPT, int RHO, int MINB = 3, bool REC_LA = false,
+          bool BULK = false>
 __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
   pdl_enter();
   static_assert(PPT <= 8, "survivor codes are (j * 32 + lane) in one byte");
@@ -337,6 +342,14 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
   TIn* rows_w = reinterpret_cast<TIn*>(H_s + ((p.h_entries + 15) & ~15u) + THREADS * PPT +
                                        ((kK1Head * (D * sizeof(TOut) + 8) + 15) & ~(size_t)15)) +
                 (size_t)(threadIdx.x >> 5) * (32 * PPT) * D;
+  static_assert(!BULK || (D * sizeof(TIn)) % 16 == 0, "bulk tiles are whole 16-byte rows");
+  if constexpr (BULK)  // two ring stages per warp in place of the survivor staging area
+    rows_w = reinterpret_cast<TIn*>(H_s + ((p.h_entries + 15) & ~15u) + THREADS * PPT +
+                                    ((kK1Head * (D * sizeof(TOut) + 8) + 15) & ~(size_t)15)) +
+             (size_t)(threadIdx.x >> 5) * 2 * (32 * PPT) * D;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(
+      H_s + ((p.h_entries + 15) & ~15u) + THREADS * PPT + ((kK1Head * (D * sizeof(TOut) + 8) + 15) & ~(size_t)15) +
+      (size_t)THREADS * PPT * D * sizeof(TIn) * (BULK ? 2 : 1)) + (threadIdx.x >> 5) * 2;
   TOut* fh_rows = reinterpret_cast<TOut*>(H_s + ((p.h_entries + 15) & ~15u) + THREADS * PPT);
   u64* fh_sum = reinterpret_cast<u64*>(fh_rows + kK1Head * D);
   uint32_t nfh = 0;
@@ -405,7 +418,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
     if (pend_on && !(pend_v & pend_m)) asm volatile("red.global.or.b32 [%0], %1;" ::"l"(pend_w), "r"(pend_m) : "memory");
     pend_on = false;
   };
-  auto process = [&](TIn (&cur)[PPT][D], uint32_t t) {
+  auto process = [&](TIn (&cur)[PPT][D], uint32_t t, const TIn* stage) {
     const bool full = t < nfull;
     const uint32_t base = t * WT + lane;
     bool keep[PPT];
@@ -509,7 +522,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
           if (keep[j]) {
             const unsigned sl = cum + __popc(mk[j] & lt);
             code_w[sl] = (uint8_t)(j * 32 + lane);
-            store_row<TIn, D>(rows_w, sl, cur[j]);
+            if constexpr (!BULK) store_row<TIn, D>(rows_w, sl, cur[j]);
           }
           cum += __popc(mk[j]);
         }
@@ -521,7 +534,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
         const unsigned cd = act ? code_w[sidx] : 0u;
         const int sj = (int)(cd >> 5), src = (int)(cd & 31);
         TIn x[D];
-        load_row_cached<TIn, D>(rows_w, act ? sidx : 0u, x);  // staged in shared memory
+        if constexpr (BULK) load_row_cached<TIn, D>(stage, act ? cd : 0u, x);  // the tile's ring stage
+        else load_row_cached<TIn, D>(rows_w, act ? sidx : 0u, x);  // staged in shared memory
         TOut u[D];
         int c[D];
 #pragma unroll
@@ -615,17 +629,50 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
     }
   };
   uint32_t t = gw;
-  if (t < ntiles) load_tile(buf_a, t);
-  while (t < ntiles) {
-    uint32_t tn = t + nw;
-    if (tn < ntiles) load_tile(buf_b, tn);
-    process(buf_a, t);
-    t = tn;
-    if (t >= ntiles) break;
-    tn = t + nw;
-    if (tn < ntiles) load_tile(buf_a, tn);
-    process(buf_b, t);
-    t = tn;
+  if constexpr (BULK) {
+    const uint32_t bar0 = smem_addr(bars), bar1 = bar0 + 8;
+    const uint32_t ring0 = smem_addr(rows_w), ring1 = ring0 + WT * D * (uint32_t)sizeof(TIn);
+    if (lane == 0) {
+      mbar_init(bar0, 1);
+      mbar_init(bar1, 1);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncwarp();
+    auto issue = [&](int st, uint32_t tt) {
+      if (lane == 0) {
+        const uint32_t rows = tt < nfull ? WT : n - tt * WT;
+        bulk_load(st ? ring1 : ring0, coords + (u64)tt * WT * D, rows * D * (uint32_t)sizeof(TIn), st ? bar1 : bar0);
+      }
+    };
+    if (t < ntiles) issue(0, t);
+    if (t + nw < ntiles) issue(1, t + nw);
+    uint32_t ph0 = 0, ph1 = 0;
+    int st = 0;
+    while (t < ntiles) {
+      mbar_wait(st ? bar1 : bar0, st ? ph1 : ph0);
+      if (st) ph1 ^= 1u; else ph0 ^= 1u;
+      const TIn* stage = rows_w + (size_t)st * WT * D;
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) load_row_cached<TIn, D>(stage, (u64)(j * 32 + lane), buf_a[j]);
+      process(buf_a, t, stage);
+      __syncwarp();
+      if (t + 2 * nw < ntiles) issue(st, t + 2 * nw);
+      t += nw;
+      st ^= 1;
+    }
+  } else {
+    if (t < ntiles) load_tile(buf_a, t);
+    while (t < ntiles) {
+      uint32_t tn = t + nw;
+      if (tn < ntiles) load_tile(buf_b, tn);
+      process(buf_a, t, nullptr);
+      t = tn;
+      if (t >= ntiles) break;
+      tn = t + nw;
+      if (tn < ntiles) load_tile(buf_a, tn);
+      process(buf_b, t, nullptr);
+      t = tn;
+    }
   }
   resolve_pending();
   warp_close(wo, stamp);
