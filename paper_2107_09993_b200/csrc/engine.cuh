@@ -810,7 +810,8 @@ struct Pipe final : PipeBase {
   void local() override {
     DevCounters* c = ctr();
     if (q.timed) ck(cudaEventRecord(ctx->ev[0], s), "event");
-    ck(cudaMemsetAsync(ctx->reset.p, 0, o_total, s), "memset");
+    // a fill kernel, not a memset node: keeps the programmatic-launch chain into K0
+    fill_words(ctx, s, ctx->reset.p, o_total / 4);
 
     // K0: sample occupancy, filter tables, sample skyline -> filter points F
     {

@@ -2132,7 +2132,15 @@ static __global__ void k_clamp_count(const u64* __restrict__ src, u64 cap, u64* 
 
 static __global__ void k_fill_u32(uint32_t* __restrict__ p, u64 count, uint32_t v) {
   pdl_enter();
-  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < count; i += (u64)gridDim.x * blockDim.x) p[i] = v;
+  const u64 tid = blockIdx.x * (u64)blockDim.x + threadIdx.x, stride = (u64)gridDim.x * blockDim.x;
+  u64 head = 0;
+  if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {  // 16-byte stores for the aligned bulk
+    const uint4 w = make_uint4(v, v, v, v);
+    uint4* q = reinterpret_cast<uint4*>(p);
+    for (u64 i = tid; i < count / 4; i += stride) q[i] = w;
+    head = count / 4 * 4;
+  }
+  for (u64 i = head + tid; i < count; i += stride) p[i] = v;
 }
 
 // ------------------------------------------------ quadrant_skyline (f1)
