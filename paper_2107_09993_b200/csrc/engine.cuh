@@ -117,6 +117,7 @@ struct skycell_gpu_ctx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_k0 = nullptr;  // K0's sample-skyline chain done (side stream, overlapped with K1)
+  cudaEvent_t ev_k0occ = nullptr;  // ... its first step: the sample's level-(la-1) occupancy OR-ed in
   skyeng::DevBuf reset, slabs, H, table, table2, table_s, staging;
   skyeng::DevBuf smp_rows, smp_ids, smp_fsum, f_rows, f_fsum, f_lists, f_offs, ids_dev;
   skyeng::DevBuf s1_rows, s1_ids, s2_rows, s2_ids, s2_fsum, flags;
@@ -660,6 +661,7 @@ struct Pipe final : PipeBase {
   u64 id_words;
   unsigned bit_blocks;
   bool k0_side = false;  // K0's sample-skyline chain runs on the side stream (joined before K4)
+  bool cover = false;    // H carries cover flags; the sample's level-(la-1) occupancy is OR-ed in (side stream)
   bool k1_head = false;  // K1 ran the filter-point head (its D stream feeds K4's points_examined)
 
   // ---- zeroed region
@@ -834,8 +836,12 @@ struct Pipe final : PipeBase {
       // H = the strict-dominance height of the sample's level-la occupancy:
       // a level-la prefix-min table (multi-CTA) shifted by one cell per dim
       launch_tables<uint8_t>(ctx, s, U(o_sla), la, D, static_cast<uint8_t*>(ctx->table2.p));
+      // cover flags (bit 7 of H) only when the sample's level-(la-1) occupancy
+      // is OR-ed into layer la-1 (sample_skyline, side stream)
+      cover = q.merge && !k1_head_wanted() && k0_overlap() && la >= 2 && !rec_la && IDENT && D <= 6 &&
+              !(std::getenv("SKYCELL_COVER") && std::getenv("SKYCELL_COVER")[0] == '0');
       sk::launch(sk::k_filter_from_table, (unsigned)std::max<u64>(1, std::min<u64>((h_entries + 255) / 256, (u64)nsm * 4)), 256, 0, s, static_cast<const uint8_t*>(ctx->table2.p), la, D, h_entries,
-                                     static_cast<uint8_t*>(ctx->H.p));
+                                     static_cast<uint8_t*>(ctx->H.p), cover ? static_cast<const uint32_t*>(U(o_sla)) : nullptr);
       tracer().mark(s, "K0: build_filter");
       ctx->launches += 2;
       // layer-rho prefix-min table of the sample: K1's test B
@@ -857,6 +863,7 @@ struct Pipe final : PipeBase {
     if (k0_side) ck(cudaEventRecord(ctx->ev_fork, s), "event");
     launch_k1(c);
     if (k0_side) sample_skyline(s2);
+    if (cover) ck(cudaStreamWaitEvent(s, ctx->ev_k0occ, 0), "join occupancy");
     if (q.timed) ck(cudaEventRecord(ctx->ev[1], s), "event");
   }
 
@@ -921,6 +928,16 @@ struct Pipe final : PipeBase {
     const bool side = st != s;
     cudaStream_t s = st;  // every launch below goes to st
     if (side) ck(cudaStreamWaitEvent(s, ctx->ev_fork, 0), "fork");
+    if (cover) {
+      // the sample's level-(la-1) occupancy into layer la-1: K1 skips the
+      // dropped points of covered rows (H bit 7); the main stream joins here
+      // before it reads the layer (ev_k0occ)
+      const u64 sw = words_at(la);
+      const unsigned g = (unsigned)std::max<u64>(1, std::min<u64>((sw + 255) / 256, (u64)nsm * 8));
+      sk::launch(sk::k_downsample, g, 256, 0, s, static_cast<const uint32_t*>(U(o_sla)), la - 1, D, sw, occ(la - 1));
+      ++ctx->launches;
+      ck(cudaEventRecord(ctx->ev_k0occ, s), "event");
+    }
     constexpr u64 kXMax = 1ull << 17;
     {
       {

@@ -205,8 +205,13 @@ __global__ void __launch_bounds__(256) k_sample(SampleParams p) {
 
 // H from a prefix-min table PM of the sample occupancy at level lf (built by
 // the multi-CTA table kernels): H[x] = all x_k >= 1 ? PM[x - 1] : none.
+// Bit 7 (entries are <= 2^lf - 1 <= 127, "none" = 255) is the row's COVER
+// flag when occ_s (the sample's level-lf occupancy) is given: every level
+// (lf-1) parent of the row's dropped cells (c_0 > H[x]) holds a sample point,
+// so K1 need not record dropped points of this row at level lf-1 -- the
+// sample's level-(lf-1) occupancy is OR-ed into that layer instead.
 static __global__ void k_filter_from_table(const uint8_t* __restrict__ PM, int lf, int d, uint32_t rows,
-                                    uint8_t* __restrict__ H) {
+                                    uint8_t* __restrict__ H, const uint32_t* __restrict__ occ_s) {
   pdl_enter();
   const uint32_t mask = (1u << lf) - 1;
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
@@ -217,7 +222,26 @@ static __global__ void k_filter_from_table(const uint8_t* __restrict__ PM, int l
       ok &= c >= 1;
       prev |= (c - 1) << (lf * (k - 1));
     }
-    H[r] = ok ? PM[prev] : (uint8_t)255;
+    uint32_t h = ok ? PM[prev] : 255u;
+    if (occ_s && h < mask) {
+      // dropped columns c0 in (h, 2^lf - 1]; their parents' columns (h+1)/2 .. (2^lf-1)/2
+      bool cover = true;
+      for (uint32_t pc = (h + 1) >> 1; pc <= (mask >> 1) && cover; ++pc) {
+        bool any = false;
+        for (uint32_t cm = 0; cm < (1u << (d - 1)) && !any; ++cm) {
+          u64 base = 0;  // child (2 pc, 2 floor(x_k / 2) + b_k): dim-0 pair 2pc, 2pc+1 in one word
+          for (int k = 1; k < d; ++k) {
+            const uint32_t xk = (r >> (lf * (k - 1))) & mask;
+            base |= (u64)((xk & ~1u) | ((cm >> (k - 1)) & 1u)) << (lf * k);
+          }
+          const u64 bit = base + 2 * pc;
+          any = ((occ_s[bit >> 5] >> (bit & 31)) & 3u) != 0;
+        }
+        cover = any;
+      }
+      if (cover) h |= 0x80u;
+    }
+    H[r] = (uint8_t)h;
   }
 }
 
@@ -446,16 +470,23 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
       if constexpr (IDENT && !REC_LA) {
 #pragma unroll
         for (int j = 0; j < PPT; ++j) {
-          uint32_t hidx = 0, lo = 0;
+          uint32_t hidx = 0;
 #pragma unroll
-          for (int k = D - 1; k >= 1; --k) {
-            hidx = hidx * mul_a + mag_col(cur[j][k], fs_a);
-            if (rec_lo) lo = lo * mul_lo + mag_col(cur[j][k], fs_lo);
-          }
+          for (int k = D - 1; k >= 1; --k) hidx = hidx * mul_a + mag_col(cur[j][k], fs_a);
           const int c0 = (int)(mag_col(cur[j][0], fs_a) - 0x4B000000u);
-          const bool fail_a = c0 > (int)H_s[hidx - hcorr];
-          if (rec_lo) set_bit_shared_if(occ_s, lo * mul_lo + mag_col(cur[j][0], fs_lo) - locorr, fail_a);
+          const uint32_t hv = H_s[hidx - hcorr];
+          const bool fail_a = c0 > (int)(hv & 0x7Fu);
           keep[j] = !fail_a;
+          if (rec_lo) {
+            // a dropped point of a covered row needs no level la-1 record
+            const bool need = fail_a && !(hv & 0x80u);
+            if (__any_sync(kFull, need)) {
+              uint32_t lo = 0;
+#pragma unroll
+              for (int k = D - 1; k >= 1; --k) lo = lo * mul_lo + mag_col(cur[j][k], fs_lo);
+              set_bit_shared_if(occ_s, lo * mul_lo + mag_col(cur[j][0], fs_lo) - locorr, need);
+            }
+          }
         }
       }
     } else
@@ -479,7 +510,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
         const float u0 = fminf(fmaxf(cur[j][0], 0.0f), 0x1.fffffep-1f);
         const int c0 = (int)(mag_col(u0, fs_a) - 0x4B000000u);
         bad |= !isfinite(probe);
-        fail_a = c0 > (int)H_s[hidx - hcorr];
+        fail_a = c0 > (int)(H_s[hidx - hcorr] & 0x7Fu);  // bit 7: the cover flag
         if constexpr (REC_LA) {
           if (valid && fail_a) set_bit_shared(occ_s, (hidx - hcorr) * mul_a + (uint32_t)c0);
         } else {
@@ -496,7 +527,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
         uint32_t hidx = 0, lo = 0;
 #pragma unroll
         for (int k = D - 1; k >= 1; --k) hidx = hidx * mul_a + (uint32_t)ca[k];
-        fail_a = ca[0] > (int)H_s[hidx];
+        fail_a = ca[0] > (int)(H_s[hidx] & 0x7Fu);
 #pragma unroll
         for (int k = D - 1; k >= 0; --k) lo = lo * mul_lo + (uint32_t)(ca[k] >> 1);
         if (valid && fail_a && rec_lo) set_bit_shared(occ_s, lo);

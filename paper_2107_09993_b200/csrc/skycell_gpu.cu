@@ -217,6 +217,7 @@ int skycell_gpu_create(int device, skycell_gpu_ctx** out, char* err, size_t err_
     ck(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming), "event");
     ck(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming), "event");
     ck(cudaEventCreateWithFlags(&ctx->ev_k0, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&ctx->ev_k0occ, cudaEventDisableTiming), "event");
     ck(cudaHostAlloc(reinterpret_cast<void**>(&ctx->host_ctr), sizeof(DevCounters), cudaHostAllocMapped), "pinned");
     ck(cudaHostAlloc(reinterpret_cast<void**>(&ctx->host_param), 64, cudaHostAllocMapped), "pinned");
     ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->host_ctr_dev), ctx->host_ctr, 0), "mapped");
@@ -248,6 +249,7 @@ void skycell_gpu_destroy(skycell_gpu_ctx* ctx) {
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->ev_k0) cudaEventDestroy(ctx->ev_k0);
+  if (ctx->ev_k0occ) cudaEventDestroy(ctx->ev_k0occ);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
