@@ -678,6 +678,8 @@ struct Pipe final : PipeBase {
   // sparse layer rho (sparse.cuh): the dense pipeline runs up to rho - 1
   static bool sparse_top(int r) { return r * D > 36 || r * (D - 1) > 30; }
 
+  // (64-point tiles in a 4-stage ring, the same shared memory: C2 K1 0.382 ->
+  // 0.550 ms, profiles/ab_k1ring4_r9k.txt)
   // K1 tiles by cp.async.bulk into a shared-memory ring (identity f32 input at
   // d = 4, whose 16-byte rows make every tile a whole number of 16-byte
   // chunks): C2 K1 0.429 -> 0.404 ms, correlated 0.409 -> 0.375 ms
@@ -736,7 +738,7 @@ struct Pipe final : PipeBase {
     // K1 geometry: persistent warps over round-robin warp tiles
     smem1 = (((size_t)lo_words * 4 + 15) & ~(size_t)15) + ((h_entries + 15) & ~15u) + (size_t)k1_threads * PPT1 +
             (((size_t)sk::kK1Head * (D * sizeof(TOut) + 8) + 15) & ~(size_t)15) +
-            (size_t)k1_threads * PPT1 * D * sizeof(TIn) * (k1_bulk() ? 2 : 1) + (size_t)(k1_threads / 32) * 16 + 16;
+            (size_t)k1_threads * PPT1 * D * sizeof(TIn) * (k1_bulk() ? 2 : 1) + (size_t)(k1_threads / 32) * 32 + 16;
     kstream = pick_stream(rho);
     ck(cudaFuncSetAttribute(kstream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1), "smem attr");
     int occ_blocks = 0;

@@ -354,7 +354,7 @@ __device__ __forceinline__ uint32_t mag_col(float u, float scale) {
 // from one lane, completion on an mbarrier) instead of per-lane LDG.128 into
 // two register buffers; survivors are read back from the ring stage.
 template <typename TIn, typename TOut, int D, bool IDENT, int THREADS, int PPT, int RHO, int MINB = 3, bool REC_LA = false,
-          bool BULK = false>
+          bool BULK = false, int NST = 2>
 __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
   pdl_enter();
   static_assert(PPT <= 8, "survivor codes are (j * 32 + lane) in one byte");
@@ -367,13 +367,13 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
                                        ((kK1Head * (D * sizeof(TOut) + 8) + 15) & ~(size_t)15)) +
                 (size_t)(threadIdx.x >> 5) * (32 * PPT) * D;
   static_assert(!BULK || (D * sizeof(TIn)) % 16 == 0, "bulk tiles are whole 16-byte rows");
-  if constexpr (BULK)  // two ring stages per warp in place of the survivor staging area
+  if constexpr (BULK)  // NST ring stages per warp in place of the survivor staging area
     rows_w = reinterpret_cast<TIn*>(H_s + ((p.h_entries + 15) & ~15u) + THREADS * PPT +
                                     ((kK1Head * (D * sizeof(TOut) + 8) + 15) & ~(size_t)15)) +
-             (size_t)(threadIdx.x >> 5) * 2 * (32 * PPT) * D;
+             (size_t)(threadIdx.x >> 5) * NST * (32 * PPT) * D;
   uint64_t* bars = reinterpret_cast<uint64_t*>(
       H_s + ((p.h_entries + 15) & ~15u) + THREADS * PPT + ((kK1Head * (D * sizeof(TOut) + 8) + 15) & ~(size_t)15) +
-      (size_t)THREADS * PPT * D * sizeof(TIn) * (BULK ? 2 : 1)) + (threadIdx.x >> 5) * 2;
+      (size_t)THREADS * PPT * D * sizeof(TIn) * (BULK ? NST : 1)) + (threadIdx.x >> 5) * NST;
   TOut* fh_rows = reinterpret_cast<TOut*>(H_s + ((p.h_entries + 15) & ~15u) + THREADS * PPT);
   u64* fh_sum = reinterpret_cast<u64*>(fh_rows + kK1Head * D);
   uint32_t nfh = 0;
@@ -661,35 +661,36 @@ __global__ void __launch_bounds__(THREADS, MINB) k_stream(StreamParams p) {
   };
   uint32_t t = gw;
   if constexpr (BULK) {
-    const uint32_t bar0 = smem_addr(bars), bar1 = bar0 + 8;
-    const uint32_t ring0 = smem_addr(rows_w), ring1 = ring0 + WT * D * (uint32_t)sizeof(TIn);
+    const uint32_t bar0 = smem_addr(bars), ring0 = smem_addr(rows_w);
+    constexpr uint32_t kStageBytes = WT * D * (uint32_t)sizeof(TIn);
     if (lane == 0) {
-      mbar_init(bar0, 1);
-      mbar_init(bar1, 1);
+#pragma unroll
+      for (int i = 0; i < NST; ++i) mbar_init(bar0 + 8 * i, 1);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncwarp();
     auto issue = [&](int st, uint32_t tt) {
       if (lane == 0) {
         const uint32_t rows = tt < nfull ? WT : n - tt * WT;
-        bulk_load(st ? ring1 : ring0, coords + (u64)tt * WT * D, rows * D * (uint32_t)sizeof(TIn), st ? bar1 : bar0);
+        bulk_load(ring0 + st * kStageBytes, coords + (u64)tt * WT * D, rows * D * (uint32_t)sizeof(TIn), bar0 + 8 * st);
       }
     };
-    if (t < ntiles) issue(0, t);
-    if (t + nw < ntiles) issue(1, t + nw);
-    uint32_t ph0 = 0, ph1 = 0;
+#pragma unroll
+    for (int i = 0; i < NST; ++i)
+      if (t + i * nw < ntiles) issue(i, t + i * nw);
+    uint32_t phases = 0;  // bit i: the parity stage i waits for next
     int st = 0;
     while (t < ntiles) {
-      mbar_wait(st ? bar1 : bar0, st ? ph1 : ph0);
-      if (st) ph1 ^= 1u; else ph0 ^= 1u;
+      mbar_wait(bar0 + 8 * st, (phases >> st) & 1u);
+      phases ^= 1u << st;
       const TIn* stage = rows_w + (size_t)st * WT * D;
 #pragma unroll
       for (int j = 0; j < PPT; ++j) load_row_cached<TIn, D>(stage, (u64)(j * 32 + lane), buf_a[j]);
       process(buf_a, t, stage);
       __syncwarp();
-      if (t + 2 * nw < ntiles) issue(st, t + 2 * nw);
+      if (t + NST * nw < ntiles) issue(st, t + NST * nw);
       t += nw;
-      st ^= 1;
+      st = st + 1 == NST ? 0 : st + 1;
     }
   } else {
     if (t < ntiles) load_tile(buf_a, t);
