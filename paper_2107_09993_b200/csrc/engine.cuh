@@ -1130,7 +1130,12 @@ struct Pipe final : PipeBase {
         const size_t sa = ((sk::kK4aHead * D * sizeof(TOut) + 15) & ~(size_t)15) + sk::kK4aHead * 8 +
                           (size_t)(kThreads / 32) * 64 * (D * sizeof(TOut) + 8 + 4) + 16;
         ck(cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sa), "smem attr");
-        sk::launch(ka, grid4, kThreads, sa, s, pa);
+        // K4a CTAs per SM (SKYCELL_K4A_CTAS; its output slack is covered by cap1)
+        static const int k4a_per_sm = [] {
+          const char* e = std::getenv("SKYCELL_K4A_CTAS");
+          return e ? std::max(1, std::min(8, std::atoi(e))) : 4;
+        }();
+        sk::launch(ka, nsm * k4a_per_sm, kThreads, sa, s, pa);
       } else {
         sk::launch(kc, grid4, kThreads, smem_pf, s, pa);
       }
